@@ -1,0 +1,208 @@
+"""ctypes bindings for the CPU checkers — TEST INFRASTRUCTURE ONLY.
+
+Two checkers live under oracle/:
+  * ``Oracle``    — oracle/libjt_oracle.so, the plain-C restatement
+                    (oracle/jt_oracle.c) of the reference parse path;
+  * ``Reference`` — oracle/_ref/libjsontape_ref.so, the UNMODIFIED reference
+                    (/root/reference/proj/src/*.cpp) built by
+                    oracle/build_ref.sh, driven through its own C ABI
+                    (proj/include/jsontape.h:29-64).
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+``--impl reference``) may import this module.  The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libjt_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libjsontape_ref.so")
+
+ERROR_NAMES = ["OK", "UTF8_ERROR", "STRING_ERROR", "NUMBER_ERROR", "TAPE_ERROR",
+               "DEPTH_ERROR", "CAPACITY", "EMPTY"]
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the C restatement (gcc only; runs here and on the GPU box)."""
+    src = os.path.join(HERE, "jt_oracle.c")
+    if force or not os.path.exists(ORACLE_SO) or \
+            os.path.getmtime(ORACLE_SO) < os.path.getmtime(src):
+        tmp = ORACLE_SO + ".tmp"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared",
+                               src, "-o", tmp, "-lm"])
+        os.replace(tmp, ORACLE_SO)
+    return ORACLE_SO
+
+
+def build_reference() -> str | None:
+    """Build oracle/_ref from /root/reference when the sources are present."""
+    subprocess.check_call(["sh", os.path.join(HERE, "build_ref.sh")])
+    return REF_SO if os.path.exists(REF_SO) else None
+
+
+@dataclass
+class ParseResult:
+    code: int
+    offset: int
+    index: bytes | None = None       # u32 little-endian positions
+    tape: bytes | None = None        # u64 words
+    strings: bytes | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def name(self) -> str:
+        return ERROR_NAMES[self.code]
+
+    def index_list(self):
+        import numpy as np
+        return np.frombuffer(self.index or b"", dtype=np.uint32)
+
+    def tape_array(self):
+        import numpy as np
+        return np.frombuffer(self.tape or b"", dtype=np.uint64)
+
+
+class _JtoResult(C.Structure):
+    _fields_ = [("code", C.c_int), ("offset", C.c_longlong),
+                ("index", C.POINTER(C.c_uint32)), ("index_count", C.c_size_t),
+                ("tape", C.POINTER(C.c_uint64)), ("tape_len", C.c_size_t),
+                ("strings", C.POINTER(C.c_uint8)), ("strings_len", C.c_size_t)]
+
+
+class Oracle:
+    """The plain-C restatement (oracle/jt_oracle.c)."""
+
+    def __init__(self):
+        self.lib = C.CDLL(build_oracle())
+        L = self.lib
+        L.jto_parse.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_JtoResult)]
+        L.jto_stage1.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_JtoResult)]
+        L.jto_free.argtypes = [C.POINTER(_JtoResult)]
+        L.jto_utf8_error_offset.argtypes = [C.c_char_p, C.c_size_t]
+        L.jto_utf8_error_offset.restype = C.c_longlong
+        L.jto_parse_number.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t,
+                                       C.POINTER(C.c_int), C.POINTER(C.c_uint64)]
+        L.jto_parse_string.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t,
+                                       C.c_char_p, C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_longlong)]
+
+    def parse(self, data: bytes) -> ParseResult:
+        r = _JtoResult()
+        self.lib.jto_parse(data, len(data), C.byref(r))
+        out = ParseResult(r.code, r.offset)
+        if r.index:
+            out.index = C.string_at(r.index, 4 * r.index_count)
+        if r.code == 0:
+            out.tape = C.string_at(r.tape, 8 * r.tape_len)
+            out.strings = C.string_at(r.strings, r.strings_len) if r.strings_len else b""
+        self.lib.jto_free(C.byref(r))
+        return out
+
+    def stage1(self, data: bytes) -> ParseResult:
+        r = _JtoResult()
+        self.lib.jto_stage1(data, len(data), C.byref(r))
+        out = ParseResult(r.code, r.offset)
+        if r.code == 0:
+            out.index = C.string_at(r.index, 4 * r.index_count) if r.index_count else b""
+        self.lib.jto_free(C.byref(r))
+        return out
+
+    def utf8_error_offset(self, data: bytes) -> int:
+        return self.lib.jto_utf8_error_offset(data, len(data))
+
+    def number(self, text: bytes):
+        """(ok, is_integer, raw 64-bit word) of parse_number on a padded token."""
+        buf = text + b"\0" * 64
+        is_int = C.c_int(0)
+        bits = C.c_uint64(0)
+        ok = self.lib.jto_parse_number(buf, len(text), 0, C.byref(is_int), C.byref(bits))
+        return bool(ok), bool(is_int.value), bits.value
+
+    def string(self, text: bytes):
+        """(ok, decoded bytes or None, error offset) of parse_string at 0."""
+        buf = text + b"\0" * 64
+        dst = C.create_string_buffer(len(text) + 64)
+        n = C.c_uint32(0)
+        e = C.c_longlong(-1)
+        ok = self.lib.jto_parse_string(buf, len(text), 0, dst, C.byref(n), C.byref(e))
+        if ok:
+            return True, dst.raw[4:4 + n.value], -1
+        return False, None, e.value
+
+
+class Reference:
+    """The unmodified reference through its own C ABI (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.jt_parser_new.restype = C.c_void_p
+        L.jt_parser_free.argtypes = [C.c_void_p]
+        L.jt_parse.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t,
+                               C.POINTER(C.c_void_p), C.POINTER(C.c_longlong)]
+        L.jt_stage1.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t,
+                                C.POINTER(C.c_longlong)]
+        L.jt_stage2.argtypes = [C.c_void_p, C.POINTER(C.c_void_p),
+                                C.POINTER(C.c_longlong)]
+        L.jt_index_count.argtypes = [C.c_void_p]
+        L.jt_index_count.restype = C.c_size_t
+        L.jt_index_positions.argtypes = [C.c_void_p]
+        L.jt_index_positions.restype = C.POINTER(C.c_uint32)
+        L.jt_document_free.argtypes = [C.c_void_p]
+        L.jt_document_dump.argtypes = [C.c_void_p]
+        L.jt_document_dump.restype = C.c_void_p
+        L.jt_string_free.argtypes = [C.c_void_p]
+        self.p = L.jt_parser_new()
+
+    def __del__(self):
+        try:
+            self.lib.jt_parser_free(self.p)
+        except Exception:
+            pass
+
+    def parse_code(self, data: bytes):
+        off = C.c_longlong(-7)
+        code = self.lib.jt_parse(self.p, data, len(data), None, C.byref(off))
+        return code, off.value
+
+    def stage1(self, data: bytes) -> ParseResult:
+        off = C.c_longlong(-7)
+        code = self.lib.jt_stage1(self.p, data, len(data), C.byref(off))
+        out = ParseResult(code, off.value)
+        if code == 0:
+            n = self.lib.jt_index_count(self.p)
+            out.index = C.string_at(self.lib.jt_index_positions(self.p), 4 * n) if n else b""
+        return out
+
+    def parse(self, data: bytes) -> ParseResult:
+        """Full parse; tape words and strings recovered from the reference's
+        own document dump is lossy, so the tape is read through the
+        jt_document struct layout instead (see _doc_words)."""
+        doc = C.c_void_p()
+        off = C.c_longlong(-7)
+        code = self.lib.jt_parse(self.p, data, len(data), C.byref(doc), C.byref(off))
+        out = ParseResult(code, off.value)
+        n = self.lib.jt_index_count(self.p)
+        if code != 1:  # index is refreshed unless stage 1 failed on UTF-8
+            out.index = C.string_at(self.lib.jt_index_positions(self.p), 4 * n) if n else b""
+        if code == 0:
+            out.tape, out.strings = _doc_words(doc.value)
+            self.lib.jt_document_free(doc)
+        return out
+
+
+def _doc_words(doc_ptr: int):
+    """jt_document{parsed_document{raw_vector<u64> tape; raw_vector<u8>
+    strings; size_t source_length}} (proj/src/capi.cpp:21-23, tape.h:49-58):
+    two libstdc++ std::vector triples (begin, end, cap)."""
+    words = (C.c_uint64 * 6).from_address(doc_ptr)
+    tb, te, _, sb, se, _ = list(words)
+    tape = C.string_at(tb, te - tb) if te > tb else b""
+    strings = C.string_at(sb, se - sb) if se > sb else b""
+    return tape, strings

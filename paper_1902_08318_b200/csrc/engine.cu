@@ -1,0 +1,660 @@
+// engine.cu — host side of the B200 parser: the jsontape C ABI.
+//
+// Mirrors proj/src/capi.cpp (the reference's C ABI) call for call, but every
+// parse runs on the GPU:
+//   jt_parser  = one CUDA stream + a grow-only device arena (padded input,
+//                two structural-index buffers, look-back records, token
+//                records, tape, strings) + pinned control block.
+//   jt_parse   = H2D copy into the padded input -> K1 -> K2..K4 -> one D2H of
+//                the control block -> D2H of tape and strings on success.
+//   jt_stage1 / jt_stage2 keep input and index device-resident in between.
+// There is no CPU fallback: without a CUDA device jt_parser_new returns NULL
+// and nothing else can be called.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <charconv>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/jsontape.h"
+#include "../../include/jsontape_b200.h"
+#include "stage1.h"
+#include "jt_common.cuh"
+#include "stage2.h"
+
+namespace {
+
+constexpr size_t kPad = 64;  // proj/src/indexer.h:17
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  bool ensure(size_t bytes) {
+    if (bytes <= cap) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)1 << 20);
+    want = (want + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return false;
+    }
+    cap = want;
+    return true;
+  }
+  template <class T>
+  T *as() const {
+    return (T *)p;
+  }
+};
+
+}  // namespace
+
+struct jt_document {
+  std::vector<uint64_t> tape;
+  std::vector<uint8_t> strings;
+};
+
+struct jt_parser {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf in;               // padded input
+  DevBuf idx[2];           // structural index, double-buffered
+  int cur = 0;             // idx[cur] = index of the last successful stage 1
+  DevBuf s1rec, s2rec;     // look-back records
+  DevBuf tok, chunk_tape, chunk_min, tile_min, super_min, super2_min, slow;
+  DevBuf tape, strings;
+  DevBuf ctrl;
+  jt::Ctrl *h_ctrl = nullptr;  // pinned
+  uint64_t in_len = 0;         // bytes in `in` (retained input)
+  size_t in_zeroed_to = 0;     // zero tail maintained up to here
+  bool have_index = false;
+  uint64_t index_count = 0;
+  mutable std::vector<uint32_t> h_index;
+  mutable bool h_index_valid = false;
+  uint64_t last_tape_len = 0, last_string_bytes = 0;
+  bool last_ok = false;
+  int launches = 0;
+  std::string err;
+  uint64_t pending_len = 0;
+  int pending_idx = -1;
+};
+
+namespace {
+
+bool cuda_ok(jt_parser *p, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return true;
+  p->err = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();
+  return false;
+}
+
+void set_off(long long *o, long long v) {
+  if (o) *o = v;
+}
+
+size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// capacity of the padded input for `len` bytes: stage 1 reads whole 16 KiB
+// tiles, stage 2 reads up to 64 bytes past len (escape / atom lookahead)
+size_t input_capacity(uint64_t len) { return round_up((size_t)len + kPad, jt::kStage1Tile) + kPad; }
+
+bool ensure_input(jt_parser *p, uint64_t len) {
+  size_t need = input_capacity(len);
+  size_t old = p->in.cap;
+  if (!p->in.ensure(need)) return false;
+  if (p->in.cap != old) p->in_zeroed_to = 0;
+  return true;
+}
+
+// zero [len, tile end + pad) so stage 1 and the lookaheads read zeros
+bool zero_tail(jt_parser *p, uint64_t len) {
+  size_t end = input_capacity(len);
+  return cuda_ok(p, cudaMemsetAsync(p->in.as<uint8_t>() + len, 0, end - len, p->stream),
+                 "memset input tail");
+}
+
+// Device buffers sized from len (S <= len); the tape/strings worst cases
+// follow the reference's reservations (tape_builder.cpp:148, 152).
+bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
+  size_t cap_tok = (size_t)len + 16;
+  if (!p->idx[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->s1rec.ensure(jt::stage1_records(len) * 2 * sizeof(uint64_t) + 64)) return false;
+  if (!p->ctrl.ensure(sizeof(jt::Ctrl))) return false;
+  return true;
+}
+
+bool ensure_stage2(jt_parser *p, uint64_t len) {
+  uint64_t cap = len + 16;
+  jt::Stage2Sizes z = jt::stage2_sizes(cap);
+  bool ok = p->s2rec.ensure(z.tiles * 6 * sizeof(uint64_t)) &&
+            p->tok.ensure((cap + 16) * sizeof(uint32_t)) &&
+            p->chunk_tape.ensure(z.chunks * sizeof(uint32_t)) &&
+            p->chunk_min.ensure(z.chunks * sizeof(int16_t)) &&
+            p->tile_min.ensure(z.tiles * sizeof(int16_t)) &&
+            p->super_min.ensure(z.supers * sizeof(int16_t)) &&
+            p->super2_min.ensure(z.supers2 * sizeof(int16_t)) &&
+            p->slow.ensure((cap + 16) * 2 * sizeof(uint32_t)) &&
+            p->tape.ensure((2 * cap + 8) * sizeof(uint64_t)) &&
+            p->strings.ensure((size_t)len + 4 * cap + 128);
+  return ok;
+}
+
+jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
+  jt::Stage1Args a{};
+  jt::Ctrl *c = p->ctrl.as<jt::Ctrl>();
+  a.in = p->in.as<uint8_t>();
+  a.len = len;
+  a.idx = p->idx[which].as<uint32_t>();
+  uint64_t nt = jt::stage1_records(len);
+  a.rec_state = p->s1rec.as<uint64_t>();
+  a.rec_count = p->s1rec.as<uint64_t>() + nt;
+  a.tile_counter = &c->s1_tile_counter;
+  a.utf8_pos = &c->utf8_pos;
+  a.total = &c->S;
+  return a;
+}
+
+jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
+  jt::Stage2Args a{};
+  a.in = p->in.as<uint8_t>();
+  a.len = len;
+  a.idx = p->idx[which].as<uint32_t>();
+  a.ctrl = p->ctrl.as<jt::Ctrl>();
+  a.tok = p->tok.as<uint32_t>();
+  a.chunk_tape = p->chunk_tape.as<uint32_t>();
+  a.chunk_min = p->chunk_min.as<int16_t>();
+  a.tile_min = p->tile_min.as<int16_t>();
+  a.super_min = p->super_min.as<int16_t>();
+  a.super2_min = p->super2_min.as<int16_t>();
+  a.rec = p->s2rec.as<uint64_t>();
+  a.slow = p->slow.as<uint32_t>();
+  a.tape = p->tape.as<uint64_t>();
+  a.strings = p->strings.as<uint8_t>();
+  a.cap_tokens = len + 16;
+  a.num_sms = p->num_sms;
+  return a;
+}
+
+// Enqueue init + K1 (+ stage 2) for `len` resident bytes; index -> idx[which]
+bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
+  p->launches = 0;
+  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  uint64_t s1w = jt::stage1_records(len) * 2;
+  uint64_t s2w = full ? z.tiles * 6 : 0;
+  if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
+                                  p->s2rec.as<uint64_t>(), s2w, p->stream),
+               "init"))
+    return false;
+  p->launches++;
+  if (!cuda_ok(p, jt::stage1_launch(s1_args(p, len, which), p->stream), "stage1")) return false;
+  p->launches++;
+  if (full) {
+    int n = 0;
+    if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n), "stage2")) return false;
+    p->launches += n;
+  } else {
+    if (!cuda_ok(p, jt::stage1_finalize_launch(p->ctrl.as<jt::Ctrl>(), p->stream), "stage1 final"))
+      return false;
+    p->launches++;
+  }
+  return cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                    p->stream),
+                 "ctrl D2H");
+}
+
+// wait for the enqueued work and publish its results into the parser
+jt_error finish(jt_parser *p, int which, bool full, long long *off) {
+  if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  const jt::Ctrl &c = *p->h_ctrl;
+  p->last_ok = false;
+  if (c.code != jt::kUtf8Error) {  // the reference refreshes the index only then
+    p->cur = which;
+    p->have_index = true;
+    p->index_count = c.S;
+    p->h_index_valid = false;
+  }
+  set_off(off, c.offset);
+  if (full && c.code == jt::kOk) {
+    p->last_ok = true;
+    p->last_tape_len = c.tape_len;
+    p->last_string_bytes = c.string_bytes;
+  }
+  return (jt_error)c.code;
+}
+
+bool upload(jt_parser *p, const char *data, size_t len) {
+  if (!ensure_input(p, len)) return false;
+  if (len && !cuda_ok(p, cudaMemcpyAsync(p->in.p, data, len, cudaMemcpyHostToDevice, p->stream),
+                      "input H2D"))
+    return false;
+  if (!zero_tail(p, len)) return false;
+  p->in_len = len;
+  return true;
+}
+
+jt_document *download(jt_parser *p) {
+  jt_document *d = new (std::nothrow) jt_document;
+  if (!d) return nullptr;
+  try {
+    d->tape.resize(p->last_tape_len);
+    d->strings.resize(p->last_string_bytes);
+  } catch (...) {
+    delete d;
+    return nullptr;
+  }
+  if (p->last_tape_len)
+    cudaMemcpyAsync(d->tape.data(), p->tape.p, p->last_tape_len * 8, cudaMemcpyDeviceToHost, p->stream);
+  if (p->last_string_bytes)
+    cudaMemcpyAsync(d->strings.data(), p->strings.p, p->last_string_bytes, cudaMemcpyDeviceToHost,
+                    p->stream);
+  if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "download")) {
+    delete d;
+    return nullptr;
+  }
+  return d;
+}
+
+jt_error parse_resident(jt_parser *p, uint64_t len, jt_document **out, long long *off) {
+  if (out) *out = nullptr;
+  if (len >= (1ULL << 32)) {  // indexer.cpp:33-34
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  int which = p->cur ^ 1;
+  if (!ensure_stage1(p, len, which) || !ensure_stage2(p, len)) {
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  if (!enqueue(p, len, which, true)) {
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  jt_error e = finish(p, which, true, off);
+  if (e == JT_OK && out) {
+    *out = download(p);
+    if (!*out) {
+      set_off(off, -1);
+      return JT_CAPACITY;
+    }
+  }
+  return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+jt_parser *jt_parser_new(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  jt_parser *p = new (std::nothrow) jt_parser;
+  if (!p) return nullptr;
+  p->device = dev;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost((void **)&p->h_ctrl, sizeof(jt::Ctrl)) != cudaSuccess ||
+      !p->ctrl.ensure(sizeof(jt::Ctrl))) {
+    cudaGetLastError();
+    if (p->own_stream) cudaStreamDestroy(p->own_stream);
+    if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
+    delete p;
+    return nullptr;
+  }
+  p->stream = p->own_stream;
+  return p;
+}
+
+void jt_parser_free(jt_parser *p) {
+  if (!p) return;
+  cudaStreamSynchronize(p->stream);
+  if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
+  delete p;
+}
+
+void jt_parser_set_flags(jt_parser *p, int use_clmul, int fast_extract, int vector_classify) {
+  (void)p;
+  (void)use_clmul;
+  (void)fast_extract;
+  (void)vector_classify;
+}
+
+jt_error jt_parse(jt_parser *p, const char *data, size_t len, jt_document **out,
+                  long long *error_offset) {
+  if (out) *out = nullptr;
+  if ((uint64_t)len >= (1ULL << 32)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  if (!upload(p, data, len)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  return parse_resident(p, len, out, error_offset);
+}
+
+jt_error jt_stage1(jt_parser *p, const char *data, size_t len, long long *error_offset) {
+  if ((uint64_t)len >= (1ULL << 32)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  if (!upload(p, data, len)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  return jt_b200_stage1_resident(p, len, error_offset);
+}
+
+size_t jt_index_count(const jt_parser *p) { return p->have_index ? (size_t)p->index_count : 0; }
+
+const uint32_t *jt_index_positions(const jt_parser *p) {
+  if (!p->h_index_valid) {
+    p->h_index.assign(p->index_count + 8, 0u);
+    if (p->index_count)
+      cudaMemcpy(p->h_index.data(), p->idx[p->cur].p, p->index_count * 4, cudaMemcpyDeviceToHost);
+    p->h_index_valid = true;
+  }
+  return p->h_index.data();
+}
+
+jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
+  if (out) *out = nullptr;
+  uint64_t len = p->in_len;
+  if (!ensure_stage2(p, len)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  // re-run stage 2 over the retained input and index: reset records and
+  // rebuild S into the control block from the host count
+  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  p->launches = 0;
+  if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), 0,
+                                  p->s2rec.as<uint64_t>(), z.tiles * 6, p->stream),
+               "init")) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  uint64_t S = p->have_index ? p->index_count : 0;
+  cudaMemcpyAsync(&p->ctrl.as<jt::Ctrl>()->S, &S, sizeof(S), cudaMemcpyHostToDevice, p->stream);
+  int n = 0;
+  if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, p->cur), p->stream, &n), "stage2") ||
+      !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl")) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  p->launches = n + 1;
+  if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  const jt::Ctrl &c = *p->h_ctrl;
+  set_off(error_offset, c.offset);
+  p->last_ok = c.code == jt::kOk;
+  if (p->last_ok) {
+    p->last_tape_len = c.tape_len;
+    p->last_string_bytes = c.string_bytes;
+    if (out) {
+      *out = download(p);
+      if (!*out) {
+        set_off(error_offset, -1);
+        return JT_CAPACITY;
+      }
+    }
+  }
+  return (jt_error)c.code;
+}
+
+void jt_document_free(jt_document *doc) { delete doc; }
+
+int jt_document_equal(const jt_document *a, const jt_document *b) {
+  return a->tape == b->tape && a->strings == b->strings ? 1 : 0;
+}
+
+// text dump, same format as tape_dump (proj/src/tape_builder.cpp:277-350)
+char *jt_document_dump(const jt_document *doc) {
+  std::string out;
+  char buf[64];
+  auto num = [&](uint64_t v) {
+    auto r = std::to_chars(buf, buf + sizeof(buf), v);
+    out.append(buf, r.ptr);
+  };
+  const auto &t = doc->tape;
+  for (size_t i = 0; i < t.size(); i++) {
+    uint64_t w = t[i];
+    uint8_t tag = (uint8_t)(w >> 56);
+    uint64_t pl = w & jt::kPayloadMask;
+    num(i);
+    out += " : ";
+    switch (tag) {
+      case 'r':
+        out += "r\t// pointing to ";
+        num(pl);
+        break;
+      case '{':
+      case '[':
+        out += (char)tag;
+        out += "\t// pointing to next tape location ";
+        num(pl);
+        out += " (first node after the scope)";
+        break;
+      case '}':
+      case ']':
+        out += (char)tag;
+        out += "\t// pointing to previous tape location ";
+        num(pl);
+        out += " (start of the scope)";
+        break;
+      case '"': {
+        out += "string \"";
+        uint32_t n = 0;
+        memcpy(&n, doc->strings.data() + pl, 4);
+        out.append((const char *)doc->strings.data() + pl + 4, n);
+        out += '"';
+        break;
+      }
+      case 'l': {
+        out += "integer ";
+        auto r = std::to_chars(buf, buf + sizeof(buf), (int64_t)t[i + 1]);
+        out.append(buf, r.ptr);
+        i++;
+        break;
+      }
+      case 'd': {
+        out += "double ";
+        double v;
+        memcpy(&v, &t[i + 1], 8);
+        auto r = std::to_chars(buf, buf + sizeof(buf), v);
+        out.append(buf, r.ptr);
+        i++;
+        break;
+      }
+      case 't': out += "true"; break;
+      case 'f': out += "false"; break;
+      case 'n': out += "null"; break;
+    }
+    out += '\n';
+  }
+  char *s = (char *)malloc(out.size() + 1);
+  if (s) memcpy(s, out.c_str(), out.size() + 1);
+  return s;
+}
+
+char *jt_document_distinct(const jt_document *doc, const char *path) {
+  (void)doc;
+  (void)path;
+  return nullptr;  // navigation/query is out of the hot-path scope
+}
+
+void jt_string_free(char *s) { free(s); }
+
+jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t *dst_len,
+                   long long *error_offset) {
+  (void)p;
+  (void)data;
+  (void)len;
+  (void)dst;
+  (void)dst_len;
+  set_off(error_offset, -1);
+  return JT_CAPACITY;  // GPU minify is §8f "next"; not in round 1
+}
+
+jt_error jt_compute_stats(jt_parser *p, const char *data, size_t len, jt_stats *out,
+                          long long *error_offset) {
+  jt_document *doc = nullptr;
+  jt_error e = jt_parse(p, data, len, &doc, error_offset);
+  if (e != JT_OK) return e;
+  jt_stats s{};
+  const auto &t = doc->tape;
+  for (size_t i = 1; i + 1 < t.size(); i++) {
+    switch ((uint8_t)(t[i] >> 56)) {
+      case 'l': s.integers++; i++; break;
+      case 'd': s.floats++; i++; break;
+      case '"': s.strings++; break;
+      case '{': s.objects++; break;
+      case '[': s.arrays++; break;
+      case 'n': s.nulls++; break;
+      case 't': s.trues++; break;
+      case 'f': s.falses++; break;
+    }
+  }
+  for (size_t i = 0; i < len; i++) s.non_ascii_bytes += ((uint8_t)data[i]) >= 0x80;
+  s.structurals = p->index_count;
+  s.bytes = len;
+  s.bytes_per_structural = s.structurals ? (double)len / (double)s.structurals : 0.0;
+  jt_document_free(doc);
+  *out = s;
+  return JT_OK;
+}
+
+int jt_oracle_validate(const char *data, size_t len) {
+  jt_parser *p = jt_parser_new();
+  if (!p) return 0;
+  jt_error e = jt_parse(p, data, len, nullptr, nullptr);
+  jt_parser_free(p);
+  return e == JT_OK ? 1 : 0;
+}
+
+char *jt_generate(const char *kind, uint64_t size, uint64_t seed, size_t *len_out) {
+  (void)kind;
+  (void)size;
+  (void)seed;
+  if (len_out) *len_out = 0;
+  return nullptr;
+}
+
+const char *jt_error_name(jt_error code) {
+  switch (code) {
+    case JT_OK: return "OK";
+    case JT_UTF8_ERROR: return "UTF8_ERROR";
+    case JT_STRING_ERROR: return "STRING_ERROR";
+    case JT_NUMBER_ERROR: return "NUMBER_ERROR";
+    case JT_TAPE_ERROR: return "TAPE_ERROR";
+    case JT_DEPTH_ERROR: return "DEPTH_ERROR";
+    case JT_CAPACITY: return "CAPACITY";
+    default: return "EMPTY";
+  }
+}
+
+// ---- B200 extensions -------------------------------------------------------
+
+void *jt_b200_input_buffer(jt_parser *p, size_t len) {
+  if ((uint64_t)len >= (1ULL << 32)) return nullptr;
+  if (!ensure_input(p, len) || !zero_tail(p, len)) return nullptr;
+  if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) return nullptr;
+  return p->in.p;
+}
+
+jt_error jt_b200_stage1_resident(jt_parser *p, size_t len, long long *error_offset) {
+  if ((uint64_t)len >= (1ULL << 32)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  p->in_len = len;
+  int which = p->cur ^ 1;
+  if (!ensure_stage1(p, len, which) || !enqueue(p, len, which, false)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  return finish(p, which, false, error_offset);
+}
+
+jt_error jt_b200_parse_resident(jt_parser *p, size_t len, long long *error_offset) {
+  p->in_len = len;
+  return parse_resident(p, len, nullptr, error_offset);
+}
+
+jt_error jt_b200_parse_async(jt_parser *p, size_t len) {
+  if ((uint64_t)len >= (1ULL << 32)) return JT_CAPACITY;
+  p->in_len = len;
+  int which = p->cur ^ 1;
+  if (!ensure_stage1(p, len, which) || !ensure_stage2(p, len) || !enqueue(p, len, which, true))
+    return JT_CAPACITY;
+  p->pending_len = len;
+  p->pending_idx = which;
+  return JT_OK;
+}
+
+jt_error jt_b200_finish(jt_parser *p, long long *error_offset) {
+  if (p->pending_idx < 0) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  int which = p->pending_idx;
+  p->pending_idx = -1;
+  return finish(p, which, true, error_offset);
+}
+
+const uint32_t *jt_b200_device_index(const jt_parser *p, size_t *count) {
+  if (count) *count = jt_index_count(p);
+  return p->idx[p->cur].as<uint32_t>();
+}
+
+const uint64_t *jt_b200_device_tape(const jt_parser *p, size_t *words) {
+  if (words) *words = p->last_ok ? p->last_tape_len : 0;
+  return p->tape.as<uint64_t>();
+}
+
+const uint8_t *jt_b200_device_strings(const jt_parser *p, size_t *bytes) {
+  if (bytes) *bytes = p->last_ok ? p->last_string_bytes : 0;
+  return p->strings.as<uint8_t>();
+}
+
+jt_error jt_b200_download(jt_parser *p, jt_document **out) {
+  *out = nullptr;
+  if (!p->last_ok) return JT_CAPACITY;
+  *out = download(p);
+  return *out ? JT_OK : JT_CAPACITY;
+}
+
+void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
+  p->stream = cuda_stream ? (cudaStream_t)cuda_stream : p->own_stream;
+}
+
+int jt_b200_last_launches(const jt_parser *p) { return p->launches; }
+
+int jt_b200_device(const jt_parser *p) { return p->device; }
+
+const char *jt_b200_last_error(const jt_parser *p) { return p->err.c_str(); }
+
+}  // extern "C"

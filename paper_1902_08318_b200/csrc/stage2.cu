@@ -1,0 +1,719 @@
+// stage2.cu — tape construction as data-parallel passes.
+//
+// Replaces tape_builder::run (proj/src/tape_builder.cpp:140-258), a
+// sequential goto machine, by:
+//   K2 k_tokens   one thread per 16-token chunk, 128 chunks per tile.
+//                 Phase A classifies tokens and validates/measures every
+//                 scalar (strings, numbers, atoms); a 3-channel decoupled
+//                 look-back gives each chunk its tape index (sum of token
+//                 widths), depth (sum of +1/-1) and string-buffer offset
+//                 (sum of 4 + decoded length).  Phase B writes scalar tape
+//                 words and decoded strings, and the per-token record
+//                 {byte, scalar-failed, depth_before} used below.
+//   K2S k_slow    exact decimal->binary64 for the few numbers Eisel-Lemire
+//                 cannot settle (numparse.cuh).
+//   KT  k_tree    min-depth summaries over 64 tiles and 64^2 tiles.
+//   K3 k_struct   one thread per chunk runs the reference's state machine
+//                 over its 16 tokens.  Its entry state is derived from the
+//                 two previous tokens; an enclosing container outside the
+//                 chunk is found as the previous token with a smaller depth
+//                 (a previous-smaller-value query over the depth min-tree).
+//                 Grammar errors go to an atomicMin keyed by token index
+//                 (first error in walk order wins);
+//                 matched brackets write both tape words (App. A.6).
+//   K4 k_final    error code/offset (string errors re-measured), root words.
+#include <cuda_runtime.h>
+
+#include "lookback.cuh"
+#include "numparse.cuh"
+#include "stage2.h"
+#include "strparse.cuh"
+
+namespace jt {
+
+namespace {
+
+constexpr int kWarps2 = kS2Threads / 32;
+
+struct InAt {
+  const uint8_t *in;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
+};
+
+__device__ __forceinline__ int tok_width(uint32_t c) {
+  if (c == ',' || c == ':') return 0;
+  if (c == '-' || (c - '0') < 10u) return 2;
+  return 1;
+}
+
+__device__ __forceinline__ int tok_delta(uint32_t c) {
+  return (c == '{' || c == '[') ? 1 : (c == '}' || c == ']') ? -1 : 0;
+}
+
+__device__ __forceinline__ int clamp16(long long d) {
+  return d < -2 ? -2 : d > 1026 ? 1026 : (int)d;
+}
+
+__device__ __forceinline__ int tok_depth(uint32_t v) { return (int)(int16_t)(v >> 16); }
+
+// ---- 3-channel look-back (tape words, depth, string bytes) --------------
+// rec[6*t + 0..2] aggregate, rec[6*t + 3..5] inclusive; bit 63 = valid.
+constexpr uint64_t kValid = 1ULL << 63;
+constexpr uint64_t kVal63 = kValid - 1;
+
+__device__ __forceinline__ long long sext63(uint64_t v) {
+  return (long long)(v << 1) >> 1;
+}
+
+struct Tri {
+  unsigned long long w, sb;
+  long long d;
+};
+
+__device__ __forceinline__ void publish(uint64_t *rec, uint64_t tile, int slot, const Tri &v) {
+  uint64_t *r = rec + 6 * tile + 3 * slot;
+  lb_store(r + 0, kValid | (v.w & kVal63));
+  lb_store(r + 1, kValid | ((uint64_t)v.d & kVal63));
+  lb_store(r + 2, kValid | (v.sb & kVal63));
+}
+
+// 0 = not ready, 1 = aggregate, 2 = inclusive
+__device__ __forceinline__ int read_rec(const uint64_t *rec, int64_t tile, Tri &v) {
+  const uint64_t *r = rec + 6 * tile;
+  uint64_t a = lb_load(r + 3), b = lb_load(r + 4), c = lb_load(r + 5);
+  if ((a & b & c) >> 63) {
+    v.w = a & kVal63;
+    v.d = sext63(b);
+    v.sb = c & kVal63;
+    return 2;
+  }
+  a = lb_load(r + 0), b = lb_load(r + 1), c = lb_load(r + 2);
+  if ((a & b & c) >> 63) {
+    v.w = a & kVal63;
+    v.d = sext63(b);
+    v.sb = c & kVal63;
+    return 1;
+  }
+  return 0;
+}
+
+__device__ Tri lookback3(const uint64_t *rec, int64_t tile) {
+  const int lane = threadIdx.x & 31;
+  Tri acc{0, 0, 0};
+  int64_t base = tile - 1;
+  for (;;) {
+    int64_t pred = base - lane;
+    Tri v{0, 0, 0};
+    int st = 2;
+    if (pred >= 0) {
+      while ((st = read_rec(rec, pred, v)) == 0) __nanosleep(32);
+    }
+    uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+    int stop = incl ? __ffs(incl) - 1 : 31;
+    if (lane > stop) v = Tri{0, 0, 0};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
+      v.sb += __shfl_xor_sync(0xffffffffu, v.sb, o);
+      v.d += __shfl_xor_sync(0xffffffffu, v.d, o);
+    }
+    acc.w += v.w;
+    acc.sb += v.sb;
+    acc.d += v.d;
+    if (incl) return acc;
+    base -= 32;
+  }
+}
+
+// ---- K2: tokens -----------------------------------------------------------
+
+__global__ void __launch_bounds__(kS2Threads) k_tokens(Stage2Args a) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_w[kWarps2], s_sb[kWarps2];
+  __shared__ long long s_d[kWarps2];
+  __shared__ int s_min[kWarps2];
+  __shared__ Tri s_base;
+  __shared__ uint64_t s_val[kTokPerThread * kS2Threads];
+
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint64_t S = ctrl->S;
+  const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const InAt at{a.in};
+
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->s2_tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    __syncthreads();
+    if (tile >= ntiles) return;
+
+    const uint64_t chunk = tile * kS2Threads + threadIdx.x;
+    const uint64_t t0 = chunk * kTokPerThread;
+    uint32_t pos[kTokPerThread];
+    uint32_t info[kTokPerThread];  // c | fail << 8 | numkind << 9
+    int n = 0;
+    if (t0 + kTokPerThread <= S) {
+      const uint4 *ip = (const uint4 *)(a.idx + t0);
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        uint4 v = ip[q];
+        pos[4 * q] = v.x;
+        pos[4 * q + 1] = v.y;
+        pos[4 * q + 2] = v.z;
+        pos[4 * q + 3] = v.w;
+      }
+      n = kTokPerThread;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kTokPerThread; k++) pos[k] = t0 + k < S ? a.idx[t0 + k] : 0u;
+      n = t0 < S ? (int)(S - t0) : 0;
+    }
+
+    // phase A: classify, validate, measure
+    unsigned long long W = 0, SB = 0;
+    long long D = 0;
+    int dmin = 0;
+#pragma unroll
+    for (int k = 0; k < kTokPerThread; k++) {
+      info[k] = 0;
+      if (k >= n) continue;
+      const uint32_t p = pos[k];
+      const uint32_t c = at(p);
+      dmin = D < dmin ? (int)D : dmin;
+      uint32_t fail = 0, nk = 0;
+      if (c == '"') {
+        str::Measure m = str::string_measure(at, p);
+        if (m.ok) SB += 4ULL + m.len;
+        else {
+          fail = 1;
+          SB += 4;
+        }
+      } else if (c == 't' || c == 'f' || c == 'n') {
+        fail = !str::atom_ok(at, a.len, p, c);
+      } else if (c == '-' || (c - '0') < 10u) {
+        num::NumResult r = num::parse_number(at, a.len, p);
+        nk = (uint32_t)r.kind;
+        fail = r.kind == num::kNumFail;
+        s_val[k * kS2Threads + threadIdx.x] = r.bits;
+      }
+      W += (unsigned long long)tok_width(c);
+      D += tok_delta(c);
+      info[k] = c | (fail << 8) | (nk << 9);
+    }
+
+    // CTA scan of (W, D, SB) and the min of depth_before
+    unsigned long long iw = W, isb = SB;
+    long long id = D;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long xw = __shfl_up_sync(0xffffffffu, iw, o);
+      unsigned long long xs = __shfl_up_sync(0xffffffffu, isb, o);
+      long long xd = __shfl_up_sync(0xffffffffu, id, o);
+      if (lane >= o) {
+        iw += xw;
+        isb += xs;
+        id += xd;
+      }
+    }
+    if (lane == 31) {
+      s_w[warp] = iw;
+      s_sb[warp] = isb;
+      s_d[warp] = id;
+    }
+    __syncthreads();
+    Tri tot{0, 0, 0}, pre{0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kWarps2; k++) {
+      if (k < warp) {
+        pre.w += s_w[k];
+        pre.sb += s_sb[k];
+        pre.d += s_d[k];
+      }
+      tot.w += s_w[k];
+      tot.sb += s_sb[k];
+      tot.d += s_d[k];
+    }
+    pre.w += iw - W;
+    pre.sb += isb - SB;
+    pre.d += id - D;
+
+    if (warp == 0) {
+      Tri base{0, 0, 0};
+      if (tile > 0) {
+        if (lane == 0) publish(a.rec, tile, 0, tot);
+        base = lookback3(a.rec, (int64_t)tile);
+      }
+      if (lane == 0) {
+        Tri inc{base.w + tot.w, base.sb + tot.sb, base.d + tot.d};
+        publish(a.rec, tile, 1, inc);
+        s_base = base;
+        if (tile == ntiles - 1) {
+          ctrl->tape_words = 1 + inc.w;
+          ctrl->string_bytes = inc.sb;
+        }
+      }
+    }
+    __syncthreads();
+
+    // phase B: emit
+    unsigned long long t = 1 + s_base.w + pre.w;
+    unsigned long long so = s_base.sb + pre.sb;
+    long long d = s_base.d + pre.d;
+    int cmin = clamp16(d + dmin);
+    if (n > 0) {
+      a.chunk_tape[chunk] = (uint32_t)t;
+      a.chunk_min[chunk] = (int16_t)cmin;
+    }
+    uint32_t toks[kTokPerThread];
+#pragma unroll
+    for (int k = 0; k < kTokPerThread; k++) {
+      if (k >= n) continue;
+      const uint32_t c = info[k] & 0xFF, fail = (info[k] >> 8) & 1, nk = info[k] >> 9;
+      toks[k] = c | (fail << 8) | ((uint32_t)(uint16_t)clamp16(d) << 16);
+      if (c == '"') {
+        if (!fail) {
+          uint8_t *dst = a.strings + so + 4;
+          uint32_t len = 0;
+          str::string_decode(at, pos[k], [&](uint32_t i, uint8_t b) {
+            dst[i] = b;
+            len = i + 1;
+          });
+          a.strings[so] = (uint8_t)len;
+          a.strings[so + 1] = (uint8_t)(len >> 8);
+          a.strings[so + 2] = (uint8_t)(len >> 16);
+          a.strings[so + 3] = (uint8_t)(len >> 24);
+          a.tape[t] = tape_word('"', so);
+          so += 4ULL + len;
+        } else {
+          so += 4;
+        }
+      } else if (c == 't' || c == 'f' || c == 'n') {
+        a.tape[t] = (uint64_t)c << 56;
+      } else if (c == '-' || (c - '0') < 10u) {
+        if (nk == num::kNumInt) {
+          a.tape[t] = (uint64_t)'l' << 56;
+          a.tape[t + 1] = s_val[k * kS2Threads + threadIdx.x];
+        } else if (nk == num::kNumFloat) {
+          a.tape[t] = (uint64_t)'d' << 56;
+          a.tape[t + 1] = s_val[k * kS2Threads + threadIdx.x];
+        } else if (nk == num::kNumSlow) {
+          a.tape[t] = (uint64_t)'d' << 56;
+          uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
+          a.slow[2 * slot] = (uint32_t)(t0 + k);
+          a.slow[2 * slot + 1] = (uint32_t)t;
+        }
+      }
+      t += (unsigned long long)tok_width(c);
+      d += tok_delta(c);
+    }
+    if (n == kTokPerThread) {
+      uint4 *tp = (uint4 *)(a.tok + t0);
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        tp[q] = make_uint4(toks[4 * q], toks[4 * q + 1], toks[4 * q + 2], toks[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kTokPerThread; k++)
+        if (k < n) a.tok[t0 + k] = toks[k];
+    }
+
+    // tile min of depth_before for the search tree
+    int m = n > 0 ? cmin : 0x7FFF;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_min[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int mm = s_min[0];
+#pragma unroll
+      for (int k = 1; k < kWarps2; k++) mm = min(mm, s_min[k]);
+      a.tile_min[tile] = (int16_t)mm;
+    }
+  }
+}
+
+// ---- K2S: exact fallback for hard floats ----------------------------------
+
+__global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint32_t n = ctrl->slow_count;
+  const InAt at{a.in};
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    uint32_t tokn = a.slow[2 * k], slot = a.slow[2 * k + 1];
+    num::Decimal dec;
+    uint64_t bits;
+    if (num::slow_decimal(at, a.len, a.idx[tokn], dec, &bits)) a.tape[slot + 1] = bits;
+    else atomicOr(&a.tok[tokn], 1u << 8);  // binary64 overflow -> NUMBER_ERROR
+  }
+}
+
+// ---- KT: upper levels of the depth min-tree --------------------------------
+
+__global__ void __launch_bounds__(1024) k_tree(Stage2Args a) {
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint64_t S = ctrl->S;
+  const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
+  const uint64_t nsup = (ntiles + kTilesPerSuper - 1) / kTilesPerSuper;
+  const uint64_t nsup2 = (nsup + kSupersPerSuper2 - 1) / kSupersPerSuper2;
+  for (uint64_t s = threadIdx.x; s < nsup; s += blockDim.x) {
+    int m = 0x7FFF;
+    uint64_t e = min((s + 1) * kTilesPerSuper, ntiles);
+    for (uint64_t t = s * kTilesPerSuper; t < e; t++) m = min(m, (int)a.tile_min[t]);
+    a.super_min[s] = (int16_t)m;
+  }
+  __syncthreads();
+  for (uint64_t s = threadIdx.x; s < nsup2; s += blockDim.x) {
+    int m = 0x7FFF;
+    uint64_t e = min((s + 1) * kSupersPerSuper2, nsup);
+    for (uint64_t t = s * kSupersPerSuper2; t < e; t++) m = min(m, (int)a.super_min[t]);
+    a.super2_min[s] = (int16_t)m;
+  }
+}
+
+// ---- K3: structure --------------------------------------------------------
+
+// nearest j < i whose depth_before <= L (the innermost container open at i
+// when L = depth_before(i) - 1), or -1
+__device__ int64_t psv(const Stage2Args &a, int64_t i, int L) {
+  if (i <= 0) return -1;
+  int64_t j = i - 1;
+  const int64_t lo = (i - 1) & ~(int64_t)(kTokPerThread - 1);
+  for (; j >= lo; --j)
+    if (tok_depth(a.tok[j]) <= L) return j;
+  int64_t c = lo / kTokPerThread - 1;  // chunks of the same tile
+  int64_t found_chunk = -1;
+  const int64_t clo = (lo / kTokPerThread) & ~(int64_t)(kS2Threads - 1);
+  for (; c >= clo; --c)
+    if (a.chunk_min[c] <= L) {
+      found_chunk = c;
+      break;
+    }
+  if (found_chunk < 0) {
+    int64_t tile = clo / kS2Threads;  // tiles of the same super
+    int64_t found_tile = -1;
+    const int64_t tlo = tile & ~(int64_t)(kTilesPerSuper - 1);
+    for (int64_t t = tile - 1; t >= tlo; --t)
+      if (a.tile_min[t] <= L) {
+        found_tile = t;
+        break;
+      }
+    if (found_tile < 0) {
+      int64_t sup = tlo / kTilesPerSuper;
+      int64_t found_sup = -1;
+      const int64_t slo = sup & ~(int64_t)(kSupersPerSuper2 - 1);
+      for (int64_t s = sup - 1; s >= slo; --s)
+        if (a.super_min[s] <= L) {
+          found_sup = s;
+          break;
+        }
+      if (found_sup < 0) {
+        for (int64_t s2 = slo / kSupersPerSuper2 - 1; s2 >= 0; --s2)
+          if (a.super2_min[s2] <= L) {
+            for (int64_t s = s2 * kSupersPerSuper2 + kSupersPerSuper2 - 1; s >= s2 * kSupersPerSuper2; --s)
+              if (a.super_min[s] <= L) {
+                found_sup = s;
+                break;
+              }
+            break;
+          }
+        if (found_sup < 0) return -1;
+      }
+      for (int64_t t = found_sup * kTilesPerSuper + kTilesPerSuper - 1; t >= found_sup * kTilesPerSuper; --t)
+        if (a.tile_min[t] <= L) {
+          found_tile = t;
+          break;
+        }
+      if (found_tile < 0) return -1;
+    }
+    for (int64_t cc = found_tile * kS2Threads + kS2Threads - 1; cc >= found_tile * kS2Threads; --cc)
+      if (a.chunk_min[cc] <= L) {
+        found_chunk = cc;
+        break;
+      }
+    if (found_chunk < 0) return -1;
+  }
+  for (j = found_chunk * kTokPerThread + kTokPerThread - 1; j >= found_chunk * kTokPerThread; --j)
+    if (tok_depth(a.tok[j]) <= L) return j;
+  return -1;
+}
+
+// tape index of token j (chunk start + widths of the tokens before it)
+__device__ uint32_t tape_of(const Stage2Args &a, int64_t j) {
+  int64_t c0 = j & ~(int64_t)(kTokPerThread - 1);
+  uint32_t t = a.chunk_tape[c0 / kTokPerThread];
+  for (int64_t k = c0; k < j; k++) t += tok_width(a.tok[k] & 0xFF);
+  return t;
+}
+
+enum : int { M_V = 0, M_OF, M_AF, M_K, M_C, M_A };
+
+__device__ __forceinline__ void report(Ctrl *ctrl, uint64_t tokn, int code) {
+  atomicMin(&ctrl->err_key, ((unsigned long long)tokn << 8) | (unsigned)code);
+}
+
+__global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint64_t S = ctrl->S;
+  const uint64_t nchunks = (S + kTokPerThread - 1) / kTokPerThread;
+  for (uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; chunk < nchunks;
+       chunk += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = chunk * kTokPerThread;
+    const uint64_t i1 = min(i0 + kTokPerThread, S);
+    uint32_t t = a.chunk_tape[chunk];
+
+    // entry state from the two previous tokens (A.5 arrival rules)
+    int mode = M_V;
+    if (i0 > 0) {
+      uint32_t v1 = a.tok[i0 - 1];
+      uint32_t c1 = v1 & 0xFF;
+      if (c1 == '{') mode = M_OF;
+      else if (c1 == '[') mode = M_AF;
+      else if (c1 == ':') mode = M_V;
+      else if (c1 == ',') {
+        int64_t j = psv(a, (int64_t)i0 - 1, tok_depth(v1) - 1);
+        mode = (j >= 0 && (a.tok[j] & 0xFF) == '{') ? M_K : M_V;
+      } else if (c1 == '"') {
+        mode = M_A;
+        if (i0 >= 2) {
+          uint32_t v2 = a.tok[i0 - 2];
+          uint32_t c2 = v2 & 0xFF;
+          if (c2 == '{') mode = M_C;
+          else if (c2 == ',') {
+            int64_t j = psv(a, (int64_t)i0 - 2, tok_depth(v2) - 1);
+            if (j >= 0 && (a.tok[j] & 0xFF) == '{') mode = M_C;
+          }
+        }
+      } else {
+        mode = M_A;
+      }
+    }
+
+    uint32_t stk[kTokPerThread];  // local openers: tape index | is_object << 31
+    int sp = 0;
+    int far_level = -100;  // cache of the last far container lookup
+    uint32_t far_tape = 0;
+    bool far_obj = false;
+    int err = 0;
+    uint64_t i = i0;
+    int depth_after = 0;
+    for (; i < i1; i++) {
+      const uint32_t v = a.tok[i];
+      const uint32_t c = v & 0xFF;
+      const bool fail = (v >> 8) & 1;
+      const int D = tok_depth(v);
+      depth_after = D + tok_delta(c);
+      bool again;
+      do {
+        again = false;
+        bool close = false, have_top = false, top_obj = false;
+        uint32_t top_tape = 0;
+        bool top_local = false;
+        switch (mode) {
+          case M_V:
+            if (c == '{' || c == '[') {
+              if (D >= kMaxDepth) {
+                err = kDepthError;
+                break;
+              }
+              stk[sp++] = t | (c == '{' ? 0x80000000u : 0u);
+              mode = c == '{' ? M_OF : M_AF;
+            } else {
+              if (c == '"') err = fail ? kStringError : 0;
+              else if (c == 't' || c == 'f' || c == 'n') err = fail ? kTapeError : 0;
+              else if (c == '-' || (c - '0') < 10u) err = fail ? kNumberError : 0;
+              else err = kTapeError;
+              mode = M_A;
+            }
+            break;
+          case M_OF:
+          case M_AF: {
+            const uint32_t want = mode == M_OF ? '}' : ']';
+            if (c == want) {
+              close = true;
+              have_top = true;
+              top_obj = mode == M_OF;
+              if (sp > 0) {
+                top_local = true;
+                top_tape = stk[sp - 1] & 0x7FFFFFFFu;
+              } else {
+                top_tape = t - 1;  // the opener is the previous token
+              }
+            } else {
+              mode = mode == M_OF ? M_K : M_V;
+              again = true;
+            }
+            break;
+          }
+          case M_K:
+            if (c != '"') err = kTapeError;
+            else if (fail) err = kStringError;
+            else mode = M_C;
+            break;
+          case M_C:
+            if (c != ':') err = kTapeError;
+            else mode = M_V;
+            break;
+          case M_A: {
+            if (D <= 0) {
+              err = kTapeError;
+              break;
+            }
+            if (sp > 0) {
+              top_local = true;
+              top_tape = stk[sp - 1] & 0x7FFFFFFFu;
+              top_obj = stk[sp - 1] >> 31;
+            } else {
+              if (far_level != D - 1) {
+                int64_t j = psv(a, (int64_t)i, D - 1);
+                if (j < 0) {
+                  err = kTapeError;
+                  break;
+                }
+                far_level = D - 1;
+                far_obj = (a.tok[j] & 0xFF) == '{';
+                far_tape = tape_of(a, j);
+              }
+              top_tape = far_tape;
+              top_obj = far_obj;
+            }
+            have_top = true;
+            if (c == ',') mode = top_obj ? M_K : M_V;
+            else if (c == (top_obj ? '}' : ']')) close = true;
+            else err = kTapeError;
+            break;
+          }
+        }
+        if (close && have_top) {
+          if (top_local) sp--;
+          else far_level = -100;
+          a.tape[t] = tape_word((uint8_t)c, top_tape);
+          a.tape[top_tape] = tape_word(top_obj ? '{' : '[', t + 1);
+          mode = M_A;
+        }
+      } while (again && !err);
+      if (err) break;
+      t += tok_width(c);
+    }
+    if (err) {
+      report(ctrl, i, err);
+      continue;
+    }
+    if (i1 == S && !(mode == M_A && depth_after == 0)) report(ctrl, S, kTapeError);
+  }
+}
+
+// ---- K4: finalize ----------------------------------------------------------
+
+__global__ void k_final(Stage2Args a) {
+  Ctrl *c = a.ctrl;
+  if (c->utf8_pos != ~0ULL) {
+    c->code = kUtf8Error;
+    c->offset = (long long)c->utf8_pos;
+    return;
+  }
+  const uint64_t S = c->S;
+  if (S == 0) {
+    c->code = kEmpty;
+    c->offset = -1;
+    return;
+  }
+  if (c->err_key != ~0ULL) {
+    uint64_t i = c->err_key >> 8;
+    int code = (int)(c->err_key & 0xFF);
+    c->code = code;
+    if (i >= S) {
+      c->offset = (long long)a.len;
+    } else if (code == kStringError) {
+      str::Measure m = str::string_measure(InAt{a.in}, a.idx[i]);
+      c->offset = (long long)m.err;
+    } else {
+      c->offset = (long long)a.idx[i];
+    }
+    return;
+  }
+  const uint64_t E = c->tape_words;
+  a.tape[0] = tape_word(kTagRoot, E);
+  a.tape[E] = tape_word(kTagRoot, 0);
+  c->tape_len = E + 1;
+  c->code = kOk;
+  c->offset = -1;
+}
+
+__global__ void k_init(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,
+                       uint64_t s2words) {
+  uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = g; k < s1words; k += stride) s1rec[k] = 0;
+  for (uint64_t k = g; k < s2words; k += stride) s2rec[k] = 0;
+  if (g == 0) {
+    Ctrl z{};
+    z.utf8_pos = ~0ULL;
+    z.err_key = ~0ULL;
+    z.code = -1;
+    z.offset = -1;
+    *ctrl = z;
+  }
+}
+
+__global__ void k_stage1_final(Ctrl *c) {
+  if (c->utf8_pos != ~0ULL) {
+    c->code = kUtf8Error;
+    c->offset = (long long)c->utf8_pos;
+  } else {
+    c->code = kOk;
+    c->offset = -1;
+  }
+}
+
+}  // namespace
+
+Stage2Sizes stage2_sizes(uint64_t cap) {
+  Stage2Sizes z;
+  z.chunks = (cap + kTokPerThread - 1) / kTokPerThread + 1;
+  z.tiles = (cap + kTokPerTile - 1) / kTokPerTile + 1;
+  z.supers = (z.tiles + kTilesPerSuper - 1) / kTilesPerSuper + 1;
+  z.supers2 = (z.supers + kSupersPerSuper2 - 1) / kSupersPerSuper2 + 1;
+  return z;
+}
+
+cudaError_t init_launch(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,
+                        uint64_t s2words, cudaStream_t stream) {
+  uint64_t m = s1words > s2words ? s1words : s2words;
+  unsigned blocks = (unsigned)((m + 255) / 256);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1184) blocks = 1184;
+  k_init<<<blocks, 256, 0, stream>>>(ctrl, s1rec, s1words, s2rec, s2words);
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_finalize_launch(Ctrl *ctrl, cudaStream_t stream) {
+  k_stage1_final<<<1, 1, 0, stream>>>(ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches) {
+  const Stage2Sizes z = stage2_sizes(a.cap_tokens);
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  // K2: persistent CTAs pulling tiles from a counter
+  uint64_t want = z.tiles;
+  unsigned g2 = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
+  if (g2 < 1) g2 = 1;
+  k_tokens<<<g2, kS2Threads, 0, stream>>>(a);
+  k_slow<<<sms, 128, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
+  uint64_t nthreads = z.chunks;
+  unsigned g3 = (unsigned)((nthreads + 127) / 128);
+  if (g3 > (unsigned)sms * 16) g3 = (unsigned)sms * 16;
+  if (g3 < 1) g3 = 1;
+  k_struct<<<g3, 128, 0, stream>>>(a);
+  k_final<<<1, 1, 0, stream>>>(a);
+  *launches = 5;
+  return cudaGetLastError();
+}
+
+}  // namespace jt

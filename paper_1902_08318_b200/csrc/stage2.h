@@ -1,0 +1,71 @@
+// stage2.h — host-side interface of the stage-2 (tape) kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace jt {
+
+constexpr int kTokPerThread = 16;                       // one "chunk"
+constexpr int kS2Threads = 128;
+constexpr int kTokPerTile = kTokPerThread * kS2Threads;  // 2048 tokens
+constexpr int kTilesPerSuper = 64;
+constexpr int kSupersPerSuper2 = 64;
+
+// Device control block, zeroed before every parse (utf8_pos / err_key set
+// to ~0 by the init kernel).
+struct Ctrl {
+  uint32_t s1_tile_counter;
+  uint32_t s2_tile_counter;
+  unsigned long long utf8_pos;  // min invalid UTF-8 offset (~0 = none)
+  uint64_t S;                   // structural index count
+  unsigned long long err_key;   // (token << 8) | code, min wins (~0 = none)
+  uint32_t slow_count;          // numbers needing the exact fallback
+  uint32_t pad;
+  uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
+  uint64_t string_bytes;
+  // results written by the finalize kernel
+  int32_t code;
+  int32_t pad2;
+  long long offset;
+  uint64_t tape_len;            // E + 1 on success
+};
+
+struct Stage2Args {
+  const uint8_t *in;
+  uint64_t len;
+  const uint32_t *idx;
+  Ctrl *ctrl;
+  uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16
+  uint32_t *chunk_tape; // per 16-token chunk: tape index of its first token
+  int16_t *chunk_min;   // per chunk: min depth_before
+  int16_t *tile_min;    // per tile
+  int16_t *super_min;   // per 64 tiles
+  int16_t *super2_min;  // per 64 supers
+  uint64_t *rec;        // 6 words per tile (look-back)
+  uint32_t *slow;       // slow-number token list (token, tape slot pairs)
+  uint64_t *tape;       // >= 2 * cap + 3 words
+  uint8_t *strings;     // >= len + 4 * cap + 64 bytes
+  uint64_t cap_tokens;  // capacity bound on S (for grid sizing)
+  int num_sms;
+};
+
+// words of look-back records / tree nodes needed for up to `cap` tokens
+struct Stage2Sizes {
+  uint64_t chunks, tiles, supers, supers2;
+};
+Stage2Sizes stage2_sizes(uint64_t cap_tokens);
+
+// Enqueue the whole stage 2 (tokens, slow numbers, tree, structure,
+// finalize); returns the number of kernel launches via *launches.
+cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches);
+
+// Reset kernel for the control block + look-back records.
+cudaError_t init_launch(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,
+                        uint64_t s2words, cudaStream_t stream);
+
+// Stage-1-only finalize: copies utf8 verdict into ctrl->code / offset.
+cudaError_t stage1_finalize_launch(Ctrl *ctrl, cudaStream_t stream);
+
+}  // namespace jt

@@ -1,0 +1,242 @@
+"""Python host mirror of the jsontape C ABI (proj/include/jsontape.h), over
+the in-tree B200 library libjsontape_b200.so (ctypes, no torch types).
+
+Same names and argument meaning as the reference's C entry points:
+``Parser.parse`` <-> jt_parse (capi.cpp:73-93), ``Parser.stage1`` <-> jt_stage1
+(95-102), ``Parser.index`` <-> jt_index_count/positions (127-131),
+``Parser.stage2`` <-> jt_stage2 (104-125); error codes are jt_error
+(jsontape.h:15-24).  Loading fails loudly when the library or a CUDA device is
+missing — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libjsontape_b200.so")
+
+OK, UTF8_ERROR, STRING_ERROR, NUMBER_ERROR, TAPE_ERROR, DEPTH_ERROR, CAPACITY, EMPTY = range(8)
+ERROR_NAMES = ["OK", "UTF8_ERROR", "STRING_ERROR", "NUMBER_ERROR", "TAPE_ERROR", "DEPTH_ERROR",
+               "CAPACITY", "EMPTY"]
+
+# every symbol include/jsontape.h and include/jsontape_b200.h declare
+EXPORTS = [
+    "jt_parser_new", "jt_parser_free", "jt_parser_set_flags", "jt_parse", "jt_stage1",
+    "jt_index_count", "jt_index_positions", "jt_stage2", "jt_document_free",
+    "jt_document_equal", "jt_document_dump", "jt_document_distinct", "jt_string_free",
+    "jt_minify", "jt_compute_stats", "jt_oracle_validate", "jt_generate", "jt_error_name",
+    "jt_b200_input_buffer", "jt_b200_stage1_resident", "jt_b200_parse_resident",
+    "jt_b200_parse_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
+    "jt_b200_device_strings", "jt_b200_download", "jt_b200_set_stream",
+    "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error",
+]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the C ABI (no device work happens here)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: run __graft_entry__.build() (no CPU fallback)")
+    L = C.CDLL(path)
+    vp, sz, ll = C.c_void_p, C.c_size_t, C.c_longlong
+    L.jt_parser_new.restype = vp
+    L.jt_parser_free.argtypes = [vp]
+    L.jt_parser_set_flags.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+    L.jt_parse.argtypes = [vp, C.c_char_p, sz, C.POINTER(vp), C.POINTER(ll)]
+    L.jt_stage1.argtypes = [vp, C.c_char_p, sz, C.POINTER(ll)]
+    L.jt_index_count.argtypes = [vp]
+    L.jt_index_count.restype = sz
+    L.jt_index_positions.argtypes = [vp]
+    L.jt_index_positions.restype = C.POINTER(C.c_uint32)
+    L.jt_stage2.argtypes = [vp, C.POINTER(vp), C.POINTER(ll)]
+    L.jt_document_free.argtypes = [vp]
+    L.jt_document_equal.argtypes = [vp, vp]
+    L.jt_document_dump.argtypes = [vp]
+    L.jt_document_dump.restype = vp
+    L.jt_string_free.argtypes = [vp]
+    L.jt_error_name.argtypes = [C.c_int]
+    L.jt_error_name.restype = C.c_char_p
+    L.jt_b200_input_buffer.argtypes = [vp, sz]
+    L.jt_b200_input_buffer.restype = vp
+    L.jt_b200_stage1_resident.argtypes = [vp, sz, C.POINTER(ll)]
+    L.jt_b200_parse_resident.argtypes = [vp, sz, C.POINTER(ll)]
+    L.jt_b200_parse_async.argtypes = [vp, sz]
+    L.jt_b200_finish.argtypes = [vp, C.POINTER(ll)]
+    L.jt_b200_device_index.argtypes = [vp, C.POINTER(sz)]
+    L.jt_b200_device_index.restype = vp
+    L.jt_b200_device_tape.argtypes = [vp, C.POINTER(sz)]
+    L.jt_b200_device_tape.restype = vp
+    L.jt_b200_device_strings.argtypes = [vp, C.POINTER(sz)]
+    L.jt_b200_device_strings.restype = vp
+    L.jt_b200_download.argtypes = [vp, C.POINTER(vp)]
+    L.jt_b200_set_stream.argtypes = [vp, vp]
+    L.jt_b200_last_launches.argtypes = [vp]
+    L.jt_b200_device.argtypes = [vp]
+    L.jt_b200_last_error.argtypes = [vp]
+    L.jt_b200_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def error_name(code: int) -> str:
+    return load_library().jt_error_name(code).decode()
+
+
+class Document:
+    """Host tape document (jt_document): u64 tape words + string buffer."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+        self._lib = load_library()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.jt_document_free(self._h)
+            self._h = None
+
+    def _raw(self):
+        # jt_document = {std::vector<u64> tape; std::vector<u8> strings}
+        w = (C.c_uint64 * 6).from_address(self._h)
+        return list(w)
+
+    @property
+    def tape(self) -> np.ndarray:
+        tb, te = self._raw()[0:2]
+        return np.frombuffer(C.string_at(tb, te - tb), dtype=np.uint64) if te > tb else \
+            np.zeros(0, np.uint64)
+
+    @property
+    def strings(self) -> bytes:
+        sb, se = self._raw()[3:5]
+        return C.string_at(sb, se - sb) if se > sb else b""
+
+    def dump(self) -> str:
+        s = self._lib.jt_document_dump(self._h)
+        out = C.string_at(s).decode("utf-8", "replace")
+        self._lib.jt_string_free(s)
+        return out
+
+    def __eq__(self, other) -> bool:
+        return bool(self._lib.jt_document_equal(self._h, other._h))
+
+
+@dataclass
+class Result:
+    code: int
+    offset: int
+    document: Document | None = None
+
+    @property
+    def name(self) -> str:
+        return ERROR_NAMES[self.code]
+
+
+class Parser:
+    """jt_parser: one CUDA stream + device arena on the current device."""
+
+    def __init__(self):
+        self._lib = load_library()
+        self._h = self._lib.jt_parser_new()
+        if not self._h:
+            raise RuntimeError("jt_parser_new failed: no usable CUDA device")
+
+    def close(self):
+        if self._h:
+            self._lib.jt_parser_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_flags(self, use_clmul=1, fast_extract=1, vector_classify=1):
+        self._lib.jt_parser_set_flags(self._h, use_clmul, fast_extract, vector_classify)
+
+    def parse(self, data: bytes, want_document: bool = True) -> Result:
+        doc = C.c_void_p()
+        off = C.c_longlong(-7)
+        code = self._lib.jt_parse(self._h, data, len(data), C.byref(doc) if want_document else None,
+                                  C.byref(off))
+        return Result(code, off.value, Document(doc.value) if doc.value else None)
+
+    def stage1(self, data: bytes) -> Result:
+        off = C.c_longlong(-7)
+        code = self._lib.jt_stage1(self._h, data, len(data), C.byref(off))
+        return Result(code, off.value)
+
+    def index(self) -> np.ndarray:
+        n = self._lib.jt_index_count(self._h)
+        if n == 0:
+            return np.zeros(0, np.uint32)
+        p = self._lib.jt_index_positions(self._h)
+        return np.frombuffer(C.string_at(p, 4 * n), dtype=np.uint32)
+
+    def stage2(self, want_document: bool = True) -> Result:
+        doc = C.c_void_p()
+        off = C.c_longlong(-7)
+        code = self._lib.jt_stage2(self._h, C.byref(doc) if want_document else None, C.byref(off))
+        return Result(code, off.value, Document(doc.value) if doc.value else None)
+
+    # ---- B200 extensions (include/jsontape_b200.h) ----
+    def input_buffer(self, n: int) -> int:
+        p = self._lib.jt_b200_input_buffer(self._h, n)
+        if not p:
+            raise MemoryError(self.last_error())
+        return p
+
+    def parse_resident(self, n: int) -> Result:
+        off = C.c_longlong(-7)
+        code = self._lib.jt_b200_parse_resident(self._h, n, C.byref(off))
+        return Result(code, off.value)
+
+    def stage1_resident(self, n: int) -> Result:
+        off = C.c_longlong(-7)
+        code = self._lib.jt_b200_stage1_resident(self._h, n, C.byref(off))
+        return Result(code, off.value)
+
+    def parse_async(self, n: int) -> int:
+        return self._lib.jt_b200_parse_async(self._h, n)
+
+    def finish(self) -> Result:
+        off = C.c_longlong(-7)
+        code = self._lib.jt_b200_finish(self._h, C.byref(off))
+        return Result(code, off.value)
+
+    def download(self) -> Document | None:
+        doc = C.c_void_p()
+        code = self._lib.jt_b200_download(self._h, C.byref(doc))
+        return Document(doc.value) if code == OK and doc.value else None
+
+    def device_tape(self):
+        n = C.c_size_t()
+        p = self._lib.jt_b200_device_tape(self._h, C.byref(n))
+        return p, n.value
+
+    def device_strings(self):
+        n = C.c_size_t()
+        p = self._lib.jt_b200_device_strings(self._h, C.byref(n))
+        return p, n.value
+
+    def device_index(self):
+        n = C.c_size_t()
+        p = self._lib.jt_b200_device_index(self._h, C.byref(n))
+        return p, n.value
+
+    def set_stream(self, stream_handle: int | None):
+        self._lib.jt_b200_set_stream(self._h, stream_handle)
+
+    def last_launches(self) -> int:
+        return self._lib.jt_b200_last_launches(self._h)
+
+    def last_error(self) -> str:
+        return self._lib.jt_b200_last_error(self._h).decode()

@@ -1,0 +1,140 @@
+"""GPU parity: the B200 kernels (through the C ABI) vs the CPU oracle.
+
+Bit-exact: code, offset, structural index, tape words (incl. float64 bit
+patterns) and string buffer.  Oracle = oracle/jt_oracle.c, itself pinned to
+the reference (tests/test_oracle_*.py).
+"""
+import random
+
+import numpy as np
+import pytest
+
+from tests.vectors import EXAMPLE_DOCUMENT, EXAMPLE_INTS, EXAMPLE_TAPE_WORDS, INDEX_KAT, KAT, SOUP_POOL
+
+pytestmark = pytest.mark.gpu
+
+
+def check_same(parser, oracle, data: bytes, where=""):
+    g = parser.parse(data)
+    o = oracle.parse(data)
+    assert (g.name, g.offset) == (o.name, o.offset), (where, data[:200])
+    if o.code == 0:
+        d = g.document
+        assert d is not None
+        assert np.array_equal(d.tape, o.tape_array()), (where, data[:200])
+        assert d.strings == o.strings, where
+    if o.code != 1:  # stage-1 index refreshed unless UTF-8 failed
+        assert np.array_equal(parser.index(), o.index_list()), (where, data[:200])
+    return g
+
+
+def test_kat_vectors(parser, oracle):
+    for data, name, off in KAT:
+        g = check_same(parser, oracle, data, "kat")
+        assert g.name == name, data
+        if off is not None:
+            assert g.offset == off, data
+
+
+def test_example_document_tape(parser):
+    r = parser.parse(EXAMPLE_DOCUMENT)
+    assert r.name == "OK"
+    t = r.document.tape
+    assert len(t) == 38
+    for i, (tag, payload) in EXAMPLE_TAPE_WORDS.items():
+        assert int(t[i]) >> 56 == ord(tag) and int(t[i]) & ((1 << 56) - 1) == payload
+    for i, v in EXAMPLE_INTS:
+        assert int(t[i]) >> 56 == ord("l")
+        assert np.int64(t[i + 1].view(np.int64)) == v
+
+
+def test_index_kat(parser):
+    for data, expect in INDEX_KAT:
+        r = parser.stage1(data)
+        assert r.name == "OK"
+        assert parser.index().tolist() == expect, data
+
+
+def test_stage1_then_stage2(parser):
+    src = b'{ "k" : [ 1 , 2 ] }'
+    assert parser.stage1(src).name == "OK"
+    assert parser.index().tolist() == [0, 2, 6, 8, 10, 12, 14, 16, 18]
+    assert parser.stage2(want_document=False).name == "OK"
+    a = parser.stage2()
+    b = parser.parse(src)
+    assert a.document == b.document
+
+
+def test_soup_fuzz(parser, oracle):
+    rng = random.Random(17)
+    for it in range(3000):
+        n = rng.randrange(0, 2000)
+        data = bytes(rng.choice(SOUP_POOL) for _ in range(n))
+        check_same(parser, oracle, data, f"soup {it}")
+
+
+def _rand_json(rng, depth=0):
+    k = rng.randrange(10 if depth < 6 else 6)
+    if k == 0:
+        return str(rng.randrange(-10**20, 10**20))
+    if k == 1:
+        return repr(rng.uniform(-1e10, 1e10)) if rng.random() < 0.5 else "%.17g" % (rng.random() * 10 ** rng.randrange(-300, 300))
+    if k == 2:
+        return rng.choice(["true", "false", "null"])
+    if k in (3, 4, 5):
+        chars = []
+        for _ in range(rng.randrange(0, 40)):
+            r = rng.random()
+            if r < 0.1:
+                chars.append(rng.choice(['\\"', "\\\\", "\\n", "\\t", "\\u00e9", "\\ud834\\udd1e", "\\/"]))
+            elif r < 0.3:
+                chars.append(rng.choice(["é", "€", "𝄞", "ж"]))
+            else:
+                chars.append(rng.choice("abcdefgh ,:[]{}"))
+        return '"' + "".join(chars) + '"'
+    if k in (6, 7):
+        return "[" + ",".join(_rand_json(rng, depth + 1) for _ in range(rng.randrange(0, 6))) + "]"
+    return "{" + ",".join('"k%d":%s' % (i, _rand_json(rng, depth + 1)) for i in range(rng.randrange(0, 6))) + "}"
+
+
+def _mutate(rng, b: bytes) -> bytes:
+    if not b:
+        return b
+    p = rng.randrange(len(b))
+    op = rng.randrange(5)
+    if op == 0:
+        return b[:p] + bytes([b[p] ^ (1 << rng.randrange(8))]) + b[p + 1:]
+    if op == 1:
+        return b[:p] + bytes([rng.choice(b'{}[]:,"\\ 0-.eE\x00\x01\xff')]) + b[p + 1:]
+    if op == 2:
+        return b[:p]
+    if op == 3:
+        return b[:p] + b[p + 1:]
+    return b[:p] + bytes([rng.randrange(256)]) + b[p:]
+
+
+def test_random_json_and_mutations(parser, oracle):
+    rng = random.Random(23)
+    for it in range(3000):
+        doc = _rand_json(rng).encode()
+        if rng.random() < 0.3:
+            doc = (" " * rng.randrange(3)).encode() + doc.replace(b",", b" , ")
+        check_same(parser, oracle, doc, f"json {it}")
+        check_same(parser, oracle, _mutate(rng, doc), f"mut {it}")
+
+
+def test_configs_small(parser, oracle):
+    from tools.gen import generate
+    for cfg, size in [(0, 1 << 20), (1, 4 << 20), (2, 4 << 20), (4, 4 << 20)]:
+        check_same(parser, oracle, generate(cfg, size), f"C{cfg}")
+    nd = generate(3, 1 << 20)
+    for k, rec in enumerate(nd.split(b"\n")[:2000]):
+        check_same(parser, oracle, rec, f"C3 record {k}")
+
+
+def test_error_sweep(parser, oracle):
+    from tools.gen import generate
+    for seed in range(1, 200):
+        err = 1 + seed % 5
+        data = generate(4, 1 << 14, seed=seed, err=err)
+        check_same(parser, oracle, data, f"C4 err {err} seed {seed}")

@@ -1,0 +1,118 @@
+"""Pin the CPU oracle (oracle/jt_oracle.c) to the reference's own known
+answers: SURVEY App. B, proj/tests/* vectors, the worked stage-1 example and
+the Fig. 1 tape, exhaustive short UTF-8, and the committed golden fixtures
+produced by the compiled reference (tests/golden/make_golden.py)."""
+import itertools
+import json
+import os
+
+import numpy as np
+
+from tests.vectors import (EXAMPLE_BLOCK, EXAMPLE_DOCUMENT, EXAMPLE_FINAL_ROW, EXAMPLE_INTS,
+                           EXAMPLE_TAPE_WORDS, INDEX_KAT, KAT)
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_kat(oracle):
+    for data, name, off in KAT:
+        r = oracle.parse(data)
+        assert r.name == name, data
+        if off is not None:
+            assert r.offset == off, data
+
+
+def test_index_kat(oracle):
+    for data, expect in INDEX_KAT:
+        assert oracle.stage1(data).index_list().tolist() == expect
+
+
+def test_worked_example_block(oracle):
+    # proj/tests/test_bitmask.cpp:127-144: final structural row of the block
+    assert len(EXAMPLE_BLOCK) == 64
+    expect = [i for i, ch in enumerate(EXAMPLE_FINAL_ROW) if ch != "_"]
+    assert oracle.stage1(EXAMPLE_BLOCK).index_list().tolist() == expect
+
+
+def test_dense_commas(oracle):
+    # test_indexer.cpp:83-91
+    for n in (1, 63, 64, 65, 127, 128, 1000):
+        assert oracle.stage1(b"," * n).index_list().tolist() == list(range(n))
+
+
+def test_example_document_tape(oracle):
+    r = oracle.parse(EXAMPLE_DOCUMENT)
+    t = r.tape_array()
+    assert r.name == "OK" and len(t) == 38
+    for i, (tag, payload) in EXAMPLE_TAPE_WORDS.items():
+        assert int(t[i]) >> 56 == ord(tag) and int(t[i]) & ((1 << 56) - 1) == payload
+    for i, v in EXAMPLE_INTS:
+        assert int(t[i]) >> 56 == ord("l") and int(t[i + 1]) == v
+
+
+def test_empty_array_tape(oracle):
+    # test_tape.cpp:33-41
+    t = oracle.parse(b"[]").tape_array().tolist()
+    assert t == [(ord("r") << 56) | 3, (ord("[") << 56) | 3, (ord("]") << 56) | 1, ord("r") << 56]
+
+
+def test_string_normalisation(oracle):
+    # test_tape.cpp:169-174 and test_strings.cpp
+    r = oracle.parse(b'["a\\u0041\\n", "\\uD834\\uDD1E"]')
+    assert r.strings == b"\x03\x00\x00\x00aA\n" + b"\x04\x00\x00\x00\xf0\x9d\x84\x9e"
+    assert oracle.string(b'"\\u0000"') == (True, b"\x00", -1)
+    for c in range(0x20):  # raw control bytes, offset 2 (test_strings.cpp:100-112)
+        assert oracle.string(b'"a' + bytes([c]) + b'b"')[2] == 2
+    for cp in range(0xD800, 0xE000):  # lone surrogates (test_strings.cpp:84-98)
+        assert not oracle.string(b'"\\u%04x"' % cp)[0]
+
+
+def test_numbers(oracle):
+    # test_numbers.cpp:72-121
+    import struct
+
+    def dbl(x):
+        return struct.unpack("<Q", struct.pack("<d", x))[0]
+    assert oracle.number(b"-9223372036854775808") == (True, True, 1 << 63)
+    assert oracle.number(b"9223372036854775808")[0] is False
+    for s, v in [(b"0.5", 0.5), (b"-0.0", -0.0), (b"1e22", 1e22), (b"5e-324", 5e-324),
+                 (b"2.2250738585072011e-308", 2.2250738585072011e-308), (b"1e-400", 0.0),
+                 (b"-1e-400", -0.0), (b"10000000000000000000.0", 1e19),
+                 (b"3.141592653589793238462643383279", 3.141592653589793)]:
+        assert oracle.number(s) == (True, False, dbl(v)), s
+    for s in [b"1e309", b"-1e309", b"1e99999999999", b"012", b"1.", b"1a", b'1"']:
+        assert oracle.number(s)[0] is False, s
+
+
+def test_utf8_exhaustive_short(oracle):
+    # acceptance.cpp:105-154 / test_utf8.cpp:99-109: verdicts vs a strict decoder
+    for n in (1, 2):
+        for t in itertools.product(range(256), repeat=n):
+            b = bytes(t)
+            try:
+                b.decode("utf-8")
+                ok = True
+            except UnicodeDecodeError:
+                ok = False
+            assert (oracle.utf8_error_offset(b) < 0) == ok, b
+
+
+def test_golden_fixtures(oracle):
+    import hashlib
+    path = os.path.join(GOLDEN, "reference_outputs.jsonl")
+    rows = [json.loads(l) for l in open(path)]
+    assert len(rows) > 100
+    for row in rows:
+        if "gen" in row:
+            from tools.gen import generate
+            cfg, size, seed, err = row["gen"]
+            data = generate(cfg, size, seed=seed, err=err)
+        else:
+            data = bytes.fromhex(row["input"])
+        r = oracle.parse(data)
+        assert (r.name, r.offset) == (row["code"], row["offset"]), row["input"][:80]
+        if "index_sha" in row:
+            assert hashlib.sha256(r.index or b"").hexdigest() == row["index_sha"]
+        if r.code == 0:
+            assert hashlib.sha256(r.tape).hexdigest() == row["tape_sha"]
+            assert hashlib.sha256(r.strings).hexdigest() == row["strings_sha"]
