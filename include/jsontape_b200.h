@@ -18,6 +18,10 @@ extern "C" {
  * failure.  Valid until the next call that changes the capacity. */
 void *jt_b200_input_buffer(jt_parser *p, size_t len);
 
+/* Fill the input buffer from host or device memory (cudaMemcpyDefault);
+ * 0 on success. */
+int jt_b200_copy_in(jt_parser *p, const void *src, size_t len);
+
 /* stage 1 / full parse over the `len` bytes in jt_b200_input_buffer; results
  * stay in device memory (see the accessors below).  Same codes and offsets
  * as jt_stage1 / jt_parse. */
@@ -43,6 +47,12 @@ void jt_b200_set_stream(jt_parser *p, void *cuda_stream);
 
 /* Number of kernel launches enqueued by the last parse call. */
 int jt_b200_last_launches(const jt_parser *p);
+
+/* Per-kernel timing of full parses (events recorded on the parser's
+ * stream): jt_b200_kernel_times fills ms[] for the last parse in launch
+ * order init, stage1, tokens, slow, tree, struct, final; returns count. */
+void jt_b200_profile(jt_parser *p, int enable);
+int jt_b200_kernel_times(jt_parser *p, float *ms, int max);
 
 /* CUDA device ordinal the parser was created on. */
 int jt_b200_device(const jt_parser *p);

@@ -72,6 +72,7 @@ struct jt_parser {
   cudaStream_t stream = nullptr;
   DevBuf in;               // padded input
   DevBuf idx[2];           // structural index, double-buffered
+  DevBuf aux[2];           // per index entry: string-buffer prefix
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
   DevBuf tok, chunk_tape, chunk_min, tile_min, super_min, super2_min, slow;
@@ -88,8 +89,13 @@ struct jt_parser {
   bool last_ok = false;
   int launches = 0;
   std::string err;
+  uint64_t s1_str_err = ~0ULL, s1_string_bytes = 0;  // retained with the index
   uint64_t pending_len = 0;
   int pending_idx = -1;
+  // optional per-kernel timing: ev[0] before init, then one per launch
+  bool prof = false;
+  cudaEvent_t ev[8] = {};
+  int prof_n = 0;
 };
 
 namespace {
@@ -131,7 +137,9 @@ bool zero_tail(jt_parser *p, uint64_t len) {
 bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
   size_t cap_tok = (size_t)len + 16;
   if (!p->idx[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
-  if (!p->s1rec.ensure(jt::stage1_records(len) * 2 * sizeof(uint64_t) + 64)) return false;
+  if (!p->aux[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->strings.ensure((size_t)len + 4 * cap_tok + 128)) return false;
+  if (!p->s1rec.ensure(jt::stage1_records(len) * 5 * sizeof(uint64_t) + 64)) return false;
   if (!p->ctrl.ensure(sizeof(jt::Ctrl))) return false;
   return true;
 }
@@ -139,7 +147,7 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
 bool ensure_stage2(jt_parser *p, uint64_t len) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
-  bool ok = p->s2rec.ensure(z.tiles * 6 * sizeof(uint64_t)) &&
+  bool ok = p->s2rec.ensure(z.tiles * 4 * sizeof(uint64_t)) &&
             p->tok.ensure((cap + 16) * sizeof(uint32_t)) &&
             p->chunk_tape.ensure(z.chunks * sizeof(uint32_t)) &&
             p->chunk_min.ensure(z.chunks * sizeof(int16_t)) &&
@@ -147,8 +155,7 @@ bool ensure_stage2(jt_parser *p, uint64_t len) {
             p->super_min.ensure(z.supers * sizeof(int16_t)) &&
             p->super2_min.ensure(z.supers2 * sizeof(int16_t)) &&
             p->slow.ensure((cap + 16) * 2 * sizeof(uint32_t)) &&
-            p->tape.ensure((2 * cap + 8) * sizeof(uint64_t)) &&
-            p->strings.ensure((size_t)len + 4 * cap + 128);
+            p->tape.ensure((2 * cap + 8) * sizeof(uint64_t));
   return ok;
 }
 
@@ -158,12 +165,16 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
+  a.aux = p->aux[which].as<uint32_t>();
+  a.strings = p->strings.as<uint8_t>();
   uint64_t nt = jt::stage1_records(len);
   a.rec_state = p->s1rec.as<uint64_t>();
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
   a.tile_counter = &c->s1_tile_counter;
   a.utf8_pos = &c->utf8_pos;
+  a.str_err = &c->str_err;
   a.total = &c->S;
+  a.total_strings = &c->string_bytes;
   return a;
 }
 
@@ -172,6 +183,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
+  a.aux = p->aux[which].as<uint32_t>();
   a.ctrl = p->ctrl.as<jt::Ctrl>();
   a.tok = p->tok.as<uint32_t>();
   a.chunk_tape = p->chunk_tape.as<uint32_t>();
@@ -191,20 +203,28 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
 // Enqueue init + K1 (+ stage 2) for `len` resident bytes; index -> idx[which]
 bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
   p->launches = 0;
+  p->prof_n = 0;
+  if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
-  uint64_t s1w = jt::stage1_records(len) * 2;
-  uint64_t s2w = full ? z.tiles * 6 : 0;
+  uint64_t s1w = jt::stage1_records(len) * 5;
+  uint64_t s2w = full ? z.tiles * 4 : 0;
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                   p->s2rec.as<uint64_t>(), s2w, p->stream),
                "init"))
     return false;
   p->launches++;
+  if (p->prof) cudaEventRecord(p->ev[1], p->stream);
   if (!cuda_ok(p, jt::stage1_launch(s1_args(p, len, which), p->stream), "stage1")) return false;
   p->launches++;
+  if (p->prof) cudaEventRecord(p->ev[2], p->stream);
   if (full) {
     int n = 0;
-    if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n), "stage2")) return false;
+    if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n,
+                                      p->prof ? p->ev + 3 : nullptr),
+                 "stage2"))
+      return false;
     p->launches += n;
+    if (p->prof) p->prof_n = 7;
   } else {
     if (!cuda_ok(p, jt::stage1_finalize_launch(p->ctrl.as<jt::Ctrl>(), p->stream), "stage1 final"))
       return false;
@@ -227,6 +247,8 @@ jt_error finish(jt_parser *p, int which, bool full, long long *off) {
     p->cur = which;
     p->have_index = true;
     p->index_count = c.S;
+    p->s1_str_err = c.str_err;
+    p->s1_string_bytes = c.string_bytes;
     p->h_index_valid = false;
   }
   set_off(off, c.offset);
@@ -383,18 +405,26 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
-  // re-run stage 2 over the retained input and index: reset records and
-  // rebuild S into the control block from the host count
+  // re-run stage 2 over the retained input, index and string payload:
+  // reset the records, then restore the stage-1 results into the control block
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   p->launches = 0;
-  if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), 0,
-                                  p->s2rec.as<uint64_t>(), z.tiles * 6, p->stream),
+  if (!cuda_ok(p, jt::init_launch(nullptr, p->s1rec.as<uint64_t>(), 0, p->s2rec.as<uint64_t>(),
+                                  z.tiles * 4, p->stream),
                "init")) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
-  uint64_t S = p->have_index ? p->index_count : 0;
-  cudaMemcpyAsync(&p->ctrl.as<jt::Ctrl>()->S, &S, sizeof(S), cudaMemcpyHostToDevice, p->stream);
+  jt::Ctrl c0{};
+  c0.utf8_pos = ~0ULL;
+  c0.err_key = ~0ULL;
+  c0.S = p->have_index ? p->index_count : 0;
+  c0.str_err = p->s1_str_err;
+  c0.string_bytes = p->s1_string_bytes;
+  c0.code = -1;
+  c0.offset = -1;
+  *p->h_ctrl = c0;
+  cudaMemcpyAsync(p->ctrl.p, p->h_ctrl, sizeof(jt::Ctrl), cudaMemcpyHostToDevice, p->stream);
   int n = 0;
   if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, p->cur), p->stream, &n), "stage2") ||
       !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
@@ -585,6 +615,14 @@ void *jt_b200_input_buffer(jt_parser *p, size_t len) {
   return p->in.p;
 }
 
+int jt_b200_copy_in(jt_parser *p, const void *src, size_t len) {
+  if (!jt_b200_input_buffer(p, len)) return -1;
+  if (len && !cuda_ok(p, cudaMemcpyAsync(p->in.p, src, len, cudaMemcpyDefault, p->stream), "copy_in"))
+    return -1;
+  p->in_len = len;
+  return cuda_ok(p, cudaStreamSynchronize(p->stream), "sync") ? 0 : -1;
+}
+
 jt_error jt_b200_stage1_resident(jt_parser *p, size_t len, long long *error_offset) {
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
@@ -652,6 +690,21 @@ void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
 }
 
 int jt_b200_last_launches(const jt_parser *p) { return p->launches; }
+
+void jt_b200_profile(jt_parser *p, int enable) {
+  if (enable && !p->ev[0])
+    for (auto &e : p->ev) cudaEventCreate(&e);
+  p->prof = enable != 0;
+}
+
+int jt_b200_kernel_times(jt_parser *p, float *ms, int max) {
+  if (!p->prof || p->prof_n == 0) return 0;
+  cudaStreamSynchronize(p->stream);
+  int n = 0;
+  for (int k = 0; k < p->prof_n && n < max; k++, n++)
+    if (cudaEventElapsedTime(&ms[n], p->ev[k], p->ev[k + 1]) != cudaSuccess) ms[n] = -1.0f;
+  return n;
+}
 
 int jt_b200_device(const jt_parser *p) { return p->device; }
 

@@ -63,3 +63,65 @@ __device__ __forceinline__ uint64_t lb_sum_exclusive(const uint64_t *rec, int64_
 }
 
 }  // namespace jt
+
+namespace jt {
+
+// Two-counter channel: each tile owns 4 words, [0..1] aggregate (a, b) and
+// [2..3] inclusive (a, b); bit 63 of every word = valid.  A reader trusts a
+// pair only when both of its words are valid (each word is written once).
+struct Pair {
+  unsigned long long a, b;
+};
+
+constexpr uint64_t kPairValid = 1ULL << 63;
+
+__device__ __forceinline__ void pair_publish(uint64_t *rec, int64_t tile, int slot, Pair v) {
+  uint64_t *r = rec + 4 * tile + 2 * slot;
+  lb_store(r, kPairValid | v.a);
+  lb_store(r + 1, kPairValid | v.b);
+}
+
+__device__ __forceinline__ int pair_read(const uint64_t *rec, int64_t tile, Pair &v) {
+  const uint64_t *r = rec + 4 * tile;
+  uint64_t x = lb_load(r + 2), y = lb_load(r + 3);
+  if ((x & y) >> 63) {
+    v.a = x & ~kPairValid;
+    v.b = y & ~kPairValid;
+    return 2;
+  }
+  x = lb_load(r), y = lb_load(r + 1);
+  if ((x & y) >> 63) {
+    v.a = x & ~kPairValid;
+    v.b = y & ~kPairValid;
+    return 1;
+  }
+  return 0;
+}
+
+// exclusive prefix of tile `tile` (> 0), one full warp
+__device__ __forceinline__ Pair pair_lookback(const uint64_t *rec, int64_t tile) {
+  const int lane = threadIdx.x & 31;
+  Pair acc{0, 0};
+  int64_t base = tile - 1;
+  for (;;) {
+    int64_t pred = base - lane;
+    Pair v{0, 0};
+    int st = 2;
+    if (pred >= 0)
+      while ((st = pair_read(rec, pred, v)) == 0) __nanosleep(32);
+    uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+    int stop = incl ? __ffs(incl) - 1 : 31;
+    if (lane > stop) v = Pair{0, 0};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v.a += __shfl_xor_sync(0xffffffffu, v.a, o);
+      v.b += __shfl_xor_sync(0xffffffffu, v.b, o);
+    }
+    acc.a += v.a;
+    acc.b += v.b;
+    if (incl) return acc;
+    base -= 32;
+  }
+}
+
+}  // namespace jt

@@ -1,20 +1,24 @@
-// stage1.cu — K1: fused UTF-8 validation + structural index, one HBM pass.
+// stage1.cu — K1: fused UTF-8 validation + structural index + string
+// payload, one HBM pass over the input.
 //
-// Replaces build_structural_index (proj/src/indexer.cpp:29-56) and
-// validate_utf8 (proj/src/utf8.cpp:127-158).  Layout: a CTA owns a 16 KiB tile
-// (256 threads x 64-byte blocks), tiles are claimed in order through an
-// atomic counter.  Per thread: 2 x 256-bit loads -> bit planes -> masks ->
-// block transfer function.  Carries {odd_backslash, in_string,
-// prev_separator} are resolved by a warp scan of transfer functions, a CTA
-// scan, and a decoupled look-back across tiles (channel 1).  Index counts
-// then go through a second look-back (channel 2) and the tile's offsets are
-// staged in shared memory as u16 and written out coalesced.
+// Replaces build_structural_index (proj/src/indexer.cpp:29-56), validate_utf8
+// (proj/src/utf8.cpp:127-158) and the byte work of parse_string
+// (stringparse.cpp:143-183).  A CTA owns a 16 KiB tile (256 threads x
+// 64-byte blocks); tiles are claimed in order through an atomic counter.
+// Per thread: 2 x 256-bit loads -> bit planes -> masks -> block transfer
+// function.  The carries {odd_backslash, in_string, prev_separator} are
+// resolved by a warp scan of transfer functions, a CTA scan and a decoupled
+// look-back across tiles (channel 1).  Then every block knows its strings:
+// its index entries and string-buffer bytes (weights, strblock.cuh) go
+// through a second look-back (channel 2: index count, string bytes), and the
+// tile's index, per-entry string offsets (aux) and string payload are staged
+// in shared memory and written out coalesced.
 #include <cuda_runtime.h>
-#include <mutex>
 
 #include "lookback.cuh"
 #include "stage1.h"
 #include "stage1_block.cuh"
+#include "strblock.cuh"
 
 namespace jt {
 
@@ -56,13 +60,58 @@ __device__ uint32_t lookback_state(const uint64_t *rec, int64_t tile) {
   }
 }
 
+// byte run copy inside shared memory (offsets from the dynamic smem base):
+// head bytes to align the destination, then funnel-shifted words
+__device__ __forceinline__ void smem_copy(uint8_t *base, uint32_t dst, uint32_t src, int n) {
+  while (n > 0 && (dst & 3)) {
+    base[dst++] = base[src++];
+    n--;
+  }
+  const uint32_t *s4 = (const uint32_t *)base;
+  uint32_t *d4 = (uint32_t *)base;
+  const uint32_t sh = (src & 3) * 8;
+  uint32_t si = src >> 2, di = dst >> 2;
+  int nw = n >> 2;
+  uint32_t lo = nw ? s4[si] : 0;
+  for (int k = 0; k < nw; k++) {
+    uint32_t hi = s4[si + k + 1];
+    d4[di + k] = __funnelshift_r(lo, hi, sh);
+    lo = hi;
+  }
+  dst += 4 * nw;
+  src += 4 * nw;
+  n -= 4 * nw;
+  while (n > 0) {
+    base[dst++] = base[src++];
+    n--;
+  }
+}
+
+struct GlobalAt {
+  const uint8_t *in;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
+};
+
+// shared memory layout (dynamic)
+constexpr int kSmemIn = kStage1Tile;            // tile input bytes
+constexpr int kSmemIdx = kStageIdx * 2;         // u16 positions
+constexpr int kSmemAux = kStageIdx * 2;         // u16 string offsets
+constexpr int kSmemPay = kStagePay;             // payload bytes
+constexpr int kSmemBytes = kSmemIn + kSmemIdx + kSmemAux + kSmemPay + 16;  // +16: word over-read
+
 __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_f[kWarps];
   __shared__ uint32_t s_warp_state[kWarps];
   __shared__ uint32_t s_warp_cnt[kWarps];
-  __shared__ uint64_t s_base;
-  extern __shared__ uint16_t s_stage[];
+  __shared__ uint32_t s_warp_sw[kWarps];
+  __shared__ int s_warp_ov[kWarps];
+  __shared__ unsigned long long s_base, s_sbase;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t *s_in = smem;
+  uint16_t *s_idx = (uint16_t *)(smem + kSmemIn);
+  uint16_t *s_aux = (uint16_t *)(smem + kSmemIn + kSmemIdx);
+  uint8_t *s_pay = smem + kSmemIn + kSmemIdx + kSmemAux;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
@@ -70,10 +119,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const int64_t tile = s_tile;
   const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
+  const GlobalAt gat{a.in};
 
   uint32_t w[16];
   ld256(a.in + blk, w);
   ld256(a.in + blk + 32, w + 8);
+  {
+    uint4 *d = (uint4 *)(s_in + threadIdx.x * 64);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    d[3] = make_uint4(w[12], w[13], w[14], w[15]);
+  }
 
   s1::Masks m;
   s1::classify64(w, m);
@@ -135,11 +192,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   uint32_t state = s_warp_state[warp];
   if (lane > 0) state = s1::apply(excl, state);
   int64_t rem = (int64_t)a.len - (int64_t)blk;
-  uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
-  uint64_t fin = s1::final_mask(m, esc0, tog, state, valid);
-  uint32_t cnt = popc64(fin);
+  const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
 
-  // CTA exclusive scan of counts
+  // masks under the resolved carry (string_mask + finalize_structurals)
+  const uint64_t esc = (state & 1) ? (esc0 ^ tog) : esc0;
+  const uint64_t uq = m.qt & ~esc;
+  const uint64_t instr = s1::prefix_xor(uq) ^ ((state & 2) ? ~0ULL : 0ULL);
+  uint64_t fin;
+  {
+    uint64_t st1 = (m.st & ~instr) | uq;
+    uint64_t cand = st1 | m.ws;
+    uint64_t pseudo = ((cand << 1) | (uint64_t)(state >> 2)) & ~m.ws & ~instr;
+    fin = (st1 | pseudo) & ~(uq & ~instr) & valid;
+  }
+  const uint32_t cnt = popc64(fin);
+
+  // strings in this block
+  const uint64_t openq = uq & instr & valid;
+  const uint64_t content = instr & ~openq & valid;
+  const uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content;
+  const uint64_t ctl = sb::control_mask(m.P) & content;
+  int ov_out = E ? sb::overhang_out(gat, blk, E) : 0;
+  int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
+  if (lane == 31) s_warp_ov[warp] = ov_out;
+  // unterminated string: the reference reads the NUL padding at len
+  if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) atomicMin(a.str_err, (unsigned long long)a.len);
+
+  // CTA exclusive scan of (index count, string bytes); the block weight of a
+  // slow block needs ov_in, which for lane 0 comes from the previous warp
   uint32_t ci = cnt;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -148,41 +228,117 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   if (lane == 31) s_warp_cnt[warp] = ci;
   __syncthreads();
-  uint32_t woff = 0, total = 0;
+  if (lane == 0) {
+    if (warp > 0) ov_in = s_warp_ov[warp - 1];
+    else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true) : 0;
+  }
+  const uint32_t local = threadIdx.x * 64;
+  auto tbyte = [&](uint64_t k) -> uint32_t {
+    uint64_t rel = local + k;
+    return rel < (uint64_t)kStage1Tile ? (uint32_t)s_in[rel] : (uint32_t)a.in[tile_base + rel];
+  };
+  uint64_t serr = ~0ULL;
+  const uint32_t sw = sb::block_strings<false>(tbyte, blk, content, openq, E, ctl, fin, ov_in, &serr,
+                                               [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
+                                               [](int, uint32_t) {});
+  if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
+  uint32_t si = sw;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, si, d);
+    if (lane >= d) si += o;
+  }
+  if (lane == 31) s_warp_sw[warp] = si;
+  __syncthreads();
+  uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0;
 #pragma unroll
   for (int k = 0; k < kWarps; k++) {
-    uint32_t c = s_warp_cnt[k];
+    uint32_t c = s_warp_cnt[k], s = s_warp_sw[k];
     woff += k < warp ? c : 0;
+    wsoff += k < warp ? s : 0;
     total += c;
+    stotal += s;
   }
-  uint32_t off = woff + ci - cnt;
-
-  // stage tile-local offsets (u16) in shared memory
-  uint32_t local = threadIdx.x * 64;
-  while (fin) {
-    s_stage[off++] = (uint16_t)(local + ctz64(fin));
-    fin &= fin - 1;
-  }
+  const uint32_t off = woff + ci - cnt;   // tile-relative index slot
+  const uint32_t soff = wsoff + si - sw;  // tile-relative string byte
 
   if (warp == 0) {
-    uint64_t base;
-    if (tile == 0) {
-      base = 0;
-    } else {
-      if (lane == 0) lb_store(a.rec_count + tile, kFlagAgg | total);
-      base = lb_sum_exclusive(a.rec_count, tile);
+    Pair base{0, 0};
+    Pair tot{total, stotal};
+    if (tile > 0) {
+      if (lane == 0) pair_publish(a.rec_count, tile, 0, tot);
+      base = pair_lookback(a.rec_count, tile);
     }
     if (lane == 0) {
-      lb_store(a.rec_count + tile, kFlagIncl | (base + total));
-      s_base = base;
-      if (tile == (int64_t)a.ntiles - 1) *a.total = base + total;
+      pair_publish(a.rec_count, tile, 1, Pair{base.a + tot.a, base.b + tot.b});
+      s_base = base.a;
+      s_sbase = base.b;
+      if (tile == (int64_t)a.ntiles - 1) {
+        *a.total = base.a + tot.a;
+        *a.total_strings = base.b + tot.b;
+      }
     }
   }
+  // stage positions + string offsets; spill to global when the tile is large
+  const bool idx_direct = total > (uint32_t)kStageIdx;
+  const bool pay_direct = stotal > (uint32_t)kStagePay;
+  if (idx_direct || pay_direct) __syncthreads();  // s_base/s_sbase needed now
+  const uint64_t gbase = (idx_direct || pay_direct) ? s_base : 0;
+  const uint64_t gsbase = (idx_direct || pay_direct) ? s_sbase : 0;
+  uint32_t slot = off;
+  uint64_t e2 = ~0ULL;
+  sb::block_strings<true>(
+      tbyte, blk, content, openq, E, ctl, fin, ov_in, &e2,
+      [&](int a0, uint32_t wdst, int n) {
+        if (pay_direct) {
+          for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
+        } else {
+          smem_copy(smem, kSmemIn + kSmemIdx + kSmemAux + soff + wdst, local + a0, n);
+        }
+      },
+      [&](uint32_t pos, uint8_t b) {
+        if (pay_direct) a.strings[gsbase + soff + pos] = b;
+        else s_pay[soff + pos] = b;
+      },
+      [&](int p, uint32_t wb) {
+        if (idx_direct) {
+          a.idx[gbase + slot] = (uint32_t)(tile_base + local + p);
+          a.aux[gbase + slot] = (uint32_t)(gsbase + soff + wb);
+        } else {
+          s_idx[slot] = (uint16_t)(local + p);
+          s_aux[slot] = (uint16_t)(soff + wb);
+        }
+        slot++;
+      });
   __syncthreads();
 
-  uint32_t *dst = a.idx + s_base;
   const uint32_t tb = (uint32_t)tile_base;
-  for (uint32_t k = threadIdx.x; k < total; k += kThreads) dst[k] = tb + s_stage[k];
+  const uint64_t gb2 = s_base, gsb2 = s_sbase;  // published before the last barrier
+  if (!idx_direct) {
+    uint32_t *dst = a.idx + gb2;
+    uint32_t *dax = a.aux + gb2;
+    const uint32_t sb32 = (uint32_t)gsb2;
+    for (uint32_t k = threadIdx.x; k < total; k += kThreads) {
+      dst[k] = tb + s_idx[k];
+      dax[k] = sb32 + s_aux[k];
+    }
+  }
+  if (!pay_direct && stotal) {
+    uint8_t *dst = a.strings + gsb2;
+    const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3) < stotal
+                              ? (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3)
+                              : stotal;
+    if (threadIdx.x < head) dst[threadIdx.x] = s_pay[threadIdx.x];
+    const uint32_t nw = (stotal - head) / 4;
+    uint32_t *dw = (uint32_t *)(dst + head);
+    const uint32_t *sp = (const uint32_t *)s_pay;
+    const uint32_t sh = head * 8;
+    for (uint32_t k = threadIdx.x; k < nw; k += kThreads) {
+      uint32_t o = (head >> 2) + k;  // head < 4, so o = k
+      dw[k] = __funnelshift_r(sp[o], sp[o + 1], sh);
+    }
+    for (uint32_t k = head + 4 * nw + threadIdx.x; k < stotal; k += kThreads) dst[k] = s_pay[k];
+  }
 }
 
 }  // namespace
@@ -197,11 +353,10 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
   uint64_t ntiles = (a.len + kStage1Tile - 1) / kStage1Tile;
   if (ntiles == 0) ntiles = 1;
   a.ntiles = ntiles;
-  const int smem = kStage1Tile * 2;
   static const cudaError_t configured =
-      cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (configured != cudaSuccess) return configured;
-  k_stage1<<<(unsigned)ntiles, kThreads, smem, stream>>>(a);
+  k_stage1<<<(unsigned)ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();
 }
 

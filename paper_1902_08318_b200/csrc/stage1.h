@@ -9,20 +9,28 @@ namespace jt {
 
 constexpr int kStage1Threads = 256;
 constexpr int kStage1Tile = kStage1Threads * 64;  // bytes per CTA tile
+// shared-memory staging capacities per tile (larger tiles spill to direct
+// global stores)
+constexpr int kStageIdx = 4096;     // index entries
+constexpr int kStagePay = 20480;    // string-buffer bytes
 
 struct Stage1Args {
   const uint8_t *in;   // padded: readable and zero from len up to the tile end + 64
   uint64_t len;
   uint32_t *idx;       // >= len + 1 entries
+  uint32_t *aux;       // per index entry: string-buffer prefix (low 32 bits)
+  uint8_t *strings;    // string buffer (payload; length fields left to stage 2)
   uint64_t *rec_state; // ntiles look-back records, zeroed
-  uint64_t *rec_count; // ntiles look-back records, zeroed
+  uint64_t *rec_count; // 4 * ntiles look-back words (count, string bytes), zeroed
   uint32_t *tile_counter;         // zeroed
   unsigned long long *utf8_pos;   // ~0 initially; min flagged offset
+  unsigned long long *str_err;    // ~0 initially; min string error offset
   uint64_t *total;                // S
+  uint64_t *total_strings;        // string buffer bytes
   uint64_t ntiles;                // filled by stage1_launch
 };
 
-// bytes of look-back records needed for `len`
+// number of tiles for `len` (look-back records: 1 + 4 words per tile)
 size_t stage1_records(uint64_t len);
 
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);

@@ -113,6 +113,19 @@ JT_HD uint64_t escaped_no_carry(uint64_t bs) {
 // changes its escaped status (the leading run grows by an odd length).
 JT_HD uint64_t carry_toggle(uint64_t bs) { return ~bs & (bs + 1); }
 
+// Backslashes at an even offset within their run (1st, 3rd, ...): inside a
+// string these start an escape sequence.  `odd_in` = the run ending at the
+// previous block's last byte has odd length, which makes a run continuing at
+// bit 0 behave as if it started at an odd position (blocks.h:58-75 uses the
+// same re-classification of its starts).
+JT_HD uint64_t unescaped_backslash(uint64_t bs, uint32_t odd_in) {
+  uint64_t starts = bs & ~(bs << 1);
+  uint64_t em = kEven ^ (uint64_t)odd_in;
+  uint64_t runs_e = bs & ~(bs + (starts & em));
+  uint64_t runs_o = bs & ~(bs + (starts & ~em));
+  return (runs_e & kEven) | (runs_o & kOdd);
+}
+
 // Transfer function of one block (or a span of blocks), 4 bytes: byte x,
 // x = odd_in | in_string_in << 1, holds odd_out | in_string_out << 1 |
 // sep_out << 2, where sep_out is the prev_separator carry (blocks.h:161).

@@ -56,88 +56,27 @@ __device__ __forceinline__ int clamp16(long long d) {
 
 __device__ __forceinline__ int tok_depth(uint32_t v) { return (int)(int16_t)(v >> 16); }
 
-// ---- 3-channel look-back (tape words, depth, string bytes) --------------
-// rec[6*t + 0..2] aggregate, rec[6*t + 3..5] inclusive; bit 63 = valid.
-constexpr uint64_t kValid = 1ULL << 63;
-constexpr uint64_t kVal63 = kValid - 1;
-
-__device__ __forceinline__ long long sext63(uint64_t v) {
-  return (long long)(v << 1) >> 1;
-}
-
-struct Tri {
-  unsigned long long w, sb;
-  long long d;
-};
-
-__device__ __forceinline__ void publish(uint64_t *rec, uint64_t tile, int slot, const Tri &v) {
-  uint64_t *r = rec + 6 * tile + 3 * slot;
-  lb_store(r + 0, kValid | (v.w & kVal63));
-  lb_store(r + 1, kValid | ((uint64_t)v.d & kVal63));
-  lb_store(r + 2, kValid | (v.sb & kVal63));
-}
-
-// 0 = not ready, 1 = aggregate, 2 = inclusive
-__device__ __forceinline__ int read_rec(const uint64_t *rec, int64_t tile, Tri &v) {
-  const uint64_t *r = rec + 6 * tile;
-  uint64_t a = lb_load(r + 3), b = lb_load(r + 4), c = lb_load(r + 5);
-  if ((a & b & c) >> 63) {
-    v.w = a & kVal63;
-    v.d = sext63(b);
-    v.sb = c & kVal63;
-    return 2;
-  }
-  a = lb_load(r + 0), b = lb_load(r + 1), c = lb_load(r + 2);
-  if ((a & b & c) >> 63) {
-    v.w = a & kVal63;
-    v.d = sext63(b);
-    v.sb = c & kVal63;
-    return 1;
-  }
-  return 0;
-}
-
-__device__ Tri lookback3(const uint64_t *rec, int64_t tile) {
-  const int lane = threadIdx.x & 31;
-  Tri acc{0, 0, 0};
-  int64_t base = tile - 1;
-  for (;;) {
-    int64_t pred = base - lane;
-    Tri v{0, 0, 0};
-    int st = 2;
-    if (pred >= 0) {
-      while ((st = read_rec(rec, pred, v)) == 0) __nanosleep(32);
-    }
-    uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
-    int stop = incl ? __ffs(incl) - 1 : 31;
-    if (lane > stop) v = Tri{0, 0, 0};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
-      v.sb += __shfl_xor_sync(0xffffffffu, v.sb, o);
-      v.d += __shfl_xor_sync(0xffffffffu, v.d, o);
-    }
-    acc.w += v.w;
-    acc.sb += v.sb;
-    acc.d += v.d;
-    if (incl) return acc;
-    base -= 32;
-  }
-}
+__device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v << 1) >> 1; }
 
 // ---- K2: tokens -----------------------------------------------------------
 
+constexpr uint64_t kMask63 = (1ULL << 63) - 1;
+
 __global__ void __launch_bounds__(kS2Threads) k_tokens(Stage2Args a) {
   __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_w[kWarps2], s_sb[kWarps2];
+  __shared__ unsigned long long s_w[kWarps2];
   __shared__ long long s_d[kWarps2];
   __shared__ int s_min[kWarps2];
-  __shared__ Tri s_base;
-  __shared__ uint64_t s_val[kTokPerThread * kS2Threads];
+  __shared__ unsigned long long s_bw;
+  __shared__ long long s_bd;
+  __shared__ uint32_t s_info[kTokPerTile];  // c | fail << 8 | numkind << 9
+  __shared__ uint64_t s_val[kTokPerTile];
 
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
+  const unsigned long long str_err = ctrl->str_err;
+  const uint32_t total_sb = (uint32_t)ctrl->string_bytes;
   const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const InAt at{a.in};
@@ -151,45 +90,23 @@ __global__ void __launch_bounds__(kS2Threads) k_tokens(Stage2Args a) {
 
     const uint64_t chunk = tile * kS2Threads + threadIdx.x;
     const uint64_t t0 = chunk * kTokPerThread;
-    uint32_t pos[kTokPerThread];
-    uint32_t info[kTokPerThread];  // c | fail << 8 | numkind << 9
-    int n = 0;
-    if (t0 + kTokPerThread <= S) {
-      const uint4 *ip = (const uint4 *)(a.idx + t0);
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        uint4 v = ip[q];
-        pos[4 * q] = v.x;
-        pos[4 * q + 1] = v.y;
-        pos[4 * q + 2] = v.z;
-        pos[4 * q + 3] = v.w;
-      }
-      n = kTokPerThread;
-    } else {
-#pragma unroll
-      for (int k = 0; k < kTokPerThread; k++) pos[k] = t0 + k < S ? a.idx[t0 + k] : 0u;
-      n = t0 < S ? (int)(S - t0) : 0;
-    }
+    const int n = t0 >= S ? 0 : (int)min((uint64_t)kTokPerThread, S - t0);
 
-    // phase A: classify, validate, measure
-    unsigned long long W = 0, SB = 0;
+    // phase A: classify and validate scalars; numbers parsed once, kept in smem
+    unsigned long long W = 0;
     long long D = 0;
     int dmin = 0;
-#pragma unroll
-    for (int k = 0; k < kTokPerThread; k++) {
-      info[k] = 0;
-      if (k >= n) continue;
-      const uint32_t p = pos[k];
+#pragma unroll 1
+    for (int k = 0; k < n; k++) {
+      const uint64_t i = t0 + k;
+      const uint32_t p = a.idx[i];
       const uint32_t c = at(p);
       dmin = D < dmin ? (int)D : dmin;
       uint32_t fail = 0, nk = 0;
       if (c == '"') {
-        str::Measure m = str::string_measure(at, p);
-        if (m.ok) SB += 4ULL + m.len;
-        else {
-          fail = 1;
-          SB += 4;
-        }
+        // the first failing string holds the minimum string-error position
+        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
+        fail = str_err >= p && str_err < end;
       } else if (c == 't' || c == 'f' || c == 'n') {
         fail = !str::atom_ok(at, a.len, p, c);
       } else if (c == '-' || (c - '0') < 10u) {
@@ -200,136 +117,108 @@ __global__ void __launch_bounds__(kS2Threads) k_tokens(Stage2Args a) {
       }
       W += (unsigned long long)tok_width(c);
       D += tok_delta(c);
-      info[k] = c | (fail << 8) | (nk << 9);
+      s_info[k * kS2Threads + threadIdx.x] = c | (fail << 8) | (nk << 9);
     }
 
-    // CTA scan of (W, D, SB) and the min of depth_before
-    unsigned long long iw = W, isb = SB;
+    // CTA scan of (W, D)
+    unsigned long long iw = W;
     long long id = D;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned long long xw = __shfl_up_sync(0xffffffffu, iw, o);
-      unsigned long long xs = __shfl_up_sync(0xffffffffu, isb, o);
       long long xd = __shfl_up_sync(0xffffffffu, id, o);
       if (lane >= o) {
         iw += xw;
-        isb += xs;
         id += xd;
       }
     }
     if (lane == 31) {
       s_w[warp] = iw;
-      s_sb[warp] = isb;
       s_d[warp] = id;
     }
     __syncthreads();
-    Tri tot{0, 0, 0}, pre{0, 0, 0};
+    unsigned long long pre_w = iw - W, tot_w = 0;
+    long long pre_d = id - D, tot_d = 0;
 #pragma unroll
     for (int k = 0; k < kWarps2; k++) {
       if (k < warp) {
-        pre.w += s_w[k];
-        pre.sb += s_sb[k];
-        pre.d += s_d[k];
+        pre_w += s_w[k];
+        pre_d += s_d[k];
       }
-      tot.w += s_w[k];
-      tot.sb += s_sb[k];
-      tot.d += s_d[k];
+      tot_w += s_w[k];
+      tot_d += s_d[k];
     }
-    pre.w += iw - W;
-    pre.sb += isb - SB;
-    pre.d += id - D;
-
     if (warp == 0) {
-      Tri base{0, 0, 0};
+      Pair base{0, 0};
+      Pair tot{tot_w, (unsigned long long)tot_d & kMask63};
       if (tile > 0) {
-        if (lane == 0) publish(a.rec, tile, 0, tot);
-        base = lookback3(a.rec, (int64_t)tile);
+        if (lane == 0) pair_publish(a.rec, (int64_t)tile, 0, tot);
+        base = pair_lookback(a.rec, (int64_t)tile);
       }
       if (lane == 0) {
-        Tri inc{base.w + tot.w, base.sb + tot.sb, base.d + tot.d};
-        publish(a.rec, tile, 1, inc);
-        s_base = base;
-        if (tile == ntiles - 1) {
-          ctrl->tape_words = 1 + inc.w;
-          ctrl->string_bytes = inc.sb;
-        }
+        Pair inc{(base.a + tot.a) & kMask63, (base.b + tot.b) & kMask63};
+        pair_publish(a.rec, (int64_t)tile, 1, inc);
+        s_bw = base.a & kMask63;
+        s_bd = sext63(base.b & kMask63);
+        if (tile == ntiles - 1) ctrl->tape_words = 1 + inc.a;
       }
     }
     __syncthreads();
 
     // phase B: emit
-    unsigned long long t = 1 + s_base.w + pre.w;
-    unsigned long long so = s_base.sb + pre.sb;
-    long long d = s_base.d + pre.d;
-    int cmin = clamp16(d + dmin);
+    unsigned long long t = 1 + s_bw + pre_w;
+    long long d = s_bd + pre_d;
+    const int cmin = clamp16(d + dmin);
     if (n > 0) {
       a.chunk_tape[chunk] = (uint32_t)t;
       a.chunk_min[chunk] = (int16_t)cmin;
     }
-    uint32_t toks[kTokPerThread];
-#pragma unroll
-    for (int k = 0; k < kTokPerThread; k++) {
-      if (k >= n) continue;
-      const uint32_t c = info[k] & 0xFF, fail = (info[k] >> 8) & 1, nk = info[k] >> 9;
-      toks[k] = c | (fail << 8) | ((uint32_t)(uint16_t)clamp16(d) << 16);
+#pragma unroll 1
+    for (int k = 0; k < n; k++) {
+      const uint64_t i = t0 + k;
+      const uint32_t v = s_info[k * kS2Threads + threadIdx.x];
+      const uint32_t c = v & 0xFF, fail = (v >> 8) & 1, nk = v >> 9;
+      a.tok[i] = c | (fail << 8) | ((uint32_t)(uint16_t)clamp16(d) << 16);
       if (c == '"') {
         if (!fail) {
-          uint8_t *dst = a.strings + so + 4;
-          uint32_t len = 0;
-          str::string_decode(at, pos[k], [&](uint32_t i, uint8_t b) {
-            dst[i] = b;
-            len = i + 1;
-          });
-          a.strings[so] = (uint8_t)len;
-          a.strings[so + 1] = (uint8_t)(len >> 8);
-          a.strings[so + 2] = (uint8_t)(len >> 16);
-          a.strings[so + 3] = (uint8_t)(len >> 24);
+          const uint32_t so = a.aux[i];
+          const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
+          const uint32_t len = nx - so - 4;
+          uint8_t *f = a.strings + so;
+          f[0] = (uint8_t)len;
+          f[1] = (uint8_t)(len >> 8);
+          f[2] = (uint8_t)(len >> 16);
+          f[3] = (uint8_t)(len >> 24);
           a.tape[t] = tape_word('"', so);
-          so += 4ULL + len;
-        } else {
-          so += 4;
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
         a.tape[t] = (uint64_t)c << 56;
       } else if (c == '-' || (c - '0') < 10u) {
-        if (nk == num::kNumInt) {
-          a.tape[t] = (uint64_t)'l' << 56;
-          a.tape[t + 1] = s_val[k * kS2Threads + threadIdx.x];
-        } else if (nk == num::kNumFloat) {
-          a.tape[t] = (uint64_t)'d' << 56;
+        if (nk == num::kNumInt || nk == num::kNumFloat) {
+          a.tape[t] = (uint64_t)(nk == num::kNumInt ? 'l' : 'd') << 56;
           a.tape[t + 1] = s_val[k * kS2Threads + threadIdx.x];
         } else if (nk == num::kNumSlow) {
           a.tape[t] = (uint64_t)'d' << 56;
           uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
-          a.slow[2 * slot] = (uint32_t)(t0 + k);
+          a.slow[2 * slot] = (uint32_t)i;
           a.slow[2 * slot + 1] = (uint32_t)t;
         }
       }
       t += (unsigned long long)tok_width(c);
       d += tok_delta(c);
     }
-    if (n == kTokPerThread) {
-      uint4 *tp = (uint4 *)(a.tok + t0);
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-        tp[q] = make_uint4(toks[4 * q], toks[4 * q + 1], toks[4 * q + 2], toks[4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kTokPerThread; k++)
-        if (k < n) a.tok[t0 + k] = toks[k];
-    }
 
     // tile min of depth_before for the search tree
-    int m = n > 0 ? cmin : 0x7FFF;
+    int mm = n > 0 ? cmin : 0x7FFF;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_min[warp] = m;
+    for (int o = 16; o > 0; o >>= 1) mm = min(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+    if (lane == 0) s_min[warp] = mm;
     __syncthreads();
     if (threadIdx.x == 0) {
-      int mm = s_min[0];
+      int m2 = s_min[0];
 #pragma unroll
-      for (int k = 1; k < kWarps2; k++) mm = min(mm, s_min[k]);
-      a.tile_min[tile] = (int16_t)mm;
+      for (int k = 1; k < kWarps2; k++) m2 = min(m2, s_min[k]);
+      a.tile_min[tile] = (int16_t)m2;
     }
   }
 }
@@ -629,8 +518,7 @@ __global__ void k_final(Stage2Args a) {
     if (i >= S) {
       c->offset = (long long)a.len;
     } else if (code == kStringError) {
-      str::Measure m = str::string_measure(InAt{a.in}, a.idx[i]);
-      c->offset = (long long)m.err;
+      c->offset = (long long)c->str_err;  // the failing string holds the minimum
     } else {
       c->offset = (long long)a.idx[i];
     }
@@ -650,9 +538,10 @@ __global__ void k_init(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t k = g; k < s1words; k += stride) s1rec[k] = 0;
   for (uint64_t k = g; k < s2words; k += stride) s2rec[k] = 0;
-  if (g == 0) {
+  if (g == 0 && ctrl) {
     Ctrl z{};
     z.utf8_pos = ~0ULL;
+    z.str_err = ~0ULL;
     z.err_key = ~0ULL;
     z.code = -1;
     z.offset = -1;
@@ -696,7 +585,8 @@ cudaError_t stage1_finalize_launch(Ctrl *ctrl, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches) {
+cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
+                          cudaEvent_t *ev) {
   const Stage2Sizes z = stage2_sizes(a.cap_tokens);
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
   // K2: persistent CTAs pulling tiles from a counter
@@ -704,14 +594,19 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   unsigned g2 = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
   if (g2 < 1) g2 = 1;
   k_tokens<<<g2, kS2Threads, 0, stream>>>(a);
+  if (ev) cudaEventRecord(ev[0], stream);
   k_slow<<<sms, 128, 0, stream>>>(a);
+  if (ev) cudaEventRecord(ev[1], stream);
   k_tree<<<1, 1024, 0, stream>>>(a);
+  if (ev) cudaEventRecord(ev[2], stream);
   uint64_t nthreads = z.chunks;
   unsigned g3 = (unsigned)((nthreads + 127) / 128);
   if (g3 > (unsigned)sms * 16) g3 = (unsigned)sms * 16;
   if (g3 < 1) g3 = 1;
   k_struct<<<g3, 128, 0, stream>>>(a);
+  if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);
+  if (ev) cudaEventRecord(ev[4], stream);
   *launches = 5;
   return cudaGetLastError();
 }

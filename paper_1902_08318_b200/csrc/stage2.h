@@ -24,7 +24,8 @@ struct Ctrl {
   uint32_t slow_count;          // numbers needing the exact fallback
   uint32_t pad;
   uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
-  uint64_t string_bytes;
+  uint64_t string_bytes;        // string buffer size (stage 1)
+  unsigned long long str_err;   // min string error position (~0 = none)
   // results written by the finalize kernel
   int32_t code;
   int32_t pad2;
@@ -36,6 +37,7 @@ struct Stage2Args {
   const uint8_t *in;
   uint64_t len;
   const uint32_t *idx;
+  const uint32_t *aux;  // per index entry: string-buffer prefix (stage 1)
   Ctrl *ctrl;
   uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16
   uint32_t *chunk_tape; // per 16-token chunk: tape index of its first token
@@ -43,7 +45,7 @@ struct Stage2Args {
   int16_t *tile_min;    // per tile
   int16_t *super_min;   // per 64 tiles
   int16_t *super2_min;  // per 64 supers
-  uint64_t *rec;        // 6 words per tile (look-back)
+  uint64_t *rec;        // 4 words per tile (look-back: tape words, depth)
   uint32_t *slow;       // slow-number token list (token, tape slot pairs)
   uint64_t *tape;       // >= 2 * cap + 3 words
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
@@ -59,7 +61,9 @@ Stage2Sizes stage2_sizes(uint64_t cap_tokens);
 
 // Enqueue the whole stage 2 (tokens, slow numbers, tree, structure,
 // finalize); returns the number of kernel launches via *launches.
-cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches);
+// `ev` (optional, 5 events) is recorded after each of the 5 kernels.
+cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
+                          cudaEvent_t *ev = nullptr);
 
 // Reset kernel for the control block + look-back records.
 cudaError_t init_launch(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,

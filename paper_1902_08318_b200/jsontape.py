@@ -32,8 +32,10 @@ EXPORTS = [
     "jt_b200_input_buffer", "jt_b200_stage1_resident", "jt_b200_parse_resident",
     "jt_b200_parse_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
     "jt_b200_device_strings", "jt_b200_download", "jt_b200_set_stream",
-    "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error",
+    "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
+    "jt_b200_kernel_times", "jt_b200_copy_in",
 ]
+KERNELS = ["init", "stage1", "tokens", "slow", "tree", "struct", "final"]
 
 _lib = None
 
@@ -82,6 +84,9 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_device.argtypes = [vp]
     L.jt_b200_last_error.argtypes = [vp]
     L.jt_b200_last_error.restype = C.c_char_p
+    L.jt_b200_profile.argtypes = [vp, C.c_int]
+    L.jt_b200_kernel_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
+    L.jt_b200_copy_in.argtypes = [vp, vp, sz]
     _lib = L
     return L
 
@@ -194,6 +199,11 @@ class Parser:
             raise MemoryError(self.last_error())
         return p
 
+    def copy_in(self, src_ptr: int, n: int):
+        """fill the device input from a host or device pointer"""
+        if self._lib.jt_b200_copy_in(self._h, src_ptr, n) != 0:
+            raise RuntimeError(self.last_error())
+
     def parse_resident(self, n: int) -> Result:
         off = C.c_longlong(-7)
         code = self._lib.jt_b200_parse_resident(self._h, n, C.byref(off))
@@ -237,6 +247,15 @@ class Parser:
 
     def last_launches(self) -> int:
         return self._lib.jt_b200_last_launches(self._h)
+
+    def profile(self, enable: bool = True):
+        self._lib.jt_b200_profile(self._h, 1 if enable else 0)
+
+    def kernel_times(self) -> dict:
+        """ms per kernel of the last full parse (needs profile(True))."""
+        buf = (C.c_float * 8)()
+        n = self._lib.jt_b200_kernel_times(self._h, buf, 8)
+        return {KERNELS[k]: buf[k] for k in range(n)}
 
     def last_error(self) -> str:
         return self._lib.jt_b200_last_error(self._h).decode()
