@@ -75,7 +75,7 @@ struct jt_parser {
   DevBuf aux[2];           // per index entry: string-buffer prefix
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
-  DevBuf tok, chunk_tape, chunk_min, tile_min, super_min, super2_min, slow;
+  DevBuf tok, tape_idx, chunk_min, tile_min, super_min, super2_min, slow;
   DevBuf tape, strings;
   DevBuf ctrl;
   jt::Ctrl *h_ctrl = nullptr;  // pinned
@@ -89,7 +89,7 @@ struct jt_parser {
   bool last_ok = false;
   int launches = 0;
   std::string err;
-  uint64_t s1_str_err = ~0ULL, s1_string_bytes = 0;  // retained with the index
+  uint64_t s1_str_err = ~0ULL, s1_string_bytes = 0, s1_tape_words = 0;  // retained with the index
   uint64_t pending_len = 0;
   int pending_idx = -1;
   // optional per-kernel timing: ev[0] before init, then one per launch
@@ -139,7 +139,9 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
   if (!p->idx[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
   if (!p->aux[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
   if (!p->strings.ensure((size_t)len + 4 * cap_tok + 128)) return false;
-  if (!p->s1rec.ensure(jt::stage1_records(len) * 5 * sizeof(uint64_t) + 64)) return false;
+  if (!p->tok.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->tape_idx.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->s1rec.ensure(jt::stage1_records(len) * 9 * sizeof(uint64_t) + 64)) return false;
   if (!p->ctrl.ensure(sizeof(jt::Ctrl))) return false;
   return true;
 }
@@ -148,8 +150,6 @@ bool ensure_stage2(jt_parser *p, uint64_t len) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
   bool ok = p->s2rec.ensure(z.tiles * 4 * sizeof(uint64_t)) &&
-            p->tok.ensure((cap + 16) * sizeof(uint32_t)) &&
-            p->chunk_tape.ensure(z.chunks * sizeof(uint32_t)) &&
             p->chunk_min.ensure(z.chunks * sizeof(int16_t)) &&
             p->tile_min.ensure(z.tiles * sizeof(int16_t)) &&
             p->super_min.ensure(z.supers * sizeof(int16_t)) &&
@@ -167,6 +167,8 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.idx = p->idx[which].as<uint32_t>();
   a.aux = p->aux[which].as<uint32_t>();
   a.strings = p->strings.as<uint8_t>();
+  a.tokrec = p->tok.as<uint32_t>();
+  a.tape_idx = p->tape_idx.as<uint32_t>();
   uint64_t nt = jt::stage1_records(len);
   a.rec_state = p->s1rec.as<uint64_t>();
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
@@ -175,6 +177,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.str_err = &c->str_err;
   a.total = &c->S;
   a.total_strings = &c->string_bytes;
+  a.tape_words = &c->tape_words;
   return a;
 }
 
@@ -186,7 +189,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.aux = p->aux[which].as<uint32_t>();
   a.ctrl = p->ctrl.as<jt::Ctrl>();
   a.tok = p->tok.as<uint32_t>();
-  a.chunk_tape = p->chunk_tape.as<uint32_t>();
+  a.tape_idx = p->tape_idx.as<uint32_t>();
   a.chunk_min = p->chunk_min.as<int16_t>();
   a.tile_min = p->tile_min.as<int16_t>();
   a.super_min = p->super_min.as<int16_t>();
@@ -206,7 +209,7 @@ bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
   p->prof_n = 0;
   if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
-  uint64_t s1w = jt::stage1_records(len) * 5;
+  uint64_t s1w = jt::stage1_records(len) * 9;
   uint64_t s2w = full ? z.tiles * 4 : 0;
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                   p->s2rec.as<uint64_t>(), s2w, p->stream),
@@ -249,6 +252,7 @@ jt_error finish(jt_parser *p, int which, bool full, long long *off) {
     p->index_count = c.S;
     p->s1_str_err = c.str_err;
     p->s1_string_bytes = c.string_bytes;
+    p->s1_tape_words = c.tape_words;
     p->h_index_valid = false;
   }
   set_off(off, c.offset);
@@ -421,6 +425,7 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   c0.S = p->have_index ? p->index_count : 0;
   c0.str_err = p->s1_str_err;
   c0.string_bytes = p->s1_string_bytes;
+  c0.tape_words = p->s1_tape_words;
   c0.code = -1;
   c0.offset = -1;
   *p->h_ctrl = c0;

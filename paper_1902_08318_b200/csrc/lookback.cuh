@@ -125,3 +125,66 @@ __device__ __forceinline__ Pair pair_lookback(const uint64_t *rec, int64_t tile)
 }
 
 }  // namespace jt
+
+namespace jt {
+
+// Four-counter channel (8 words per tile: [0..3] aggregate, [4..7]
+// inclusive; bit 63 = valid).  Signed counters travel as 63-bit two's
+// complement and are sign-extended by the reader (sext63).
+struct Quad {
+  unsigned long long v[4];
+};
+
+constexpr uint64_t kQuadMask = (1ULL << 63) - 1;
+
+__device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v << 1) >> 1; }
+
+__device__ __forceinline__ void quad_publish(uint64_t *rec, int64_t tile, int slot, const Quad &q) {
+  uint64_t *r = rec + 8 * tile + 4 * slot;
+#pragma unroll
+  for (int k = 0; k < 4; k++) lb_store(r + k, kPairValid | (q.v[k] & kQuadMask));
+}
+
+__device__ __forceinline__ int quad_read(const uint64_t *rec, int64_t tile, Quad &q) {
+  const uint64_t *r = rec + 8 * tile;
+#pragma unroll
+  for (int slot = 1; slot >= 0; --slot) {
+    uint64_t x0 = lb_load(r + 4 * slot), x1 = lb_load(r + 4 * slot + 1);
+    uint64_t x2 = lb_load(r + 4 * slot + 2), x3 = lb_load(r + 4 * slot + 3);
+    if ((x0 & x1 & x2 & x3) >> 63) {
+      q.v[0] = x0 & kQuadMask;
+      q.v[1] = x1 & kQuadMask;
+      q.v[2] = x2 & kQuadMask;
+      q.v[3] = x3 & kQuadMask;
+      return slot + 1;
+    }
+  }
+  return 0;
+}
+
+// exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp
+__device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile) {
+  const int lane = threadIdx.x & 31;
+  Quad acc{{0, 0, 0, 0}};
+  int64_t base = tile - 1;
+  for (;;) {
+    int64_t pred = base - lane;
+    Quad q{{0, 0, 0, 0}};
+    int st = 2;
+    if (pred >= 0)
+      while ((st = quad_read(rec, pred, q)) == 0) __nanosleep(32);
+    uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+    int stop = incl ? __ffs(incl) - 1 : 31;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      unsigned long long x = lane > stop ? 0ULL : q.v[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      acc.v[k] = (acc.v[k] + x) & kQuadMask;
+    }
+    if (incl) return acc;
+    base -= 32;
+  }
+}
+
+}  // namespace jt

@@ -96,8 +96,24 @@ struct GlobalAt {
 constexpr int kSmemIn = kStage1Tile;            // tile input bytes
 constexpr int kSmemIdx = kStageIdx * 2;         // u16 positions
 constexpr int kSmemAux = kStageIdx * 2;         // u16 string offsets
-constexpr int kSmemPay = kStagePay;             // payload bytes
-constexpr int kSmemBytes = kSmemIn + kSmemIdx + kSmemAux + kSmemPay + 16;  // +16: word over-read
+constexpr int kSmemC = kStageIdx;               // u8 token bytes
+constexpr int kSmemT = kStageIdx * 2;           // u16 tile-relative tape index
+constexpr int kSmemD = kStageIdx * 2;           // i16 tile-relative depth
+constexpr int kSmemPay = kStagePay;             // payload bytes (last: word over-read)
+constexpr int kOffPay = kSmemIn + kSmemIdx + kSmemAux + kSmemC + kSmemT + kSmemD;
+constexpr int kSmemBytes = kOffPay + kSmemPay + 16;
+
+__device__ __forceinline__ int tok_width(uint32_t c) {  // tape words per token
+  if (c == ',' || c == ':') return 0;
+  if (c == '-' || (c - '0') < 10u) return 2;
+  return 1;
+}
+
+__device__ __forceinline__ int tok_delta(uint32_t c) {
+  return (c == '{' || c == '[') ? 1 : (c == '}' || c == ']') ? -1 : 0;
+}
+
+__device__ __forceinline__ int clamp16(long long d) { return d < -2 ? -2 : d > 1026 ? 1026 : (int)d; }
 
 __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
@@ -105,13 +121,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_warp_state[kWarps];
   __shared__ uint32_t s_warp_cnt[kWarps];
   __shared__ uint32_t s_warp_sw[kWarps];
+  __shared__ uint32_t s_warp_tw[kWarps];
+  __shared__ int s_warp_td[kWarps];
   __shared__ int s_warp_ov[kWarps];
-  __shared__ unsigned long long s_base, s_sbase;
+  __shared__ unsigned long long s_base, s_sbase, s_tbase;
+  __shared__ long long s_dbase;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *s_in = smem;
   uint16_t *s_idx = (uint16_t *)(smem + kSmemIn);
   uint16_t *s_aux = (uint16_t *)(smem + kSmemIn + kSmemIdx);
-  uint8_t *s_pay = smem + kSmemIn + kSmemIdx + kSmemAux;
+  uint8_t *s_c = smem + kSmemIn + kSmemIdx + kSmemAux;
+  uint16_t *s_trel = (uint16_t *)(smem + kSmemIn + kSmemIdx + kSmemAux + kSmemC);
+  int16_t *s_drel = (int16_t *)(smem + kSmemIn + kSmemIdx + kSmemAux + kSmemC + kSmemT);
+  uint8_t *s_pay = smem + kOffPay;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
@@ -119,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const int64_t tile = s_tile;
   const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
+  const uint32_t local = threadIdx.x * 64;
   const GlobalAt gat{a.in};
 
   uint32_t w[16];
@@ -206,6 +229,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     fin = (st1 | pseudo) & ~(uq & ~instr) & valid;
   }
   const uint32_t cnt = popc64(fin);
+  // tape words and depth change of the block's tokens (A.4 widths / +-1)
+  uint32_t tw = 0;
+  int td = 0;
+  {
+    uint64_t fm = fin;
+    while (fm) {
+      uint32_t c = s_in[local + ctz64(fm)];
+      tw += (uint32_t)tok_width(c);
+      td += tok_delta(c);
+      fm &= fm - 1;
+    }
+  }
 
   // strings in this block
   const uint64_t openq = uq & instr & valid;
@@ -232,7 +267,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     if (warp > 0) ov_in = s_warp_ov[warp - 1];
     else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true) : 0;
   }
-  const uint32_t local = threadIdx.x * 64;
   auto tbyte = [&](uint64_t k) -> uint32_t {
     uint64_t rel = local + k;
     return rel < (uint64_t)kStage1Tile ? (uint32_t)s_in[rel] : (uint32_t)a.in[tile_base + rel];
@@ -248,34 +282,63 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     uint32_t o = __shfl_up_sync(0xffffffffu, si, d);
     if (lane >= d) si += o;
   }
-  if (lane == 31) s_warp_sw[warp] = si;
+  uint32_t ti = tw;
+  int di = td;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, ti, d);
+    int od = __shfl_up_sync(0xffffffffu, di, d);
+    if (lane >= d) {
+      ti += o;
+      di += od;
+    }
+  }
+  if (lane == 31) {
+    s_warp_sw[warp] = si;
+    s_warp_tw[warp] = ti;
+    s_warp_td[warp] = di;
+  }
   __syncthreads();
-  uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0;
+  uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
+  int wdoff = 0, dtotal = 0;
 #pragma unroll
   for (int k = 0; k < kWarps; k++) {
-    uint32_t c = s_warp_cnt[k], s = s_warp_sw[k];
+    uint32_t c = s_warp_cnt[k], s = s_warp_sw[k], t = s_warp_tw[k];
+    int dd = s_warp_td[k];
     woff += k < warp ? c : 0;
     wsoff += k < warp ? s : 0;
+    wtoff += k < warp ? t : 0;
+    wdoff += k < warp ? dd : 0;
     total += c;
     stotal += s;
+    ttotal += t;
+    dtotal += dd;
   }
+  const uint32_t toff = wtoff + ti - tw;  // tile-relative tape words
+  const int doff = wdoff + di - td;       // tile-relative depth
   const uint32_t off = woff + ci - cnt;   // tile-relative index slot
   const uint32_t soff = wsoff + si - sw;  // tile-relative string byte
 
   if (warp == 0) {
-    Pair base{0, 0};
-    Pair tot{total, stotal};
+    Quad base{{0, 0, 0, 0}};
+    Quad tot{{total, stotal, ttotal, (unsigned long long)(long long)dtotal & kQuadMask}};
     if (tile > 0) {
-      if (lane == 0) pair_publish(a.rec_count, tile, 0, tot);
-      base = pair_lookback(a.rec_count, tile);
+      if (lane == 0) quad_publish(a.rec_count, tile, 0, tot);
+      base = quad_lookback(a.rec_count, tile);
     }
     if (lane == 0) {
-      pair_publish(a.rec_count, tile, 1, Pair{base.a + tot.a, base.b + tot.b});
-      s_base = base.a;
-      s_sbase = base.b;
+      Quad inc;
+#pragma unroll
+      for (int k = 0; k < 4; k++) inc.v[k] = (base.v[k] + tot.v[k]) & kQuadMask;
+      quad_publish(a.rec_count, tile, 1, inc);
+      s_base = base.v[0];
+      s_sbase = base.v[1];
+      s_tbase = base.v[2];
+      s_dbase = sext63(base.v[3]);
       if (tile == (int64_t)a.ntiles - 1) {
-        *a.total = base.a + tot.a;
-        *a.total_strings = base.b + tot.b;
+        *a.total = inc.v[0];
+        *a.total_strings = inc.v[1];
+        *a.tape_words = 1 + inc.v[2];
       }
     }
   }
@@ -285,7 +348,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   if (idx_direct || pay_direct) __syncthreads();  // s_base/s_sbase needed now
   const uint64_t gbase = (idx_direct || pay_direct) ? s_base : 0;
   const uint64_t gsbase = (idx_direct || pay_direct) ? s_sbase : 0;
-  uint32_t slot = off;
+  const uint64_t gtbase = idx_direct ? s_tbase : 0;
+  const long long gdbase = idx_direct ? s_dbase : 0;
+  uint32_t slot = off, trun = toff;
+  int drun = doff;
   uint64_t e2 = ~0ULL;
   sb::block_strings<true>(
       tbyte, blk, content, openq, E, ctl, fin, ov_in, &e2,
@@ -293,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         if (pay_direct) {
           for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
         } else {
-          smem_copy(smem, kSmemIn + kSmemIdx + kSmemAux + soff + wdst, local + a0, n);
+          smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
         }
       },
       [&](uint32_t pos, uint8_t b) {
@@ -301,13 +367,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         else s_pay[soff + pos] = b;
       },
       [&](int p, uint32_t wb) {
+        const uint32_t c = s_in[local + p];
         if (idx_direct) {
           a.idx[gbase + slot] = (uint32_t)(tile_base + local + p);
           a.aux[gbase + slot] = (uint32_t)(gsbase + soff + wb);
+          a.tokrec[gbase + slot] = c | ((uint32_t)(uint16_t)clamp16(gdbase + drun) << 16);
+          a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + trun);
         } else {
           s_idx[slot] = (uint16_t)(local + p);
           s_aux[slot] = (uint16_t)(soff + wb);
+          s_c[slot] = (uint8_t)c;
+          s_trel[slot] = (uint16_t)trun;
+          s_drel[slot] = (int16_t)drun;
         }
+        trun += (uint32_t)tok_width(c);
+        drun += tok_delta(c);
         slot++;
       });
   __syncthreads();
@@ -317,10 +391,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   if (!idx_direct) {
     uint32_t *dst = a.idx + gb2;
     uint32_t *dax = a.aux + gb2;
+    uint32_t *drc = a.tokrec + gb2;
+    uint32_t *dtp = a.tape_idx + gb2;
     const uint32_t sb32 = (uint32_t)gsb2;
+    const uint32_t tb32 = (uint32_t)(1 + s_tbase);
+    const long long db = s_dbase;
     for (uint32_t k = threadIdx.x; k < total; k += kThreads) {
       dst[k] = tb + s_idx[k];
       dax[k] = sb32 + s_aux[k];
+      drc[k] = (uint32_t)s_c[k] | ((uint32_t)(uint16_t)clamp16(db + s_drel[k]) << 16);
+      dtp[k] = tb32 + s_trel[k];
     }
   }
   if (!pay_direct && stotal) {

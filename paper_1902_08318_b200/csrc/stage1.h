@@ -20,17 +20,20 @@ struct Stage1Args {
   uint32_t *idx;       // >= len + 1 entries
   uint32_t *aux;       // per index entry: string-buffer prefix (low 32 bits)
   uint8_t *strings;    // string buffer (payload; length fields left to stage 2)
+  uint32_t *tokrec;    // per index entry: byte | clamped depth_before << 16
+  uint32_t *tape_idx;  // per index entry: tape word index
   uint64_t *rec_state; // ntiles look-back records, zeroed
-  uint64_t *rec_count; // 4 * ntiles look-back words (count, string bytes), zeroed
+  uint64_t *rec_count; // 8 * ntiles look-back words (count, strings, tape, depth), zeroed
   uint32_t *tile_counter;         // zeroed
   unsigned long long *utf8_pos;   // ~0 initially; min flagged offset
   unsigned long long *str_err;    // ~0 initially; min string error offset
   uint64_t *total;                // S
   uint64_t *total_strings;        // string buffer bytes
+  uint64_t *tape_words;           // 1 + sum of token widths
   uint64_t ntiles;                // filled by stage1_launch
 };
 
-// number of tiles for `len` (look-back records: 1 + 4 words per tile)
+// number of tiles for `len` (look-back records: 1 + 8 words per tile)
 size_t stage1_records(uint64_t len);
 
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);

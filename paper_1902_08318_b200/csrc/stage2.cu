@@ -58,168 +58,65 @@ __device__ __forceinline__ int tok_depth(uint32_t v) { return (int)(int16_t)(v >
 
 __device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v << 1) >> 1; }
 
-// ---- K2: tokens -----------------------------------------------------------
+// ---- K2: scalars, one thread per token ---------------------------------
 
-constexpr uint64_t kMask63 = (1ULL << 63) - 1;
-
-__global__ void __launch_bounds__(kS2Threads) k_tokens(Stage2Args a) {
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_w[kWarps2];
-  __shared__ long long s_d[kWarps2];
-  __shared__ int s_min[kWarps2];
-  __shared__ unsigned long long s_bw;
-  __shared__ long long s_bd;
-  __shared__ uint32_t s_info[kTokPerTile];  // c | fail << 8 | numkind << 9
-  __shared__ uint64_t s_val[kTokPerTile];
-
+__global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const unsigned long long str_err = ctrl->str_err;
   const uint32_t total_sb = (uint32_t)ctrl->string_bytes;
-  const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const InAt at{a.in};
-
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->s2_tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    __syncthreads();
-    if (tile >= ntiles) return;
-
-    const uint64_t chunk = tile * kS2Threads + threadIdx.x;
-    const uint64_t t0 = chunk * kTokPerThread;
-    const int n = t0 >= S ? 0 : (int)min((uint64_t)kTokPerThread, S - t0);
-
-    // phase A: classify and validate scalars; numbers parsed once, kept in smem
-    unsigned long long W = 0;
-    long long D = 0;
-    int dmin = 0;
-#pragma unroll 1
-    for (int k = 0; k < n; k++) {
-      const uint64_t i = t0 + k;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < S;
+       base += stride) {
+    const uint64_t i = base + (threadIdx.x & 31);
+    const bool live = i < S;
+    const uint32_t rec = live ? a.tok[i] : 0u;
+    // chunk minimum of depth_before (16 tokens = half a warp)
+    int m = live ? (int)(int16_t)(rec >> 16) : 0x7FFF;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (live && (i & 15) == 0) a.chunk_min[i >> 4] = (int16_t)m;
+    if (!live) continue;
+    const uint32_t c = rec & 0xFF;
+    uint32_t fail = 0;
+    if (c == '"') {
       const uint32_t p = a.idx[i];
-      const uint32_t c = at(p);
-      dmin = D < dmin ? (int)D : dmin;
-      uint32_t fail = 0, nk = 0;
-      if (c == '"') {
-        // the first failing string holds the minimum string-error position
-        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
-        fail = str_err >= p && str_err < end;
-      } else if (c == 't' || c == 'f' || c == 'n') {
-        fail = !str::atom_ok(at, a.len, p, c);
-      } else if (c == '-' || (c - '0') < 10u) {
-        num::NumResult r = num::parse_number(at, a.len, p);
-        nk = (uint32_t)r.kind;
-        fail = r.kind == num::kNumFail;
-        s_val[k * kS2Threads + threadIdx.x] = r.bits;
+      const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
+      fail = str_err >= p && str_err < end;  // the failing string holds the minimum
+      if (!fail) {
+        const uint32_t so = a.aux[i];
+        const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
+        const uint32_t len = nx - so - 4;
+        uint8_t *f = a.strings + so;
+        f[0] = (uint8_t)len;
+        f[1] = (uint8_t)(len >> 8);
+        f[2] = (uint8_t)(len >> 16);
+        f[3] = (uint8_t)(len >> 24);
+        a.tape[a.tape_idx[i]] = tape_word('"', so);
       }
-      W += (unsigned long long)tok_width(c);
-      D += tok_delta(c);
-      s_info[k * kS2Threads + threadIdx.x] = c | (fail << 8) | (nk << 9);
-    }
-
-    // CTA scan of (W, D)
-    unsigned long long iw = W;
-    long long id = D;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long xw = __shfl_up_sync(0xffffffffu, iw, o);
-      long long xd = __shfl_up_sync(0xffffffffu, id, o);
-      if (lane >= o) {
-        iw += xw;
-        id += xd;
-      }
-    }
-    if (lane == 31) {
-      s_w[warp] = iw;
-      s_d[warp] = id;
-    }
-    __syncthreads();
-    unsigned long long pre_w = iw - W, tot_w = 0;
-    long long pre_d = id - D, tot_d = 0;
-#pragma unroll
-    for (int k = 0; k < kWarps2; k++) {
-      if (k < warp) {
-        pre_w += s_w[k];
-        pre_d += s_d[k];
-      }
-      tot_w += s_w[k];
-      tot_d += s_d[k];
-    }
-    if (warp == 0) {
-      Pair base{0, 0};
-      Pair tot{tot_w, (unsigned long long)tot_d & kMask63};
-      if (tile > 0) {
-        if (lane == 0) pair_publish(a.rec, (int64_t)tile, 0, tot);
-        base = pair_lookback(a.rec, (int64_t)tile);
-      }
-      if (lane == 0) {
-        Pair inc{(base.a + tot.a) & kMask63, (base.b + tot.b) & kMask63};
-        pair_publish(a.rec, (int64_t)tile, 1, inc);
-        s_bw = base.a & kMask63;
-        s_bd = sext63(base.b & kMask63);
-        if (tile == ntiles - 1) ctrl->tape_words = 1 + inc.a;
+    } else if (c == 't' || c == 'f' || c == 'n') {
+      const uint32_t p = a.idx[i];
+      fail = !str::atom_ok(at, a.len, p, c);
+      if (!fail) a.tape[a.tape_idx[i]] = (uint64_t)c << 56;
+    } else if (c == '-' || (c - '0') < 10u) {
+      const uint32_t p = a.idx[i];
+      num::NumResult r = num::parse_number(at, a.len, p);
+      const uint32_t t = a.tape_idx[i];
+      if (r.kind == num::kNumFail) {
+        fail = 1;
+      } else if (r.kind == num::kNumSlow) {
+        a.tape[t] = (uint64_t)'d' << 56;
+        uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
+        a.slow[2 * slot] = (uint32_t)i;
+        a.slow[2 * slot + 1] = t;
+      } else {
+        a.tape[t] = (uint64_t)(r.kind == num::kNumInt ? 'l' : 'd') << 56;
+        a.tape[t + 1] = r.bits;
       }
     }
-    __syncthreads();
-
-    // phase B: emit
-    unsigned long long t = 1 + s_bw + pre_w;
-    long long d = s_bd + pre_d;
-    const int cmin = clamp16(d + dmin);
-    if (n > 0) {
-      a.chunk_tape[chunk] = (uint32_t)t;
-      a.chunk_min[chunk] = (int16_t)cmin;
-    }
-#pragma unroll 1
-    for (int k = 0; k < n; k++) {
-      const uint64_t i = t0 + k;
-      const uint32_t v = s_info[k * kS2Threads + threadIdx.x];
-      const uint32_t c = v & 0xFF, fail = (v >> 8) & 1, nk = v >> 9;
-      a.tok[i] = c | (fail << 8) | ((uint32_t)(uint16_t)clamp16(d) << 16);
-      if (c == '"') {
-        if (!fail) {
-          const uint32_t so = a.aux[i];
-          const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
-          const uint32_t len = nx - so - 4;
-          uint8_t *f = a.strings + so;
-          f[0] = (uint8_t)len;
-          f[1] = (uint8_t)(len >> 8);
-          f[2] = (uint8_t)(len >> 16);
-          f[3] = (uint8_t)(len >> 24);
-          a.tape[t] = tape_word('"', so);
-        }
-      } else if (c == 't' || c == 'f' || c == 'n') {
-        a.tape[t] = (uint64_t)c << 56;
-      } else if (c == '-' || (c - '0') < 10u) {
-        if (nk == num::kNumInt || nk == num::kNumFloat) {
-          a.tape[t] = (uint64_t)(nk == num::kNumInt ? 'l' : 'd') << 56;
-          a.tape[t + 1] = s_val[k * kS2Threads + threadIdx.x];
-        } else if (nk == num::kNumSlow) {
-          a.tape[t] = (uint64_t)'d' << 56;
-          uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
-          a.slow[2 * slot] = (uint32_t)i;
-          a.slow[2 * slot + 1] = (uint32_t)t;
-        }
-      }
-      t += (unsigned long long)tok_width(c);
-      d += tok_delta(c);
-    }
-
-    // tile min of depth_before for the search tree
-    int mm = n > 0 ? cmin : 0x7FFF;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mm = min(mm, __shfl_xor_sync(0xffffffffu, mm, o));
-    if (lane == 0) s_min[warp] = mm;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int m2 = s_min[0];
-#pragma unroll
-      for (int k = 1; k < kWarps2; k++) m2 = min(m2, s_min[k]);
-      a.tile_min[tile] = (int16_t)m2;
-    }
+    if (fail) a.tok[i] = rec | 0x100u;
   }
 }
 
@@ -239,25 +136,40 @@ __global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
   }
 }
 
-// ---- KT: upper levels of the depth min-tree --------------------------------
+// ---- KT: depth min-tree above the chunks --------------------------------
 
-__global__ void __launch_bounds__(1024) k_tree(Stage2Args a) {
+__global__ void __launch_bounds__(256) k_tree(Stage2Args a) {
+  __shared__ bool s_last;
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
+  const uint64_t nchunks = (S + kTokPerThread - 1) / kTokPerThread;
   const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    int m = 0x7FFF;
+    const uint64_t e = min((t + 1) * kS2Threads, nchunks);
+    for (uint64_t c = t * kS2Threads; c < e; c++) m = min(m, (int)a.chunk_min[c]);
+    a.tile_min[t] = (int16_t)m;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->tree_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   const uint64_t nsup = (ntiles + kTilesPerSuper - 1) / kTilesPerSuper;
   const uint64_t nsup2 = (nsup + kSupersPerSuper2 - 1) / kSupersPerSuper2;
   for (uint64_t s = threadIdx.x; s < nsup; s += blockDim.x) {
     int m = 0x7FFF;
-    uint64_t e = min((s + 1) * kTilesPerSuper, ntiles);
-    for (uint64_t t = s * kTilesPerSuper; t < e; t++) m = min(m, (int)a.tile_min[t]);
+    const uint64_t e = min((s + 1) * kTilesPerSuper, ntiles);
+    for (uint64_t t = s * kTilesPerSuper; t < e; t++) m = min(m, (int)((volatile int16_t *)a.tile_min)[t]);
     a.super_min[s] = (int16_t)m;
   }
   __syncthreads();
   for (uint64_t s = threadIdx.x; s < nsup2; s += blockDim.x) {
     int m = 0x7FFF;
-    uint64_t e = min((s + 1) * kSupersPerSuper2, nsup);
+    const uint64_t e = min((s + 1) * kSupersPerSuper2, nsup);
     for (uint64_t t = s * kSupersPerSuper2; t < e; t++) m = min(m, (int)a.super_min[t]);
     a.super2_min[s] = (int16_t)m;
   }
@@ -331,12 +243,7 @@ __device__ int64_t psv(const Stage2Args &a, int64_t i, int L) {
 }
 
 // tape index of token j (chunk start + widths of the tokens before it)
-__device__ uint32_t tape_of(const Stage2Args &a, int64_t j) {
-  int64_t c0 = j & ~(int64_t)(kTokPerThread - 1);
-  uint32_t t = a.chunk_tape[c0 / kTokPerThread];
-  for (int64_t k = c0; k < j; k++) t += tok_width(a.tok[k] & 0xFF);
-  return t;
-}
+__device__ __forceinline__ uint32_t tape_of(const Stage2Args &a, int64_t j) { return a.tape_idx[j]; }
 
 enum : int { M_V = 0, M_OF, M_AF, M_K, M_C, M_A };
 
@@ -353,7 +260,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
        chunk += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i0 = chunk * kTokPerThread;
     const uint64_t i1 = min(i0 + kTokPerThread, S);
-    uint32_t t = a.chunk_tape[chunk];
+    uint32_t t = a.tape_idx[i0];
 
     // entry state from the two previous tokens (A.5 arrival rules)
     int mode = M_V;
@@ -589,15 +496,18 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
                           cudaEvent_t *ev) {
   const Stage2Sizes z = stage2_sizes(a.cap_tokens);
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
-  // K2: persistent CTAs pulling tiles from a counter
-  uint64_t want = z.tiles;
-  unsigned g2 = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
+  // K2: one thread per token, grid sized for the capacity bound, grid-stride
+  uint64_t g = (a.cap_tokens + 255) / 256;
+  unsigned g2 = (unsigned)(g < (uint64_t)sms * 16 ? g : (uint64_t)sms * 16);
   if (g2 < 1) g2 = 1;
-  k_tokens<<<g2, kS2Threads, 0, stream>>>(a);
+  k_scalars<<<g2, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[0], stream);
   k_slow<<<sms, 128, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[1], stream);
-  k_tree<<<1, 1024, 0, stream>>>(a);
+  unsigned gt = (unsigned)((z.tiles + 255) / 256);
+  if (gt > (unsigned)sms) gt = (unsigned)sms;
+  if (gt < 1) gt = 1;
+  k_tree<<<gt, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
   uint64_t nthreads = z.chunks;
   unsigned g3 = (unsigned)((nthreads + 127) / 128);

@@ -22,7 +22,7 @@ struct Ctrl {
   uint64_t S;                   // structural index count
   unsigned long long err_key;   // (token << 8) | code, min wins (~0 = none)
   uint32_t slow_count;          // numbers needing the exact fallback
-  uint32_t pad;
+  uint32_t tree_done;           // blocks of the tree kernel finished
   uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
   uint64_t string_bytes;        // string buffer size (stage 1)
   unsigned long long str_err;   // min string error position (~0 = none)
@@ -39,9 +39,9 @@ struct Stage2Args {
   const uint32_t *idx;
   const uint32_t *aux;  // per index entry: string-buffer prefix (stage 1)
   Ctrl *ctrl;
-  uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16
-  uint32_t *chunk_tape; // per 16-token chunk: tape index of its first token
-  int16_t *chunk_min;   // per chunk: min depth_before
+  uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16 (stage 1 + scalars)
+  const uint32_t *tape_idx;  // per token: tape word index (stage 1)
+  int16_t *chunk_min;   // per 16-token chunk: min depth_before
   int16_t *tile_min;    // per tile
   int16_t *super_min;   // per 64 tiles
   int16_t *super2_min;  // per 64 supers
