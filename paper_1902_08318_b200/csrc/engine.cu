@@ -75,7 +75,7 @@ struct jt_parser {
   DevBuf aux[2];           // per index entry: string-buffer prefix
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
-  DevBuf tok, tape_idx, chunk_min, tile_min, super_min, super2_min, slow;
+  DevBuf tok, tape_idx, m1, m2, mhi, slow;  // m3 lives in s2rec (zeroed by init)
   DevBuf tape, strings;
   DevBuf ctrl;
   jt::Ctrl *h_ctrl = nullptr;  // pinned
@@ -149,11 +149,9 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
 bool ensure_stage2(jt_parser *p, uint64_t len) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
-  bool ok = p->s2rec.ensure(z.tiles * 4 * sizeof(uint64_t)) &&
-            p->chunk_min.ensure(z.chunks * sizeof(int16_t)) &&
-            p->tile_min.ensure(z.tiles * sizeof(int16_t)) &&
-            p->super_min.ensure(z.supers * sizeof(int16_t)) &&
-            p->super2_min.ensure(z.supers2 * sizeof(int16_t)) &&
+  bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 64) &&
+            p->m1.ensure(z.n1 * sizeof(int16_t)) && p->m2.ensure(z.n2 * sizeof(int16_t)) &&
+            p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
             p->slow.ensure((cap + 16) * 2 * sizeof(uint32_t)) &&
             p->tape.ensure((2 * cap + 8) * sizeof(uint64_t));
   return ok;
@@ -190,11 +188,12 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.ctrl = p->ctrl.as<jt::Ctrl>();
   a.tok = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
-  a.chunk_min = p->chunk_min.as<int16_t>();
-  a.tile_min = p->tile_min.as<int16_t>();
-  a.super_min = p->super_min.as<int16_t>();
-  a.super2_min = p->super2_min.as<int16_t>();
-  a.rec = p->s2rec.as<uint64_t>();
+  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  a.m1 = p->m1.as<int16_t>();
+  a.m2 = p->m2.as<int16_t>();
+  a.m3 = p->s2rec.as<int32_t>();
+  a.mhi = p->mhi.as<int16_t>();
+  for (int k = 0; k < 4; k++) a.hi_off[k] = z.hi_off[k];
   a.slow = p->slow.as<uint32_t>();
   a.tape = p->tape.as<uint64_t>();
   a.strings = p->strings.as<uint8_t>();
@@ -210,7 +209,7 @@ bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
   if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   uint64_t s1w = jt::stage1_records(len) * 9;
-  uint64_t s2w = full ? z.tiles * 4 : 0;
+  uint64_t s2w = full ? z.n3 / 2 + 1 : 0;  // m3 (int32) words
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                   p->s2rec.as<uint64_t>(), s2w, p->stream),
                "init"))
@@ -414,7 +413,7 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   p->launches = 0;
   if (!cuda_ok(p, jt::init_launch(nullptr, p->s1rec.as<uint64_t>(), 0, p->s2rec.as<uint64_t>(),
-                                  z.tiles * 4, p->stream),
+                                  z.n3 / 2 + 1, p->stream),
                "init")) {
     set_off(error_offset, -1);
     return JT_CAPACITY;

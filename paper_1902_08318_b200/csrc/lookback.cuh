@@ -162,28 +162,51 @@ __device__ __forceinline__ int quad_read(const uint64_t *rec, int64_t tile, Quad
   return 0;
 }
 
+// Window of the look-back: each lane reads kLbPer predecessor records per
+// round, so one round covers 32 * kLbPer tiles.  With ~0.5-1 us per round
+// trip, the window size bounds how fast the inclusive frontier advances
+// (window x tile bytes per round trip), so it must be wide.
+constexpr int kLbPer = 4;
+
 // exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp
 __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile) {
   const int lane = threadIdx.x & 31;
   Quad acc{{0, 0, 0, 0}};
   int64_t base = tile - 1;
   for (;;) {
-    int64_t pred = base - lane;
-    Quad q{{0, 0, 0, 0}};
-    int st = 2;
-    if (pred >= 0)
-      while ((st = quad_read(rec, pred, q)) == 0) __nanosleep(32);
-    uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+    // lane l owns predecessors base - kLbPer*l - j, j = 0 (nearest) .. kLbPer-1
+    Quad q[kLbPer];
+    int st[kLbPer];
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {
+      int64_t pred = base - (int64_t)kLbPer * lane - j;
+      q[j] = Quad{{0, 0, 0, 0}};
+      st[j] = 2;
+      if (pred >= 0)
+        while ((st[j] = quad_read(rec, pred, q[j])) == 0) __nanosleep(32);
+    }
+    // per lane: sum from the nearest up to and including its first inclusive
+    Quad mine{{0, 0, 0, 0}};
+    bool has_incl = false;
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {
+      if (!has_incl) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) mine.v[k] += q[j].v[k];
+        has_incl = st[j] == 2;
+      }
+    }
+    uint32_t incl = __ballot_sync(0xffffffffu, has_incl);
     int stop = incl ? __ffs(incl) - 1 : 31;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      unsigned long long x = lane > stop ? 0ULL : q.v[k];
+      unsigned long long x = lane > stop ? 0ULL : (mine.v[k] & kQuadMask);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       acc.v[k] = (acc.v[k] + x) & kQuadMask;
     }
     if (incl) return acc;
-    base -= 32;
+    base -= 32 * kLbPer;
   }
 }
 

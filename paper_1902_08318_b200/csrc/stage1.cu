@@ -34,29 +34,51 @@ __device__ __forceinline__ void ld256(const uint8_t *p, uint32_t *w) {
                : "l"(p));
 }
 
-// state look-back (channel 1), one full warp; returns the tile's carry-in
+// state look-back (channel 1), one full warp; returns the tile's carry-in.
+// Each lane reads kLbPer predecessors per round (see lookback.cuh).
 __device__ uint32_t lookback_state(const uint64_t *rec, int64_t tile) {
   const int lane = threadIdx.x & 31;
   uint32_t G = 0;
   bool haveG = false;
   int64_t base = tile - 1;
   for (;;) {
-    int64_t pred = base - lane;
-    uint64_t v = pred >= 0 ? lb_wait(rec + pred) : (kFlagIncl | s1::kInitState);
-    uint32_t incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-    uint32_t pay = (uint32_t)v;
+    uint64_t v[kLbPer];
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {
+      int64_t pred = base - (int64_t)kLbPer * lane - j;
+      v[j] = pred >= 0 ? lb_wait(rec + pred) : (kFlagIncl | s1::kInitState);
+    }
+    // per lane, nearest first: either a resolved state (an inclusive record
+    // was found, later aggregates applied on top) or a composed function
+    uint32_t fn = 0, stt = 0;
+    bool have_fn = false, resolved = false;
+#pragma unroll
+    for (int j = kLbPer - 1; j >= 0; --j) {  // farthest to nearest
+      uint32_t pay = (uint32_t)v[j];
+      if ((v[j] >> 62) == 2) {
+        resolved = true;
+        stt = pay & 7;
+        have_fn = false;
+      } else if (resolved) {
+        stt = s1::apply(pay, stt);
+      } else {
+        fn = have_fn ? s1::compose(pay, fn) : pay;
+        have_fn = true;
+      }
+    }
+    uint32_t incl = __ballot_sync(0xffffffffu, resolved);
     if (incl) {
       int k = __ffs(incl) - 1;
-      uint32_t s = __shfl_sync(0xffffffffu, pay, k);
-      for (int l = k - 1; l >= 0; --l) s = s1::apply(__shfl_sync(0xffffffffu, pay, l), s);
+      uint32_t s = __shfl_sync(0xffffffffu, stt, k);
+      for (int l = k - 1; l >= 0; --l) s = s1::apply(__shfl_sync(0xffffffffu, fn, l), s);
       if (haveG) s = s1::apply(G, s);
       return s;
     }
-    uint32_t H = __shfl_sync(0xffffffffu, pay, 31);
-    for (int l = 30; l >= 0; --l) H = s1::compose(__shfl_sync(0xffffffffu, pay, l), H);
+    uint32_t H = __shfl_sync(0xffffffffu, fn, 31);
+    for (int l = 30; l >= 0; --l) H = s1::compose(__shfl_sync(0xffffffffu, fn, l), H);
     G = haveG ? s1::compose(G, H) : H;
     haveG = true;
-    base -= 32;
+    base -= 32 * kLbPer;
   }
 }
 

@@ -61,62 +61,75 @@ __device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v <
 // ---- K2: scalars, one thread per token ---------------------------------
 
 __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
+  __shared__ int s_wmin[8];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const unsigned long long str_err = ctrl->str_err;
   const uint32_t total_sb = (uint32_t)ctrl->string_bytes;
   const InAt at{a.in};
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < S;
-       base += stride) {
-    const uint64_t i = base + (threadIdx.x & 31);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t stride = (uint64_t)gridDim.x * 256;
+  for (uint64_t base = (uint64_t)blockIdx.x * 256; base < S; base += stride) {
+    const uint64_t i = base + threadIdx.x;
     const bool live = i < S;
     const uint32_t rec = live ? a.tok[i] : 0u;
-    // chunk minimum of depth_before (16 tokens = half a warp)
+    // depth min-tree levels 1 (16 tokens), 2 (256), 3 (4096)
     int m = live ? (int)(int16_t)(rec >> 16) : 0x7FFF;
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (live && (i & 15) == 0) a.chunk_min[i >> 4] = (int16_t)m;
-    if (!live) continue;
-    const uint32_t c = rec & 0xFF;
-    uint32_t fail = 0;
-    if (c == '"') {
-      const uint32_t p = a.idx[i];
-      const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
-      fail = str_err >= p && str_err < end;  // the failing string holds the minimum
-      if (!fail) {
-        const uint32_t so = a.aux[i];
-        const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
-        const uint32_t len = nx - so - 4;
-        uint8_t *f = a.strings + so;
-        f[0] = (uint8_t)len;
-        f[1] = (uint8_t)(len >> 8);
-        f[2] = (uint8_t)(len >> 16);
-        f[3] = (uint8_t)(len >> 24);
-        a.tape[a.tape_idx[i]] = tape_word('"', so);
+    if (live && (i & 15) == 0) a.m1[i >> 4] = (int16_t)m;
+    m = min(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    if (lane == 0) s_wmin[warp] = m;
+    if (live) {
+      const uint32_t c = rec & 0xFF;
+      uint32_t fail = 0;
+      if (c == '"') {
+        const uint32_t p = a.idx[i];
+        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
+        fail = str_err >= p && str_err < end;  // the failing string holds the minimum
+        if (!fail) {
+          const uint32_t so = a.aux[i];
+          const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
+          const uint32_t len = nx - so - 4;
+          uint8_t *f = a.strings + so;
+          f[0] = (uint8_t)len;
+          f[1] = (uint8_t)(len >> 8);
+          f[2] = (uint8_t)(len >> 16);
+          f[3] = (uint8_t)(len >> 24);
+          a.tape[a.tape_idx[i]] = tape_word('"', so);
+        }
+      } else if (c == 't' || c == 'f' || c == 'n') {
+        const uint32_t p = a.idx[i];
+        fail = !str::atom_ok(at, a.len, p, c);
+        if (!fail) a.tape[a.tape_idx[i]] = (uint64_t)c << 56;
+      } else if (c == '-' || (c - '0') < 10u) {
+        const uint32_t p = a.idx[i];
+        num::NumResult r = num::parse_number(at, a.len, p);
+        const uint32_t t = a.tape_idx[i];
+        if (r.kind == num::kNumFail) {
+          fail = 1;
+        } else if (r.kind == num::kNumSlow) {
+          a.tape[t] = (uint64_t)'d' << 56;
+          uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
+          a.slow[2 * slot] = (uint32_t)i;
+          a.slow[2 * slot + 1] = t;
+        } else {
+          a.tape[t] = (uint64_t)(r.kind == num::kNumInt ? 'l' : 'd') << 56;
+          a.tape[t + 1] = r.bits;
+        }
       }
-    } else if (c == 't' || c == 'f' || c == 'n') {
-      const uint32_t p = a.idx[i];
-      fail = !str::atom_ok(at, a.len, p, c);
-      if (!fail) a.tape[a.tape_idx[i]] = (uint64_t)c << 56;
-    } else if (c == '-' || (c - '0') < 10u) {
-      const uint32_t p = a.idx[i];
-      num::NumResult r = num::parse_number(at, a.len, p);
-      const uint32_t t = a.tape_idx[i];
-      if (r.kind == num::kNumFail) {
-        fail = 1;
-      } else if (r.kind == num::kNumSlow) {
-        a.tape[t] = (uint64_t)'d' << 56;
-        uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
-        a.slow[2 * slot] = (uint32_t)i;
-        a.slow[2 * slot + 1] = t;
-      } else {
-        a.tape[t] = (uint64_t)(r.kind == num::kNumInt ? 'l' : 'd') << 56;
-        a.tape[t + 1] = r.bits;
-      }
+      if (fail) a.tok[i] = rec | 0x100u;
     }
-    if (fail) a.tok[i] = rec | 0x100u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int mm = s_wmin[0];
+#pragma unroll
+      for (int k = 1; k < 8; k++) mm = min(mm, s_wmin[k]);
+      a.m2[base >> 8] = (int16_t)mm;
+      atomicMax(&a.m3[base >> 12], 0x7FFF - mm);
+    }
+    __syncthreads();
   }
 }
 
@@ -138,108 +151,110 @@ __global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
 
 // ---- KT: depth min-tree above the chunks --------------------------------
 
-__global__ void __launch_bounds__(256) k_tree(Stage2Args a) {
-  __shared__ bool s_last;
+__global__ void __launch_bounds__(1024) k_tree(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
-  const uint64_t nchunks = (S + kTokPerThread - 1) / kTokPerThread;
-  const uint64_t ntiles = (S + kTokPerTile - 1) / kTokPerTile;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
-       t += (uint64_t)gridDim.x * blockDim.x) {
+  uint64_t n = (S + 4095) / 4096;  // level-3 entries
+  uint64_t n4 = (n + 15) / 16;
+  int16_t *l4 = a.mhi + a.hi_off[0];
+  for (uint64_t e = threadIdx.x; e < n4; e += blockDim.x) {
     int m = 0x7FFF;
-    const uint64_t e = min((t + 1) * kS2Threads, nchunks);
-    for (uint64_t c = t * kS2Threads; c < e; c++) m = min(m, (int)a.chunk_min[c]);
-    a.tile_min[t] = (int16_t)m;
+    uint64_t end = min(16 * e + 16, n);
+    for (uint64_t c = 16 * e; c < end; c++) m = min(m, 0x7FFF - a.m3[c]);
+    l4[e] = (int16_t)m;
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->tree_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const uint64_t nsup = (ntiles + kTilesPerSuper - 1) / kTilesPerSuper;
-  const uint64_t nsup2 = (nsup + kSupersPerSuper2 - 1) / kSupersPerSuper2;
-  for (uint64_t s = threadIdx.x; s < nsup; s += blockDim.x) {
-    int m = 0x7FFF;
-    const uint64_t e = min((s + 1) * kTilesPerSuper, ntiles);
-    for (uint64_t t = s * kTilesPerSuper; t < e; t++) m = min(m, (int)((volatile int16_t *)a.tile_min)[t]);
-    a.super_min[s] = (int16_t)m;
-  }
-  __syncthreads();
-  for (uint64_t s = threadIdx.x; s < nsup2; s += blockDim.x) {
-    int m = 0x7FFF;
-    const uint64_t e = min((s + 1) * kSupersPerSuper2, nsup);
-    for (uint64_t t = s * kSupersPerSuper2; t < e; t++) m = min(m, (int)a.super_min[t]);
-    a.super2_min[s] = (int16_t)m;
+  n = n4;
+  for (int lv = 1; lv < 4; lv++) {
+    __syncthreads();
+    const int16_t *src = a.mhi + a.hi_off[lv - 1];
+    int16_t *dst = a.mhi + a.hi_off[lv];
+    uint64_t nn = (n + 15) / 16;
+    for (uint64_t e = threadIdx.x; e < nn; e += blockDim.x) {
+      int m = 0x7FFF;
+      uint64_t end = min(16 * e + 16, n);
+      for (uint64_t c = 16 * e; c < end; c++) m = min(m, (int)src[c]);
+      dst[e] = (int16_t)m;
+    }
+    n = nn;
   }
 }
 
 // ---- K3: structure --------------------------------------------------------
 
+// 16 values of one group at tree level `lv` (group g = elements 16g..16g+15)
+__device__ __forceinline__ void load_group(const Stage2Args &a, int lv, int64_t g, int v[16]) {
+  if (lv == 0) {
+    const uint4 *p = (const uint4 *)(a.tok + 16 * g);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      uint4 x = p[q];
+      v[4 * q] = tok_depth(x.x);
+      v[4 * q + 1] = tok_depth(x.y);
+      v[4 * q + 2] = tok_depth(x.z);
+      v[4 * q + 3] = tok_depth(x.w);
+    }
+  } else if (lv == 3) {
+    const int4 *p = (const int4 *)(a.m3 + 16 * g);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      int4 x = p[q];
+      v[4 * q] = 0x7FFF - x.x;
+      v[4 * q + 1] = 0x7FFF - x.y;
+      v[4 * q + 2] = 0x7FFF - x.z;
+      v[4 * q + 3] = 0x7FFF - x.w;
+    }
+  } else {
+    const int16_t *base = lv == 1 ? a.m1 : lv == 2 ? a.m2 : a.mhi + a.hi_off[lv - 4];
+    const uint4 *p = (const uint4 *)(base + 16 * g);
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      uint4 x = p[q];
+      uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        v[8 * q + 2 * k] = (int)(int16_t)(w[k] & 0xFFFF);
+        v[8 * q + 2 * k + 1] = (int)(int16_t)(w[k] >> 16);
+      }
+    }
+  }
+}
+
 // nearest j < i whose depth_before <= L (the innermost container open at i
-// when L = depth_before(i) - 1), or -1
+// when L = depth_before(i) - 1), or -1: climb the fan-out-16 min-tree until a
+// group left of the path holds a value <= L, then descend to its last such
+// leaf.  One vector load per level.
 __device__ int64_t psv(const Stage2Args &a, int64_t i, int L) {
   if (i <= 0) return -1;
-  int64_t j = i - 1;
-  const int64_t lo = (i - 1) & ~(int64_t)(kTokPerThread - 1);
-  for (; j >= lo; --j)
-    if (tok_depth(a.tok[j]) <= L) return j;
-  int64_t c = lo / kTokPerThread - 1;  // chunks of the same tile
-  int64_t found_chunk = -1;
-  const int64_t clo = (lo / kTokPerThread) & ~(int64_t)(kS2Threads - 1);
-  for (; c >= clo; --c)
-    if (a.chunk_min[c] <= L) {
-      found_chunk = c;
+  int64_t x = i - 1;
+  int lv = 0;
+  int v[16];
+  for (;;) {
+    const int64_t g = x >> 4;
+    const int hi = (int)(x & 15);
+    load_group(a, lv, g, v);
+    int found = -1;
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+      if (k <= hi && v[k] <= L) found = k;
+    if (found >= 0) {
+      x = (g << 4) + found;
       break;
     }
-  if (found_chunk < 0) {
-    int64_t tile = clo / kS2Threads;  // tiles of the same super
-    int64_t found_tile = -1;
-    const int64_t tlo = tile & ~(int64_t)(kTilesPerSuper - 1);
-    for (int64_t t = tile - 1; t >= tlo; --t)
-      if (a.tile_min[t] <= L) {
-        found_tile = t;
-        break;
-      }
-    if (found_tile < 0) {
-      int64_t sup = tlo / kTilesPerSuper;
-      int64_t found_sup = -1;
-      const int64_t slo = sup & ~(int64_t)(kSupersPerSuper2 - 1);
-      for (int64_t s = sup - 1; s >= slo; --s)
-        if (a.super_min[s] <= L) {
-          found_sup = s;
-          break;
-        }
-      if (found_sup < 0) {
-        for (int64_t s2 = slo / kSupersPerSuper2 - 1; s2 >= 0; --s2)
-          if (a.super2_min[s2] <= L) {
-            for (int64_t s = s2 * kSupersPerSuper2 + kSupersPerSuper2 - 1; s >= s2 * kSupersPerSuper2; --s)
-              if (a.super_min[s] <= L) {
-                found_sup = s;
-                break;
-              }
-            break;
-          }
-        if (found_sup < 0) return -1;
-      }
-      for (int64_t t = found_sup * kTilesPerSuper + kTilesPerSuper - 1; t >= found_sup * kTilesPerSuper; --t)
-        if (a.tile_min[t] <= L) {
-          found_tile = t;
-          break;
-        }
-      if (found_tile < 0) return -1;
-    }
-    for (int64_t cc = found_tile * kS2Threads + kS2Threads - 1; cc >= found_tile * kS2Threads; --cc)
-      if (a.chunk_min[cc] <= L) {
-        found_chunk = cc;
-        break;
-      }
-    if (found_chunk < 0) return -1;
+    if (g == 0 || lv == kTreeLevels - 1) return -1;
+    x = g - 1;
+    lv++;
   }
-  for (j = found_chunk * kTokPerThread + kTokPerThread - 1; j >= found_chunk * kTokPerThread; --j)
-    if (tok_depth(a.tok[j]) <= L) return j;
-  return -1;
+  while (lv > 0) {
+    lv--;
+    load_group(a, lv, x, v);
+    int found = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+      if (v[k] <= L) found = k;
+    x = (x << 4) + found;
+  }
+  return x;
 }
 
 // tape index of token j (chunk start + widths of the tokens before it)
@@ -255,11 +270,21 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
-  const uint64_t nchunks = (S + kTokPerThread - 1) / kTokPerThread;
+  const uint64_t nchunks = (S + kStructTok - 1) / kStructTok;
   for (uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; chunk < nchunks;
        chunk += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = chunk * kTokPerThread;
-    const uint64_t i1 = min(i0 + kTokPerThread, S);
+    const uint64_t i0 = chunk * kStructTok;
+    const uint64_t i1 = min(i0 + kStructTok, S);
+    uint32_t recs[kStructTok];
+    if (i1 - i0 == kStructTok) {
+      const uint4 *rp = (const uint4 *)(a.tok + i0);
+      uint4 r0 = rp[0], r1 = rp[1];
+      recs[0] = r0.x, recs[1] = r0.y, recs[2] = r0.z, recs[3] = r0.w;
+      recs[4] = r1.x, recs[5] = r1.y, recs[6] = r1.z, recs[7] = r1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kStructTok; k++) recs[k] = i0 + k < i1 ? a.tok[i0 + k] : 0u;
+    }
     uint32_t t = a.tape_idx[i0];
 
     // entry state from the two previous tokens (A.5 arrival rules)
@@ -289,7 +314,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
       }
     }
 
-    uint32_t stk[kTokPerThread];  // local openers: tape index | is_object << 31
+    uint32_t stk[kStructTok];  // local openers: tape index | is_object << 31
     int sp = 0;
     int far_level = -100;  // cache of the last far container lookup
     uint32_t far_tape = 0;
@@ -297,8 +322,10 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
     int err = 0;
     uint64_t i = i0;
     int depth_after = 0;
-    for (; i < i1; i++) {
-      const uint32_t v = a.tok[i];
+#pragma unroll
+    for (int k = 0; k < kStructTok; k++) {
+      if (i >= i1) break;
+      const uint32_t v = recs[k];
       const uint32_t c = v & 0xFF;
       const bool fail = (v >> 8) & 1;
       const int D = tok_depth(v);
@@ -394,6 +421,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
       } while (again && !err);
       if (err) break;
       t += tok_width(c);
+      i++;
     }
     if (err) {
       report(ctrl, i, err);
@@ -470,10 +498,19 @@ __global__ void k_stage1_final(Ctrl *c) {
 
 Stage2Sizes stage2_sizes(uint64_t cap) {
   Stage2Sizes z;
-  z.chunks = (cap + kTokPerThread - 1) / kTokPerThread + 1;
+  z.chunks = (cap + kStructTok - 1) / kStructTok + 1;
   z.tiles = (cap + kTokPerTile - 1) / kTokPerTile + 1;
-  z.supers = (z.tiles + kTilesPerSuper - 1) / kTilesPerSuper + 1;
-  z.supers2 = (z.supers + kSupersPerSuper2 - 1) / kSupersPerSuper2 + 1;
+  // every level padded by one group (vector loads of a whole group)
+  z.n1 = (cap + 15) / 16 + 32;
+  z.n2 = (cap + 255) / 256 + 32;
+  z.n3 = (cap + 4095) / 4096 + 32;
+  uint64_t n = (cap + 4095) / 4096, off = 0;
+  for (int k = 0; k < 4; k++) {
+    n = (n + 15) / 16;
+    z.hi_off[k] = off;
+    off += (n + 32 + 15) & ~(uint64_t)15;
+  }
+  z.nhi = off;
   return z;
 }
 
@@ -504,10 +541,7 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[0], stream);
   k_slow<<<sms, 128, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[1], stream);
-  unsigned gt = (unsigned)((z.tiles + 255) / 256);
-  if (gt > (unsigned)sms) gt = (unsigned)sms;
-  if (gt < 1) gt = 1;
-  k_tree<<<gt, 256, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
   uint64_t nthreads = z.chunks;
   unsigned g3 = (unsigned)((nthreads + 127) / 128);

@@ -10,8 +10,11 @@ namespace jt {
 constexpr int kTokPerThread = 16;                       // one "chunk"
 constexpr int kS2Threads = 128;
 constexpr int kTokPerTile = kTokPerThread * kS2Threads;  // 2048 tokens
-constexpr int kTilesPerSuper = 64;
-constexpr int kSupersPerSuper2 = 64;
+constexpr int kStructTok = 8;                           // tokens per k_struct thread
+// depth min-tree over the tokens, fan-out 16: level 0 = token records,
+// level 1 = per 16 tokens (m1), 2 = per 256 (m2), 3 = per 4096 (m3, int32
+// encoded 0x7FFF - min for atomicMax), levels 4..7 = mhi (int16)
+constexpr int kTreeLevels = 8;
 
 // Device control block, zeroed before every parse (utf8_pos / err_key set
 // to ~0 by the init kernel).
@@ -41,11 +44,11 @@ struct Stage2Args {
   Ctrl *ctrl;
   uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16 (stage 1 + scalars)
   const uint32_t *tape_idx;  // per token: tape word index (stage 1)
-  int16_t *chunk_min;   // per 16-token chunk: min depth_before
-  int16_t *tile_min;    // per tile
-  int16_t *super_min;   // per 64 tiles
-  int16_t *super2_min;  // per 64 supers
-  uint64_t *rec;        // 4 words per tile (look-back: tape words, depth)
+  int16_t *m1;          // tree level 1 (per 16 tokens)
+  int16_t *m2;          // tree level 2 (per 256 tokens)
+  int32_t *m3;          // tree level 3 (per 4096 tokens), encoded, zeroed by init
+  int16_t *mhi;         // tree levels 4..7, at offsets hi_off[0..3]
+  uint64_t hi_off[4];
   uint32_t *slow;       // slow-number token list (token, tape slot pairs)
   uint64_t *tape;       // >= 2 * cap + 3 words
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
@@ -55,7 +58,8 @@ struct Stage2Args {
 
 // words of look-back records / tree nodes needed for up to `cap` tokens
 struct Stage2Sizes {
-  uint64_t chunks, tiles, supers, supers2;
+  uint64_t chunks, tiles, n1, n2, n3, nhi;
+  uint64_t hi_off[4];
 };
 Stage2Sizes stage2_sizes(uint64_t cap_tokens);
 
