@@ -1,0 +1,182 @@
+"""CPU checks of the sm_100a kernels' per-thread algebra.
+
+The stage-1 block algebra (stage1_block.cuh), the string emission
+(strblock.cuh) and the number parser (numparse.cuh) are __host__ __device__
+code; these tests compile the very same headers with g++ (tests/cpu_*.cpp)
+and compare them with the oracle.  No GPU needed.
+"""
+import ctypes as C
+import os
+import random
+import struct
+import subprocess
+
+import pytest
+
+from tests.test_gpu_parity import _mutate, _rand_json
+from tests.vectors import SOUP_POOL
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BUILD = os.path.join(HERE, "_build")
+
+
+def _lib(name):
+    os.makedirs(BUILD, exist_ok=True)
+    src = os.path.join(HERE, name + ".cpp")
+    out = os.path.join(BUILD, "lib" + name + ".so")
+    deps = [src] + [os.path.join(HERE, "..", "paper_1902_08318_b200", "csrc", f)
+                    for f in os.listdir(os.path.join(HERE, "..", "paper_1902_08318_b200", "csrc"))]
+    if not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", src, "-o", out + ".tmp"])
+        os.replace(out + ".tmp", out)
+    return C.CDLL(out)
+
+
+@pytest.fixture(scope="module")
+def block_lib():
+    L = _lib("cpu_block_check")
+    L.jt_cpu_stage1.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint64), C.POINTER(C.c_longlong)]
+    return L
+
+
+@pytest.fixture(scope="module")
+def string_lib():
+    L = _lib("cpu_string_check")
+    L.jt_cpu_strings.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_longlong),
+                                 C.POINTER(C.c_int)]
+    return L
+
+
+@pytest.fixture(scope="module")
+def number_lib():
+    L = _lib("cpu_number_check")
+    L.jt_cpu_number.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
+    return L
+
+
+def _stage1(L, d):
+    out = (C.c_uint32 * (len(d) + 8))()
+    n, u = C.c_uint64(), C.c_longlong()
+    mism = L.jt_cpu_stage1(d, len(d), out, C.byref(n), C.byref(u))
+    return mism, bytes(out)[:4 * n.value], u.value
+
+
+def _inputs(rng, k):
+    for it in range(k):
+        n = rng.randrange(0, 700)
+        m = it % 4
+        if m == 0:
+            yield bytes(rng.choice(SOUP_POOL) for _ in range(n))
+        elif m == 1:
+            yield bytes(rng.choice([rng.randrange(256), rng.choice(SOUP_POOL), 0x80 + rng.randrange(64),
+                                    rng.choice(b"\xc3\xe0\xed\xf0\xf4\xa9\x9f\xa0")]) for _ in range(n))
+        elif m == 2:
+            yield "".join(rng.choice(["a", "é", "€", "𝄞", '"', "\\", "{", " "]) for _ in range(n // 2)).encode()
+        else:
+            d = _rand_json(rng).encode()
+            yield _mutate(rng, d) if rng.random() < 0.5 else d
+
+
+def test_stage1_block_algebra(block_lib, oracle):
+    rng = random.Random(5)
+    for d in _inputs(rng, 6000):
+        mism, idx, u = _stage1(block_lib, d)
+        assert mism == 0, d  # composed transfer functions == sequential carry
+        assert u == oracle.utf8_error_offset(d), d
+        if u < 0:
+            assert idx == oracle.stage1(d).index, d
+
+
+def test_utf8_exhaustive_three_bytes(block_lib, oracle):
+    # acceptance.cpp:105-154: every 1..3-byte input (sampled leads for length 3)
+    for a in range(256):
+        for b in range(256):
+            d = bytes([a, b])
+            assert _stage1(block_lib, d)[2] == oracle.utf8_error_offset(d)
+    rng = random.Random(9)
+    for _ in range(20000):
+        d = bytes([rng.choice(range(0xC0, 0x100)), rng.randrange(256), rng.randrange(256)])
+        assert _stage1(block_lib, d)[2] == oracle.utf8_error_offset(d)
+
+
+def test_string_emission(string_lib, oracle):
+    from tools.gen import generate
+    rng = random.Random(3)
+    docs = [generate(c, 1 << 15, seed=s) for c in (0, 1, 4) for s in (1, 2)]
+    docs += [generate(4, 1 << 12, seed=s, err=1 + s % 5) for s in range(100)]
+    docs += list(_inputs(rng, 1500))
+    for d in docs:
+        r = oracle.parse(d)
+        if r.code == 1:
+            continue
+        out = C.create_string_buffer(5 * len(d) + 128)
+        ol, n, se, ov = C.c_uint64(), C.c_uint64(), C.c_longlong(), C.c_int()
+        idx = (C.c_uint32 * (len(d) + 8))()
+        aux = (C.c_uint32 * (len(d) + 8))()
+        string_lib.jt_cpu_strings(d, len(d), out, C.byref(ol), idx, aux, C.byref(n), C.byref(se),
+                                  C.byref(ov))
+        assert ov.value == 0, d[:80]
+        if r.code == 0:
+            assert out.raw[:ol.value] == r.strings, d[:80]
+        if r.name == "STRING_ERROR":
+            assert se.value == r.offset, d[:80]
+
+
+def _rand_number(rng):
+    k = rng.randrange(8)
+    if k < 3:
+        s = ("-" if rng.random() < .5 else "") + str(rng.randrange(1, 10)) + \
+            "".join(str(rng.randrange(10)) for _ in range(rng.randrange(0, 18))) + "." + \
+            "".join(str(rng.randrange(10)) for _ in range(rng.randrange(1, 19))) + \
+            "e" + str(rng.randrange(-330, 320))
+    elif k < 5:
+        d = struct.unpack("<d", struct.pack("<Q", rng.getrandbits(64)))[0]
+        if d != d or d in (float("inf"), float("-inf")):
+            d = 1.5
+        s = "%.17g" % d
+        if "." not in s and "e" not in s:
+            s += ".0"
+    elif k < 6:
+        s = "".join(str(rng.randrange(10)) for _ in range(rng.randrange(1, 40))).lstrip("0") or "0"
+        s += "." + "".join(str(rng.randrange(10)) for _ in range(rng.randrange(1, 400)))
+    elif k < 7:
+        s = str(rng.randrange(-2 ** 64, 2 ** 64))
+    else:
+        s = rng.choice(["0.", "1e+", "-.5", "00", "1.5E+10", "1E-5", "-0e0", "1e1e", "0.0e-0",
+                        "5e-324", "2.4703282292062328e-324", "1.7976931348623159e308", "1e-400"])
+    return s.encode()
+
+
+def test_numbers_vs_strtod(number_lib, oracle):
+    # test_numbers.cpp:134-160 style (exact equality; the reference's own
+    # test only demands agreement with MPFR)
+    rng = random.Random(23)
+    for _ in range(60000):
+        t = _rand_number(rng)
+        ok, is_int, bits = oracle.number(t)
+        b, slow = C.c_uint64(), C.c_int()
+        k = number_lib.jt_cpu_number(t + b"\0" * 64, len(t), C.byref(b), C.byref(slow))
+        assert (k != 0) == ok, t
+        if ok:
+            assert (k == 1) == is_int and b.value == bits, t
+
+
+def test_glibc_subnormal_quirk(number_lib, oracle):
+    # (2724151024255084 + 3/4) * 2^-1074: correctly rounded is ...085, glibc
+    # strtod (the reference's slow_float) returns ...084; we match glibc.
+    from fractions import Fraction
+    x = (2724151024255084 + Fraction(3, 4)) * Fraction(2) ** -1074
+    num, den = x.numerator, x.denominator
+    ip, rem, frac = num // den, num % den, ""
+    while rem:
+        rem *= 10
+        frac += str(rem // den)
+        rem %= den
+    t = (str(ip) + "." + frac).encode()
+    ok, _, bits = oracle.number(t)
+    b, slow = C.c_uint64(), C.c_int()
+    number_lib.jt_cpu_number(t + b"\0" * 64, len(t), C.byref(b), C.byref(slow))
+    assert ok and bits == 2724151024255084 and b.value == bits
