@@ -450,13 +450,18 @@ size_t stage1_records(uint64_t len) {
   return (size_t)(ntiles == 0 ? 1 : ntiles);
 }
 
+cudaError_t stage1_configure() {
+  static const cudaError_t configured =
+      cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  return configured;
+}
+
 cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
   Stage1Args a = args_in;
   uint64_t ntiles = (a.len + kStage1Tile - 1) / kStage1Tile;
   if (ntiles == 0) ntiles = 1;
   a.ntiles = ntiles;
-  static const cudaError_t configured =
-      cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
   k_stage1<<<(unsigned)ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();

@@ -38,4 +38,7 @@ size_t stage1_records(uint64_t len);
 
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
 
+// one-time kernel attributes (dynamic shared memory); call outside capture
+cudaError_t stage1_configure();
+
 }  // namespace jt

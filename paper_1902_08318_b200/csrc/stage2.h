@@ -25,7 +25,7 @@ struct Ctrl {
   uint64_t S;                   // structural index count
   unsigned long long err_key;   // (token << 8) | code, min wins (~0 = none)
   uint32_t slow_count;          // numbers needing the exact fallback
-  uint32_t tree_done;           // blocks of the tree kernel finished
+  uint32_t num_count;           // number tokens queued for k_numbers
   uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
   uint64_t string_bytes;        // string buffer size (stage 1)
   unsigned long long str_err;   // min string error position (~0 = none)
@@ -50,6 +50,7 @@ struct Stage2Args {
   int16_t *mhi;         // tree levels 4..7, at offsets hi_off[0..3]
   uint64_t hi_off[4];
   uint32_t *slow;       // slow-number token list (token, tape slot pairs)
+  uint32_t *numlist;    // number tokens (compacted by k_scalars)
   uint64_t *tape;       // >= 2 * cap + 3 words
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
   uint64_t cap_tokens;  // capacity bound on S (for grid sizing)
