@@ -75,7 +75,7 @@ struct jt_parser {
   DevBuf aux[2];           // per index entry: string-buffer prefix
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
-  DevBuf tok, tape_idx, m1, m2, mhi, slow, numlist;  // m3 lives in s2rec (zeroed by init)
+  DevBuf tok, tape_idx, m1, m2, mhi, slow, numlist, scopebits;  // m3 lives in s2rec (zeroed by init)
   DevBuf tape, strings;
   DevBuf ctrl;
   jt::Ctrl *h_ctrl = nullptr;  // pinned
@@ -157,11 +157,12 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
 bool ensure_stage2(jt_parser *p, uint64_t len) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
-  bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 64) &&
+  bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 128 + (cap / 256 + 2) * 32) &&
             p->m1.ensure(z.n1 * sizeof(int16_t)) && p->m2.ensure(z.n2 * sizeof(int16_t)) &&
             p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
             p->slow.ensure((cap + 16) * 2 * sizeof(uint32_t)) &&
             p->numlist.ensure((cap + 16) * sizeof(uint32_t)) &&
+            p->scopebits.ensure((cap / 32 + 16) * sizeof(uint32_t)) &&
             p->tape.ensure((2 * cap + 8) * sizeof(uint64_t));
   return ok;
 }
@@ -205,6 +206,8 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   for (int k = 0; k < 4; k++) a.hi_off[k] = z.hi_off[k];
   a.slow = p->slow.as<uint32_t>();
   a.numlist = p->numlist.as<uint32_t>();
+  a.scopebits = p->scopebits.as<uint32_t>();
+  a.stk_rec = (uint64_t *)((uint8_t *)p->s2rec.p + ((z.n3 * sizeof(int32_t) + 64 + 63) & ~(size_t)63));
   a.tape = p->tape.as<uint64_t>();
   a.strings = p->strings.as<uint8_t>();
   a.cap_tokens = len + 16;
@@ -216,7 +219,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
 uint64_t buffers_sig(jt_parser *p, int which) {
   const void *ptrs[] = {p->in.p, p->idx[which].p, p->aux[which].p, p->s1rec.p, p->s2rec.p,
                         p->tok.p, p->tape_idx.p, p->m1.p, p->m2.p, p->mhi.p, p->slow.p,
-                        p->tape.p, p->strings.p, p->ctrl.p, p->numlist.p,
+                        p->tape.p, p->strings.p, p->ctrl.p, p->numlist.p, p->scopebits.p,
                         (const void *)p->h_ctrl};
   uint64_t h = 1469598103934665603ULL;
   for (const void *q : ptrs) h = (h ^ (uint64_t)(uintptr_t)q) * 1099511628211ULL;
@@ -267,7 +270,8 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
   if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   uint64_t s1w = jt::stage1_records(len) * 9;
-  uint64_t s2w = full ? z.n3 / 2 + 1 : 0;  // m3 (int32) words
+  // m3 (int32) + k_scalars look-back records, zeroed together
+  uint64_t s2w = full ? ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4 : 0;
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                   p->s2rec.as<uint64_t>(), s2w, p->stream),
                "init"))
@@ -474,7 +478,8 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   p->launches = 0;
   if (!cuda_ok(p, jt::init_launch(nullptr, p->s1rec.as<uint64_t>(), 0, p->s2rec.as<uint64_t>(),
-                                  z.n3 / 2 + 1, p->stream),
+                                  ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4,
+                                  p->stream),
                "init")) {
     set_off(error_offset, -1);
     return JT_CAPACITY;

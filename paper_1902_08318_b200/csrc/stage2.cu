@@ -83,6 +83,224 @@ __device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v <
 
 // ---- K2: scalars, one thread per token ---------------------------------
 
+// Stack of container kinds as a 64-bit shift register: bit 0 = innermost
+// open container (1 = object).  A token range acts on it as "pop k, then
+// push m kinds P" (P bit 0 = last push); these transfers compose without
+// knowing the absolute depth, so a scan gives every token the kind of its
+// enclosing container.  Exact while the document's depth stays <= 64.
+struct StackT {
+  uint64_t P;
+  uint32_t k, m;
+};
+
+__device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t n) { return n >= 64 ? 0 : x << n; }
+__device__ __forceinline__ uint64_t shr64(uint64_t x, uint32_t n) { return n >= 64 ? 0 : x >> n; }
+
+// t2 after t1
+__device__ __forceinline__ StackT stack_compose(const StackT &t2, const StackT &t1) {
+  StackT r;
+  if (t2.k <= t1.m) {
+    r.k = t1.k;
+    r.m = t1.m - t2.k + t2.m;
+    r.P = shl64(shr64(t1.P, t2.k), t2.m) | t2.P;
+  } else {
+    r.k = t1.k + t2.k - t1.m;
+    r.m = t2.m;
+    r.P = t2.P;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t stack_apply(const StackT &t, uint64_t S) {
+  return shl64(shr64(S, t.k), t.m) | t.P;
+}
+
+constexpr uint64_t kV = 1ULL << 63;
+
+__device__ __forceinline__ void stk_publish_agg(uint64_t *rec, uint64_t tile, const StackT &t) {
+  lb_store(rec + 4 * tile, kV | (t.P & 0xFFFFFFFFULL) | ((uint64_t)(t.k & 0x7FFFFFFF) << 32));
+  lb_store(rec + 4 * tile + 1, kV | (t.P >> 32) | ((uint64_t)t.m << 32));
+}
+
+__device__ __forceinline__ void stk_publish_incl(uint64_t *rec, uint64_t tile, uint64_t S) {
+  lb_store(rec + 4 * tile + 2, kV | (S & 0xFFFFFFFFULL));
+  lb_store(rec + 4 * tile + 3, kV | (S >> 32));
+}
+
+// 2 = inclusive (S), 1 = aggregate (t), 0 = not ready
+__device__ __forceinline__ int stk_read(const uint64_t *rec, int64_t tile, StackT &t, uint64_t &S) {
+  uint64_t x = lb_load(rec + 4 * tile + 2), y = lb_load(rec + 4 * tile + 3);
+  if ((x & y) >> 63) {
+    S = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
+    return 2;
+  }
+  x = lb_load(rec + 4 * tile), y = lb_load(rec + 4 * tile + 1);
+  if ((x & y) >> 63) {
+    t.P = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
+    t.k = (uint32_t)((x >> 32) & 0x7FFFFFFF);
+    t.m = (uint32_t)((y >> 32) & 0x7FFFFFFF);
+    return 1;
+  }
+  return 0;
+}
+
+// incoming stack register of tile `tile` > 0 (one full warp); each lane
+// reads kLbPer predecessors per round (lookback.cuh)
+__device__ uint64_t stk_lookback(const uint64_t *rec, int64_t tile) {
+  const int lane = threadIdx.x & 31;
+  StackT G{0, 0, 0};
+  int64_t base = tile - 1;
+  for (;;) {
+    StackT t[kLbPer];
+    uint64_t Sv[kLbPer];
+    int st[kLbPer];
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {
+      int64_t pred = base - (int64_t)kLbPer * lane - j;
+      t[j] = StackT{0, 0, 0};
+      Sv[j] = 0;
+      st[j] = 2;
+      if (pred >= 0)
+        while ((st[j] = stk_read(rec, pred, t[j], Sv[j])) == 0) __nanosleep(32);
+    }
+    // per lane, farthest to nearest: resolved stack or composed transfer
+    StackT fn{0, 0, 0};
+    uint64_t sv = 0;
+    bool resolved = false;
+#pragma unroll
+    for (int j = kLbPer - 1; j >= 0; --j) {
+      if (st[j] == 2) {
+        resolved = true;
+        sv = Sv[j];
+        fn = StackT{0, 0, 0};
+      } else if (resolved) {
+        sv = stack_apply(t[j], sv);
+      } else {
+        fn = stack_compose(t[j], fn);
+      }
+    }
+    uint32_t incl = __ballot_sync(0xffffffffu, resolved);
+    if (incl) {
+      int kk = __ffs(incl) - 1;
+      uint64_t s0 = __shfl_sync(0xffffffffu, sv, kk);
+      for (int l = kk - 1; l >= 0; --l) {
+        StackT u;
+        u.P = __shfl_sync(0xffffffffu, fn.P, l);
+        u.k = __shfl_sync(0xffffffffu, fn.k, l);
+        u.m = __shfl_sync(0xffffffffu, fn.m, l);
+        s0 = stack_apply(u, s0);
+      }
+      return stack_apply(G, s0);
+    }
+    StackT H{0, 0, 0};
+    for (int l = 31; l >= 0; --l) {
+      StackT u;
+      u.P = __shfl_sync(0xffffffffu, fn.P, l);
+      u.k = __shfl_sync(0xffffffffu, fn.k, l);
+      u.m = __shfl_sync(0xffffffffu, fn.m, l);
+      H = stack_compose(u, H);
+    }
+    G = stack_compose(G, H);
+    base -= 32 * kLbPer;
+  }
+}
+
+// ---- K2K: container-kind stack scan -----------------------------------------
+// 4096 tokens per CTA (16 per thread); per token the kind of its innermost
+// open container (scopebits, 16 bits per thread) and the max depth.
+constexpr int kStkTok = 16;
+
+__global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
+  __shared__ uint32_t s_tile;
+  __shared__ StackT s_wt[8];
+  __shared__ uint64_t s_wS[8];
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint64_t S = ctrl->S;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->stk_tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    __syncthreads();
+    if (tile >= ntiles) return;
+    const uint64_t i0 = (tile * 256 + threadIdx.x) * kStkTok;
+    uint32_t recs[kStkTok];
+    if (i0 + kStkTok <= S) {
+      const uint4 *rp = (const uint4 *)(a.tok + i0);
+#pragma unroll
+      for (int q = 0; q < kStkTok / 4; q++) {
+        uint4 r = rp[q];
+        recs[4 * q] = r.x, recs[4 * q + 1] = r.y, recs[4 * q + 2] = r.z, recs[4 * q + 3] = r.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kStkTok; k++) recs[k] = i0 + k < S ? a.tok[i0 + k] : (uint32_t)' ';
+    }
+    // thread transfer over its 16 tokens (scope bits need the incoming stack)
+    StackT tt{0, 0, 0};
+    int dmax = 0;
+#pragma unroll
+    for (int k = 0; k < kStkTok; k++) {
+      const uint32_t c = recs[k] & 0xFF;
+      if (c == '{' || c == '[') {
+        tt = stack_compose(StackT{c == '{' ? 1ULL : 0ULL, 0, 1}, tt);
+        dmax = max(dmax, (int)(int16_t)(recs[k] >> 16) + 1);
+      } else if (c == '}' || c == ']') {
+        tt = stack_compose(StackT{0, 1, 0}, tt);
+      }
+    }
+    StackT inc = tt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      StackT o;
+      o.P = __shfl_up_sync(0xffffffffu, inc.P, d);
+      o.k = __shfl_up_sync(0xffffffffu, inc.k, d);
+      o.m = __shfl_up_sync(0xffffffffu, inc.m, d);
+      if (lane >= d) inc = stack_compose(inc, o);
+    }
+    StackT ex;
+    ex.P = __shfl_up_sync(0xffffffffu, inc.P, 1);
+    ex.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
+    ex.m = __shfl_up_sync(0xffffffffu, inc.m, 1);
+    if (lane == 0) ex = StackT{0, 0, 0};
+    if (lane == 31) s_wt[warp] = inc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax);
+    __syncthreads();
+    if (warp == 0) {
+      StackT agg = s_wt[0];
+      for (int k = 1; k < 8; k++) agg = stack_compose(s_wt[k], agg);
+      uint64_t S0 = 0;
+      if (tile > 0) {
+        if (lane == 0) stk_publish_agg(a.stk_rec, tile, agg);
+        S0 = stk_lookback(a.stk_rec, (int64_t)tile);
+      }
+      if (lane == 0) {
+        stk_publish_incl(a.stk_rec, tile, stack_apply(agg, S0));
+        uint64_t sw = S0;
+        for (int k = 0; k < 8; k++) {
+          s_wS[k] = sw;
+          sw = stack_apply(s_wt[k], sw);
+        }
+      }
+    }
+    __syncthreads();
+    uint64_t St = stack_apply(ex, s_wS[warp]);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < kStkTok; k++) {
+      const uint32_t c = recs[k] & 0xFF;
+      bits |= (uint32_t)(St & 1) << k;
+      if (c == '{' || c == '[') St = (St << 1) | (c == '{' ? 1ULL : 0ULL);
+      else if (c == '}' || c == ']') St >>= 1;
+    }
+    if (i0 < S) ((uint16_t *)a.scopebits)[i0 / kStkTok] = (uint16_t)bits;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   __shared__ int s_wmin[8];
   Ctrl *ctrl = a.ctrl;
@@ -317,6 +535,12 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const uint64_t nchunks = (S + kStructTok - 1) / kStructTok;
+  const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_scalars)
+  auto scope_obj = [&](int64_t j) -> bool {  // innermost container of token j is an object
+    if (shallow) return (a.scopebits[j >> 5] >> (j & 31)) & 1;  // 16-bit words, same bit order
+    int64_t o = psv(a, j, tok_depth(a.tok[j]) - 1);
+    return o >= 0 && (a.tok[o] & 0xFF) == '{';
+  };
   for (uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; chunk < nchunks;
        chunk += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i0 = chunk * kStructTok;
@@ -344,8 +568,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
       else if (c1 == '[') mode = M_AF;
       else if (c1 == ':') mode = M_V;
       else if (c1 == ',') {
-        int64_t j = psv(a, (int64_t)i0 - 1, tok_depth(v1) - 1);
-        mode = (j >= 0 && (a.tok[j] & 0xFF) == '{') ? M_K : M_V;
+        mode = scope_obj((int64_t)i0 - 1) ? M_K : M_V;
       } else if (c1 == '"') {
         mode = M_A;
         if (i0 >= 2) {
@@ -353,8 +576,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
           uint32_t c2 = v2 & 0xFF;
           if (c2 == '{') mode = M_C;
           else if (c2 == ',') {
-            int64_t j = psv(a, (int64_t)i0 - 2, tok_depth(v2) - 1);
-            if (j >= 0 && (a.tok[j] & 0xFF) == '{') mode = M_C;
+            if (scope_obj((int64_t)i0 - 2)) mode = M_C;
           }
         }
       } else {
@@ -438,6 +660,8 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
               top_local = true;
               top_tape = stk[sp - 1] & 0x7FFFFFFFu;
               top_obj = stk[sp - 1] >> 31;
+            } else if (shallow && c == ',') {
+              top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
             } else {
               if (far_level != D - 1) {
                 int64_t j = psv(a, (int64_t)i, D - 1);
@@ -585,6 +809,11 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   uint64_t g = (a.cap_tokens + 255) / 256;
   unsigned g2 = (unsigned)(g < (uint64_t)sms * 16 ? g : (uint64_t)sms * 16);
   if (g2 < 1) g2 = 1;
+  {
+    uint64_t nst = (a.cap_tokens + 4095) / 4096;
+    unsigned gs = (unsigned)(nst < (uint64_t)sms * 4 ? nst : (uint64_t)sms * 4);
+    k_stack<<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
+  }
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[0], stream);
@@ -600,7 +829,7 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[4], stream);
-  *launches = 6;
+  *launches = 7;
   return cudaGetLastError();
 }
 

@@ -26,6 +26,8 @@ struct Ctrl {
   unsigned long long err_key;   // (token << 8) | code, min wins (~0 = none)
   uint32_t slow_count;          // numbers needing the exact fallback
   uint32_t num_count;           // number tokens queued for k_numbers
+  int32_t max_depth;            // max depth_after over all tokens (clamped)
+  uint32_t stk_tile_counter;    // k_stack tile claims
   uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
   uint64_t string_bytes;        // string buffer size (stage 1)
   unsigned long long str_err;   // min string error position (~0 = none)
@@ -51,6 +53,8 @@ struct Stage2Args {
   uint64_t hi_off[4];
   uint32_t *slow;       // slow-number token list (token, tape slot pairs)
   uint32_t *numlist;    // number tokens (compacted by k_scalars)
+  uint32_t *scopebits;  // bit i: innermost container of token i is an object
+  uint64_t *stk_rec;    // k_scalars look-back records (4 words per 256 tokens), zeroed
   uint64_t *tape;       // >= 2 * cap + 3 words
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
   uint64_t cap_tokens;  // capacity bound on S (for grid sizing)
