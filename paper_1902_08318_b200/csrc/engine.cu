@@ -75,7 +75,7 @@ struct jt_parser {
   DevBuf aux[2];           // per index entry: string-buffer prefix
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
-  DevBuf tok, tape_idx, m1, m2, mhi, slow, numlist, scopebits;  // m3 lives in s2rec (zeroed by init)
+  DevBuf tok, tape_idx, m1, m2, mhi, slow, numlist, scopebits, tile_flags;  // m3 lives in s2rec (zeroed by init)
   DevBuf tape, strings;
   DevBuf ctrl;
   jt::Ctrl *h_ctrl = nullptr;  // pinned
@@ -149,6 +149,7 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
   if (!p->strings.ensure((size_t)len + 4 * cap_tok + 128)) return false;
   if (!p->tok.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
   if (!p->tape_idx.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->tile_flags.ensure(jt::stage1_records(len) * sizeof(uint32_t) + 64)) return false;
   if (!p->s1rec.ensure(jt::stage1_records(len) * 9 * sizeof(uint64_t) + 64)) return false;
   if (!p->ctrl.ensure(sizeof(jt::Ctrl))) return false;
   return true;
@@ -177,6 +178,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.strings = p->strings.as<uint8_t>();
   a.tokrec = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
+  a.tile_flags = p->tile_flags.as<uint32_t>();
   uint64_t nt = jt::stage1_records(len);
   a.rec_state = p->s1rec.as<uint64_t>();
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
@@ -198,6 +200,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.ctrl = p->ctrl.as<jt::Ctrl>();
   a.tok = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
+  a.tile_flags = p->tile_flags.as<uint32_t>();
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   a.m1 = p->m1.as<int16_t>();
   a.m2 = p->m2.as<int16_t>();
@@ -220,6 +223,7 @@ uint64_t buffers_sig(jt_parser *p, int which) {
   const void *ptrs[] = {p->in.p, p->idx[which].p, p->aux[which].p, p->s1rec.p, p->s2rec.p,
                         p->tok.p, p->tape_idx.p, p->m1.p, p->m2.p, p->mhi.p, p->slow.p,
                         p->tape.p, p->strings.p, p->ctrl.p, p->numlist.p, p->scopebits.p,
+                        p->tile_flags.p,
                         (const void *)p->h_ctrl};
   uint64_t h = 1469598103934665603ULL;
   for (const void *q : ptrs) h = (h ^ (uint64_t)(uintptr_t)q) * 1099511628211ULL;

@@ -118,11 +118,19 @@ struct GlobalAt {
 constexpr int kSmemIn = kStage1Tile;            // tile input bytes
 constexpr int kSmemIdx = kStageIdx * 2;         // u16 positions
 constexpr int kSmemAux = kStageIdx * 2;         // u16 string offsets
-constexpr int kSmemC = kStageIdx;               // u8 token bytes
-constexpr int kSmemT = kStageIdx * 2;           // u16 tile-relative tape index
-constexpr int kSmemD = kStageIdx * 2;           // i16 tile-relative depth
+// per-block record for the copy-out: masks of the block's tokens and the
+// block's tile-relative offsets (index entries get their string offset, tape
+// index and depth from popcounts below their bit)
+struct BlockRec {
+  uint64_t content, openq, w1, w2, op, cl;
+  uint32_t soff, toff;
+  int32_t doff;
+  uint32_t fast;
+};
+constexpr int kSmemBlk = kThreads * (int)sizeof(BlockRec);
 constexpr int kSmemPay = kStagePay;             // payload bytes (last: word over-read)
-constexpr int kOffPay = kSmemIn + kSmemIdx + kSmemAux + kSmemC + kSmemT + kSmemD;
+constexpr int kOffBlk = kSmemIn + kSmemIdx + kSmemAux;
+constexpr int kOffPay = kOffBlk + kSmemBlk;
 constexpr int kSmemBytes = kOffPay + kSmemPay + 16;
 
 __device__ __forceinline__ int tok_width(uint32_t c) {  // tape words per token
@@ -152,9 +160,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   uint8_t *s_in = smem;
   uint16_t *s_idx = (uint16_t *)(smem + kSmemIn);
   uint16_t *s_aux = (uint16_t *)(smem + kSmemIn + kSmemIdx);
-  uint8_t *s_c = smem + kSmemIn + kSmemIdx + kSmemAux;
-  uint16_t *s_trel = (uint16_t *)(smem + kSmemIn + kSmemIdx + kSmemAux + kSmemC);
-  int16_t *s_drel = (int16_t *)(smem + kSmemIn + kSmemIdx + kSmemAux + kSmemC + kSmemT);
+  BlockRec *s_blk = (BlockRec *)(smem + kOffBlk);
   uint8_t *s_pay = smem + kOffPay;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -251,18 +257,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     fin = (st1 | pseudo) & ~(uq & ~instr) & valid;
   }
   const uint32_t cnt = popc64(fin);
-  // tape words and depth change of the block's tokens (A.4 widths / +-1)
-  uint32_t tw = 0;
-  int td = 0;
-  {
-    uint64_t fm = fin;
-    while (fm) {
-      uint32_t c = s_in[local + ctz64(fm)];
-      tw += (uint32_t)tok_width(c);
-      td += tok_delta(c);
-      fm &= fm - 1;
-    }
-  }
+  // token widths (A.4: 0 for , :  2 for numbers, else 1) and depth changes
+  // as masks, so every sum below is a popcount
+  const uint64_t w1m = fin & ~m.cc, w2m = fin & m.num;
+  const uint64_t opm = fin & m.open, clm = fin & m.close;
+  const uint32_t tw = popc64(w1m) + popc64(w2m);
+  const int td = popc64(opm) - popc64(clm);
 
   // strings in this block
   const uint64_t openq = uq & instr & valid;
@@ -293,11 +293,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     uint64_t rel = local + k;
     return rel < (uint64_t)kStage1Tile ? (uint32_t)s_in[rel] : (uint32_t)a.in[tile_base + rel];
   };
-  uint64_t serr = ~0ULL;
-  const uint32_t sw = sb::block_strings<false>(tbyte, blk, content, openq, E, ctl, fin, ov_in, &serr,
-                                               [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
-                                               [](int, uint32_t) {});
-  if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
+  const bool fast = ((E | ctl) == 0) && ov_in == 0;
+  uint32_t sw;
+  if (fast) {
+    sw = 4u * popc64(openq) + popc64(content);
+  } else {
+    uint64_t serr = ~0ULL;
+    sw = sb::block_strings<false>(tbyte, blk, content, openq, E, ctl, fin, ov_in, &serr,
+                                  [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
+                                  [](int, uint32_t) {});
+    if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
+  }
   uint32_t si = sw;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -364,7 +370,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
     }
   }
-  // stage positions + string offsets; spill to global when the tile is large
+  s_blk[threadIdx.x] = BlockRec{content, openq, w1m, w2m, opm, clm, soff, toff, doff, fast ? 1u : 0u};
+  // stage positions (+ string offsets of slow blocks) and the string
+  // payload; spill to global when the tile is larger than the staging
   const bool idx_direct = total > (uint32_t)kStageIdx;
   const bool pay_direct = stotal > (uint32_t)kStagePay;
   if (idx_direct || pay_direct) __syncthreads();  // s_base/s_sbase needed now
@@ -372,45 +380,76 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint64_t gsbase = (idx_direct || pay_direct) ? s_sbase : 0;
   const uint64_t gtbase = idx_direct ? s_tbase : 0;
   const long long gdbase = idx_direct ? s_dbase : 0;
-  uint32_t slot = off, trun = toff;
-  int drun = doff;
-  uint64_t e2 = ~0ULL;
-  sb::block_strings<true>(
-      tbyte, blk, content, openq, E, ctl, fin, ov_in, &e2,
-      [&](int a0, uint32_t wdst, int n) {
-        if (pay_direct) {
-          for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
-        } else {
-          smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
-        }
-      },
-      [&](uint32_t pos, uint8_t b) {
-        if (pay_direct) a.strings[gsbase + soff + pos] = b;
-        else s_pay[soff + pos] = b;
-      },
-      [&](int p, uint32_t wb) {
-        const uint32_t c = s_in[local + p];
-        if (idx_direct) {
-          a.idx[gbase + slot] = (uint32_t)(tile_base + local + p);
-          a.aux[gbase + slot] = (uint32_t)(gsbase + soff + wb);
-          a.tokrec[gbase + slot] = c | ((uint32_t)(uint16_t)clamp16(gdbase + drun) << 16);
-          a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + trun);
-        } else {
-          s_idx[slot] = (uint16_t)(local + p);
-          s_aux[slot] = (uint16_t)(soff + wb);
-          s_c[slot] = (uint8_t)c;
-          s_trel[slot] = (uint16_t)trun;
-          s_drel[slot] = (int16_t)drun;
-        }
-        trun += (uint32_t)tok_width(c);
-        drun += tok_delta(c);
-        slot++;
-      });
+  auto direct_entry = [&](uint32_t slot, int p, uint32_t wb) {
+    const uint64_t below = sb::low_bits(p);
+    const uint32_t c = s_in[local + p];
+    const uint32_t t = toff + popc64(w1m & below) + popc64(w2m & below);
+    const long long d = gdbase + doff + popc64(opm & below) - popc64(clm & below);
+    a.idx[gbase + slot] = (uint32_t)(tile_base + local + p);
+    a.aux[gbase + slot] = (uint32_t)(gsbase + soff + wb);
+    a.tokrec[gbase + slot] = c | ((uint32_t)(uint16_t)clamp16(d) << 16);
+    a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + t);
+  };
+  if (fast) {
+    uint64_t cm = content;
+    while (cm) {  // string runs, 4-byte gaps before each run opened here
+      const int a0 = ctz64(cm);
+      const uint64_t sh = cm >> a0;
+      const int n = ~sh == 0 ? 64 - a0 : ctz64(~sh);
+      const uint64_t below = sb::low_bits(a0);
+      const uint32_t wdst = 4u * popc64(openq & below) + popc64(content & below);
+      if (pay_direct) {
+        for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
+      } else {
+        smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
+      }
+      cm &= ~(sb::low_bits(n) << a0);
+    }
+    uint64_t fm = fin;
+    uint32_t slot = off;
+    while (fm) {
+      const int p = ctz64(fm);
+      fm &= fm - 1;
+      if (idx_direct) {
+        const uint64_t below = sb::low_bits(p);
+        direct_entry(slot, p, 4u * popc64(openq & below) + popc64(content & below));
+      } else {
+        s_idx[slot] = (uint16_t)(local + p);
+      }
+      slot++;
+    }
+  } else {
+    uint32_t slot = off;
+    uint64_t e2 = ~0ULL;
+    sb::block_strings<true>(
+        tbyte, blk, content, openq, E, ctl, fin, ov_in, &e2,
+        [&](int a0, uint32_t wdst, int n) {
+          if (pay_direct) {
+            for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
+          } else {
+            smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
+          }
+        },
+        [&](uint32_t pos, uint8_t b) {
+          if (pay_direct) a.strings[gsbase + soff + pos] = b;
+          else s_pay[soff + pos] = b;
+        },
+        [&](int p, uint32_t wb) {
+          if (idx_direct) {
+            direct_entry(slot, p, wb);
+          } else {
+            s_idx[slot] = (uint16_t)(local + p);
+            s_aux[slot] = (uint16_t)(soff + wb);
+          }
+          slot++;
+        });
+  }
   __syncthreads();
 
   const uint32_t tb = (uint32_t)tile_base;
   const uint64_t gb2 = s_base, gsb2 = s_sbase;  // published before the last barrier
   if (!idx_direct) {
+    // one thread per index entry: offsets from the block record's masks
     uint32_t *dst = a.idx + gb2;
     uint32_t *dax = a.aux + gb2;
     uint32_t *drc = a.tokrec + gb2;
@@ -419,12 +458,37 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     const uint32_t tb32 = (uint32_t)(1 + s_tbase);
     const long long db = s_dbase;
     for (uint32_t k = threadIdx.x; k < total; k += kThreads) {
-      dst[k] = tb + s_idx[k];
-      dax[k] = sb32 + s_aux[k];
-      drc[k] = (uint32_t)s_c[k] | ((uint32_t)(uint16_t)clamp16(db + s_drel[k]) << 16);
-      dtp[k] = tb32 + s_trel[k];
+      const uint32_t pos = s_idx[k];
+      const BlockRec &r = s_blk[pos >> 6];
+      const uint64_t below = sb::low_bits((int)(pos & 63));
+      const uint32_t aux = r.fast ? r.soff + 4u * popc64(r.openq & below) + popc64(r.content & below)
+                                  : (uint32_t)s_aux[k];
+      const uint32_t t = r.toff + popc64(r.w1 & below) + popc64(r.w2 & below);
+      const int d = r.doff + popc64(r.op & below) - popc64(r.cl & below);
+      const uint32_t c = s_in[pos];
+      dst[k] = tb + pos;
+      dax[k] = sb32 + aux;
+      drc[k] = c | ((uint32_t)(uint16_t)clamp16(db + d) << 16);
+      dtp[k] = tb32 + t;
+      if (c == '"' && k + 1 < total && !pay_direct) {
+        // string length = next entry's string offset - this one - 4 (the
+        // string buffer is contiguous in token order); the last entry of a
+        // tile is left to k_scalars
+        const uint32_t p2 = s_idx[k + 1];
+        const BlockRec &r2 = s_blk[p2 >> 6];
+        const uint64_t b2 = sb::low_bits((int)(p2 & 63));
+        const uint32_t aux2 = r2.fast ? r2.soff + 4u * popc64(r2.openq & b2) + popc64(r2.content & b2)
+                                      : (uint32_t)s_aux[k + 1];
+        const uint32_t len = aux2 - aux - 4;
+        s_pay[aux] = (uint8_t)len;
+        s_pay[aux + 1] = (uint8_t)(len >> 8);
+        s_pay[aux + 2] = (uint8_t)(len >> 16);
+        s_pay[aux + 3] = (uint8_t)(len >> 24);
+      }
     }
   }
+  if (threadIdx.x == 0) a.tile_flags[tile] = (idx_direct || pay_direct) ? 1u : 0u;
+  __syncthreads();  // length fields staged before the payload copy-out
   if (!pay_direct && stotal) {
     uint8_t *dst = a.strings + gsb2;
     const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3) < stotal

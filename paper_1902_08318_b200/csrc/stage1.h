@@ -22,6 +22,7 @@ struct Stage1Args {
   uint8_t *strings;    // string buffer (payload; length fields left to stage 2)
   uint32_t *tokrec;    // per index entry: byte | clamped depth_before << 16
   uint32_t *tape_idx;  // per index entry: tape word index
+  uint32_t *tile_flags; // per tile: 1 = string lengths left to stage 2 (spill mode)
   uint64_t *rec_state; // ntiles look-back records, zeroed
   uint64_t *rec_count; // 8 * ntiles look-back words (count, strings, tape, depth), zeroed
   uint32_t *tile_counter;         // zeroed

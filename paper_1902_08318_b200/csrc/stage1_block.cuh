@@ -65,6 +65,9 @@ JT_HD void transpose32(const uint32_t w[8], uint32_t p[8]) {
 
 struct Masks {
   uint64_t bs, qt, st, ws;  // backslash, quote, structural, whitespace
+  uint64_t open, close;     // { [   and   } ]
+  uint64_t cc;              // , :
+  uint64_t num;             // - and digits (number token starts)
   uint64_t P[8];            // bit planes (kept for the UTF-8 check)
 };
 
@@ -93,6 +96,11 @@ JT_HD void classify64(const uint32_t w[16], Masks &m) {
   uint64_t comma = hi001 & n4 & P[3] & P[2] & n1 & n0;
   uint64_t colon = hi001 & P[4] & P[3] & n2 & P[1] & n0;
   m.st = brackets | comma | colon;
+  m.open = brackets & P[1];   // low nibble 1011
+  m.close = brackets & P[2];  // low nibble 1101
+  m.cc = comma | colon;
+  // '-' = 0010 1101, '0'..'9' = 0011 0000..1001
+  m.num = (hi001 & n4 & P[3] & P[2] & n1 & P[0]) | (n7 & n6 & P[5] & P[4] & (n3 | (n2 & n1)));
   // 0x20 = 0010 0000 ; 0x09 0x0A 0x0D = 0000 1001 / 1010 / 1101
   uint64_t hi000 = n7 & n6 & n4;
   uint64_t space = hi000 & P[5] & n3 & n2 & n1 & n0;

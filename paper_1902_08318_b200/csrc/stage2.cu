@@ -331,13 +331,17 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
         fail = str_err >= p && str_err < end;  // the failing string holds the minimum
         if (!fail) {
           const uint32_t so = a.aux[i];
-          const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
-          const uint32_t len = nx - so - 4;
-          uint8_t *f = a.strings + so;
-          f[0] = (uint8_t)len;
-          f[1] = (uint8_t)(len >> 8);
-          f[2] = (uint8_t)(len >> 16);
-          f[3] = (uint8_t)(len >> 24);
+          // stage 1 wrote the length unless the next token is in another
+          // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
+          if (end > a.len || (p >> 14) != ((uint32_t)end >> 14) || a.tile_flags[p >> 14]) {
+            const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
+            const uint32_t len = nx - so - 4;
+            uint8_t *f = a.strings + so;
+            f[0] = (uint8_t)len;
+            f[1] = (uint8_t)(len >> 8);
+            f[2] = (uint8_t)(len >> 16);
+            f[3] = (uint8_t)(len >> 24);
+          }
           a.tape[a.tape_idx[i]] = tape_word('"', so);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
@@ -530,39 +534,104 @@ __device__ __forceinline__ void report(Ctrl *ctrl, uint64_t tokn, int code) {
   atomicMin(&ctrl->err_key, ((unsigned long long)tokn << 8) | (unsigned)code);
 }
 
-__global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
+// K3 works on 4096-token tiles: token records plus a 3-level min-depth tree
+// (16 / 256 / 4096) in shared memory, so the enclosing-container search
+// (psv) only leaves the tile when the container opened before it.
+constexpr int kK3Tok = 16;
+constexpr int kK3Tile = 256 * kK3Tok;
+
+struct TileTree {
+  const uint32_t *tok;  // shared: 4096 records
+  const int16_t *l1;    // shared: 256 group minima
+  const int16_t *l2;    // shared: 16 group minima
+  int64_t base;
+};
+
+// nearest j < i (j >= tile base) with depth_before <= L inside the tile, or
+// the global search below the tile
+__device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, int L) {
+  const int64_t x = i - 1 - T.base;
+  if (x >= 0) {
+    const int g = (int)(x >> 4);
+    for (int k = (int)(x & 15); k >= 0; --k)
+      if (tok_depth(T.tok[g * 16 + k]) <= L) return T.base + g * 16 + k;
+    int hit = -1;
+    const int G = g >> 4;
+    for (int h = g - 1; h >= G * 16; --h)
+      if (T.l1[h] <= L) {
+        hit = h;
+        break;
+      }
+    if (hit < 0) {
+      for (int H = G - 1; H >= 0 && hit < 0; --H)
+        if (T.l2[H] <= L)
+          for (int h = H * 16 + 15; h >= H * 16; --h)
+            if (T.l1[h] <= L) {
+              hit = h;
+              break;
+            }
+    }
+    if (hit >= 0)
+      for (int k = 15; k >= 0; --k)
+        if (tok_depth(T.tok[hit * 16 + k]) <= L) return T.base + hit * 16 + k;
+  }
+  return psv(a, T.base, L);
+}
+
+__global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
+  __shared__ __align__(16) uint32_t s_tok[kK3Tile];
+  __shared__ int16_t s_l1[256];
+  __shared__ int16_t s_l2[16];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
-  const uint64_t nchunks = (S + kStructTok - 1) / kStructTok;
-  const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_scalars)
+  const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
+  const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
   auto scope_obj = [&](int64_t j) -> bool {  // innermost container of token j is an object
     if (shallow) return (a.scopebits[j >> 5] >> (j & 31)) & 1;  // 16-bit words, same bit order
     int64_t o = psv(a, j, tok_depth(a.tok[j]) - 1);
     return o >= 0 && (a.tok[o] & 0xFF) == '{';
   };
-  for (uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; chunk < nchunks;
-       chunk += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = chunk * kStructTok;
-    const uint64_t i1 = min(i0 + kStructTok, S);
-    uint32_t recs[kStructTok];
-    if (i1 - i0 == kStructTok) {
-      const uint4 *rp = (const uint4 *)(a.tok + i0);
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t tbase = tile * kK3Tile;
+    {
+      const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
+      uint4 *d = (uint4 *)(s_tok + threadIdx.x * kK3Tok);
+      int m = 0x7FFF;
+      if (i0 + kK3Tok <= S) {
+        const uint4 *rp = (const uint4 *)(a.tok + i0);
 #pragma unroll
-      for (int q = 0; q < kStructTok / 4; q++) {
-        uint4 r = rp[q];
-        recs[4 * q] = r.x, recs[4 * q + 1] = r.y, recs[4 * q + 2] = r.z, recs[4 * q + 3] = r.w;
+        for (int q = 0; q < kK3Tok / 4; q++) {
+          uint4 r = rp[q];
+          d[q] = r;
+          m = min(m, min(min(tok_depth(r.x), tok_depth(r.y)), min(tok_depth(r.z), tok_depth(r.w))));
+        }
+      } else {
+        for (int k = 0; k < kK3Tok; k++) {
+          uint32_t r = i0 + k < S ? a.tok[i0 + k] : 0x7FFF0000u;
+          s_tok[threadIdx.x * kK3Tok + k] = r;
+          m = min(m, tok_depth(r));
+        }
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kStructTok; k++) recs[k] = i0 + k < i1 ? a.tok[i0 + k] : 0u;
+      s_l1[threadIdx.x] = (int16_t)m;
     }
+    __syncthreads();
+    if (threadIdx.x < 16) {
+      int m = 0x7FFF;
+      for (int k = 0; k < 16; k++) m = min(m, (int)s_l1[threadIdx.x * 16 + k]);
+      s_l2[threadIdx.x] = (int16_t)m;
+    }
+    __syncthreads();
+    const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase};
+    const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
+    const uint64_t i1 = min(i0 + kK3Tok, S);
+    if (i0 < S) do {
+    const uint32_t *recs = s_tok + threadIdx.x * kK3Tok;
     uint32_t t = a.tape_idx[i0];
-
     // entry state from the two previous tokens (A.5 arrival rules)
     int mode = M_V;
     if (i0 > 0) {
-      uint32_t v1 = a.tok[i0 - 1];
+      uint32_t v1 = i0 - 1 >= tbase ? s_tok[i0 - 1 - tbase] : a.tok[i0 - 1];
       uint32_t c1 = v1 & 0xFF;
       if (c1 == '{') mode = M_OF;
       else if (c1 == '[') mode = M_AF;
@@ -572,7 +641,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
       } else if (c1 == '"') {
         mode = M_A;
         if (i0 >= 2) {
-          uint32_t v2 = a.tok[i0 - 2];
+          uint32_t v2 = i0 - 2 >= tbase ? s_tok[i0 - 2 - tbase] : a.tok[i0 - 2];
           uint32_t c2 = v2 & 0xFF;
           if (c2 == '{') mode = M_C;
           else if (c2 == ',') {
@@ -584,7 +653,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
       }
     }
 
-    uint32_t stk[kStructTok];  // local openers: tape index | is_object << 31
+    uint32_t stk[kK3Tok];  // local openers: tape index | is_object << 31
     int sp = 0;
     int far_level = -100;  // cache of the last far container lookup
     uint32_t far_tape = 0;
@@ -592,8 +661,7 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
     int err = 0;
     uint64_t i = i0;
     int depth_after = 0;
-#pragma unroll
-    for (int k = 0; k < kStructTok; k++) {
+    for (int k = 0; k < kK3Tok; k++) {
       if (i >= i1) break;
       const uint32_t v = recs[k];
       const uint32_t c = v & 0xFF;
@@ -664,13 +732,13 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
               top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
             } else {
               if (far_level != D - 1) {
-                int64_t j = psv(a, (int64_t)i, D - 1);
+                int64_t j = psv_tile(a, T, (int64_t)i, D - 1);
                 if (j < 0) {
                   err = kTapeError;
                   break;
                 }
                 far_level = D - 1;
-                far_obj = (a.tok[j] & 0xFF) == '{';
+                far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
                 far_tape = tape_of(a, j);
               }
               top_tape = far_tape;
@@ -697,9 +765,11 @@ __global__ void __launch_bounds__(128) k_struct(Stage2Args a) {
     }
     if (err) {
       report(ctrl, i, err);
-      continue;
+      break;
     }
     if (i1 == S && !(mode == M_A && depth_after == 0)) report(ctrl, S, kTapeError);
+    } while (false);
+    __syncthreads();
   }
 }
 
@@ -821,11 +891,11 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[1], stream);
   k_tree<<<1, 1024, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
-  uint64_t nthreads = z.chunks;
-  unsigned g3 = (unsigned)((nthreads + 127) / 128);
-  if (g3 > (unsigned)sms * 16) g3 = (unsigned)sms * 16;
-  if (g3 < 1) g3 = 1;
-  k_struct<<<g3, 128, 0, stream>>>(a);
+  {
+    uint64_t nt = (a.cap_tokens + kK3Tile - 1) / kK3Tile;
+    unsigned g3 = (unsigned)(nt < (uint64_t)sms * 4 ? nt : (uint64_t)sms * 4);
+    k_struct<<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  }
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[4], stream);

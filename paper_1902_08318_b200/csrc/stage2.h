@@ -46,6 +46,7 @@ struct Stage2Args {
   Ctrl *ctrl;
   uint32_t *tok;        // per token: c | fail << 8 | (int16 depth_before) << 16 (stage 1 + scalars)
   const uint32_t *tape_idx;  // per token: tape word index (stage 1)
+  const uint32_t *tile_flags;  // per stage-1 tile: 1 = string lengths not written
   int16_t *m1;          // tree level 1 (per 16 tokens)
   int16_t *m2;          // tree level 2 (per 256 tokens)
   int32_t *m3;          // tree level 3 (per 4096 tokens), encoded, zeroed by init
