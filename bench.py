@@ -111,6 +111,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(value: float, dist=None, device="cpu") -> float:
+    """Max of a per-rank scalar (device time of the timed region) over all
+    ranks; identity without a process group."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(bytes_per_rank: int, steps: int, world: int, max_total_ms: float) -> float:
+    """Whole-job GB/s: every rank parses its own copy (replicas, weak
+    scaling), so all ranks' bytes divided by the slowest rank's time."""
+    return world * bytes_per_rank * steps / (max_total_ms / 1e3) / 1e9
+
+
 def cpu_reference_time(data: bytes, reps: int):
     """Reference jt_parse (oracle/_ref, unmodified sources) on 1 core."""
     from oracle.pyoracle import Reference
@@ -240,12 +257,8 @@ def main():
     if dist:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = sum(step_ms)
-    if dist:
-        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
-    value = world * n * args.steps / (tot_ms / 1e3) / 1e9
+    tot_ms = max_over_ranks(sum(step_ms), dist, "cuda")
+    value = job_throughput(n, args.steps, world, tot_ms)
 
     # per-kernel times (separate profiled passes) for the roofline
     p.profile(True)
@@ -284,12 +297,8 @@ def main():
         p._lib.jt_document_free(doc_ptr)
         if k >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
-    e2e_tot = sum(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_tot], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_tot = float(t.item())
-    e2e_v = world * n * args.steps / (e2e_tot / 1e3) / 1e9
+    e2e_tot = max_over_ranks(sum(e2e_ms), dist, "cuda")
+    e2e_v = job_throughput(n, args.steps, world, e2e_tot)
 
     if rank == 0:
         cpu = None

@@ -109,6 +109,35 @@ __device__ __forceinline__ void smem_copy(uint8_t *base, uint32_t dst, uint32_t 
   }
 }
 
+// Block-relative bytes of the tile: shared memory inside the tile, global
+// memory past its end; window12 loads 12 bytes at once (aligned 32-bit loads
+// + funnel shifts) for the escape decoder.
+struct TileBytes {
+  const uint8_t *s;    // shared tile copy
+  const uint8_t *g;    // global tile base
+  uint32_t local;      // block offset in the tile
+  __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
+    uint64_t rel = local + k;
+    return rel < (uint64_t)kStage1Tile ? (uint32_t)s[rel] : (uint32_t)g[rel];
+  }
+  __device__ __forceinline__ void window12(uint64_t k, uint32_t w[3]) const {
+    const uint32_t rel = (uint32_t)(local + k);
+    if (rel + 16 <= (uint32_t)kStage1Tile) {
+      const uint32_t *s4 = (const uint32_t *)s + (rel >> 2);
+      const uint32_t sh = (rel & 3) * 8;
+      uint32_t a0 = s4[0], a1 = s4[1], a2 = s4[2], a3 = s4[3];
+      w[0] = __funnelshift_r(a0, a1, sh);
+      w[1] = __funnelshift_r(a1, a2, sh);
+      w[2] = __funnelshift_r(a2, a3, sh);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 3; q++)
+        w[q] = (uint32_t)g[rel + 4 * q] | ((uint32_t)g[rel + 4 * q + 1] << 8) |
+               ((uint32_t)g[rel + 4 * q + 2] << 16) | ((uint32_t)g[rel + 4 * q + 3] << 24);
+    }
+  }
+};
+
 struct GlobalAt {
   const uint8_t *in;
   __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
@@ -289,10 +318,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     if (warp > 0) ov_in = s_warp_ov[warp - 1];
     else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true) : 0;
   }
-  auto tbyte = [&](uint64_t k) -> uint32_t {
-    uint64_t rel = local + k;
-    return rel < (uint64_t)kStage1Tile ? (uint32_t)s_in[rel] : (uint32_t)a.in[tile_base + rel];
-  };
+  const TileBytes tbyte{s_in, a.in + tile_base, local};
   const bool fast = ((E | ctl) == 0) && ov_in == 0;
   uint32_t sw;
   if (fast) {

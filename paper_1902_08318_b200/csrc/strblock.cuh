@@ -134,6 +134,43 @@ JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str) {
 
 JT_HD uint64_t low_bits(int n) { return n >= 64 ? ~0ULL : ((1ULL << n) - 1); }
 
+JT_HD int hexv(uint32_t c) {
+  uint32_t d = c - '0';
+  if (d < 10u) return (int)d;
+  uint32_t l = (c | 0x20) - 'a';
+  return l < 6u ? (int)(l + 10) : -1;
+}
+
+JT_HD int hex4w(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  int a = hexv(b0), b = hexv(b1), c = hexv(b2), d = hexv(b3);
+  if ((a | b | c | d) < 0) return -1;
+  return (a << 12) | (b << 8) | (c << 4) | d;
+}
+
+// handle_escape (stringparse.cpp:73-102) on a 12-byte register window
+// starting at the backslash: w[k] holds bytes 4k..4k+3 (little endian).
+// Returns the consumed length (2, 6 or 12) and the code point, 0 if invalid.
+JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
+  const uint32_t e = (w[0] >> 8) & 0xFF;
+  if (e != 'u') {
+    uint32_t d = str::escape_char(e);
+    *cp = d;
+    return d ? 2 : 0;
+  }
+  int v = hex4w((w[0] >> 16) & 0xFF, w[0] >> 24, w[1] & 0xFF, (w[1] >> 8) & 0xFF);
+  if (v < 0) return 0;
+  if (v >= 0xD800 && v <= 0xDBFF) {
+    if (((w[1] >> 16) & 0xFF) != '\\' || (w[1] >> 24) != 'u') return 0;
+    int lo = hex4w(w[2] & 0xFF, (w[2] >> 8) & 0xFF, (w[2] >> 16) & 0xFF, w[2] >> 24);
+    if (lo < 0xDC00 || lo > 0xDFFF) return 0;
+    *cp = 0x10000u + ((((uint32_t)v - 0xD800u) << 10) | ((uint32_t)lo - 0xDC00u));
+    return 12;
+  }
+  if (v >= 0xDC00 && v <= 0xDFFF) return 0;
+  *cp = (uint32_t)v;
+  return 6;
+}
+
 // String bytes of one block, by segments between escape starts.  Inside a
 // segment the weights are popcounts (4 per opening quote, 1 per string
 // byte) and the payload is copied as runs; each escape start is decoded.
@@ -186,8 +223,9 @@ JT_HD uint32_t block_strings(Byte byte, uint64_t blk, uint64_t content, uint64_t
     }
     w += 4u * popc64(oseg) + popc64(cseg);
     if (e >= 64) break;
-    uint32_t cp = 0;
-    int L = str::escape_at(byte, (uint64_t)e, &cp);
+    uint32_t cp = 0, win[3];
+    byte.window12((uint64_t)e, win);
+    int L = escape_window(win, &cp);
     if (L == 0) {  // invalid escape: error at the backslash
       uint64_t x = blk + (uint64_t)e;
       if (x < *err) *err = x;

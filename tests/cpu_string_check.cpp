@@ -45,7 +45,17 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     int rem = (int)(len - blk);
     if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) serr = serr < len ? serr : len;
     uint64_t base = sw_total;
-    auto byte = [&](uint64_t k) -> uint32_t { return at(blk + k); };
+    struct Byte {
+      const std::vector<uint8_t> *b;
+      uint64_t blk;
+      uint32_t operator()(uint64_t k) const { return blk + k < b->size() ? (*b)[blk + k] : 0; }
+      void window12(uint64_t k, uint32_t w[3]) const {
+        for (int q = 0; q < 3; q++) {
+          w[q] = 0;
+          for (int j = 0; j < 4; j++) w[q] |= (*this)(k + 4 * q + j) << (8 * j);
+        }
+      }
+    } byte{&buf, blk};
     uint64_t e1 = ~0ULL;
     uint32_t wm = sb::block_strings<false>(byte, blk, content, openq, E, ctl, fin, ov_in, &e1,
                                            [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
