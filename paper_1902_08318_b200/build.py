@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libjsontape_b200.so")
 SOURCES = ["stage1.cu", "stage2.cu", "engine.cu"]
 HEADERS = ["jt_common.cuh", "stage1_block.cuh", "lookback.cuh", "numparse.cuh", "strparse.cuh",
-           "stage1.h", "stage2.h", "pow5_table.inc"]
+           "strblock.cuh", "stage1.h", "stage2.h", "pow5_table.inc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
@@ -28,8 +28,10 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(verbose: bool = False, force: bool = False, defines: tuple = (), lib: str = LIB) -> str:
+    """Compile and link.  `defines`/`lib` build an instrumented variant
+    (e.g. defines=("JT_TIMELINE",)) next to the product library."""
+    objdir = os.path.join(HERE, "build" + "".join("_" + d.lower() for d in defines))
     os.makedirs(objdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + \
         [os.path.join(ROOT, "include", "jsontape.h"), os.path.join(ROOT, "include", "jsontape_b200.h")]
@@ -39,22 +41,22 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC] + FLAGS + ["-c", s, "-o", o]
+            cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or r.returncode:
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode:
                 raise RuntimeError("nvcc failed for " + src)
-    if force or _stale(LIB, objs):
-        tmp = LIB + ".tmp"
+    if force or _stale(lib, objs):
+        tmp = lib + ".tmp"
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
                "-o", tmp] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

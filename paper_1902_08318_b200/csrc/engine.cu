@@ -765,6 +765,13 @@ void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
 
 int jt_b200_last_launches(const jt_parser *p) { return p->launches; }
 
+#ifdef JT_TIMELINE
+// instrumented builds only: K1 per-tile timeline (16 words per tile)
+int jt_b200_timeline(unsigned long long *host, size_t n) {
+  return jt::stage1_timeline(host, n) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 void jt_b200_profile(jt_parser *p, int enable) {
   if (enable && !p->ev[0])
     for (auto &e : p->ev) cudaEventCreate(&e);

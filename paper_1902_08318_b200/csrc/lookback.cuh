@@ -11,6 +11,31 @@
 
 #include <stdint.h>
 
+// JT_TIMELINE (instrumented builds only, never the product library): per-tile
+// %globaltimer stamps and look-back counters, read back with
+// jt_b200_timeline().  Slot k of tile t is g_tl[16 t + k].
+#ifdef JT_TIMELINE
+namespace jt {
+constexpr int kTlTiles = 1 << 17;
+static __device__ unsigned long long g_tl[kTlTiles * 16];  // per TU; stage1.cu reads its copy
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+}  // namespace jt
+#define JT_TL(tile, k) \
+  do { if ((tile) < jt::kTlTiles) jt::g_tl[(tile) * 16 + (k)] = jt::tl_now(); } while (0)
+#define JT_TLV(tile, k, v) \
+  do { if ((tile) < jt::kTlTiles) jt::g_tl[(tile) * 16 + (k)] = (v); } while (0)
+#define JT_TLADD(tile, k, v) \
+  do { if ((tile) < jt::kTlTiles && (v)) atomicAdd(&jt::g_tl[(tile) * 16 + (k)], (unsigned long long)(v)); } while (0)
+#else
+#define JT_TL(tile, k) do { } while (0)
+#define JT_TLV(tile, k, v) do { } while (0)
+#define JT_TLADD(tile, k, v) do { } while (0)
+#endif
+
 namespace jt {
 
 constexpr uint64_t kFlagAgg = 1ULL << 62;
@@ -163,33 +188,62 @@ __device__ __forceinline__ int quad_read(const uint64_t *rec, int64_t tile, Quad
 }
 
 // Window of the look-back: each lane reads kLbPer predecessor records per
-// round, so one round covers 32 * kLbPer tiles.  With ~0.5-1 us per round
-// trip, the window size bounds how fast the inclusive frontier advances
-// (window x tile bytes per round trip), so it must be wide.
+// round, so one round covers 32 * kLbPer tiles.  All loads of a round are
+// issued before any is waited on (a round costs one L2 round trip, ~1 us
+// under load); only records still empty are re-polled.
 constexpr int kLbPer = 4;
-
+constexpr int kQuadPer = 2;
+__device__ __forceinline__ void quad_issue(const uint64_t *rec, int64_t tile, uint64_t x[8]) {
+  const uint64_t *r = rec + 8 * tile;
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = lb_load(r + k);
+}
+__device__ __forceinline__ int quad_decode(const uint64_t x[8], Quad &q) {
+#pragma unroll
+  for (int slot = 1; slot >= 0; --slot) {
+    const uint64_t *y = x + 4 * slot;
+    if ((y[0] & y[1] & y[2] & y[3]) >> 63) {
+#pragma unroll
+      for (int k = 0; k < 4; k++) q.v[k] = y[k] & kQuadMask;
+      return slot + 1;
+    }
+  }
+  return 0;
+}
 // exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp
 __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile) {
   const int lane = threadIdx.x & 31;
   Quad acc{{0, 0, 0, 0}};
   int64_t base = tile - 1;
   for (;;) {
-    // lane l owns predecessors base - kLbPer*l - j, j = 0 (nearest) .. kLbPer-1
-    Quad q[kLbPer];
-    int st[kLbPer];
+    // lane l owns predecessors base - kQuadPer*l - j, j = 0 (nearest) .. kQuadPer-1
+    Quad q[kQuadPer];
+    int st[kQuadPer];
+    uint64_t x[kQuadPer][8];
 #pragma unroll
-    for (int j = 0; j < kLbPer; j++) {
-      int64_t pred = base - (int64_t)kLbPer * lane - j;
+    for (int j = 0; j < kQuadPer; j++) {
+      int64_t pred = base - (int64_t)kQuadPer * lane - j;
+      if (pred >= 0) quad_issue(rec, pred, x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kQuadPer; j++) {
+      int64_t pred = base - (int64_t)kQuadPer * lane - j;
       q[j] = Quad{{0, 0, 0, 0}};
       st[j] = 2;
-      if (pred >= 0)
-        while ((st[j] = quad_read(rec, pred, q[j])) == 0) __nanosleep(32);
+      if (pred >= 0) {
+        while ((st[j] = quad_decode(x[j], q[j])) == 0) {
+          __nanosleep(32);
+          quad_issue(rec, pred, x[j]);
+          JT_TLADD(tile, 12, 1);
+        }
+      }
     }
+    JT_TLADD(tile, 11, lane == 0);
     // per lane: sum from the nearest up to and including its first inclusive
     Quad mine{{0, 0, 0, 0}};
     bool has_incl = false;
 #pragma unroll
-    for (int j = 0; j < kLbPer; j++) {
+    for (int j = 0; j < kQuadPer; j++) {
       if (!has_incl) {
 #pragma unroll
         for (int k = 0; k < 4; k++) mine.v[k] += q[j].v[k];
@@ -206,8 +260,7 @@ __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile)
       acc.v[k] = (acc.v[k] + x) & kQuadMask;
     }
     if (incl) return acc;
-    base -= 32 * kLbPer;
+    base -= 32 * kQuadPer;
   }
 }
-
 }  // namespace jt

@@ -42,12 +42,24 @@ __device__ uint32_t lookback_state(const uint64_t *rec, int64_t tile) {
   bool haveG = false;
   int64_t base = tile - 1;
   for (;;) {
+    // issue the whole window before waiting on any record: one round trip
+    // per round, not one per predecessor
     uint64_t v[kLbPer];
 #pragma unroll
     for (int j = 0; j < kLbPer; j++) {
       int64_t pred = base - (int64_t)kLbPer * lane - j;
-      v[j] = pred >= 0 ? lb_wait(rec + pred) : (kFlagIncl | s1::kInitState);
+      v[j] = pred >= 0 ? lb_load(rec + pred) : (kFlagIncl | s1::kInitState);
     }
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {
+      int64_t pred = base - (int64_t)kLbPer * lane - j;
+      while ((v[j] >> 62) == 0) {
+        __nanosleep(32);
+        v[j] = lb_load(rec + pred);
+        JT_TLADD(tile, 10, 1);
+      }
+    }
+    JT_TLADD(tile, 9, lane == 0);
     // per lane, nearest first: either a resolved state (an inclusive record
     // was found, later aggregates applied on top) or a composed function
     uint32_t fn = 0, stt = 0;
@@ -196,6 +208,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
+  if (threadIdx.x == 0) {
+    JT_TL(tile, 0);
+#ifdef JT_TIMELINE
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    JT_TLV(tile, 8, smid);
+#endif
+  }
   const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
   const uint32_t local = threadIdx.x * 64;
@@ -255,9 +275,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     if (tile == 0) {
       carry = s1::kInitState;
     } else {
-      if (lane == 0) lb_store(a.rec_state + tile, kFlagAgg | agg);
+      if (lane == 0) {
+        JT_TL(tile, 1);
+        lb_store(a.rec_state + tile, kFlagAgg | agg);
+      }
       carry = lookback_state(a.rec_state, tile);
     }
+    if (lane == 0) JT_TL(tile, 2);
     if (lane == 0) {
       lb_store(a.rec_state + tile, kFlagIncl | s1::apply(agg, carry));
       uint32_t c = carry;
@@ -373,14 +397,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint32_t off = woff + ci - cnt;   // tile-relative index slot
   const uint32_t soff = wsoff + si - sw;  // tile-relative string byte
 
-  if (warp == 0) {
+  // Look-back 2.  The aggregate goes out now; the prefix is only needed by
+  // the copy-out (staging below is tile-relative), so warp 0 emits its own
+  // blocks first and looks back afterwards, when the predecessors have most
+  // likely published their inclusive prefixes (one round trip, no polling).
+  // Tiles that overflow the staging write to global directly and resolve
+  // first.
+  const bool idx_direct = total > (uint32_t)kStageIdx;
+  const bool pay_direct = stotal > (uint32_t)kStagePay;
+  const bool direct = idx_direct || pay_direct;  // CTA-uniform
+  const Quad tot{{total, stotal, ttotal, (unsigned long long)(long long)dtotal & kQuadMask}};
+  auto resolve_counts = [&]() {  // warp 0
     Quad base{{0, 0, 0, 0}};
-    Quad tot{{total, stotal, ttotal, (unsigned long long)(long long)dtotal & kQuadMask}};
-    if (tile > 0) {
-      if (lane == 0) quad_publish(a.rec_count, tile, 0, tot);
-      base = quad_lookback(a.rec_count, tile);
-    }
+    if (tile > 0) base = quad_lookback(a.rec_count, tile);
     if (lane == 0) {
+      JT_TL(tile, 5);
       Quad inc;
 #pragma unroll
       for (int k = 0; k < 4; k++) inc.v[k] = (base.v[k] + tot.v[k]) & kQuadMask;
@@ -395,15 +426,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         *a.tape_words = 1 + inc.v[2];
       }
     }
+  };
+  if (threadIdx.x == 0 && tile > 0) {
+    JT_TL(tile, 4);
+    quad_publish(a.rec_count, tile, 0, tot);
   }
+  if (direct && warp == 0) resolve_counts();
+  if (threadIdx.x == 0) JT_TL(tile, 6);
   s_blk[threadIdx.x] = BlockRec{content, openq, w1m, w2m, opm, clm, soff, toff, doff, fast ? 1u : 0u};
   // stage positions (+ string offsets of slow blocks) and the string
   // payload; spill to global when the tile is larger than the staging
-  const bool idx_direct = total > (uint32_t)kStageIdx;
-  const bool pay_direct = stotal > (uint32_t)kStagePay;
-  if (idx_direct || pay_direct) __syncthreads();  // s_base/s_sbase needed now
-  const uint64_t gbase = (idx_direct || pay_direct) ? s_base : 0;
-  const uint64_t gsbase = (idx_direct || pay_direct) ? s_sbase : 0;
+  if (direct) __syncthreads();  // s_base/s_sbase needed now
+  const uint64_t gbase = direct ? s_base : 0;
+  const uint64_t gsbase = direct ? s_sbase : 0;
   const uint64_t gtbase = idx_direct ? s_tbase : 0;
   const long long gdbase = idx_direct ? s_dbase : 0;
   auto direct_entry = [&](uint32_t slot, int p, uint32_t wb) {
@@ -470,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           slot++;
         });
   }
+  if (!direct && warp == 0) resolve_counts();
   __syncthreads();
 
   const uint32_t tb = (uint32_t)tile_base;
@@ -531,9 +567,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
     for (uint32_t k = head + 4 * nw + threadIdx.x; k < stotal; k += kThreads) dst[k] = s_pay[k];
   }
+  if (threadIdx.x == 0) JT_TL(tile, 7);
 }
 
 }  // namespace
+
+#ifdef JT_TIMELINE
+// copy (and clear) the K1 timeline; instrumented builds only
+cudaError_t stage1_timeline(unsigned long long *host, size_t n) {
+  if (n > (size_t)kTlTiles * 16) n = (size_t)kTlTiles * 16;
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_tl, n * sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  static unsigned long long zero[4096];
+  for (size_t off = 0; off < (size_t)kTlTiles * 16; off += 4096)
+    if ((e = cudaMemcpyToSymbol(g_tl, zero, sizeof(zero), off * sizeof(unsigned long long))) != cudaSuccess)
+      return e;
+  return cudaSuccess;
+}
+#endif
 
 size_t stage1_records(uint64_t len) {
   uint64_t ntiles = (len + kStage1Tile - 1) / kStage1Tile;

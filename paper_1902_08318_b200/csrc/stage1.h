@@ -42,4 +42,8 @@ cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
 // one-time kernel attributes (dynamic shared memory); call outside capture
 cudaError_t stage1_configure();
 
+#ifdef JT_TIMELINE
+cudaError_t stage1_timeline(unsigned long long *host, size_t n);
+#endif
+
 }  // namespace jt

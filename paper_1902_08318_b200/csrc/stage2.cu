@@ -127,14 +127,19 @@ __device__ __forceinline__ void stk_publish_incl(uint64_t *rec, uint64_t tile, u
   lb_store(rec + 4 * tile + 3, kV | (S >> 32));
 }
 
-// 2 = inclusive (S), 1 = aggregate (t), 0 = not ready
-__device__ __forceinline__ int stk_read(const uint64_t *rec, int64_t tile, StackT &t, uint64_t &S) {
-  uint64_t x = lb_load(rec + 4 * tile + 2), y = lb_load(rec + 4 * tile + 3);
+__device__ __forceinline__ void stk_issue(const uint64_t *rec, int64_t tile, uint64_t r[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; k++) r[k] = lb_load(rec + 4 * tile + k);
+}
+
+// 2 = inclusive (S), 1 = aggregate (t), 0 = not ready; r = the 4 record words
+__device__ __forceinline__ int stk_decode(const uint64_t r[4], StackT &t, uint64_t &S) {
+  uint64_t x = r[2], y = r[3];
   if ((x & y) >> 63) {
     S = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
     return 2;
   }
-  x = lb_load(rec + 4 * tile), y = lb_load(rec + 4 * tile + 1);
+  x = r[0], y = r[1];
   if ((x & y) >> 63) {
     t.P = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
     t.k = (uint32_t)((x >> 32) & 0x7FFFFFFF);
@@ -154,14 +159,24 @@ __device__ uint64_t stk_lookback(const uint64_t *rec, int64_t tile) {
     StackT t[kLbPer];
     uint64_t Sv[kLbPer];
     int st[kLbPer];
+    uint64_t r[kLbPer][4];
+#pragma unroll
+    for (int j = 0; j < kLbPer; j++) {  // whole window in flight, then wait
+      int64_t pred = base - (int64_t)kLbPer * lane - j;
+      if (pred >= 0) stk_issue(rec, pred, r[j]);
+    }
 #pragma unroll
     for (int j = 0; j < kLbPer; j++) {
       int64_t pred = base - (int64_t)kLbPer * lane - j;
       t[j] = StackT{0, 0, 0};
       Sv[j] = 0;
       st[j] = 2;
-      if (pred >= 0)
-        while ((st[j] = stk_read(rec, pred, t[j], Sv[j])) == 0) __nanosleep(32);
+      if (pred >= 0) {
+        while ((st[j] = stk_decode(r[j], t[j], Sv[j])) == 0) {
+          __nanosleep(32);
+          stk_issue(rec, pred, r[j]);
+        }
+      }
     }
     // per lane, farthest to nearest: resolved stack or composed transfer
     StackT fn{0, 0, 0};
