@@ -180,7 +180,8 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.tape_idx = p->tape_idx.as<uint32_t>();
   a.tile_flags = p->tile_flags.as<uint32_t>();
   uint64_t nt = jt::stage1_records(len);
-  a.rec_state = p->s1rec.as<uint64_t>();
+  a.fn = (uint32_t *)p->s1rec.as<uint64_t>();  // 2 x ntiles u32 in the ntiles-word channel-1 area
+  a.carry = a.fn + nt;
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
   a.tile_counter = &c->s1_tile_counter;
   a.utf8_pos = &c->utf8_pos;
@@ -232,7 +233,7 @@ uint64_t buffers_sig(jt_parser *p, int which) {
 
 bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full);
 
-// Full parses without profiling replay a CUDA graph of the 7 launches + the
+// Full parses without profiling replay a CUDA graph of the 9 launches + the
 // control-block D2H (captured on first use for this length/stream/buffers).
 bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
   if (!full || p->prof) return enqueue_direct(p, len, which, full);
@@ -283,7 +284,7 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
   p->launches++;
   if (p->prof) cudaEventRecord(p->ev[1], p->stream);
   if (!cuda_ok(p, jt::stage1_launch(s1_args(p, len, which), p->stream), "stage1")) return false;
-  p->launches++;
+  p->launches += jt::kStage1Launches;
   if (p->prof) cudaEventRecord(p->ev[2], p->stream);
   if (full) {
     int n = 0;

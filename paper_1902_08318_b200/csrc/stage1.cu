@@ -34,65 +34,6 @@ __device__ __forceinline__ void ld256(const uint8_t *p, uint32_t *w) {
                : "l"(p));
 }
 
-// state look-back (channel 1), one full warp; returns the tile's carry-in.
-// Each lane reads kLbPer predecessors per round (see lookback.cuh).
-__device__ uint32_t lookback_state(const uint64_t *rec, int64_t tile) {
-  const int lane = threadIdx.x & 31;
-  uint32_t G = 0;
-  bool haveG = false;
-  int64_t base = tile - 1;
-  for (;;) {
-    // issue the whole window before waiting on any record: one round trip
-    // per round, not one per predecessor
-    uint64_t v[kLbPer];
-#pragma unroll
-    for (int j = 0; j < kLbPer; j++) {
-      int64_t pred = base - (int64_t)kLbPer * lane - j;
-      v[j] = pred >= 0 ? lb_load(rec + pred) : (kFlagIncl | s1::kInitState);
-    }
-#pragma unroll
-    for (int j = 0; j < kLbPer; j++) {
-      int64_t pred = base - (int64_t)kLbPer * lane - j;
-      while ((v[j] >> 62) == 0) {
-        __nanosleep(32);
-        v[j] = lb_load(rec + pred);
-        JT_TLADD(tile, 10, 1);
-      }
-    }
-    JT_TLADD(tile, 9, lane == 0);
-    // per lane, nearest first: either a resolved state (an inclusive record
-    // was found, later aggregates applied on top) or a composed function
-    uint32_t fn = 0, stt = 0;
-    bool have_fn = false, resolved = false;
-#pragma unroll
-    for (int j = kLbPer - 1; j >= 0; --j) {  // farthest to nearest
-      uint32_t pay = (uint32_t)v[j];
-      if ((v[j] >> 62) == 2) {
-        resolved = true;
-        stt = pay & 7;
-        have_fn = false;
-      } else if (resolved) {
-        stt = s1::apply(pay, stt);
-      } else {
-        fn = have_fn ? s1::compose(pay, fn) : pay;
-        have_fn = true;
-      }
-    }
-    uint32_t incl = __ballot_sync(0xffffffffu, resolved);
-    if (incl) {
-      int k = __ffs(incl) - 1;
-      uint32_t s = __shfl_sync(0xffffffffu, stt, k);
-      for (int l = k - 1; l >= 0; --l) s = s1::apply(__shfl_sync(0xffffffffu, fn, l), s);
-      if (haveG) s = s1::apply(G, s);
-      return s;
-    }
-    uint32_t H = __shfl_sync(0xffffffffu, fn, 31);
-    for (int l = 30; l >= 0; --l) H = s1::compose(__shfl_sync(0xffffffffu, fn, l), H);
-    G = haveG ? s1::compose(G, H) : H;
-    haveG = true;
-    base -= 32 * kLbPer;
-  }
-}
 
 // byte run copy inside shared memory (offsets from the dynamic smem base):
 // head bytes to align the destination, then funnel-shifted words
@@ -186,6 +127,107 @@ __device__ __forceinline__ int tok_delta(uint32_t c) {
 
 __device__ __forceinline__ int clamp16(long long d) { return d < -2 ? -2 : d > 1026 ? 1026 : (int)d; }
 
+// ---- K0: carry-in of every tile (reduce-then-scan) --------------------------
+// The tile carry (odd backslash run, in-string, previous byte a separator;
+// blocks.h:31-35) is a 3-bit state whose per-block transfer functions compose
+// (stage1_block.cuh).  K0a reduces each 16 KiB tile to one function, K0b scans
+// the functions in one CTA, and K1 reads its carry-in at start: no chained
+// look-back on this channel.
+
+// K0a: transfer function of each tile.  128 threads x 2 blocks per tile, all
+// four 32-byte loads of a thread issued together.
+constexpr int kFnThreads = kStage1Tile / 128;
+__global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint32_t *fn) {
+  __shared__ uint32_t s_f[kFnThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t blk = (uint64_t)blockIdx.x * kStage1Tile + (uint64_t)threadIdx.x * 128;
+  uint32_t w[32];
+  ld256(in + blk, w);
+  ld256(in + blk + 32, w + 8);
+  ld256(in + blk + 64, w + 16);
+  ld256(in + blk + 96, w + 24);
+  uint32_t f2[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    s1::Masks m;
+    s1::classify64(w + 16 * h, m);
+    f2[h] = s1::block_function(m, s1::escaped_no_carry(m.bs), s1::carry_toggle(m.bs));
+  }
+  uint32_t inc = s1::compose(f2[1], f2[0]);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc = s1::compose(inc, o);
+  }
+  if (lane == 31) s_f[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t agg = s_f[0];
+#pragma unroll
+    for (int k = 1; k < kFnThreads / 32; k++) agg = s1::compose(s_f[k], agg);
+    fn[blockIdx.x] = agg;
+  }
+}
+
+// K0b: carry-in of every tile = (f[t-1] o ... o f[0])(kInitState); one CTA,
+// each thread a contiguous chunk of tiles
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn, uint32_t *carry,
+                                                             uint64_t ntiles) {
+  __shared__ uint32_t s_agg[kScanThreads / 32];
+  __shared__ uint32_t s_has[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t per = (ntiles + kScanThreads - 1) / kScanThreads;
+  const uint64_t lo = threadIdx.x * per;
+  const uint64_t hi = lo + per < ntiles ? lo + per : ntiles;
+  // the chunk is read in batches of independent loads (one round trip per
+  // batch, not per tile)
+  constexpr int kBatch = 16;
+  uint32_t acc = 0;
+  bool has = lo < hi;
+  for (uint64_t b = lo; b < hi; b += kBatch) {
+    uint32_t v[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; j++) v[j] = b + j < hi ? __ldg(fn + b + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < kBatch; j++)
+      if (b + j < hi) acc = (b + j == lo) ? v[j] : s1::compose(v[j], acc);
+  }
+  // warp inclusive scan over (has, acc)
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, acc, d);
+    uint32_t oh = __shfl_up_sync(0xffffffffu, has ? 1u : 0u, d);
+    if (lane >= d && oh) {
+      acc = has ? s1::compose(acc, o) : o;
+      has = true;
+    }
+  }
+  if (lane == 31) {
+    s_agg[warp] = acc;
+    s_has[warp] = has;
+  }
+  __syncthreads();
+  // exclusive prefix state of this thread: earlier warps, then earlier lanes
+  uint32_t state = s1::kInitState;
+  for (int k = 0; k < warp; k++)
+    if (s_has[k]) state = s1::apply(s_agg[k], state);
+  uint32_t ex = __shfl_up_sync(0xffffffffu, acc, 1);
+  uint32_t exh = __shfl_up_sync(0xffffffffu, has ? 1u : 0u, 1);
+  if (lane > 0 && exh) state = s1::apply(ex, state);
+  for (uint64_t b = lo; b < hi; b += kBatch) {
+    uint32_t v[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; j++) v[j] = b + j < hi ? __ldg(fn + b + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < kBatch; j++)
+      if (b + j < hi) {
+        carry[b + j] = state;
+        state = s1::apply(v[j], state);
+      }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_f[kWarps];
@@ -221,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint32_t local = threadIdx.x * 64;
   const GlobalAt gat{a.in};
 
+  const uint32_t carry_in = a.carry[tile];  // K0b output, read early
   uint32_t w[16];
   ld256(a.in + blk, w);
   ld256(a.in + blk + 32, w + 8);
@@ -266,29 +309,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   __syncthreads();
 
-  // tile aggregate, look-back for the carry-in, warp carry states
-  if (warp == 0) {
-    uint32_t agg = s_warp_f[0];
-#pragma unroll
-    for (int k = 1; k < kWarps; k++) agg = s1::compose(s_warp_f[k], agg);
-    uint32_t carry;
-    if (tile == 0) {
-      carry = s1::kInitState;
-    } else {
-      if (lane == 0) {
-        JT_TL(tile, 1);
-        lb_store(a.rec_state + tile, kFlagAgg | agg);
-      }
-      carry = lookback_state(a.rec_state, tile);
-    }
-    if (lane == 0) JT_TL(tile, 2);
-    if (lane == 0) {
-      lb_store(a.rec_state + tile, kFlagIncl | s1::apply(agg, carry));
-      uint32_t c = carry;
-      for (int k = 0; k < kWarps; k++) {
-        s_warp_state[k] = c;
-        c = s1::apply(s_warp_f[k], c);
-      }
+  // warp carry states from the tile's carry-in (K0 pre-pass, no look-back)
+  if (threadIdx.x == 0) {
+    uint32_t c = carry_in;
+    for (int k = 0; k < kWarps; k++) {
+      s_warp_state[k] = c;
+      c = s1::apply(s_warp_f[k], c);
     }
   }
   __syncthreads();
@@ -604,6 +630,8 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
   a.ntiles = ntiles;
   const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
+  k_carry_fn<<<(unsigned)ntiles, kFnThreads, 0, stream>>>(a.in, a.fn);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, ntiles);
   k_stage1<<<(unsigned)ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();
 }

@@ -23,7 +23,8 @@ struct Stage1Args {
   uint32_t *tokrec;    // per index entry: byte | clamped depth_before << 16
   uint32_t *tape_idx;  // per index entry: tape word index
   uint32_t *tile_flags; // per tile: 1 = string lengths left to stage 2 (spill mode)
-  uint64_t *rec_state; // ntiles look-back records, zeroed
+  uint32_t *fn;        // ntiles carry transfer functions (K0a)
+  uint32_t *carry;     // ntiles carry-in states (K0b)
   uint64_t *rec_count; // 8 * ntiles look-back words (count, strings, tape, depth), zeroed
   uint32_t *tile_counter;         // zeroed
   unsigned long long *utf8_pos;   // ~0 initially; min flagged offset
@@ -37,6 +38,7 @@ struct Stage1Args {
 // number of tiles for `len` (look-back records: 1 + 8 words per tile)
 size_t stage1_records(uint64_t len);
 
+constexpr int kStage1Launches = 3;  // K0a carry functions, K0b carry scan, K1
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
 
 // one-time kernel attributes (dynamic shared memory); call outside capture
