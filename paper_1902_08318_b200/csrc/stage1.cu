@@ -99,19 +99,19 @@ struct GlobalAt {
 // shared memory layout (dynamic)
 constexpr int kSmemIn = kStage1Tile;            // tile input bytes
 constexpr int kSmemIdx = kStageIdx * 2;         // u16 positions
-constexpr int kSmemAux = kStageIdx * 2;         // u16 string offsets
 // per-block record for the copy-out: masks of the block's tokens and the
 // block's tile-relative offsets (index entries get their string offset, tape
-// index and depth from popcounts below their bit)
+// index and depth from popcounts below their bit; W = string weight mask,
+// strblock.cuh escape_weights)
 struct BlockRec {
-  uint64_t content, openq, w1, w2, op, cl;
+  uint64_t W, openq, w1, w2, op, cl;
   uint32_t soff, toff;
   int32_t doff;
-  uint32_t fast;
+  uint32_t pad;
 };
 constexpr int kSmemBlk = kThreads * (int)sizeof(BlockRec);
 constexpr int kSmemPay = kStagePay;             // payload bytes (last: word over-read)
-constexpr int kOffBlk = kSmemIn + kSmemIdx + kSmemAux;
+constexpr int kOffBlk = kSmemIn + kSmemIdx;
 constexpr int kOffPay = kOffBlk + kSmemBlk;
 constexpr int kSmemBytes = kOffPay + kSmemPay + 16;
 
@@ -242,7 +242,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *s_in = smem;
   uint16_t *s_idx = (uint16_t *)(smem + kSmemIn);
-  uint16_t *s_aux = (uint16_t *)(smem + kSmemIn + kSmemIdx);
   BlockRec *s_blk = (BlockRec *)(smem + kOffBlk);
   uint8_t *s_pay = smem + kOffPay;
 
@@ -348,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint64_t content = instr & ~openq & valid;
   const uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content;
   const uint64_t ctl = sb::control_mask(m.P) & content;
+  // escapes reaching into the next block: ov | spill << 8 (strblock.cuh)
   int ov_out = E ? sb::overhang_out(gat, blk, E) : 0;
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
@@ -364,22 +364,26 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   if (lane == 31) s_warp_cnt[warp] = ci;
   __syncthreads();
+  // the tile's first block also gets the decoded bytes an escape of the
+  // previous tile spills into it (that tile's staging drops them)
+  uint32_t spill_bytes = 0;
   if (lane == 0) {
     if (warp > 0) ov_in = s_warp_ov[warp - 1];
-    else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true) : 0;
+    else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true, &spill_bytes) : 0;
   }
   const TileBytes tbyte{s_in, a.in + tile_base, local};
-  const bool fast = ((E | ctl) == 0) && ov_in == 0;
-  uint32_t sw;
-  if (fast) {
-    sw = 4u * popc64(openq) + popc64(content);
-  } else {
-    uint64_t serr = ~0ULL;
-    sw = sb::block_strings<false>(tbyte, blk, content, openq, E, ctl, fin, ov_in, &serr,
-                                  [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
-                                  [](int, uint32_t) {});
+  const int vin = ov_in >> 8;
+  ov_in &= 0xFF;
+  // string weight mask: the plain string bytes, or for blocks with escapes
+  // the decoded-length positions of each escape (strblock.cuh)
+  const bool esc_work = ((E & ~sb::low_bits(ov_in)) | (uint64_t)ov_in) != 0;
+  uint64_t W = content;
+  {
+    uint64_t serr = ctl ? blk + (uint64_t)ctz64(ctl) : ~0ULL;
+    if (esc_work) W = sb::escape_weights(tbyte, blk, content, E, ov_in, vin, &serr);
     if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
   }
+  const uint32_t sw = 4u * popc64(openq) + popc64(W);
   uint32_t si = sw;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   if (direct && warp == 0) resolve_counts();
   if (threadIdx.x == 0) JT_TL(tile, 6);
-  s_blk[threadIdx.x] = BlockRec{content, openq, w1m, w2m, opm, clm, soff, toff, doff, fast ? 1u : 0u};
+  s_blk[threadIdx.x] = BlockRec{W, openq, w1m, w2m, opm, clm, soff, toff, doff, 0u};
   // stage positions (+ string offsets of slow blocks) and the string
   // payload; spill to global when the tile is larger than the staging
   if (direct) __syncthreads();  // s_base/s_sbase needed now
@@ -477,20 +481,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     a.tokrec[gbase + slot] = c | ((uint32_t)(uint16_t)clamp16(d) << 16);
     a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + t);
   };
-  if (fast) {
-    uint64_t cm = content;
+  {
+    // plain runs (escape positions get placeholder bytes, rewritten below;
+    // the first vin bits belong to the previous block's escape)
+    uint64_t cm = W & ~sb::low_bits(vin);
     while (cm) {  // string runs, 4-byte gaps before each run opened here
       const int a0 = ctz64(cm);
       const uint64_t sh = cm >> a0;
       const int n = ~sh == 0 ? 64 - a0 : ctz64(~sh);
       const uint64_t below = sb::low_bits(a0);
-      const uint32_t wdst = 4u * popc64(openq & below) + popc64(content & below);
+      const uint32_t wdst = 4u * popc64(openq & below) + popc64(W & below);
       if (pay_direct) {
         for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
       } else {
         smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
       }
       cm &= ~(sb::low_bits(n) << a0);
+    }
+    if (esc_work) {
+      auto put = [&](uint32_t pos, uint8_t b) {
+        if (pay_direct) a.strings[gsbase + soff + pos] = b;
+        else s_pay[soff + pos] = b;
+      };
+      for (int k = 0; k < vin && threadIdx.x == 0; k++) put((uint32_t)k, (uint8_t)(spill_bytes >> (8 * k)));
+      sb::escape_emit(tbyte, E, ov_in, openq, W, put);
     }
     uint64_t fm = fin;
     uint32_t slot = off;
@@ -499,37 +513,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       fm &= fm - 1;
       if (idx_direct) {
         const uint64_t below = sb::low_bits(p);
-        direct_entry(slot, p, 4u * popc64(openq & below) + popc64(content & below));
+        direct_entry(slot, p, 4u * popc64(openq & below) + popc64(W & below));
       } else {
         s_idx[slot] = (uint16_t)(local + p);
       }
       slot++;
     }
-  } else {
-    uint32_t slot = off;
-    uint64_t e2 = ~0ULL;
-    sb::block_strings<true>(
-        tbyte, blk, content, openq, E, ctl, fin, ov_in, &e2,
-        [&](int a0, uint32_t wdst, int n) {
-          if (pay_direct) {
-            for (int k = 0; k < n; k++) a.strings[gsbase + soff + wdst + k] = s_in[local + a0 + k];
-          } else {
-            smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
-          }
-        },
-        [&](uint32_t pos, uint8_t b) {
-          if (pay_direct) a.strings[gsbase + soff + pos] = b;
-          else s_pay[soff + pos] = b;
-        },
-        [&](int p, uint32_t wb) {
-          if (idx_direct) {
-            direct_entry(slot, p, wb);
-          } else {
-            s_idx[slot] = (uint16_t)(local + p);
-            s_aux[slot] = (uint16_t)(soff + wb);
-          }
-          slot++;
-        });
   }
   if (!direct && warp == 0) resolve_counts();
   __syncthreads();
@@ -549,8 +538,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       const uint32_t pos = s_idx[k];
       const BlockRec &r = s_blk[pos >> 6];
       const uint64_t below = sb::low_bits((int)(pos & 63));
-      const uint32_t aux = r.fast ? r.soff + 4u * popc64(r.openq & below) + popc64(r.content & below)
-                                  : (uint32_t)s_aux[k];
+      const uint32_t aux = r.soff + 4u * popc64(r.openq & below) + popc64(r.W & below);
       const uint32_t t = r.toff + popc64(r.w1 & below) + popc64(r.w2 & below);
       const int d = r.doff + popc64(r.op & below) - popc64(r.cl & below);
       const uint32_t c = s_in[pos];
@@ -565,8 +553,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         const uint32_t p2 = s_idx[k + 1];
         const BlockRec &r2 = s_blk[p2 >> 6];
         const uint64_t b2 = sb::low_bits((int)(p2 & 63));
-        const uint32_t aux2 = r2.fast ? r2.soff + 4u * popc64(r2.openq & b2) + popc64(r2.content & b2)
-                                      : (uint32_t)s_aux[k + 1];
+        const uint32_t aux2 = r2.soff + 4u * popc64(r2.openq & b2) + popc64(r2.W & b2);
         const uint32_t len = aux2 - aux - 4;
         s_pay[aux] = (uint8_t)len;
         s_pay[aux + 1] = (uint8_t)(len >> 8);

@@ -14,8 +14,9 @@
 // escape, unterminated string) are reported as byte positions; the first
 // failing string is the one holding the minimum position.
 //
-// Blocks without escapes or control bytes (the common case) take the mask
-// fast path; others run a sequential walker over their bytes.
+// Blocks with escapes decode them (escape_weights) into a weight mask W so
+// that every block uses the same popcount formulas; the decoded bytes are
+// written after the plain runs (escape_emit).
 #pragma once
 
 #include "jt_common.cuh"
@@ -62,31 +63,44 @@ JT_HD int encode(uint32_t cp, uint8_t out[4]) {
 // can overhang, and whether it is consumed as the low half of a surrogate
 // pair depends on starts >= 40, so the answer does not depend on the
 // block's own incoming overhang (<= 11 bytes).
+// Decoded length of a valid escape (L = 2, 6 or 12 input bytes).
+JT_HD int out_len(int L, uint32_t cp) {
+  return L == 2 ? 1 : cp < 0x80 ? 1 : cp < 0x800 ? 2 : cp < 0x10000 ? 3 : 4;
+}
+
+// Returns ov | spill << 8: ov = input bytes, spill = weight bytes (see
+// escape_weights) of the last escape that fall into the next block.
 template <class At>
 JT_HD int overhang_out(At at, uint64_t blk, uint64_t E) {
   uint64_t cand = E & (~0ULL << 40);
   if (!(E >> 52)) return 0;
   // walk starts from bit 40 upward, skipping consumed lows
   int p = 40;
-  int ov = 0;
+  int ov = 0, spill = 0;
   while (p < 64) {
     uint64_t rest = cand >> p;
     if (!rest) break;
     p += ctz64(rest);
     uint32_t cp;
     int L = str::escape_at(at, blk + (uint64_t)p, &cp);
+    int n = L ? out_len(L, cp) : 0;
     if (L == 0) L = 2;  // invalid: the document fails anyway; stay bounded
-    if (p + L > 64) ov = p + L - 64;
+    if (p + L > 64) {
+      ov = p + L - 64;
+      spill = p + n > 64 ? p + n - 64 : 0;
+    }
     p += L;
   }
-  return ov;
+  return ov | (spill << 8);
 }
 
-// Overhang into block `blk` from the bytes before it, computed without the
-// previous block's masks: odd_in = parity of the backslash run ending at
+// Overhang into block `blk` from the bytes before it (ov | spill << 8 as
+// overhang_out; *spill_bytes = the spilled decoded bytes, little endian),
+// computed without the previous block's masks: odd_in = parity of the backslash run ending at
 // blk-1, in_str = blk-1 is inside a string.  Used for a tile's first block.
 template <class At>
-JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str) {
+JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str, uint32_t *spill_bytes) {
+  *spill_bytes = 0;
   if (!in_str || blk == 0) return 0;
   const uint64_t lo = blk >= 12 ? blk - 12 : 0;
   // escape starts among [lo, blk): unescaped backslashes, after the last
@@ -116,7 +130,7 @@ JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str) {
     }
     p = q;
   }
-  int ov = 0;
+  int ov = 0, spill = 0;
   uint64_t s = lo;
   while (starts && s < blk) {
     uint32_t k = (uint32_t)(s - (blk - 12));
@@ -125,11 +139,22 @@ JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str) {
     s += (uint64_t)ctz32(rest);
     uint32_t cp;
     int L = str::escape_at(at, s, &cp);
+    int n = L ? out_len(L, cp) : 0;
     if (L == 0) L = 2;
-    if (s + (uint64_t)L > blk) ov = (int)(s + (uint64_t)L - blk);
+    if (s + (uint64_t)L > blk) {
+      ov = (int)(s + (uint64_t)L - blk);
+      spill = s + (uint64_t)n > blk ? (int)(s + (uint64_t)n - blk) : 0;
+      *spill_bytes = 0;
+      if (spill) {  // decoded bytes n - spill .. n-1 land in this block
+        uint8_t b[4];
+        if (L == 2) b[0] = (uint8_t)cp;
+        else encode(cp, b);
+        for (int k = 0; k < spill; k++) *spill_bytes |= (uint32_t)b[n - spill + k] << (8 * k);
+      }
+    }
     s += (uint64_t)L;
   }
-  return ov;
+  return ov | (spill << 8);
 }
 
 JT_HD uint64_t low_bits(int n) { return n >= 64 ? ~0ULL : ((1ULL << n) - 1); }
@@ -171,136 +196,58 @@ JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
   return 6;
 }
 
-// String bytes of one block, by segments between escape starts.  Inside a
-// segment the weights are popcounts (4 per opening quote, 1 per string
-// byte) and the payload is copied as runs; each escape start is decoded.
-// kEmit = false measures only.  `byte(k)` returns block-relative byte k
-// (k may run past 63 into the next block), `copy_run(a, w, n)` copies block
-// bytes [a, a+n) to payload offset w, `put(w, b)` stores one payload byte,
-// `mark(p, w)` records index entry p with string offset w.  *err gets the
-// minimum string error position (control byte or invalid escape).
-template <bool kEmit, class Byte, class CopyRun, class Put, class Mark>
-JT_HD uint32_t block_strings(Byte byte, uint64_t blk, uint64_t content, uint64_t openq,
-                             uint64_t E, uint64_t ctl, uint64_t fin, int ov, uint64_t *err,
-                             CopyRun copy_run, Put put, Mark mark) {
-  uint32_t w = 0;
-  if (kEmit && ov > 0) {  // index entries inside the incoming escape (invalid input)
-    uint64_t fm = fin & low_bits(ov);
-    while (fm) {
-      mark(ctz64(fm), 0u);
-      fm &= fm - 1;
-    }
-  }
-  int p = ov;
-  while (p < 64) {
-    const uint64_t from = ~0ULL << p;
-    const uint64_t rest = E & from;
-    const int e = rest ? ctz64(rest) : 64;
-    const uint64_t seg = from & low_bits(e);
-    const uint64_t cseg = content & seg, oseg = openq & seg;
-    const uint64_t cs = ctl & seg;
-    if (cs) {
-      uint64_t x = blk + (uint64_t)ctz64(cs);
-      if (x < *err) *err = x;
-    }
-    if (kEmit) {
-      uint64_t fm = fin & seg;
-      while (fm) {
-        int f = ctz64(fm);
-        uint64_t below = low_bits(f);
-        mark(f, w + 4u * popc64(oseg & below) + popc64(cseg & below));
-        fm &= fm - 1;
-      }
-      uint64_t cm = cseg;
-      while (cm) {
-        int a0 = ctz64(cm);
-        uint64_t sh = cm >> a0;
-        int n = ~sh == 0 ? 64 - a0 : ctz64(~sh);
-        uint64_t below = low_bits(a0);
-        copy_run(a0, w + 4u * popc64(oseg & below) + popc64(cseg & below), n);
-        cm &= ~(low_bits(n) << a0);
-      }
-    }
-    w += 4u * popc64(oseg) + popc64(cseg);
-    if (e >= 64) break;
+// Weight mask of a block with escapes.  Every valid escape sequence
+// [p, p+L) is given the weight of its decoded bytes by counting its first n
+// positions [p, p+n) (n <= L always); its other bytes weigh 0.  Then every
+// block's string-buffer prefix at bit x is 4*popc(openq below x) +
+// popc(W below x), the same formula as for blocks without escapes.  ov_in /
+// vin = input / weight bytes of an escape begun in the previous block.
+// *err gets the minimum invalid-escape position (handle_escape,
+// stringparse.cpp:73-102).
+template <class Byte>
+JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, uint64_t E, int ov_in,
+                              int vin, uint64_t *err) {
+  uint64_t cov = low_bits(ov_in), virt = low_bits(vin);
+  uint64_t rest = E & ~cov;
+  while (rest) {
+    const int p = ctz64(rest);
     uint32_t cp = 0, win[3];
-    byte.window12((uint64_t)e, win);
-    int L = escape_window(win, &cp);
-    if (L == 0) {  // invalid escape: error at the backslash
-      uint64_t x = blk + (uint64_t)e;
-      if (x < *err) *err = x;
-      p = e + 1;
-      continue;
+    byte.window12((uint64_t)p, win);
+    const int L = escape_window(win, &cp);
+    int end = p + 1;
+    if (L == 0) {
+      if (blk + (uint64_t)p < *err) *err = blk + (uint64_t)p;
+    } else {
+      end = p + L;
+      cov |= low_bits(end) & ~low_bits(p);
+      virt |= low_bits(p + out_len(L, cp)) & ~low_bits(p);
     }
-    uint8_t b[4];
-    int n = L == 2 ? (b[0] = (uint8_t)cp, 1) : encode(cp, b);
-    if (kEmit) {
-      for (int k = 0; k < n; k++) put(w + (uint32_t)k, b[k]);
-      uint64_t fm = fin & (low_bits(e + L < 64 ? e + L : 64) & ~low_bits(e + 1));
-      while (fm) {  // index entries inside an escape (invalid input only)
-        mark(ctz64(fm), w + (uint32_t)n);
-        fm &= fm - 1;
-      }
-    }
-    w += (uint32_t)n;
-    p = e + L;
+    rest = E & ~low_bits(end);
   }
-  return w;
+  return (content & ~cov) | virt;
 }
 
-// Slow-path walker over one block.  Calls emit(pos_in_block, byte) for each
-// payload byte in order and mark(pos_in_block, weight_before) for each index
-// entry; returns the block weight.  *err gets the first string error
-// position (absolute) or stays ~0.  `content`, `openq`, `E`, `fin` are the
-// block masks, `ov` the incoming overhang.
-template <class At, class Emit, class Mark>
-JT_HD uint32_t walk_block(At at, uint64_t blk, uint64_t content, uint64_t openq, uint64_t E,
-                          uint64_t ctl, uint64_t fin, int ov, uint64_t *err, Emit emit,
-                          Mark mark) {
-  uint32_t w = 0;
-  int p = 0;
-  // index entries inside the overhang region are impossible in a valid
-  // string; still report them (bounded behaviour on invalid input)
-  while (p < ov && p < 64) {
-    if ((fin >> p) & 1) mark(p, w);
-    p++;
-  }
-  while (p < 64) {
-    if ((fin >> p) & 1) mark(p, w);
-    uint64_t bit = 1ULL << p;
-    if (E & bit) {
-      uint32_t cp;
-      int L = str::escape_at(at, blk + (uint64_t)p, &cp);
-      if (L == 0) {
-        uint64_t e = blk + (uint64_t)p;
-        if (e < *err) *err = e;
-        p++;
-        continue;
-      }
+// Decoded bytes of the block's escapes at their string-buffer offsets
+// (`put(w, b)`, w block-relative), after the plain runs were copied.
+template <class Byte, class Put>
+JT_HD void escape_emit(Byte byte, uint64_t E, int ov_in, uint64_t openq, uint64_t W, Put put) {
+  uint64_t rest = E & ~low_bits(ov_in);
+  while (rest) {
+    const int p = ctz64(rest);
+    uint32_t cp = 0, win[3];
+    byte.window12((uint64_t)p, win);
+    const int L = escape_window(win, &cp);
+    int end = p + 1;
+    if (L != 0) {
       uint8_t b[4];
-      int n = L == 2 ? (b[0] = (uint8_t)cp, 1) : encode(cp, b);
-      for (int k = 0; k < n; k++) emit(w + (uint32_t)k, b[k]);
-      w += (uint32_t)n;
-      // index entries cannot fall inside an escape of a valid string
-      int end = p + L;
-      for (int k = p + 1; k < end && k < 64; k++)
-        if ((fin >> k) & 1) mark(k, w);
-      p = end;
-      continue;
+      const int n = L == 2 ? (b[0] = (uint8_t)cp, 1) : encode(cp, b);
+      const uint64_t below = low_bits(p);
+      const uint32_t w = 4u * popc64(openq & below) + popc64(W & below);
+      for (int k = 0; k < n; k++) put(w + (uint32_t)k, b[k]);
+      end = p + L;
     }
-    if (content & bit) {
-      if (ctl & bit) {
-        uint64_t e = blk + (uint64_t)p;
-        if (e < *err) *err = e;
-      }
-      emit(w, (uint8_t)at(blk + (uint64_t)p));
-      w++;
-    } else if (openq & bit) {
-      w += 4;
-    }
-    p++;
+    rest = E & ~low_bits(end);
   }
-  return w;
 }
 
 }  // namespace sb

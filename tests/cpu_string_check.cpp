@@ -40,7 +40,8 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     uint64_t openq = uq & instr & valid, content = instr & ~openq & valid;
     uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content, ctl = sb::control_mask(m.P) & content;
     int ov_in = ov_prev;
-    int ov_scan = (state & 2) ? sb::overhang_in_scan(at, blk, true) : 0;
+    uint32_t spill_bytes = 0;
+    int ov_scan = (state & 2) ? sb::overhang_in_scan(at, blk, true, &spill_bytes) : 0;
     if (ov_scan != ov_in) *ov_mismatch += 1;
     int rem = (int)(len - blk);
     if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) serr = serr < len ? serr : len;
@@ -56,20 +57,40 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
         }
       }
     } byte{&buf, blk};
-    uint64_t e1 = ~0ULL;
-    uint32_t wm = sb::block_strings<false>(byte, blk, content, openq, E, ctl, fin, ov_in, &e1,
-                                           [](int, uint32_t, int) {}, [](uint32_t, uint8_t) {},
-                                           [](int, uint32_t) {});
-    uint32_t we = sb::block_strings<true>(
-        byte, blk, content, openq, E, ctl, fin, ov_in, &serr,
-        [&](int a0, uint32_t wdst, int nb) { memcpy(out + base + wdst, buf.data() + blk + a0, nb); },
-        [&](uint32_t pos, uint8_t v) { out[base + pos] = v; },
-        [&](int p, uint32_t wb) {
-          idx[n] = (uint32_t)(blk + p);
-          aux[n++] = (uint32_t)(base + wb);
-        });
-    if (wm != we || e1 != (serr < e1 ? e1 : e1)) {}
-    if (wm != we) *ov_mismatch += 1000;
+    // K1's order: weight mask, block weight, runs, escape bytes, entries
+    const int vin = ov_in >> 8, ov = ov_in & 0xFF;
+    if (ctl) {
+      uint64_t x = blk + (uint64_t)ctz64(ctl);
+      if (x < serr) serr = x;
+    }
+    uint64_t W = content;
+    if ((E & ~sb::low_bits(ov)) | (uint64_t)ov) W = sb::escape_weights(byte, blk, content, E, ov, vin, &serr);
+    const uint32_t we = 4u * popc64(openq) + popc64(W);
+    uint64_t cm = W & ~sb::low_bits(vin);
+    while (cm) {
+      const int a0 = ctz64(cm);
+      const uint64_t sh = cm >> a0;
+      const int nb = ~sh == 0 ? 64 - a0 : ctz64(~sh);
+      const uint64_t below = sb::low_bits(a0);
+      memcpy(out + base + 4u * popc64(openq & below) + popc64(W & below), buf.data() + blk + a0, nb);
+      cm &= ~(sb::low_bits(nb) << a0);
+    }
+    // K1 tiles (16 KiB): the first block of a tile writes the bytes an
+    // escape of the previous tile spills into it; that tile's own writes
+    // past its end are dropped (staging)
+    const bool tile_first = (blk % 16384) == 0;
+    const uint64_t tile_end = (blk / 16384) * 16384 + 16384;
+    if (tile_first)
+      for (int k = 0; k < vin; k++) out[base + k] = (uint8_t)(spill_bytes >> (8 * k));
+    sb::escape_emit(byte, E, ov, openq, W, [&](uint32_t pos, uint8_t v) {
+      if (blk + 64 < tile_end || pos < we) out[base + pos] = v;
+    });
+    for (uint64_t fm = fin; fm; fm &= fm - 1) {
+      const int p = ctz64(fm);
+      const uint64_t below = sb::low_bits(p);
+      idx[n] = (uint32_t)(blk + p);
+      aux[n++] = (uint32_t)(base + 4u * popc64(openq & below) + popc64(W & below));
+    }
     sw_total += we;
     ov_prev = E ? sb::overhang_out(at, blk, E) : 0;
     state = s1::apply(f, state);

@@ -132,6 +132,23 @@ def test_configs_small(parser, oracle):
         check_same(parser, oracle, rec, f"C3 record {k}")
 
 
+def test_escape_block_and_tile_boundaries(parser, oracle):
+    """Escapes whose sequence or decoded bytes straddle a 64-byte block or a
+    16 KiB K1 tile boundary (stage1.cu: spill bytes, overhang_in_scan)."""
+    escs = [b"\\n", b"\\u00e9", b"\\u20ac", b"\\ud83d\\ude00", b"\\\\", b"\\u0041"]
+    for boundary in (64, 128, 16384, 32768):
+        for esc in escs:
+            for shift in range(0, 14):
+                pos = boundary - shift  # the escape begins here
+                head = b'["' + b"b" * (pos - 2)
+                doc = head + esc + b"xyz" * 5 + b'", 1]'
+                assert doc.index(esc) == pos
+                check_same(parser, oracle, doc, f"esc {esc!r} at {boundary}-{shift}")
+                # the same escape repeated back to back across the boundary
+                doc2 = head + esc * 8 + b'"]'
+                check_same(parser, oracle, doc2, f"esc run {esc!r} at {boundary}-{shift}")
+
+
 def test_error_sweep(parser, oracle):
     from tools.gen import generate
     for seed in range(1, 200):

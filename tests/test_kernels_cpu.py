@@ -108,6 +108,13 @@ def test_string_emission(string_lib, oracle):
     docs = [generate(c, 1 << 15, seed=s) for c in (0, 1, 4) for s in (1, 2)]
     docs += [generate(4, 1 << 12, seed=s, err=1 + s % 5) for s in range(100)]
     docs += list(_inputs(rng, 1500))
+    # escapes straddling block / 16 KiB tile boundaries (the harness models
+    # K1's tiles: spill bytes written by the next tile's first block)
+    for boundary in (64, 16384):
+        for esc in (b"\\n", b"\\u00e9", b"\\u20ac", b"\\ud83d\\ude00"):
+            for shift in range(0, 14):
+                head = b'["' + b"b" * (boundary - shift - 2)
+                docs += [head + esc + b'xyz", 1]', head + esc * 8 + b'"]']
     for d in docs:
         r = oracle.parse(d)
         if r.code == 1:
