@@ -347,8 +347,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint64_t content = instr & ~openq & valid;
   const uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content;
   const uint64_t ctl = sb::control_mask(m.P) & content;
+  const TileBytes tbyte{s_in, a.in + tile_base, local};
+  sb::EscClass ec{0, 0, 0, 0};
+  if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? tbyte(64) : 0u);
   // escapes reaching into the next block: ov | spill << 8 (strblock.cuh)
-  int ov_out = E ? sb::overhang_out(gat, blk, E) : 0;
+  int ov_out = E ? sb::escape_overhang(gat, blk, ec) : 0;
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
   // unterminated string: the reference reads the NUL padding at len
@@ -371,16 +374,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     if (warp > 0) ov_in = s_warp_ov[warp - 1];
     else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true, &spill_bytes) : 0;
   }
-  const TileBytes tbyte{s_in, a.in + tile_base, local};
   const int vin = ov_in >> 8;
   ov_in &= 0xFF;
   // string weight mask: the plain string bytes, or for blocks with escapes
-  // the decoded-length positions of each escape (strblock.cuh)
-  const bool esc_work = ((E & ~sb::low_bits(ov_in)) | (uint64_t)ov_in) != 0;
+  // the weight positions of each escape (strblock.cuh)
+  if (ov_in) ec = sb::restrict_from(ec, ov_in);
+  const bool esc_work = (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov_in) != 0;
   uint64_t W = content;
   {
     uint64_t serr = ctl ? blk + (uint64_t)ctz64(ctl) : ~0ULL;
-    if (esc_work) W = sb::escape_weights(tbyte, blk, content, E, ov_in, vin, &serr);
+    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr);
     if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
   }
   const uint32_t sw = 4u * popc64(openq) + popc64(W);
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         else s_pay[soff + pos] = b;
       };
       for (int k = 0; k < vin && threadIdx.x == 0; k++) put((uint32_t)k, (uint8_t)(spill_bytes >> (8 * k)));
-      sb::escape_emit(tbyte, E, ov_in, openq, W, put);
+      sb::escape_fixups(tbyte, ec, openq, W, sw, put);
     }
     uint64_t fm = fin;
     uint32_t slot = off;

@@ -68,6 +68,15 @@ JT_HD int out_len(int L, uint32_t cp) {
   return L == 2 ? 1 : cp < 0x80 ? 1 : cp < 0x800 ? 2 : cp < 0x10000 ? 3 : 4;
 }
 
+// Weight positions of a valid escape at p (see escape_weights): a two-byte
+// escape weighs on its second byte [p+1, p+2), so that \\ \" \/ need no
+// rewrite; a \u escape on [p, p+n).  Returns how many of them are >= end.
+JT_HD int spill_of(int p, int L, int n, int end) {
+  if (n == 0) return 0;  // invalid escape: no weight moves
+  const int a = L == 2 ? p + 1 : p, b = a + n;
+  return b > end ? b - (a > end ? a : end) : 0;
+}
+
 // Returns ov | spill << 8: ov = input bytes, spill = weight bytes (see
 // escape_weights) of the last escape that fall into the next block.
 template <class At>
@@ -87,7 +96,7 @@ JT_HD int overhang_out(At at, uint64_t blk, uint64_t E) {
     if (L == 0) L = 2;  // invalid: the document fails anyway; stay bounded
     if (p + L > 64) {
       ov = p + L - 64;
-      spill = p + n > 64 ? p + n - 64 : 0;
+      spill = spill_of(p, L, n, 64);
     }
     p += L;
   }
@@ -143,7 +152,7 @@ JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str, uint32_t *spill_byt
     if (L == 0) L = 2;
     if (s + (uint64_t)L > blk) {
       ov = (int)(s + (uint64_t)L - blk);
-      spill = s + (uint64_t)n > blk ? (int)(s + (uint64_t)n - blk) : 0;
+      spill = spill_of((int)(s - (blk - 64)), L, n, 64);
       *spill_bytes = 0;
       if (spill) {  // decoded bytes n - spill .. n-1 land in this block
         uint8_t b[4];
@@ -196,19 +205,84 @@ JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
   return 6;
 }
 
-// Weight mask of a block with escapes.  Every valid escape sequence
-// [p, p+L) is given the weight of its decoded bytes by counting its first n
-// positions [p, p+n) (n <= L always); its other bytes weigh 0.  Then every
-// block's string-buffer prefix at bit x is 4*popc(openq below x) +
-// popc(W below x), the same formula as for blocks without escapes.  ov_in /
-// vin = input / weight bytes of an escape begun in the previous block.
-// *err gets the minimum invalid-escape position (handle_escape,
+// Escape starts of a block by the class of the following byte: two-byte
+// escapes whose output is that byte (\" \\ \/), two-byte escapes that are
+// translated (\b \f \n \r \t), \u escapes, and invalid ones (handle_escape,
 // stringparse.cpp:73-102).
+struct EscClass {
+  uint64_t sim, tr, u, bad;
+};
+
+// 0 if c is not a two-byte escape letter, else the decoded byte
+JT_HD uint32_t simple_decode(uint32_t c) {
+  switch (c) {
+    case '"': return '"';
+    case '\\': return '\\';
+    case '/': return '/';
+    case 'b': return 0x08;
+    case 'f': return 0x0C;
+    case 'n': return 0x0A;
+    case 'r': return 0x0D;
+    case 't': return 0x09;
+    default: return 0;
+  }
+}
+
+// E = escape starts; c64 = the byte after bit 63 (next block's byte 0).
+JT_HD EscClass classify_escapes(const uint64_t P[8], uint64_t qt, uint64_t bs, uint64_t E,
+                                uint32_t c64) {
+  const uint64_t n7 = ~P[7], n6 = ~P[6], n5 = ~P[5], n4 = ~P[4], n3 = ~P[3], n2 = ~P[2],
+                 n1 = ~P[1], n0 = ~P[0];
+  const uint64_t slash = n7 & n6 & P[5] & n4 & P[3] & P[2] & P[1] & P[0];  // 0x2F
+  const uint64_t h6 = n7 & P[6] & P[5] & n4;                              // 0x6_
+  const uint64_t h7 = n7 & P[6] & P[5] & P[4];                            // 0x7_
+  const uint64_t lb = h6 & n3 & n2 & P[1] & n0;                           // b 0x62
+  const uint64_t lf = h6 & n3 & P[2] & P[1] & n0;                         // f 0x66
+  const uint64_t ln = h6 & P[3] & P[2] & P[1] & n0;                       // n 0x6E
+  const uint64_t lr = h7 & n3 & n2 & P[1] & n0;                           // r 0x72
+  const uint64_t lt = h7 & n3 & P[2] & n1 & n0;                           // t 0x74
+  const uint64_t lu = h7 & n3 & P[2] & n1 & P[0];                         // u 0x75
+  const uint64_t S = qt | bs | slash, T = lb | lf | ln | lr | lt;
+  const uint32_t d64 = simple_decode(c64);
+  const uint64_t s64 = (d64 != 0 && (c64 == '"' || c64 == '\\' || c64 == '/')) ? 1 : 0;
+  const uint64_t t64 = (d64 != 0 && !s64) ? 1 : 0, u64 = c64 == 'u' ? 1 : 0;
+  const uint64_t nS = (S >> 1) | (s64 << 63), nT = (T >> 1) | (t64 << 63),
+                 nU = (lu >> 1) | (u64 << 63);
+  return EscClass{E & nS, E & nT, E & nU, E & ~(nS | nT | nU)};
+}
+
+JT_HD EscClass restrict_from(const EscClass &c, int ov_in) {
+  const uint64_t k = ~low_bits(ov_in);
+  return EscClass{c.sim & k, c.tr & k, c.u & k, c.bad & k};
+}
+
+// ov | spill << 8 of a block's escapes (see overhang_out).  A two-byte escape
+// at bit 63 covers the next block's byte 0, which also carries its weight.
+template <class At>
+JT_HD int escape_overhang(At at, uint64_t blk, const EscClass &c) {
+  if ((c.sim | c.tr) >> 63) return 1 | (1 << 8);
+  if (c.bad >> 63) return 1;
+  return c.u ? overhang_out(at, blk, c.u) : 0;
+}
+
+// Weight mask of a block with escapes.  Every valid escape sequence [p, p+L)
+// carries the weight of its decoded bytes on n of its own positions: the
+// second byte of a two-byte escape (so that \\ \" \/ are already right when
+// the plain runs are copied), the first n bytes of a \u escape; its other
+// bytes weigh 0.  Then every block's string-buffer prefix at bit x is
+// 4*popc(openq below x) + popc(W below x), the same formula as for blocks
+// without escapes.  ov_in / vin = input / weight bytes of an escape begun in
+// the previous block; c must be restrict_from(ov_in).  *err gets the
+// minimum invalid-escape position.
 template <class Byte>
-JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, uint64_t E, int ov_in,
+JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const EscClass &c, int ov_in,
                               int vin, uint64_t *err) {
-  uint64_t cov = low_bits(ov_in), virt = low_bits(vin);
-  uint64_t rest = E & ~cov;
+  uint64_t cov = low_bits(ov_in) | c.sim | c.tr, virt = low_bits(vin);
+  if (c.bad) {
+    const uint64_t x = blk + (uint64_t)ctz64(c.bad);
+    if (x < *err) *err = x;
+  }
+  uint64_t rest = c.u;
   while (rest) {
     const int p = ctz64(rest);
     uint32_t cp = 0, win[3];
@@ -222,16 +296,26 @@ JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, uint64_
       cov |= low_bits(end) & ~low_bits(p);
       virt |= low_bits(p + out_len(L, cp)) & ~low_bits(p);
     }
-    rest = E & ~low_bits(end);
+    rest = c.u & ~low_bits(end);
   }
   return (content & ~cov) | virt;
 }
 
-// Decoded bytes of the block's escapes at their string-buffer offsets
-// (`put(w, b)`, w block-relative), after the plain runs were copied.
+// Decoded bytes that the plain-run copy did not produce: translated two-byte
+// escapes, a two-byte escape at bit 63 (its byte belongs to the next block's
+// weight, which that block does not copy), and \u escapes.  `put(w, b)`, w
+// block-relative; sw = the block's total weight.
 template <class Byte, class Put>
-JT_HD void escape_emit(Byte byte, uint64_t E, int ov_in, uint64_t openq, uint64_t W, Put put) {
-  uint64_t rest = E & ~low_bits(ov_in);
+JT_HD void escape_fixups(Byte byte, const EscClass &c, uint64_t openq, uint64_t W, uint32_t sw,
+                         Put put) {
+  uint64_t t = c.tr | (c.sim & (1ULL << 63));
+  while (t) {
+    const int q = ctz64(t) + 1;
+    t &= t - 1;
+    const uint32_t w = q < 64 ? 4u * popc64(openq & low_bits(q)) + popc64(W & low_bits(q)) : sw;
+    put(w, (uint8_t)simple_decode(byte((uint64_t)q)));
+  }
+  uint64_t rest = c.u;
   while (rest) {
     const int p = ctz64(rest);
     uint32_t cp = 0, win[3];
@@ -240,13 +324,13 @@ JT_HD void escape_emit(Byte byte, uint64_t E, int ov_in, uint64_t openq, uint64_
     int end = p + 1;
     if (L != 0) {
       uint8_t b[4];
-      const int n = L == 2 ? (b[0] = (uint8_t)cp, 1) : encode(cp, b);
+      const int n = encode(cp, b);
       const uint64_t below = low_bits(p);
       const uint32_t w = 4u * popc64(openq & below) + popc64(W & below);
       for (int k = 0; k < n; k++) put(w + (uint32_t)k, b[k]);
       end = p + L;
     }
-    rest = E & ~low_bits(end);
+    rest = c.u & ~low_bits(end);
   }
 }
 

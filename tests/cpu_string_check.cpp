@@ -39,6 +39,9 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     uint64_t fin = s1::final_mask(m, esc0, tog, state, valid);
     uint64_t openq = uq & instr & valid, content = instr & ~openq & valid;
     uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content, ctl = sb::control_mask(m.P) & content;
+    sb::EscClass ec{0, 0, 0, 0};
+    if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? at(blk + 64) : 0u);
+    const sb::EscClass ec_full = ec;
     int ov_in = ov_prev;
     uint32_t spill_bytes = 0;
     int ov_scan = (state & 2) ? sb::overhang_in_scan(at, blk, true, &spill_bytes) : 0;
@@ -63,8 +66,9 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
       uint64_t x = blk + (uint64_t)ctz64(ctl);
       if (x < serr) serr = x;
     }
+    if (ov) ec = sb::restrict_from(ec, ov);
     uint64_t W = content;
-    if ((E & ~sb::low_bits(ov)) | (uint64_t)ov) W = sb::escape_weights(byte, blk, content, E, ov, vin, &serr);
+    if (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov) W = sb::escape_weights(byte, blk, content, ec, ov, vin, &serr);
     const uint32_t we = 4u * popc64(openq) + popc64(W);
     uint64_t cm = W & ~sb::low_bits(vin);
     while (cm) {
@@ -82,7 +86,7 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     const uint64_t tile_end = (blk / 16384) * 16384 + 16384;
     if (tile_first)
       for (int k = 0; k < vin; k++) out[base + k] = (uint8_t)(spill_bytes >> (8 * k));
-    sb::escape_emit(byte, E, ov, openq, W, [&](uint32_t pos, uint8_t v) {
+    sb::escape_fixups(byte, ec, openq, W, we, [&](uint32_t pos, uint8_t v) {
       if (blk + 64 < tile_end || pos < we) out[base + pos] = v;
     });
     for (uint64_t fm = fin; fm; fm &= fm - 1) {
@@ -92,7 +96,7 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
       aux[n++] = (uint32_t)(base + 4u * popc64(openq & below) + popc64(W & below));
     }
     sw_total += we;
-    ov_prev = E ? sb::overhang_out(at, blk, E) : 0;
+    ov_prev = E ? sb::escape_overhang(at, blk, ec_full) : 0;
     state = s1::apply(f, state);
   }
   // stage 2's share: length fields from aux differences
