@@ -54,6 +54,28 @@ int jt_b200_last_launches(const jt_parser *p);
 void jt_b200_profile(jt_parser *p, int enable);
 int jt_b200_kernel_times(jt_parser *p, float *ms, int max);
 
+/* ---- Byte-range sharding of one document across GPUs ----
+ * Shard g of G parses bytes [begin, end) of a document whose len bytes are
+ * resident in the parser's input buffer (jt_b200_input_buffer /
+ * jt_b200_copy_in).  begin is a multiple of 16384; shard 0 starts at 0 and
+ * shard G-1 ends at len.  Four phases, each enqueued asynchronously on the
+ * parser's stream, write a fixed-size summary (jt_b200_shard_summary_bytes)
+ * to a caller device buffer; the caller all-gathers the G summaries of a
+ * phase (NCCL all_gather, or device copies when emulating shards on one
+ * GPU) and passes them to the next phase.  Replaces, for one document, the
+ * single sequential pass of jt_parse (proj/src/capi.cpp:70-93; carries as in
+ * blocks.h:31-35 and tape_builder.cpp:140-258). */
+size_t jt_b200_shard_summary_bytes(int phase);
+int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end);
+int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *summary);
+/* Document result (same code/offset as jt_parse of the whole document); waits. */
+jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *error_offset);
+/* out[7]: document tape index of local word out[1], local words, document
+ * string offset of local byte 0, string bytes, first token index, tokens. */
+int jt_b200_shard_extent(const jt_parser *p, unsigned long long *out);
+/* Copy this shard's tape words and string bytes (sizes from the extent) to host. */
+int jt_b200_shard_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
+
 /* CUDA device ordinal the parser was created on. */
 int jt_b200_device(const jt_parser *p);
 

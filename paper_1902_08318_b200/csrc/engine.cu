@@ -30,6 +30,7 @@
 namespace {
 
 constexpr size_t kPad = 64;  // proj/src/indexer.h:17
+constexpr size_t kShardBoundOff = (sizeof(jt::Shard) + 255) & ~(size_t)255;
 
 struct DevBuf {
   void *p = nullptr;
@@ -100,6 +101,12 @@ struct jt_parser {
     uint64_t sig = 0;
     int launches = 0;
   } graph[2];
+  // byte-range shard of a document (shard.h), between jt_b200_shard_begin
+  // and jt_b200_shard_finish
+  bool shard_on = false;
+  jt::Shard *h_shard = nullptr;  // pinned
+  DevBuf shard;                  // Shard + open-container stack
+  uint64_t shard_len = 0;        // document length
   // optional per-kernel timing: ev[0] before init, then one per launch
   bool prof = false;
   cudaEvent_t ev[8] = {};
@@ -168,8 +175,11 @@ bool ensure_stage2(jt_parser *p, uint64_t len) {
   return ok;
 }
 
-jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
+jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0,
+                       uint64_t end = ~0ULL) {
   jt::Stage1Args a{};
+  a.begin = begin;
+  a.end = end == ~0ULL ? len : end;
   jt::Ctrl *c = p->ctrl.as<jt::Ctrl>();
   a.in = p->in.as<uint8_t>();
   a.len = len;
@@ -179,7 +189,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.tokrec = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
   a.tile_flags = p->tile_flags.as<uint32_t>();
-  uint64_t nt = jt::stage1_records(len);
+  uint64_t nt = jt::stage1_records(a.end - a.begin);
   a.fn = (uint32_t *)p->s1rec.as<uint64_t>();  // 2 x ntiles u32 in the ntiles-word channel-1 area
   a.carry = a.fn + nt;
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
@@ -189,10 +199,14 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which) {
   a.total = &c->S;
   a.total_strings = &c->string_bytes;
   a.tape_words = &c->tape_words;
+  a.depth_total = &c->depth_total;
   return a;
 }
 
-jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
+// cap_len: bytes whose tokens this parse handles (the shard's range, or len)
+jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len = ~0ULL,
+                       bool sharded = false) {
+  if (cap_len == ~0ULL) cap_len = len;
   jt::Stage2Args a{};
   a.in = p->in.as<uint8_t>();
   a.len = len;
@@ -202,7 +216,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.tok = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
   a.tile_flags = p->tile_flags.as<uint32_t>();
-  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  jt::Stage2Sizes z = jt::stage2_sizes(cap_len + 16);
   a.m1 = p->m1.as<int16_t>();
   a.m2 = p->m2.as<int16_t>();
   a.m3 = p->s2rec.as<int32_t>();
@@ -214,8 +228,12 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which) {
   a.stk_rec = (uint64_t *)((uint8_t *)p->s2rec.p + ((z.n3 * sizeof(int32_t) + 64 + 63) & ~(size_t)63));
   a.tape = p->tape.as<uint64_t>();
   a.strings = p->strings.as<uint8_t>();
-  a.cap_tokens = len + 16;
+  a.cap_tokens = cap_len + 16;
   a.num_sms = p->num_sms;
+  if (sharded) {
+    a.sh = p->shard.as<jt::Shard>();
+    a.bound = (uint64_t *)(p->shard.as<uint8_t>() + kShardBoundOff);
+  }
   return a;
 }
 
@@ -423,6 +441,7 @@ void jt_parser_free(jt_parser *p) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
   if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
+  if (p->h_shard) cudaFreeHost(p->h_shard);
   delete p;
 }
 
@@ -762,6 +781,182 @@ jt_error jt_b200_download(jt_parser *p, jt_document **out) {
 
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
   p->stream = cuda_stream ? (cudaStream_t)cuda_stream : p->own_stream;
+}
+
+// ---- byte-range shards (shard.h, include/jsontape_b200.h) -------------------
+
+size_t jt_b200_shard_summary_bytes(int phase) {
+  switch (phase) {
+    case 0: return sizeof(jt::Sum0);
+    case 1: return sizeof(jt::Sum1);
+    case 2: return sizeof(jt::Sum2);
+    case 3: return sizeof(jt::Sum3);
+    default: return 0;
+  }
+}
+
+int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
+  if (G == 0 || g >= G || (uint64_t)len >= (1ULL << 32) || begin % jt::kStage1Tile != 0 ||
+      !(begin < end) || end > len || (g + 1 == G) != (end == len) || (g == 0) != (begin == 0)) {
+    p->err = "shard_begin: bad shard layout";
+    return -1;
+  }
+  if (!p->h_shard && cudaMallocHost((void **)&p->h_shard, sizeof(jt::Shard)) != cudaSuccess) {
+    cudaGetLastError();
+    p->h_shard = nullptr;
+    p->err = "shard_begin: pinned allocation";
+    return -1;
+  }
+  const uint64_t range = end - begin;
+  if (!ensure_input(p, len) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
+      !p->shard.ensure(kShardBoundOff + jt::kBoundMax * sizeof(uint64_t))) {
+    p->err = "shard_begin: device allocation";
+    return -1;
+  }
+  jt::Shard h{};
+  h.g = g;
+  h.G = G;
+  h.begin = begin;
+  h.end = end;
+  h.len = len;
+  *p->h_shard = h;
+  if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
+                                  p->stream),
+               "shard upload"))
+    return -1;
+  p->shard_on = true;
+  p->shard_len = len;
+  p->in_len = len;
+  p->cur = 0;
+  p->last_ok = false;
+  p->have_index = false;
+  p->h_index_valid = false;
+  return 0;
+}
+
+// Enqueue phase 0..3 of this shard (shard.h).  `gathered` = device pointer
+// to the G summaries of the previous phase (ignored for phase 0); this
+// phase's summary goes to the device pointer `summary`.
+int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *summary) {
+  if (!p->shard_on || !summary || (phase > 0 && !gathered)) {
+    p->err = "shard_phase: no shard or missing buffers";
+    return -1;
+  }
+  const jt::Shard &h = *p->h_shard;
+  const uint64_t len = p->shard_len, range = h.end - h.begin;
+  int n = 0;
+  bool ok = true;
+  switch (phase) {
+    case 0: {
+      jt::Stage2Sizes z = jt::stage2_sizes(range + 16);
+      uint64_t s1w = jt::stage1_records(range) * 9;
+      uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((range + 16) / 256 + 2) * 4;
+      ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
+                                      p->s2rec.as<uint64_t>(), s2w, p->stream),
+                   "init") &&
+           cuda_ok(p, jt::stage1_shard_phase0(s1_args(p, len, 0, h.begin, h.end), (jt::Sum0 *)summary,
+                                              p->stream),
+                   "shard phase 0");
+      n = 3;
+      break;
+    }
+    case 1:
+      ok = cuda_ok(p, jt::stage1_shard_phase1(s1_args(p, len, 0, h.begin, h.end),
+                                              (const jt::Sum0 *)gathered, h.g, p->stream),
+                   "shard phase 1") &&
+           cuda_ok(p, jt::shard_sum1_launch(s2_args(p, len, 0, range, true), (jt::Sum1 *)summary, p->stream),
+                   "shard sum1");
+      n = 3;
+      break;
+    case 2:
+      ok = cuda_ok(p, jt::shard_phase2_launch(s2_args(p, len, 0, range, true), (const jt::Sum1 *)gathered,
+                                              (jt::Sum2 *)summary, p->stream, &n),
+                   "shard phase 2");
+      break;
+    case 3: {
+      jt::Stage2Args a = s2_args(p, len, 0, range, true);
+      a.sum3 = (jt::Sum3 *)summary;
+      ok = cuda_ok(p, jt::shard_phase3_launch(a, (const jt::Sum2 *)gathered, p->stream, &n),
+                   "shard phase 3");
+      break;
+    }
+    default:
+      p->err = "shard_phase: phase must be 0..3";
+      return -1;
+  }
+  p->launches = phase == 0 ? n : p->launches + n;
+  return ok ? 0 : -1;
+}
+
+// Global result from the gathered phase-3 summaries; waits for the shard's
+// stream.  On JT_OK this shard's tape words and string bytes stay on the
+// device (jt_b200_device_tape / _strings, placed by jt_b200_shard_extent).
+jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *error_offset) {
+  if (!p->shard_on || !gathered) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  const jt::Shard &h = *p->h_shard;
+  const uint64_t range = h.end - h.begin;
+  if (!cuda_ok(p, jt::shard_finish_launch(s2_args(p, p->shard_len, 0, range, true),
+                                          (const jt::Sum3 *)gathered, p->stream),
+               "shard finish") ||
+      !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl D2H") ||
+      !cuda_ok(p, cudaMemcpyAsync(p->h_shard, p->shard.p, sizeof(jt::Shard), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "shard D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  p->launches += 1;
+  const jt::Ctrl &c = *p->h_ctrl;
+  set_off(error_offset, c.offset);
+  if (c.code != jt::kUtf8Error) {
+    p->have_index = true;
+    p->index_count = c.S;
+    p->h_index_valid = false;
+  }
+  p->last_ok = c.code == jt::kOk;
+  return (jt_error)c.code;
+}
+
+// Where this shard's results sit in the document: out[0] = document tape
+// index of local tape word out[1], out[2] = local words from there, out[3] =
+// document string offset of local string byte 0, out[4] = string bytes,
+// out[5] = document index of the shard's first token, out[6] = its tokens.
+int jt_b200_shard_extent(const jt_parser *p, unsigned long long *out) {
+  if (!p->shard_on || !p->h_shard) return -1;
+  const jt::Shard &h = *p->h_shard;
+  const jt::Ctrl &c = *p->h_ctrl;
+  const uint64_t lo = h.g == 0 ? 0 : 1;
+  const uint64_t hi = c.tape_words + (h.is_last ? 1 : 0);  // local words [lo, hi)
+  out[0] = h.tape_base + lo;
+  out[1] = lo;
+  out[2] = hi - lo;
+  out[3] = h.string_base;
+  out[4] = c.string_bytes;
+  out[5] = h.token_base;
+  out[6] = c.S;
+  return 0;
+}
+
+// Copy this shard's tape words (extent out[2] words) and string bytes
+// (out[4]) into host buffers.
+int jt_b200_shard_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {
+  unsigned long long e[7];
+  if (jt_b200_shard_extent(p, e) != 0) return -1;
+  if (e[2] && !cuda_ok(p, cudaMemcpyAsync(tape, p->tape.as<uint64_t>() + e[1], e[2] * 8,
+                                          cudaMemcpyDeviceToHost, p->stream),
+                       "shard tape D2H"))
+    return -1;
+  if (e[4] && !cuda_ok(p, cudaMemcpyAsync(strings, p->strings.p, e[4], cudaMemcpyDeviceToHost,
+                                          p->stream),
+                       "shard strings D2H"))
+    return -1;
+  return cuda_ok(p, cudaStreamSynchronize(p->stream), "sync") ? 0 : -1;
 }
 
 int jt_b200_last_launches(const jt_parser *p) { return p->launches; }

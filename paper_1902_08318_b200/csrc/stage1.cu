@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "lookback.cuh"
+#include "shard.h"
 #include "stage1.h"
 #include "stage1_block.cuh"
 #include "strblock.cuh"
@@ -125,7 +126,9 @@ __device__ __forceinline__ int tok_delta(uint32_t c) {
   return (c == '{' || c == '[') ? 1 : (c == '}' || c == ']') ? -1 : 0;
 }
 
-__device__ __forceinline__ int clamp16(long long d) { return d < -2 ? -2 : d > 1026 ? 1026 : (int)d; }
+// depth_before, relative to the range start (a shard adds its base in stage
+// 2); clamped where the document has already failed (|d| > kMaxDepth + base)
+__device__ __forceinline__ int clamp16(long long d) { return d < -8192 ? -8192 : d > 8192 ? 8192 : (int)d; }
 
 // ---- K0: carry-in of every tile (reduce-then-scan) --------------------------
 // The tile carry (odd backslash run, in-string, previous byte a separator;
@@ -169,11 +172,14 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint
   }
 }
 
-// K0b: carry-in of every tile = (f[t-1] o ... o f[0])(kInitState); one CTA,
-// each thread a contiguous chunk of tiles
+// K0b: carry-in of every tile = (f[t-1] o ... o f[0])(init); one CTA, each
+// thread a contiguous chunk of tiles.  init = kInitState, or for shard g the
+// state after shards 0..g-1 (their composed functions, `gathered`).  With
+// carry == nullptr it only writes the composition of all tiles (*total).
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn, uint32_t *carry,
-                                                             uint64_t ntiles) {
+                                                             uint64_t ntiles, const Sum0 *gathered,
+                                                             uint32_t g, Sum0 *total) {
   __shared__ uint32_t s_agg[kScanThreads / 32];
   __shared__ uint32_t s_has[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -208,8 +214,24 @@ __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn,
     s_has[warp] = has;
   }
   __syncthreads();
-  // exclusive prefix state of this thread: earlier warps, then earlier lanes
+  if (carry == nullptr) {
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      bool th = false;
+      for (int k = 0; k < kScanThreads / 32; k++)
+        if (s_has[k]) {
+          t = th ? s1::compose(s_agg[k], t) : s_agg[k];
+          th = true;
+        }
+      total->fn = t;  // a range has at least one tile
+    }
+    return;
+  }
+  // exclusive prefix state of this thread: earlier shards, earlier warps,
+  // then earlier lanes
   uint32_t state = s1::kInitState;
+  if (gathered)
+    for (uint32_t h = 0; h < g; h++) state = s1::apply(gathered[h].fn, state);
   for (int k = 0; k < warp; k++)
     if (s_has[k]) state = s1::apply(s_agg[k], state);
   uint32_t ex = __shfl_up_sync(0xffffffffu, acc, 1);
@@ -248,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
   __syncthreads();
-  const int64_t tile = s_tile;
+  const int64_t tile = s_tile;  // tile of the range; byte offset below is global
   if (threadIdx.x == 0) {
     JT_TL(tile, 0);
 #ifdef JT_TIMELINE
@@ -257,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     JT_TLV(tile, 8, smid);
 #endif
   }
-  const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
+  const uint64_t tile_base = a.begin + (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
   const uint32_t local = threadIdx.x * 64;
   const GlobalAt gat{a.in};
@@ -457,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         *a.total = inc.v[0];
         *a.total_strings = inc.v[1];
         *a.tape_words = 1 + inc.v[2];
+        *a.depth_total = sext63(inc.v[3]);
       }
     }
   };
@@ -613,16 +636,38 @@ cudaError_t stage1_configure() {
   return configured;
 }
 
-cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
+static Stage1Args with_tiles(const Stage1Args &args_in) {
   Stage1Args a = args_in;
-  uint64_t ntiles = (a.len + kStage1Tile - 1) / kStage1Tile;
+  uint64_t ntiles = (a.end - a.begin + kStage1Tile - 1) / kStage1Tile;
   if (ntiles == 0) ntiles = 1;
   a.ntiles = ntiles;
+  return a;
+}
+
+cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
   const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
-  k_carry_fn<<<(unsigned)ntiles, kFnThreads, 0, stream>>>(a.in, a.fn);
-  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, ntiles);
-  k_stage1<<<(unsigned)ntiles, kThreads, kSmemBytes, stream>>>(a);
+  k_carry_fn<<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr);
+  k_stage1<<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_shard_phase0(const Stage1Args &args_in, Sum0 *out, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  k_carry_fn<<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, nullptr, a.ntiles, nullptr, 0, out);
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_shard_phase1(const Stage1Args &args_in, const Sum0 *gathered, uint32_t g,
+                                cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  const cudaError_t configured = stage1_configure();
+  if (configured != cudaSuccess) return configured;
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, gathered, g, nullptr);
+  k_stage1<<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,9 @@ struct Stage1Args {
   uint64_t *total;                // S
   uint64_t *total_strings;        // string buffer bytes
   uint64_t *tape_words;           // 1 + sum of token widths
-  uint64_t ntiles;                // filled by stage1_launch
+  int64_t *depth_total;           // depth change over the range
+  uint64_t begin, end;            // byte range [begin, end): a shard, or [0, len)
+  uint64_t ntiles;                // filled by the launchers
 };
 
 // number of tiles for `len` (look-back records: 1 + 8 words per tile)
@@ -40,6 +42,13 @@ size_t stage1_records(uint64_t len);
 
 constexpr int kStage1Launches = 3;  // K0a carry functions, K0b carry scan, K1
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
+
+struct Sum0;
+// sharded stage 1 (shard.h): phase 0 = K0a + the shard's composed carry
+// function; phase 1 = carry-in from all shards' functions, K0b, K1
+cudaError_t stage1_shard_phase0(const Stage1Args &args, Sum0 *out, cudaStream_t stream);
+cudaError_t stage1_shard_phase1(const Stage1Args &args, const Sum0 *gathered, uint32_t g,
+                                cudaStream_t stream);
 
 // one-time kernel attributes (dynamic shared memory); call outside capture
 cudaError_t stage1_configure();

@@ -81,6 +81,47 @@ __device__ __forceinline__ int tok_depth(uint32_t v) { return (int)(int16_t)(v >
 
 __device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v << 1) >> 1; }
 
+// This shard's place in the document (shard.h); the whole document when
+// unsharded.  Token / tape / string indices inside the kernels stay local;
+// the bases turn them into document values where they are written.
+struct View {
+  bool sharded, is_last;
+  uint64_t begin, token_base, tape_base, string_base, S_total, next_pos, next_aux;
+  int64_t depth_base;
+  uint32_t prev[2], prev_n;
+  uint64_t S0;
+  int open_n;
+};
+
+__device__ View view_of(const Stage2Args &a) {
+  View v{};
+  const Ctrl *c = a.ctrl;
+  if (a.sh != nullptr && a.sh->G > 0) {
+    const Shard *h = a.sh;
+    v.sharded = true;
+    v.is_last = h->is_last != 0;
+    v.begin = h->begin;
+    v.token_base = h->token_base;
+    v.tape_base = h->tape_base;
+    v.string_base = h->string_base;
+    v.S_total = h->S_total;
+    v.next_pos = h->next_pos;
+    v.next_aux = h->next_aux;
+    v.depth_base = h->depth_base;
+    v.prev[0] = h->prev[0];
+    v.prev[1] = h->prev[1];
+    v.prev_n = h->prev_n;
+    v.S0 = h->S0;
+    v.open_n = h->open_n;
+  } else {
+    v.is_last = true;
+    v.S_total = c->S;
+    v.next_pos = a.len + 1;
+    v.next_aux = c->string_bytes;
+  }
+  return v;
+}
+
 // ---- K2: scalars, one thread per token ---------------------------------
 
 // Stack of container kinds as a 64-bit shift register: bit 0 = innermost
@@ -234,6 +275,7 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   const uint64_t S = ctrl->S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
+  const View vw = view_of(a);
   for (;;) {
     if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->stk_tile_counter, 1u);
     __syncthreads();
@@ -283,12 +325,12 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
     if (lane == 31) s_wt[warp] = inc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax);
+    if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax + (int)vw.depth_base);
     __syncthreads();
     if (warp == 0) {
       StackT agg = s_wt[0];
       for (int k = 1; k < 8; k++) agg = stack_compose(s_wt[k], agg);
-      uint64_t S0 = 0;
+      uint64_t S0 = vw.S0;  // containers open at the shard start (0 unsharded)
       if (tile > 0) {
         if (lane == 0) stk_publish_agg(a.stk_rec, tile, agg);
         S0 = stk_lookback(a.stk_rec, (int64_t)tile);
@@ -322,7 +364,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const unsigned long long str_err = ctrl->str_err;
-  const uint32_t total_sb = (uint32_t)ctrl->string_bytes;
+  const View vw = view_of(a);
   const InAt at{a.in};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t stride = (uint64_t)gridDim.x * 256;
@@ -342,14 +384,15 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
       uint32_t fail = 0;
       if (c == '"') {
         const uint32_t p = a.idx[i];
-        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : a.len + 1;
+        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : vw.next_pos;
         fail = str_err >= p && str_err < end;  // the failing string holds the minimum
         if (!fail) {
           const uint32_t so = a.aux[i];
           // stage 1 wrote the length unless the next token is in another
           // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
-          if (end > a.len || (p >> 14) != ((uint32_t)end >> 14) || a.tile_flags[p >> 14]) {
-            const uint32_t nx = i + 1 < S ? a.aux[i + 1] : total_sb;
+          const uint64_t lt = (p - vw.begin) >> 14;
+          if (end > a.len || lt != ((end - vw.begin) >> 14) || a.tile_flags[lt]) {
+            const uint32_t nx = i + 1 < S ? a.aux[i + 1] : (uint32_t)vw.next_aux;
             const uint32_t len = nx - so - 4;
             uint8_t *f = a.strings + so;
             f[0] = (uint8_t)len;
@@ -357,7 +400,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
             f[2] = (uint8_t)(len >> 16);
             f[3] = (uint8_t)(len >> 24);
           }
-          a.tape[a.tape_idx[i]] = tape_word('"', so);
+          a.tape[a.tape_idx[i]] = tape_word('"', vw.string_base + so);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
         const uint32_t p = a.idx[i];
@@ -602,11 +645,40 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   const uint64_t S = ctrl->S;
   const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
   const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
-  auto scope_obj = [&](int64_t j) -> bool {  // innermost container of token j is an object
-    if (shallow) return (a.scopebits[j >> 5] >> (j & 31)) & 1;  // 16-bit words, same bit order
-    int64_t o = psv(a, j, tok_depth(a.tok[j]) - 1);
-    return o >= 0 && (a.tok[o] & 0xFF) == '{';
+  const View vw = view_of(a);
+  const int db = (int)vw.depth_base;
+  // container open at document level L before this shard (shard.h)
+  auto bound_at = [&](int L, uint64_t *tape, bool *obj) -> bool {
+    if (!vw.sharded || L < 0 || L >= vw.open_n) return false;
+    const uint64_t e = a.bound[L];
+    *tape = e & ((1ULL << 56) - 1);
+    *obj = (e >> 56) == '{';
+    return true;
   };
+  auto scope_obj = [&](int64_t j) -> bool {  // innermost container of token j is an object
+    if (j < 0) {  // a token of an earlier shard: the innermost container at the boundary
+      uint64_t tp;
+      bool ob = false;
+      return bound_at(vw.open_n - 1, &tp, &ob) && ob;
+    }
+    if (shallow) return (a.scopebits[j >> 5] >> (j & 31)) & 1;  // 16-bit words, same bit order
+    const int D = tok_depth(a.tok[j]);
+    int64_t o = psv(a, j, D - 1);
+    if (o < 0) {
+      uint64_t tp;
+      bool ob = false;
+      return bound_at(D + db - 1, &tp, &ob) && ob;
+    }
+    return (a.tok[o] & 0xFF) == '{';
+  };
+  // token j's record; j < 0: the tokens before the shard (byte only)
+  auto rec_at = [&](int64_t j, uint64_t tbase) -> uint32_t {
+    if (j >= (int64_t)tbase) return s_tok[j - tbase];
+    if (j >= 0) return a.tok[j];
+    return vw.prev[-j - 1];
+  };
+  const int64_t before = vw.sharded ? (int64_t)vw.prev_n : 0;  // tokens before the shard
+  const uint64_t tb = vw.tape_base;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t tbase = tile * kK3Tile;
     {
@@ -642,11 +714,11 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     const uint64_t i1 = min(i0 + kK3Tok, S);
     if (i0 < S) do {
     const uint32_t *recs = s_tok + threadIdx.x * kK3Tok;
-    uint32_t t = a.tape_idx[i0];
+    uint32_t t = a.tape_idx[i0];  // local tape index (document index = tb + t)
     // entry state from the two previous tokens (A.5 arrival rules)
     int mode = M_V;
-    if (i0 > 0) {
-      uint32_t v1 = i0 - 1 >= tbase ? s_tok[i0 - 1 - tbase] : a.tok[i0 - 1];
+    if ((int64_t)i0 + before > 0) {
+      uint32_t v1 = rec_at((int64_t)i0 - 1, tbase);
       uint32_t c1 = v1 & 0xFF;
       if (c1 == '{') mode = M_OF;
       else if (c1 == '[') mode = M_AF;
@@ -655,8 +727,8 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
         mode = scope_obj((int64_t)i0 - 1) ? M_K : M_V;
       } else if (c1 == '"') {
         mode = M_A;
-        if (i0 >= 2) {
-          uint32_t v2 = i0 - 2 >= tbase ? s_tok[i0 - 2 - tbase] : a.tok[i0 - 2];
+        if ((int64_t)i0 + before >= 2) {
+          uint32_t v2 = rec_at((int64_t)i0 - 2, tbase);
           uint32_t c2 = v2 & 0xFF;
           if (c2 == '{') mode = M_C;
           else if (c2 == ',') {
@@ -668,10 +740,10 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
       }
     }
 
-    uint32_t stk[kK3Tok];  // local openers: tape index | is_object << 31
+    uint32_t stk[kK3Tok];  // local openers: local tape index | is_object << 31
     int sp = 0;
     int far_level = -100;  // cache of the last far container lookup
-    uint32_t far_tape = 0;
+    uint64_t far_tape = 0;  // document tape index
     bool far_obj = false;
     int err = 0;
     uint64_t i = i0;
@@ -681,13 +753,13 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
       const uint32_t v = recs[k];
       const uint32_t c = v & 0xFF;
       const bool fail = (v >> 8) & 1;
-      const int D = tok_depth(v);
+      const int D = tok_depth(v) + db;  // document depth
       depth_after = D + tok_delta(c);
       bool again;
       do {
         again = false;
         bool close = false, have_top = false, top_obj = false;
-        uint32_t top_tape = 0;
+        uint64_t top_tape = 0;  // document tape index of the enclosing opener
         bool top_local = false;
         switch (mode) {
           case M_V:
@@ -715,9 +787,9 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
               top_obj = mode == M_OF;
               if (sp > 0) {
                 top_local = true;
-                top_tape = stk[sp - 1] & 0x7FFFFFFFu;
+                top_tape = tb + (stk[sp - 1] & 0x7FFFFFFFu);
               } else {
-                top_tape = t - 1;  // the opener is the previous token
+                top_tape = tb + t - 1;  // the opener is the previous token
               }
             } else {
               mode = mode == M_OF ? M_K : M_V;
@@ -741,20 +813,21 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
             }
             if (sp > 0) {
               top_local = true;
-              top_tape = stk[sp - 1] & 0x7FFFFFFFu;
+              top_tape = tb + (stk[sp - 1] & 0x7FFFFFFFu);
               top_obj = stk[sp - 1] >> 31;
             } else if (shallow && c == ',') {
               top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
             } else {
               if (far_level != D - 1) {
-                int64_t j = psv_tile(a, T, (int64_t)i, D - 1);
-                if (j < 0) {
+                int64_t j = psv_tile(a, T, (int64_t)i, D - 1 - db);
+                if (j >= 0) {
+                  far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
+                  far_tape = tb + tape_of(a, j);
+                } else if (!bound_at(D - 1, &far_tape, &far_obj)) {
                   err = kTapeError;
                   break;
                 }
                 far_level = D - 1;
-                far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
-                far_tape = tape_of(a, j);
               }
               top_tape = far_tape;
               top_obj = far_obj;
@@ -770,7 +843,16 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
           if (top_local) sp--;
           else far_level = -100;
           a.tape[t] = tape_word((uint8_t)c, top_tape);
-          a.tape[top_tape] = tape_word(top_obj ? '{' : '[', t + 1);
+          const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1);
+          if (top_tape > tb) {
+            a.tape[top_tape - tb] = ow;
+          } else {  // the opener lives in an earlier shard: patched after the last exchange
+            const uint32_t k = atomicAdd(&a.sum3->patch_n, 1u);
+            if (k < (uint32_t)kBoundMax) {
+              a.sum3->patch[2 * k] = top_tape;
+              a.sum3->patch[2 * k + 1] = ow;
+            }
+          }
           mode = M_A;
         }
       } while (again && !err);
@@ -779,10 +861,11 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
       i++;
     }
     if (err) {
-      report(ctrl, i, err);
+      report(ctrl, vw.token_base + i, err);
       break;
     }
-    if (i1 == S && !(mode == M_A && depth_after == 0)) report(ctrl, S, kTapeError);
+    if (i1 == S && vw.is_last && !(mode == M_A && depth_after == 0))
+      report(ctrl, vw.token_base + S, kTapeError);
     } while (false);
     __syncthreads();
   }
@@ -841,6 +924,211 @@ __global__ void k_init(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *
   }
 }
 
+// ---- shards (shard.h) -------------------------------------------------------
+
+// phase-1 summary of this shard (after K1)
+__global__ void k_sum1(Stage2Args a, Sum1 *out) {
+  const Ctrl *c = a.ctrl;
+  Sum1 r{};
+  r.S = c->S;
+  r.sb = c->string_bytes;
+  r.T = c->tape_words - 1;
+  r.dtotal = c->depth_total;
+  r.utf8_pos = c->utf8_pos;
+  r.str_err = c->str_err;
+  r.first_pos = r.S ? a.idx[0] : 0;
+  r.first_aux = r.S ? a.aux[0] : 0;
+  r.last[0] = r.S >= 1 ? (a.tok[r.S - 1] & 0xFF) : 0;
+  r.last[1] = r.S >= 2 ? (a.tok[r.S - 2] & 0xFF) : 0;
+  *out = r;
+}
+
+// bases of shard g from all phase-1 summaries; document-wide first UTF-8
+// and string errors into the control block (stage 2 reads them there)
+__global__ void k_apply1(Stage2Args a, const Sum1 *gs) {
+  Shard *h = a.sh;
+  Ctrl *c = a.ctrl;
+  const uint32_t g = h->g, G = h->G;
+  uint64_t tok = 0, tape = 0, str = 0, S = 0, T = 0, sb = 0;
+  int64_t dep = 0;
+  unsigned long long u8 = ~0ULL, se = ~0ULL;
+  for (uint32_t k = 0; k < G; k++) {
+    if (k == g) {
+      h->token_base = tok;
+      h->tape_base = tape;
+      h->string_base = str;
+      h->depth_base = dep;
+    }
+    tok += gs[k].S;
+    tape += gs[k].T;
+    str += gs[k].sb;
+    dep += gs[k].dtotal;
+    S += gs[k].S;
+    T += gs[k].T;
+    sb += gs[k].sb;
+    if (gs[k].utf8_pos < u8) u8 = gs[k].utf8_pos;
+    if (gs[k].str_err < se) se = gs[k].str_err;
+  }
+  h->S_total = S;
+  h->E_total = 1 + T;
+  h->sb_total = sb;
+  h->is_last = g + 1 == G;
+  // the next shard that has a token
+  h->next_pos = h->len + 1;
+  h->next_aux = sb - h->string_base;
+  uint64_t run = 0;
+  for (uint32_t k = g; k < G; k++) {
+    if (k > g && gs[k].S > 0) {
+      h->next_pos = gs[k].first_pos;
+      h->next_aux = run + gs[k].first_aux;
+      break;
+    }
+    run += gs[k].sb;
+  }
+  // the two tokens before the shard
+  uint32_t n = 0;
+  h->prev[0] = h->prev[1] = 0;
+  for (int k = (int)g - 1; k >= 0 && n < 2; --k) {
+    if (gs[k].S >= 1 && n < 2) h->prev[n++] = gs[k].last[0];
+    if (gs[k].S >= 2 && n < 2) h->prev[n++] = gs[k].last[1];
+  }
+  h->prev_n = n;
+  c->utf8_pos = u8;
+  c->str_err = se;
+}
+
+// containers opened in this shard and still open at its end (outermost
+// first), and how many closers pop containers opened before it
+__global__ void __launch_bounds__(1024) k_bound(Stage2Args a, Sum2 *out) {
+  __shared__ int s_min;
+  const Ctrl *c = a.ctrl;
+  const uint64_t S = c->S;
+  const View vw = view_of(a);
+  const int fin = (int)c->depth_total;
+  if (threadIdx.x == 0) s_min = fin < 0 ? fin : 0;  // depth_before of token 0 is 0
+  __syncthreads();
+  if (c->utf8_pos == ~0ULL && S > 0) {
+    const uint64_t n3 = (S + 4095) / 4096;
+    int m = 0x7FFF;
+    for (uint64_t k = threadIdx.x; k < n3; k += blockDim.x) m = min(m, 0x7FFF - a.m3[k]);
+    atomicMin(&s_min, m);
+  }
+  __syncthreads();
+  const int mn = s_min;
+  int n = fin - mn;
+  if (n > kBoundMax) n = kBoundMax;  // deeper than kMaxDepth: the document fails anyway
+  if (c->utf8_pos != ~0ULL) n = 0;
+  if (threadIdx.x == 0) {
+    out->unmatched = -mn;
+    out->n = n;
+  }
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int64_t j = psv(a, (int64_t)S, mn + k);
+    uint64_t e = 0;
+    if (j >= 0) e = ((uint64_t)(a.tok[j] & 0xFF) << 56) | (vw.tape_base + a.tape_idx[j]);
+    out->open[k] = e;
+  }
+}
+
+// containers open at the start of shard g: walking the earlier shards
+// backwards, each keeps the openers that later closers do not pop
+__global__ void __launch_bounds__(1024) k_apply2(Stage2Args a, const Sum2 *gs) {
+  __shared__ int s_keep[64], s_at[64];
+  __shared__ int s_n;
+  Shard *h = a.sh;
+  const uint32_t g = h->g;
+  if (threadIdx.x == 0) {
+    long long pop = 0;
+    for (int k = (int)g - 1; k >= 0; --k) {
+      const long long nk = gs[k].n;
+      const long long keep = nk > pop ? nk - pop : 0;
+      pop = (pop > nk ? pop - nk : 0) + gs[k].unmatched;
+      if (k < 64) s_keep[k] = (int)keep;
+    }
+    int at = 0;
+    for (uint32_t k = 0; k < g && k < 64; k++) {
+      s_at[k] = at;
+      at += s_keep[k];
+    }
+    s_n = at < kBoundMax ? at : kBoundMax;
+    a.sum3->patch_n = 0;
+  }
+  __syncthreads();
+  for (uint32_t k = 0; k < g && k < 64; k++)
+    for (int e = threadIdx.x; e < s_keep[k]; e += blockDim.x)
+      if (s_at[k] + e < kBoundMax) a.bound[s_at[k] + e] = gs[k].open[e];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int n = s_n;
+    uint64_t S0 = 0;
+    for (int k = 0; k < 64 && k < n; k++) S0 |= (uint64_t)((a.bound[n - 1 - k] >> 56) == '{') << k;
+    h->S0 = S0;
+    h->open_n = n;
+  }
+}
+
+// this shard's first error (document token numbering) and root words
+__global__ void k_final_shard(Stage2Args a) {
+  const Ctrl *c = a.ctrl;
+  const View vw = view_of(a);
+  Sum3 *r = a.sum3;
+  r->err_key = ~0ULL;
+  r->offset = -1;
+  if (c->utf8_pos != ~0ULL) return;
+  if (c->err_key != ~0ULL) {
+    const uint64_t i = c->err_key >> 8;
+    const int code = (int)(c->err_key & 0xFF);
+    r->err_key = c->err_key;
+    if (i >= vw.S_total) r->offset = (long long)a.len;
+    else if (code == kStringError) r->offset = (long long)c->str_err;
+    else r->offset = (long long)a.idx[i - vw.token_base];
+  }
+  const uint64_t E = a.sh->E_total;
+  if (vw.token_base == 0 && vw.tape_base == 0 && a.sh->g == 0) a.tape[0] = tape_word(kTagRoot, E);
+  if (vw.is_last) a.tape[E - vw.tape_base] = tape_word(kTagRoot, 0);
+}
+
+// document result from all shards' first errors; bracket patches into this
+// shard's part of the tape
+__global__ void __launch_bounds__(256) k_shard_finish(Stage2Args a, const Sum3 *gs) {
+  Ctrl *c = a.ctrl;
+  Shard *h = a.sh;
+  const uint32_t G = h->G;
+  if (threadIdx.x == 0) {
+    if (c->utf8_pos != ~0ULL) {
+      c->code = kUtf8Error;
+      c->offset = (long long)c->utf8_pos;
+    } else if (h->S_total == 0) {
+      c->code = kEmpty;
+      c->offset = -1;
+    } else {
+      unsigned long long best = ~0ULL;
+      long long off = -1;
+      for (uint32_t k = 0; k < G; k++)
+        if (gs[k].err_key < best) {
+          best = gs[k].err_key;
+          off = gs[k].offset;
+        }
+      if (best != ~0ULL) {
+        c->code = (int)(best & 0xFF);
+        c->offset = off;
+      } else {
+        c->code = kOk;
+        c->offset = -1;
+      }
+    }
+  }
+  if (c->utf8_pos != ~0ULL) return;
+  const uint64_t lo = h->tape_base, hi = h->tape_base + c->tape_words;  // local words [1, tape_words)
+  for (uint32_t k = 0; k < G; k++) {
+    const uint32_t n = gs[k].patch_n < (uint32_t)kBoundMax ? gs[k].patch_n : (uint32_t)kBoundMax;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const uint64_t at = gs[k].patch[2 * e];
+      if (at > lo && at < hi) a.tape[at - lo] = gs[k].patch[2 * e + 1];
+    }
+  }
+}
+
 __global__ void k_stage1_final(Ctrl *c) {
   if (c->utf8_pos != ~0ULL) {
     c->code = kUtf8Error;
@@ -886,6 +1174,60 @@ cudaError_t stage1_finalize_launch(Ctrl *ctrl, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+static unsigned grid_tokens(const Stage2Args &a) {
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  uint64_t g = (a.cap_tokens + 255) / 256;
+  unsigned g2 = (unsigned)(g < (uint64_t)sms * 16 ? g : (uint64_t)sms * 16);
+  return g2 < 1 ? 1 : g2;
+}
+
+static void launch_stack(const Stage2Args &a, cudaStream_t stream) {
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  uint64_t nst = (a.cap_tokens + 4095) / 4096;
+  unsigned gs = (unsigned)(nst < (uint64_t)sms * 4 ? nst : (uint64_t)sms * 4);
+  k_stack<<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
+}
+
+static void launch_struct(const Stage2Args &a, cudaStream_t stream) {
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  uint64_t nt = (a.cap_tokens + kK3Tile - 1) / kK3Tile;
+  unsigned g3 = (unsigned)(nt < (uint64_t)sms * 4 ? nt : (uint64_t)sms * 4);
+  k_struct<<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+}
+
+cudaError_t shard_sum1_launch(const Stage2Args &a, Sum1 *out, cudaStream_t stream) {
+  k_sum1<<<1, 1, 0, stream>>>(a, out);
+  return cudaGetLastError();
+}
+
+cudaError_t shard_phase2_launch(const Stage2Args &a, const Sum1 *gathered, Sum2 *out,
+                                cudaStream_t stream, int *launches) {
+  const unsigned g2 = grid_tokens(a);
+  k_apply1<<<1, 1, 0, stream>>>(a, gathered);
+  k_scalars<<<g2, 256, 0, stream>>>(a);
+  k_numbers<<<g2, 256, 0, stream>>>(a);
+  k_slow<<<8, 64, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
+  k_bound<<<1, 1024, 0, stream>>>(a, out);
+  *launches = 6;
+  return cudaGetLastError();
+}
+
+cudaError_t shard_phase3_launch(const Stage2Args &a, const Sum2 *gathered, cudaStream_t stream,
+                                int *launches) {
+  k_apply2<<<1, 1024, 0, stream>>>(a, gathered);
+  launch_stack(a, stream);
+  launch_struct(a, stream);
+  k_final_shard<<<1, 1, 0, stream>>>(a);
+  *launches = 4;
+  return cudaGetLastError();
+}
+
+cudaError_t shard_finish_launch(const Stage2Args &a, const Sum3 *gathered, cudaStream_t stream) {
+  k_shard_finish<<<1, 256, 0, stream>>>(a, gathered);
+  return cudaGetLastError();
+}
+
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
                           cudaEvent_t *ev) {
   const Stage2Sizes z = stage2_sizes(a.cap_tokens);
@@ -894,11 +1236,6 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   uint64_t g = (a.cap_tokens + 255) / 256;
   unsigned g2 = (unsigned)(g < (uint64_t)sms * 16 ? g : (uint64_t)sms * 16);
   if (g2 < 1) g2 = 1;
-  {
-    uint64_t nst = (a.cap_tokens + 4095) / 4096;
-    unsigned gs = (unsigned)(nst < (uint64_t)sms * 4 ? nst : (uint64_t)sms * 4);
-    k_stack<<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
-  }
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[0], stream);
@@ -906,11 +1243,8 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[1], stream);
   k_tree<<<1, 1024, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
-  {
-    uint64_t nt = (a.cap_tokens + kK3Tile - 1) / kK3Tile;
-    unsigned g3 = (unsigned)(nt < (uint64_t)sms * 4 ? nt : (uint64_t)sms * 4);
-    k_struct<<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
-  }
+  launch_stack(a, stream);  // container kinds (scope bits) for k_struct
+  launch_struct(a, stream);
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[4], stream);

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "shard.h"
+
 namespace jt {
 
 constexpr int kTokPerThread = 16;                       // one "chunk"
@@ -31,6 +33,7 @@ struct Ctrl {
   uint64_t tape_words;          // E = 1 + sum of token widths (root close index)
   uint64_t string_bytes;        // string buffer size (stage 1)
   unsigned long long str_err;   // min string error position (~0 = none)
+  int64_t depth_total;          // depth change over the (shard's) tokens
   // results written by the finalize kernel
   int32_t code;
   int32_t pad2;
@@ -60,6 +63,10 @@ struct Stage2Args {
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
   uint64_t cap_tokens;  // capacity bound on S (for grid sizing)
   int num_sms;
+  // byte-range sharding (shard.h); sh == nullptr: unsharded
+  Shard *sh;
+  uint64_t *bound;      // kBoundMax: containers open at the shard start (kind << 56 | tape)
+  Sum3 *sum3;           // phase-3 summary (error, cross-shard bracket patches)
 };
 
 // words of look-back records / tree nodes needed for up to `cap` tokens
@@ -74,6 +81,18 @@ Stage2Sizes stage2_sizes(uint64_t cap_tokens);
 // `ev` (optional, 5 events) is recorded after each of the 5 kernels.
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
                           cudaEvent_t *ev = nullptr);
+
+// Sharded stage 2 (shard.h).  phase 2: bases from the gathered Sum1s, then
+// scalars / numbers / depth tree and this shard's open containers (Sum2);
+// phase 3: the container stack at the shard start from the gathered Sum2s,
+// then stack scan, structure and the local first error (Sum3).
+cudaError_t shard_sum1_launch(const Stage2Args &a, Sum1 *out, cudaStream_t stream);
+cudaError_t shard_phase2_launch(const Stage2Args &a, const Sum1 *gathered, Sum2 *out,
+                                cudaStream_t stream, int *launches);
+cudaError_t shard_phase3_launch(const Stage2Args &a, const Sum2 *gathered, cudaStream_t stream,
+                                int *launches);
+// global first error and the bracket patches that land in this shard
+cudaError_t shard_finish_launch(const Stage2Args &a, const Sum3 *gathered, cudaStream_t stream);
 
 // Reset kernel for the control block + look-back records.
 cudaError_t init_launch(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,
