@@ -13,9 +13,12 @@ full parse (stage 1 + stage 2, the jt_parse path) of that document.
   roofline = dominant kernel: algorithmic bytes / its event-timed duration
   cpu_baseline = the unmodified reference (oracle/_ref) on 1 core
 
-N > 1 (torchrun): each rank parses its own copy of the document (replicas,
-weak scaling; the single-document path has no cross-GPU exchange in this
-round); value = all ranks' bytes / max-over-ranks time.
+N > 1 (torchrun, one process per GPU): ONE document of N x 64 MiB, split
+into N tile-aligned byte ranges; rank g parses shard g (paper_1902_08318_b200
+.shard: four phases with an NCCL all_gather of a small summary after each:
+carry functions, counts, open-container stacks, first error + bracket
+patches).  Per-GPU work is fixed as N grows (weak scaling); value = document
+bytes / max-over-ranks device time.  --shard runs this path at N = 1 too.
 
 --impl reference: the reference's own CPU parser (oracle/_ref, jt_parse) on
 the same document, rank 0 only.
@@ -182,6 +185,112 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank: int, world: int, local: int, torch, dist):
+    """One document, world byte-range shards, NCCL exchanges (see header)."""
+    from paper_1902_08318_b200 import Parser
+    from paper_1902_08318_b200 import shard as SH
+    from tools.gen import generate
+    size = args.size or SIZE
+    data = generate(args.config, size * world)
+    n = len(data)
+    begin, end = SH.layout(n, world)[rank]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    p = Parser()
+    p.set_stream(stream.cuda_stream)
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    p.copy_in(host.data_ptr(), n)  # whole document resident: the halo is everything
+    torch.cuda.synchronize()
+    if dist is None:  # --shard at N = 1: a one-rank NCCL group for the same exchanges
+        import torch.distributed as D
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        D.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        dist = D
+    ex = SH.nccl_exchange(dist, world)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    name, off = SH.run_shard(p, n, rank, world, ex)
+    assert name == "OK", (name, off)
+    ext = SH.extent(p)  # tape words ext[2], string bytes ext[4], tokens ext[6]
+    launches = p.last_launches()
+    for _ in range(args.warmup):
+        flush.zero_()
+        assert SH.run_shard(p, n, rank, world, ex)[0] == "OK"
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        clk.wait_first()
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            mark = (lambda ph, k=k: mids[k].record(stream) if ph == 1 else None)
+            assert SH.run_shard(p, n, rank, world, ex, mark=mark)[0] == "OK"
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    s1_ms = statistics.median(s.elapsed_time(m) for s, m in zip(starts, mids))
+    tot_ms = max_over_ranks(sum(step_ms), dist, "cuda")
+    value = n * args.steps / (tot_ms / 1e3) / 1e9
+
+    # e2e: pinned host bytes of this shard (+64 B before, 64 KiB after) -> device,
+    # sharded parse, this shard's tape words and string bytes -> pinned host
+    lo, hi = max(0, begin - 64), min(n, end + (64 << 10))
+    tape_h = torch.empty(max(1, ext[2]) * 8, dtype=torch.uint8).pin_memory()
+    str_h = torch.empty(max(1, ext[4]), dtype=torch.uint8).pin_memory()
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        assert p._lib.jt_b200_copy_in_range(p._h, host.data_ptr(), lo, hi - lo) == 0
+        assert SH.run_shard(p, n, rank, world, ex)[0] == "OK"
+        assert p._lib.jt_b200_shard_download(p._h, tape_h.data_ptr(), str_h.data_ptr()) == 0
+        e1.record(stream)
+        e1.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_tot = max_over_ranks(sum(e2e_ms), dist, "cuda")
+    e2e_v = n * args.steps / (e2e_tot / 1e3) / 1e9
+
+    peak, peak_src = peaks()
+    rn = end - begin
+    B1 = rn + 4 * ext[6]
+    B2 = rn + 8 * ext[2] + ext[4]
+    per_step = tot_ms / args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": (WORKLOAD if args.config == CONFIG else f"config {args.config}")
+                       + f"; one document of {world} x {size} bytes, {world} byte-range shards",
+                       "bytes": n, "shard_bytes": rn,
+                       "l2": "flushed before every step (256 MiB memset, outside the events)",
+                       "parallelism": f"{world} shards (NCCL all_gather x4 per parse)"},
+            "stage1_gbs": n / (s1_ms / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "full parse of rank 0's shard",
+                         "achieved": B2 / (per_step / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": B2 / (per_step / 1e3) / 1e9 / peak, "traffic": None,
+                         "peak_source": peak_src},
+            "roofline_stage1": {"achieved": B1 / (s1_ms / 1e3) / 1e9,
+                                "frac": B1 / (s1_ms / 1e3) / 1e9 / peak, "bytes": B1},
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_v, "unit": "GB/s", "h2d_bytes_per_step": hi - lo,
+                    "d2h_bytes_per_step": 8 * ext[2] + ext[4]},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,6 +300,7 @@ def main():
     ap.add_argument("--config", type=int, default=CONFIG)
     ap.add_argument("--size", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="byte-range shard path even at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,6 +316,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if world > 1 or args.shard:
+        return run_sharded(args, rank, world, local, torch, dist)
 
     from paper_1902_08318_b200 import Parser
     from tools.gen import generate

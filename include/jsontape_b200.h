@@ -73,6 +73,9 @@ jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *err
 /* out[7]: document tape index of local word out[1], local words, document
  * string offset of local byte 0, string bytes, first token index, tokens. */
 int jt_b200_shard_extent(const jt_parser *p, unsigned long long *out);
+/* Enqueue (no wait) a copy of bytes [offset, offset + n) of a host or device
+ * document into the same positions of the input buffer (a shard's range). */
+int jt_b200_copy_in_range(jt_parser *p, const void *src, size_t offset, size_t n);
 /* Copy this shard's tape words and string bytes (sizes from the extent) to host. */
 int jt_b200_shard_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
 

@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <charconv>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -61,9 +63,85 @@ struct DevBuf {
 
 }  // namespace
 
+namespace {
+
+// Host storage of documents: page-locked blocks from a process-wide pool, so
+// the tape and string buffer come back from HBM at full PCIe/C2C speed and a
+// document costs no page faults or zero fill (a std::vector would do both).
+// Blocks are size classes (powers of two >= 1 MiB), recycled on
+// jt_document_free from any thread, never returned to the OS.
+struct PinnedPool {
+  std::mutex m;
+  std::multimap<size_t, void *> free_blocks;
+  static PinnedPool &get() {
+    static PinnedPool pool;
+    return pool;
+  }
+  void *take(size_t bytes, size_t *cap, bool *pinned) {
+    size_t c = (size_t)1 << 20;
+    while (c < bytes) c <<= 1;
+    *cap = c;
+    {
+      std::lock_guard<std::mutex> g(m);
+      auto it = free_blocks.find(c);
+      if (it != free_blocks.end()) {
+        void *b = it->second;
+        free_blocks.erase(it);
+        *pinned = true;
+        return b;
+      }
+    }
+    void *b = nullptr;
+    if (cudaMallocHost(&b, c) == cudaSuccess) {
+      *pinned = true;
+      return b;
+    }
+    cudaGetLastError();
+    *pinned = false;  // pageable fallback, freed with free()
+    return malloc(c);
+  }
+  void give(void *b, size_t cap) {
+    std::lock_guard<std::mutex> g(m);
+    free_blocks.emplace(cap, b);
+  }
+};
+
+// vector-like view of part of a document block
+template <class T>
+struct Span {
+  T *p = nullptr;
+  size_t n = 0;
+  size_t size() const { return n; }
+  T *data() const { return p; }
+  const T &operator[](size_t i) const { return p[i]; }
+  const T *begin() const { return p; }
+  const T *end() const { return p + n; }
+  bool operator==(const Span &o) const { return n == o.n && (n == 0 || memcmp(p, o.p, n * sizeof(T)) == 0); }
+};
+
+}  // namespace
+
+// Layout read by paper_1902_08318_b200/jsontape.py (Document): tape pointer,
+// words, strings pointer, bytes.
 struct jt_document {
-  std::vector<uint64_t> tape;
-  std::vector<uint8_t> strings;
+  Span<uint64_t> tape;
+  Span<uint8_t> strings;
+  void *block = nullptr;
+  size_t block_cap = 0;
+  bool pinned = false;
+  ~jt_document() {
+    if (!block) return;
+    if (pinned) PinnedPool::get().give(block, block_cap);
+    else free(block);
+  }
+  bool alloc(size_t words, size_t bytes) {
+    const size_t tb = (words * 8 + 63) & ~(size_t)63;
+    block = PinnedPool::get().take(tb + bytes + 64, &block_cap, &pinned);
+    if (!block) return false;
+    tape = Span<uint64_t>{(uint64_t *)block, words};
+    strings = Span<uint8_t>{(uint8_t *)block + tb, bytes};
+    return true;
+  }
 };
 
 struct jt_parser {
@@ -361,10 +439,7 @@ bool upload(jt_parser *p, const char *data, size_t len) {
 jt_document *download(jt_parser *p) {
   jt_document *d = new (std::nothrow) jt_document;
   if (!d) return nullptr;
-  try {
-    d->tape.resize(p->last_tape_len);
-    d->strings.resize(p->last_string_bytes);
-  } catch (...) {
+  if (!d->alloc(p->last_tape_len, p->last_string_bytes)) {
     delete d;
     return nullptr;
   }
@@ -715,6 +790,17 @@ int jt_b200_copy_in(jt_parser *p, const void *src, size_t len) {
     return -1;
   p->in_len = len;
   return cuda_ok(p, cudaStreamSynchronize(p->stream), "sync") ? 0 : -1;
+}
+
+// Enqueue (no wait) a copy of bytes [offset, offset + n) of a host or device
+// document `src` into the same positions of the input buffer.
+int jt_b200_copy_in_range(jt_parser *p, const void *src, size_t offset, size_t n) {
+  if (offset + n > p->in.cap) return -1;
+  if (n && !cuda_ok(p, cudaMemcpyAsync(p->in.as<uint8_t>() + offset, (const uint8_t *)src + offset, n,
+                                       cudaMemcpyDefault, p->stream),
+                    "copy_in_range"))
+    return -1;
+  return 0;
 }
 
 jt_error jt_b200_stage1_resident(jt_parser *p, size_t len, long long *error_offset) {

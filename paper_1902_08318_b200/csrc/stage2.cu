@@ -636,6 +636,7 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
   return psv(a, T.base, L);
 }
 
+template <bool kShard>
 __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   __shared__ __align__(16) uint32_t s_tok[kK3Tile];
   __shared__ int16_t s_l1[256];
@@ -645,27 +646,46 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   const uint64_t S = ctrl->S;
   const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
   const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
-  const View vw = view_of(a);
-  const int db = (int)vw.depth_base;
+  // this shard's place in the document, as scalars (a View captured by the
+  // lambdas below would live in local memory)
+  // (tape indices fit 32 bits: tape_idx is u32)
+  constexpr bool sharded = kShard;
+  bool is_last = true;
+  int db = 0, open_n = 0;
+  uint32_t tb = 0;
+  uint64_t token_base = 0;
+  uint32_t prev0 = 0, prev1 = 0;
+  int64_t before = 0;
+  if (kShard) {
+    const View vw = view_of(a);
+    is_last = vw.is_last;
+    db = (int)vw.depth_base;
+    open_n = vw.open_n;
+    tb = (uint32_t)vw.tape_base;
+    token_base = vw.token_base;
+    prev0 = vw.prev[0];
+    prev1 = vw.prev[1];
+    before = (int64_t)vw.prev_n;  // tokens before the shard
+  }
   // container open at document level L before this shard (shard.h)
-  auto bound_at = [&](int L, uint64_t *tape, bool *obj) -> bool {
-    if (!vw.sharded || L < 0 || L >= vw.open_n) return false;
+  auto bound_at = [&](int L, uint32_t *tape, bool *obj) -> bool {
+    if (!sharded || L < 0 || L >= open_n) return false;
     const uint64_t e = a.bound[L];
-    *tape = e & ((1ULL << 56) - 1);
+    *tape = (uint32_t)(e & ((1ULL << 56) - 1));
     *obj = (e >> 56) == '{';
     return true;
   };
   auto scope_obj = [&](int64_t j) -> bool {  // innermost container of token j is an object
     if (j < 0) {  // a token of an earlier shard: the innermost container at the boundary
-      uint64_t tp;
+      uint32_t tp;
       bool ob = false;
-      return bound_at(vw.open_n - 1, &tp, &ob) && ob;
+      return bound_at(open_n - 1, &tp, &ob) && ob;
     }
     if (shallow) return (a.scopebits[j >> 5] >> (j & 31)) & 1;  // 16-bit words, same bit order
     const int D = tok_depth(a.tok[j]);
     int64_t o = psv(a, j, D - 1);
     if (o < 0) {
-      uint64_t tp;
+      uint32_t tp;
       bool ob = false;
       return bound_at(D + db - 1, &tp, &ob) && ob;
     }
@@ -675,10 +695,8 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   auto rec_at = [&](int64_t j, uint64_t tbase) -> uint32_t {
     if (j >= (int64_t)tbase) return s_tok[j - tbase];
     if (j >= 0) return a.tok[j];
-    return vw.prev[-j - 1];
+    return j == -1 ? prev0 : prev1;
   };
-  const int64_t before = vw.sharded ? (int64_t)vw.prev_n : 0;  // tokens before the shard
-  const uint64_t tb = vw.tape_base;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t tbase = tile * kK3Tile;
     {
@@ -743,7 +761,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     uint32_t stk[kK3Tok];  // local openers: local tape index | is_object << 31
     int sp = 0;
     int far_level = -100;  // cache of the last far container lookup
-    uint64_t far_tape = 0;  // document tape index
+    uint32_t far_tape = 0;  // document tape index
     bool far_obj = false;
     int err = 0;
     uint64_t i = i0;
@@ -759,7 +777,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
       do {
         again = false;
         bool close = false, have_top = false, top_obj = false;
-        uint64_t top_tape = 0;  // document tape index of the enclosing opener
+        uint32_t top_tape = 0;  // document tape index of the enclosing opener
         bool top_local = false;
         switch (mode) {
           case M_V:
@@ -844,7 +862,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
           else far_level = -100;
           a.tape[t] = tape_word((uint8_t)c, top_tape);
           const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1);
-          if (top_tape > tb) {
+          if (!kShard || top_tape > tb) {
             a.tape[top_tape - tb] = ow;
           } else {  // the opener lives in an earlier shard: patched after the last exchange
             const uint32_t k = atomicAdd(&a.sum3->patch_n, 1u);
@@ -861,11 +879,11 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
       i++;
     }
     if (err) {
-      report(ctrl, vw.token_base + i, err);
+      report(ctrl, token_base + i, err);
       break;
     }
-    if (i1 == S && vw.is_last && !(mode == M_A && depth_after == 0))
-      report(ctrl, vw.token_base + S, kTapeError);
+    if (i1 == S && is_last && !(mode == M_A && depth_after == 0))
+      report(ctrl, token_base + S, kTapeError);
     } while (false);
     __syncthreads();
   }
@@ -1192,7 +1210,8 @@ static void launch_struct(const Stage2Args &a, cudaStream_t stream) {
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
   uint64_t nt = (a.cap_tokens + kK3Tile - 1) / kK3Tile;
   unsigned g3 = (unsigned)(nt < (uint64_t)sms * 4 ? nt : (uint64_t)sms * 4);
-  k_struct<<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  if (a.sh) k_struct<true><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  else k_struct<false><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
 }
 
 cudaError_t shard_sum1_launch(const Stage2Args &a, Sum1 *out, cudaStream_t stream) {

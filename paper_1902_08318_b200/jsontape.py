@@ -35,7 +35,7 @@ EXPORTS = [
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
-    "jt_b200_shard_download",
+    "jt_b200_shard_download", "jt_b200_copy_in_range",
 ]
 KERNELS = ["init", "stage1", "tokens", "slow", "tree", "struct", "final"]
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_finish.argtypes = [vp, vp, C.POINTER(ll)]
     L.jt_b200_shard_extent.argtypes = [vp, C.POINTER(C.c_ulonglong)]
     L.jt_b200_shard_download.argtypes = [vp, vp, vp]
+    L.jt_b200_copy_in_range.argtypes = [vp, vp, sz, sz]
     _lib = L
     return L
 
@@ -117,20 +118,18 @@ class Document:
             self._h = None
 
     def _raw(self):
-        # jt_document = {std::vector<u64> tape; std::vector<u8> strings}
-        w = (C.c_uint64 * 6).from_address(self._h)
-        return list(w)
+        # jt_document (engine.cu): {u64 *tape; size_t words; u8 *strings; size_t bytes; ...}
+        return list((C.c_uint64 * 4).from_address(self._h))
 
     @property
     def tape(self) -> np.ndarray:
-        tb, te = self._raw()[0:2]
-        return np.frombuffer(C.string_at(tb, te - tb), dtype=np.uint64) if te > tb else \
-            np.zeros(0, np.uint64)
+        tp, tn = self._raw()[0:2]
+        return np.frombuffer(C.string_at(tp, tn * 8), dtype=np.uint64) if tn else np.zeros(0, np.uint64)
 
     @property
     def strings(self) -> bytes:
-        sb, se = self._raw()[3:5]
-        return C.string_at(sb, se - sb) if se > sb else b""
+        sp, sn = self._raw()[2:4]
+        return C.string_at(sp, sn) if sn else b""
 
     def dump(self) -> str:
         s = self._lib.jt_document_dump(self._h)

@@ -60,10 +60,11 @@ def _finish(parser: Parser, gathered) -> tuple[str, int]:
     return ERROR_NAMES[code], off.value
 
 
-def run_shard(parser: Parser, length: int, g: int, G: int, exchange, device=None):
+def run_shard(parser: Parser, length: int, g: int, G: int, exchange, device=None, mark=None):
     """Parse shard g of G of the `length` bytes resident in `parser`'s input
     buffer; `exchange(phase, local)` returns the G gathered summaries as one
-    uint8 CUDA tensor.  Returns (error name, offset) for the whole document."""
+    uint8 CUDA tensor.  Returns (error name, offset) for the whole document.
+    `mark(phase)` (optional) is called after each phase's exchange."""
     import torch
     stream = torch.cuda.current_stream()
     if stream.cuda_stream == 0:
@@ -76,6 +77,8 @@ def run_shard(parser: Parser, length: int, g: int, G: int, exchange, device=None
         out = torch.empty(summary_bytes(k), dtype=torch.uint8, device=device or "cuda")
         _phase(parser, k, gathered, out)
         gathered = exchange(k, out)
+        if mark:
+            mark(k)
     return _finish(parser, gathered)
 
 
@@ -85,7 +88,12 @@ def nccl_exchange(dist, world: int):
 
     def ex(phase, local):
         out = torch.empty(world * local.numel(), dtype=torch.uint8, device=local.device)
-        dist.all_gather_into_tensor(out, local)
+        try:
+            dist.all_gather_into_tensor(out, local)
+        except (RuntimeError, NotImplementedError, AttributeError):  # backends without it
+            parts = [torch.empty_like(local) for _ in range(world)]
+            dist.all_gather(parts, local)
+            out = torch.cat(parts)
         return out
     return ex
 

@@ -47,3 +47,59 @@ def test_max_over_ranks_gloo():
 def test_single_process_identity():
     import bench
     assert bench.max_over_ranks(3.5) == 3.5
+
+
+def _shard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_1902_08318_b200 import shard as SH
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ex = SH.nccl_exchange(dist, world)
+    out = []
+    for phase, nb in enumerate((16, 80, 16400, 32800)):  # Sum0..Sum3 sizes (shard.h)
+        local = torch.full((nb,), rank + 1 + 10 * phase, dtype=torch.uint8)
+        local[0] = rank
+        g = ex(phase, local)
+        out.append([(int(g[k * nb]), int(g[k * nb + 1])) for k in range(world)])
+    q.put((rank, out, SH.layout(5 * SH.TILE + 123, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_exchange_gloo():
+    """bench.py --gpus N shards one document; every phase all-gathers a fixed
+    size summary that must arrive in rank order on every rank (the shard
+    bases are prefix sums over it)."""
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    layouts = {tuple(r[2]) for r in res}
+    assert len(layouts) == 1  # every rank derives the same byte ranges
+    for rank, out, _ in res:
+        for phase, slots in enumerate(out):
+            assert slots == [(k, k + 1 + 10 * phase) for k in range(world)]
+
+
+def test_shard_summary_sizes():
+    """the sizes the gloo test assumes are the library's (shard.h)"""
+    from paper_1902_08318_b200 import shard as SH
+    assert [SH.summary_bytes(k) for k in range(4)] == [16, 80, 16400, 32800]
+
+
+def test_shard_layout_cpu():
+    from paper_1902_08318_b200.shard import TILE, layout
+    for n, G in [(TILE, 1), (5 * TILE + 7, 3), (64 * TILE, 8), (100 * TILE - 1, 7)]:
+        lo = layout(n, G)
+        assert lo[0][0] == 0 and lo[-1][1] == n
+        assert all(b % TILE == 0 and b < e for b, e in lo)
+        assert all(lo[k][1] == lo[k + 1][0] for k in range(G - 1))
+    with pytest.raises(ValueError):
+        layout(TILE, 2)
