@@ -54,6 +54,28 @@ int jt_b200_last_launches(const jt_parser *p);
 void jt_b200_profile(jt_parser *p, int enable);
 int jt_b200_kernel_times(jt_parser *p, float *ms, int max);
 
+/* ---- NDJSON records (BASELINE config C3) ----
+ * The len resident bytes are '\n'-separated records (the last one may lack
+ * the '\n'); each is parsed as jt_parse(record) would parse it alone
+ * (proj/src/capi.cpp:70-93), all in one GPU pass with per-record carries
+ * (in-string state and depth reset at every '\n').  Results per record:
+ * code, offset relative to the record start, and on JT_OK the record's tape
+ * (record-relative indices, root words at both ends) and string buffer,
+ * stored back to back on the device. */
+typedef struct {
+  int32_t code;             /* jt_error */
+  int32_t reserved;
+  long long offset;         /* relative to the record start, -1 if none */
+  uint64_t tape_begin;      /* index of the record's root word in the device tape */
+  uint64_t tape_words;      /* root .. root close; 0 unless JT_OK */
+  uint64_t string_begin;    /* offset of its strings in the device string buffer */
+  uint64_t string_bytes;
+} jt_b200_record;
+int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records);
+const void *jt_b200_records(const jt_parser *p); /* host jt_b200_record[n_records] */
+void jt_b200_records_size(const jt_parser *p, unsigned long long *out);
+int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
+
 /* ---- Byte-range sharding of one document across GPUs ----
  * Shard g of G parses bytes [begin, end) of a document whose len bytes are
  * resident in the parser's input buffer (jt_b200_input_buffer /

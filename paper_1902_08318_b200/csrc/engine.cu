@@ -185,6 +185,9 @@ struct jt_parser {
   jt::Shard *h_shard = nullptr;  // pinned
   DevBuf shard;                  // Shard + open-container stack
   uint64_t shard_len = 0;        // document length
+  // NDJSON record mode (jt_b200_parse_records)
+  DevBuf recs, nlbuf;
+  std::vector<jt::RecordResult> h_records;
   // optional per-kernel timing: ev[0] before init, then one per launch
   bool prof = false;
   cudaEvent_t ev[8] = {};
@@ -867,6 +870,131 @@ jt_error jt_b200_download(jt_parser *p, jt_document **out) {
 
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
   p->stream = cuda_stream ? (cudaStream_t)cuda_stream : p->own_stream;
+}
+
+// ---- NDJSON records (include/jsontape_b200.h) -------------------------------
+
+// Parse the len resident bytes as '\n'-separated records, each as jt_parse of
+// the record alone would.  Waits; one host sync after the newline count.
+int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
+  if (n_records) *n_records = 0;
+  if ((uint64_t)len >= (1ULL << 32) || !ensure_input(p, len) || !ensure_stage1(p, len, 0) ||
+      !ensure_stage2(p, len) ||
+      !p->nlbuf.ensure(jt::stage1_records(len) * 2 * sizeof(uint32_t) + 64)) {
+    p->err = "parse_records: allocation";
+    return -1;
+  }
+  p->in_len = len;
+  p->cur = 0;
+  p->have_index = false;
+  p->h_index_valid = false;
+  p->last_ok = false;
+  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  const uint64_t s1w = jt::stage1_records(len) * 9;
+  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
+  jt::Ctrl *ctrl = p->ctrl.as<jt::Ctrl>();
+  jt::Stage1Args a1 = s1_args(p, len, 0);
+  a1.records = true;
+  a1.nl_count = p->nlbuf.as<uint32_t>();
+  a1.nl_base = a1.nl_count + jt::stage1_records(len);
+  a1.nl_total = &ctrl->n_newlines;
+  if (!cuda_ok(p, jt::init_launch(ctrl, p->s1rec.as<uint64_t>(), s1w, p->s2rec.as<uint64_t>(), s2w,
+                                  p->stream),
+               "init") ||
+      !cuda_ok(p, jt::stage1_records_count(a1, p->stream), "records count") ||
+      !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
+    return -1;
+  const uint64_t nl = p->h_ctrl->n_newlines, nr = nl + 2;
+  const size_t cap_tok = (size_t)len + 16;
+  // carve: start (nr+1), kend, tend, send, utf8, serr, end_err (nr each), rec_of (cap_tok),
+  // err (nr u64), results (nr)
+  const size_t u32s = (nr + 1) + 6 * nr + cap_tok + 64;
+  const size_t bytes = round_up(u32s * 4, 256) + nr * 8 + nr * sizeof(jt::RecordResult) + 512;
+  if (!p->recs.ensure(bytes)) {
+    p->err = "parse_records: record arrays";
+    return -1;
+  }
+  uint32_t *q = p->recs.as<uint32_t>();
+  a1.rec_start = q;
+  q += nr + 1;
+  a1.rec_kend = q;
+  q += nr;
+  a1.rec_tend = q;
+  q += nr;
+  a1.rec_send = q;
+  q += nr;
+  a1.rec_utf8 = q;
+  q += nr;
+  a1.rec_serr = q;
+  q += nr;
+  uint32_t *end_err = q;
+  q += nr;
+  a1.rec_of = q;
+  unsigned long long *err = (unsigned long long *)(p->recs.as<uint8_t>() + round_up(u32s * 4, 256));
+  jt::RecordResult *res = (jt::RecordResult *)(err + nr);
+  jt::Stage2Args a2 = s2_args(p, len, 0);
+  a2.records = true;
+  a2.rec_of = a1.rec_of;
+  a2.rec_start = a1.rec_start;
+  a2.rec_kend = a1.rec_kend;
+  a2.rec_tend = a1.rec_tend;
+  a2.rec_send = a1.rec_send;
+  a2.rec_utf8 = a1.rec_utf8;
+  a2.rec_serr = a1.rec_serr;
+  a2.rec_err = err;
+  a2.rec_end_err = end_err;
+  a2.results = res;
+  int n2 = 0;
+  if (!cuda_ok(p, jt::records_init_launch(a2, p->stream), "records init") ||
+      !cuda_ok(p, jt::stage1_records_main(a1, p->stream), "records stage 1") ||
+      !cuda_ok(p, jt::records_stage2_launch(a2, p->stream, &n2), "records stage 2") ||
+      !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
+    return -1;
+  p->launches = 1 + 2 + 2 + 1 + n2;
+  uint8_t last = 0;
+  if (len) cudaMemcpy(&last, p->in.as<uint8_t>() + len - 1, 1, cudaMemcpyDeviceToHost);
+  const uint64_t n = nl + ((len > 0 && last != '\n') ? 1 : 0);
+  try {
+    p->h_records.resize(n);
+  } catch (...) {
+    p->err = "parse_records: host results";
+    return -1;
+  }
+  if (n && !cuda_ok(p, cudaMemcpy(p->h_records.data(), res, n * sizeof(jt::RecordResult),
+                                  cudaMemcpyDeviceToHost),
+                    "results D2H"))
+    return -1;
+  // the device tape / string buffer hold all records back to back
+  p->last_tape_len = n ? p->h_ctrl->tape_words + 2 * (n - 1) + 1 : 0;
+  p->last_string_bytes = p->h_ctrl->string_bytes;
+  if (n_records) *n_records = n;
+  return 0;
+}
+
+const void *jt_b200_records(const jt_parser *p) { return p->h_records.data(); }
+
+// Copy all records' tape words and string bytes (jt_b200_record ranges) to host.
+int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {
+  if (p->last_tape_len &&
+      !cuda_ok(p, cudaMemcpy(tape, p->tape.p, p->last_tape_len * 8, cudaMemcpyDeviceToHost), "tape D2H"))
+    return -1;
+  if (p->last_string_bytes &&
+      !cuda_ok(p, cudaMemcpy(strings, p->strings.p, p->last_string_bytes, cudaMemcpyDeviceToHost),
+               "strings D2H"))
+    return -1;
+  return 0;
+}
+
+// Sizes of the last jt_b200_parse_records output: out[0] tape words, out[1] string bytes.
+void jt_b200_records_size(const jt_parser *p, unsigned long long *out) {
+  out[0] = p->last_tape_len;
+  out[1] = p->last_string_bytes;
 }
 
 // ---- byte-range shards (shard.h, include/jsontape_b200.h) -------------------

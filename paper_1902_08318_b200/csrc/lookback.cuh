@@ -210,7 +210,19 @@ __device__ __forceinline__ int quad_decode(const uint64_t x[8], Quad &q) {
   }
   return 0;
 }
-// exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp
+// Segmented counter (record mode depth): bit 62 = the span contains a
+// reset, bits 61:0 = the change since its last reset (62-bit two's
+// complement).  seg_combine(earlier, later).
+constexpr uint64_t kSegFlag = 1ULL << 62;
+constexpr uint64_t kSegMask = kSegFlag - 1;
+__device__ __forceinline__ uint64_t seg_combine(uint64_t e, uint64_t l) {
+  return (l & kSegFlag) ? l : ((e & kSegFlag) | ((e + l) & kSegMask));
+}
+__device__ __forceinline__ long long seg_value(uint64_t v) { return (long long)(v << 2) >> 2; }
+
+// exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp;
+// kSeg3: counter 3 is a segmented counter (seg_combine) instead of a sum
+template <bool kSeg3 = false>
 __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile) {
   const int lane = threadIdx.x & 31;
   Quad acc{{0, 0, 0, 0}};
@@ -246,18 +258,30 @@ __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile)
     for (int j = 0; j < kQuadPer; j++) {
       if (!has_incl) {
 #pragma unroll
-        for (int k = 0; k < 4; k++) mine.v[k] += q[j].v[k];
+        for (int k = 0; k < 3; k++) mine.v[k] += q[j].v[k];
+        mine.v[3] = kSeg3 ? seg_combine(q[j].v[3], mine.v[3]) : mine.v[3] + q[j].v[3];
         has_incl = st[j] == 2;
       }
     }
     uint32_t incl = __ballot_sync(0xffffffffu, has_incl);
     int stop = incl ? __ffs(incl) - 1 : 31;
+    int stop3 = stop;
+    if (kSeg3) {  // a reset makes everything before it irrelevant for counter 3
+      const uint32_t fl = __ballot_sync(0xffffffffu, lane <= stop && (mine.v[3] & kSegFlag));
+      if (fl) stop3 = __ffs(fl) - 1;
+    }
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      unsigned long long x = lane > stop ? 0ULL : (mine.v[k] & kQuadMask);
+      const int lim = k == 3 ? stop3 : stop;
+      unsigned long long x = lane > lim ? 0ULL : (mine.v[k] & (kSeg3 && k == 3 ? kSegMask : kQuadMask));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      acc.v[k] = (acc.v[k] + x) & kQuadMask;
+      if (kSeg3 && k == 3) {
+        const bool fl = stop3 < stop || (__shfl_sync(0xffffffffu, mine.v[3], stop3) & kSegFlag);
+        acc.v[3] = seg_combine((fl ? kSegFlag : 0) | (x & kSegMask), acc.v[3]);
+      } else {
+        acc.v[k] = (acc.v[k] + x) & kQuadMask;
+      }
     }
     if (incl) return acc;
     base -= 32 * kQuadPer;

@@ -115,6 +115,14 @@ constexpr int kSmemPay = kStagePay;             // payload bytes (last: word ove
 constexpr int kOffBlk = kSmemIn + kSmemIdx;
 constexpr int kOffPay = kOffBlk + kSmemBlk;
 constexpr int kSmemBytes = kOffPay + kSmemPay + 16;
+// record (NDJSON) mode: per-block newline data for the copy-out
+struct RecBlk {
+  uint64_t fin, nl;  // index entries, '\n' bytes
+  uint32_t off;      // tile-relative index slot of the block
+  uint32_t rid;      // record id at the block start (newlines before it)
+};
+constexpr int kOffRec = (kSmemBytes + 15) & ~15;
+constexpr int kSmemBytesRec = kOffRec + kThreads * (int)sizeof(RecBlk);
 
 __device__ __forceinline__ int tok_width(uint32_t c) {  // tape words per token
   if (c == ',' || c == ':') return 0;
@@ -140,9 +148,13 @@ __device__ __forceinline__ int clamp16(long long d) { return d < -8192 ? -8192 :
 // K0a: transfer function of each tile.  128 threads x 2 blocks per tile, all
 // four 32-byte loads of a thread issued together.
 constexpr int kFnThreads = kStage1Tile / 128;
-__global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint32_t *fn) {
+template <bool kRec>
+__global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint32_t *fn,
+                                                          uint32_t *nl_count) {
   __shared__ uint32_t s_f[kFnThreads / 32];
+  __shared__ uint32_t s_nl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (kRec && threadIdx.x == 0) s_nl = 0;
   const uint64_t blk = (uint64_t)blockIdx.x * kStage1Tile + (uint64_t)threadIdx.x * 128;
   uint32_t w[32];
   ld256(in + blk, w);
@@ -150,11 +162,18 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint
   ld256(in + blk + 64, w + 16);
   ld256(in + blk + 96, w + 24);
   uint32_t f2[2];
+  uint32_t nlc = 0;
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     s1::Masks m;
     s1::classify64(w + 16 * h, m);
-    f2[h] = s1::block_function(m, s1::escaped_no_carry(m.bs), s1::carry_toggle(m.bs));
+    if constexpr (kRec) {
+      const uint64_t nl = s1::newline_mask(m.P);  // bytes past len are 0, never newlines
+      nlc += popc64(nl);
+      f2[h] = s1::block_function_rec(m, s1::escaped_no_carry(m.bs), s1::carry_toggle(m.bs), nl);
+    } else {
+      f2[h] = s1::block_function(m, s1::escaped_no_carry(m.bs), s1::carry_toggle(m.bs));
+    }
   }
   uint32_t inc = s1::compose(f2[1], f2[0]);
 #pragma unroll
@@ -163,12 +182,19 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint
     if (lane >= d) inc = s1::compose(inc, o);
   }
   if (lane == 31) s_f[warp] = inc;
+  if constexpr (kRec) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nlc += __shfl_xor_sync(0xffffffffu, nlc, o);
+  }
   __syncthreads();
+  if (kRec && lane == 0) atomicAdd(&s_nl, nlc);
+  if (kRec) __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t agg = s_f[0];
 #pragma unroll
     for (int k = 1; k < kFnThreads / 32; k++) agg = s1::compose(s_f[k], agg);
     fn[blockIdx.x] = agg;
+    if (kRec) nl_count[blockIdx.x] = s_nl;
   }
 }
 
@@ -179,9 +205,12 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn, uint32_t *carry,
                                                              uint64_t ntiles, const Sum0 *gathered,
-                                                             uint32_t g, Sum0 *total) {
+                                                             uint32_t g, Sum0 *total,
+                                                             const uint32_t *nl_count,
+                                                             uint32_t *nl_base, uint64_t *nl_total) {
   __shared__ uint32_t s_agg[kScanThreads / 32];
   __shared__ uint32_t s_has[kScanThreads / 32];
+  __shared__ uint32_t s_nlw[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t per = (ntiles + kScanThreads - 1) / kScanThreads;
   const uint64_t lo = threadIdx.x * per;
@@ -248,10 +277,43 @@ __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn,
         state = s1::apply(v[j], state);
       }
   }
+  if (nl_count == nullptr) return;
+  // record mode: exclusive prefix of the tiles' newline counts (record ids)
+  uint32_t mine = 0;
+  for (uint64_t t = lo; t < hi; t++) mine += nl_count[t];
+  uint32_t incl = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_nlw[warp] = incl;
+  __syncthreads();
+  uint32_t run = incl - mine;
+  for (int k = 0; k < warp; k++) run += s_nlw[k];
+  for (uint64_t t = lo; t < hi; t++) {
+    nl_base[t] = run;
+    run += nl_count[t];
+  }
+  if (threadIdx.x == kScanThreads - 1) *nl_total = run;
 }
 
+// record mode: per-record error slots (~0 = none), first record start
+__global__ void k_rec_init(Stage1Args a) {
+  const uint64_t n = *a.nl_total + 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
+    a.rec_utf8[k] = ~0u;
+    a.rec_serr[k] = ~0u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.rec_start[0] = 0;
+}
+
+template <bool kRec>
 __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp_nl[kWarps];
+  __shared__ uint32_t s_warp_tdf[kWarps];
   __shared__ uint32_t s_warp_f[kWarps];
   __shared__ uint32_t s_warp_state[kWarps];
   __shared__ uint32_t s_warp_cnt[kWarps];
@@ -266,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   uint16_t *s_idx = (uint16_t *)(smem + kSmemIn);
   BlockRec *s_blk = (BlockRec *)(smem + kOffBlk);
   uint8_t *s_pay = smem + kOffPay;
+  RecBlk *s_rec = (RecBlk *)(smem + kOffRec);  // record mode only
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
@@ -300,7 +363,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   s1::classify64(w, m);
   const uint64_t esc0 = s1::escaped_no_carry(m.bs);
   const uint64_t tog = s1::carry_toggle(m.bs);
-  const uint32_t f = s1::block_function(m, esc0, tog);
+  uint64_t nl = 0;  // record mode: '\n' bytes end records
+  uint32_t f;
+  if constexpr (kRec) {
+    nl = s1::newline_mask(m.P);
+    f = s1::block_function_rec(m, esc0, tog, nl);
+  } else {
+    f = s1::block_function(m, esc0, tog);
+  }
+  const uint32_t nlc = popc64(nl);
+  uint32_t nli = nlc;
+  if constexpr (kRec) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, nli, d);
+      if (lane >= d) nli += o;
+    }
+    if (lane == 31) s_warp_nl[warp] = nli;
+  }
 
   // warp inclusive scan of transfer functions
   uint32_t inc = f;
@@ -315,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   // fused UTF-8 validity: needs only the 3 bytes before the block
   uint32_t prev = __shfl_up_sync(0xffffffffu, w[15], 1);
   if (lane == 0) prev = blk >= 4 ? *(const uint32_t *)(a.in + blk - 4) : 0u;
-  if ((m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3) {
+  if (!kRec && (m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3) {
     if (s1::utf8_block_error(m.P, prev, blk + 64 >= a.len)) {
       const uint8_t *in = a.in;
       const uint64_t len = a.len;
@@ -329,6 +409,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
   }
   __syncthreads();
+
+  // record mode: record id at the block start; UTF-8 errors per record
+  uint32_t rid_blk = 0;
+  if constexpr (kRec) {
+    rid_blk = a.nl_base[tile] + nli - nlc;
+    for (int k = 0; k < warp; k++) rid_blk += s_warp_nl[k];
+    if ((m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3 &&
+        s1::utf8_block_error(m.P, prev, blk + 64 >= a.len)) {
+      const uint8_t *in = a.in;
+      const uint64_t len = a.len;
+      auto at = [in, len](uint64_t i) -> uint32_t { return i < len ? in[i] : 0u; };
+      uint64_t lo = blk >= 3 ? blk - 3 : 0, hi = blk + 64 < len ? blk + 64 : len;
+      for (uint64_t i = lo; i < hi; i++)
+        if (s1::utf8_flagged(at, i, len)) {
+          uint32_t rid = rid_blk;
+          if (i >= blk) {
+            rid += popc64(nl & sb::low_bits((int)(i - blk)));
+          } else {
+            for (uint64_t j = i; j < blk; j++) rid -= in[j] == '\n';
+          }
+          atomicMin(a.rec_utf8 + rid, (uint32_t)i);
+        }
+    }
+  }
 
   // warp carry states from the tile's carry-in (K0 pre-pass, no look-back)
   if (threadIdx.x == 0) {
@@ -348,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   // masks under the resolved carry (string_mask + finalize_structurals)
   const uint64_t esc = (state & 1) ? (esc0 ^ tog) : esc0;
   const uint64_t uq = m.qt & ~esc;
-  const uint64_t instr = s1::prefix_xor(uq) ^ ((state & 2) ? ~0ULL : 0ULL);
+  const uint64_t instr = kRec ? s1::instr_records(uq, state & 2, nl)
+                              : s1::prefix_xor(uq) ^ ((state & 2) ? ~0ULL : 0ULL);
   uint64_t fin;
   {
     uint64_t st1 = (m.st & ~instr) | uq;
@@ -362,7 +467,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint64_t w1m = fin & ~m.cc, w2m = fin & m.num;
   const uint64_t opm = fin & m.open, clm = fin & m.close;
   const uint32_t tw = popc64(w1m) + popc64(w2m);
-  const int td = popc64(opm) - popc64(clm);
+  int td = popc64(opm) - popc64(clm);
+  uint32_t tdf = 0;  // record mode: the block resets the depth (a newline)
+  if constexpr (kRec) {
+    if (nl) {
+      const int last = 63 - clz64(nl);
+      const uint64_t above = last >= 63 ? 0ULL : (~0ULL << (last + 1));
+      td = popc64(opm & above) - popc64(clm & above);
+      tdf = 1;
+    }
+  }
 
   // strings in this block
   const uint64_t openq = uq & instr & valid;
@@ -376,8 +490,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   int ov_out = E ? sb::escape_overhang(gat, blk, ec) : 0;
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
-  // unterminated string: the reference reads the NUL padding at len
-  if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) atomicMin(a.str_err, (unsigned long long)a.len);
+  // unterminated string: the reference reads the NUL padding at len (in
+  // record mode: at the record's end, a newline or len)
+  if constexpr (kRec) {
+    for (uint64_t q = nl; q; q &= q - 1) {
+      const int r = ctz64(q);
+      const uint32_t before = r > 0 ? (uint32_t)((instr >> (r - 1)) & 1) : ((state >> 1) & 1);
+      if (before) atomicMin(a.rec_serr + rid_blk + popc64(nl & sb::low_bits(r)), (uint32_t)(blk + r));
+    }
+    if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1))
+      atomicMin(a.rec_serr + rid_blk + popc64(nl & sb::low_bits((int)rem)), (uint32_t)a.len);
+  } else {
+    if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) atomicMin(a.str_err, (unsigned long long)a.len);
+  }
 
   // CTA exclusive scan of (index count, string bytes); the block weight of a
   // slow block needs ov_in, which for lane 0 comes from the previous warp
@@ -405,8 +530,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   uint64_t W = content;
   {
     uint64_t serr = ctl ? blk + (uint64_t)ctz64(ctl) : ~0ULL;
-    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr);
-    if (serr != ~0ULL) atomicMin(a.str_err, (unsigned long long)serr);
+    uint64_t em = ctl;  // record mode: every error candidate of the block
+    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr, kRec ? &em : nullptr);
+    if constexpr (kRec) {
+      while (em) {  // the first error of each record in the block
+        const int q = ctz64(em);
+        atomicMin(a.rec_serr + rid_blk + popc64(nl & sb::low_bits(q)), (uint32_t)(blk + q));
+        const uint64_t nxt = nl & ~sb::low_bits(q + 1);
+        em = nxt ? em & ~sb::low_bits(ctz64(nxt) + 1) : 0;
+      }
+    } else if (serr != ~0ULL) {
+      atomicMin(a.str_err, (unsigned long long)serr);
+    }
   }
   const uint32_t sw = 4u * popc64(openq) + popc64(W);
   uint32_t si = sw;
@@ -417,38 +552,55 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   uint32_t ti = tw;
   int di = td;
+  uint32_t df = tdf;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     uint32_t o = __shfl_up_sync(0xffffffffu, ti, d);
     int od = __shfl_up_sync(0xffffffffu, di, d);
+    uint32_t of = kRec ? __shfl_up_sync(0xffffffffu, df, d) : 0u;
     if (lane >= d) {
       ti += o;
-      di += od;
+      if (!df) di += od;  // segmented (record mode); df == 0 otherwise
+      df |= of;
     }
   }
+  // block-exclusive depth (record mode: segmented) from the previous lane
+  int dex = __shfl_up_sync(0xffffffffu, di, 1);
+  uint32_t dexf = kRec ? __shfl_up_sync(0xffffffffu, df, 1) : 0u;
+  if (lane == 0) dex = 0, dexf = 0;
   if (lane == 31) {
     s_warp_sw[warp] = si;
     s_warp_tw[warp] = ti;
     s_warp_td[warp] = di;
+    s_warp_tdf[warp] = df;
   }
   __syncthreads();
   uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
   int wdoff = 0, dtotal = 0;
 #pragma unroll
+  uint32_t wdf = 0, dtf = 0;  // record mode: resets before this warp / in the tile
   for (int k = 0; k < kWarps; k++) {
     uint32_t c = s_warp_cnt[k], s = s_warp_sw[k], t = s_warp_tw[k];
     int dd = s_warp_td[k];
+    const uint32_t fk = kRec ? s_warp_tdf[k] : 0u;
     woff += k < warp ? c : 0;
     wsoff += k < warp ? s : 0;
     wtoff += k < warp ? t : 0;
-    wdoff += k < warp ? dd : 0;
+    if (k < warp) {
+      wdoff = fk ? dd : wdoff + dd;
+      wdf |= fk;
+    }
     total += c;
     stotal += s;
     ttotal += t;
-    dtotal += dd;
+    dtotal = fk ? dd : dtotal + dd;
+    dtf |= fk;
   }
   const uint32_t toff = wtoff + ti - tw;  // tile-relative tape words
-  const int doff = wdoff + di - td;       // tile-relative depth
+  // tile-relative depth at the block start (segmented in record mode:
+  // doff_f = a reset lies between the tile start and the block)
+  const int doff = dexf ? dex : wdoff + dex;
+  const uint32_t doff_f = wdf | dexf;
   const uint32_t off = woff + ci - cnt;   // tile-relative index slot
   const uint32_t soff = wsoff + si - sw;  // tile-relative string byte
 
@@ -461,25 +613,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const bool idx_direct = total > (uint32_t)kStageIdx;
   const bool pay_direct = stotal > (uint32_t)kStagePay;
   const bool direct = idx_direct || pay_direct;  // CTA-uniform
-  const Quad tot{{total, stotal, ttotal, (unsigned long long)(long long)dtotal & kQuadMask}};
+  const uint64_t tdepth = kRec ? ((dtf ? kSegFlag : 0ULL) | ((uint64_t)(long long)dtotal & kSegMask))
+                                : ((unsigned long long)(long long)dtotal & kQuadMask);
+  const Quad tot{{total, stotal, ttotal, tdepth}};
   auto resolve_counts = [&]() {  // warp 0
     Quad base{{0, 0, 0, 0}};
-    if (tile > 0) base = quad_lookback(a.rec_count, tile);
+    if (tile > 0) base = quad_lookback<kRec>(a.rec_count, tile);
     if (lane == 0) {
       JT_TL(tile, 5);
       Quad inc;
 #pragma unroll
-      for (int k = 0; k < 4; k++) inc.v[k] = (base.v[k] + tot.v[k]) & kQuadMask;
+      for (int k = 0; k < 3; k++) inc.v[k] = (base.v[k] + tot.v[k]) & kQuadMask;
+      inc.v[3] = kRec ? seg_combine(base.v[3], tot.v[3]) : ((base.v[3] + tot.v[3]) & kQuadMask);
       quad_publish(a.rec_count, tile, 1, inc);
       s_base = base.v[0];
       s_sbase = base.v[1];
       s_tbase = base.v[2];
-      s_dbase = sext63(base.v[3]);
+      s_dbase = kRec ? seg_value(base.v[3]) : sext63(base.v[3]);
       if (tile == (int64_t)a.ntiles - 1) {
         *a.total = inc.v[0];
         *a.total_strings = inc.v[1];
         *a.tape_words = 1 + inc.v[2];
-        *a.depth_total = sext63(inc.v[3]);
+        *a.depth_total = kRec ? seg_value(inc.v[3]) : sext63(inc.v[3]);
       }
     }
   };
@@ -489,7 +644,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   if (direct && warp == 0) resolve_counts();
   if (threadIdx.x == 0) JT_TL(tile, 6);
-  s_blk[threadIdx.x] = BlockRec{W, openq, w1m, w2m, opm, clm, soff, toff, doff, 0u};
+  s_blk[threadIdx.x] = BlockRec{W, openq, w1m, w2m, opm, clm, soff, toff, doff, doff_f};
+  if constexpr (kRec) s_rec[threadIdx.x] = RecBlk{fin, nl, off, rid_blk};
   // stage positions (+ string offsets of slow blocks) and the string
   // payload; spill to global when the tile is larger than the staging
   if (direct) __syncthreads();  // s_base/s_sbase needed now
@@ -501,11 +657,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     const uint64_t below = sb::low_bits(p);
     const uint32_t c = s_in[local + p];
     const uint32_t t = toff + popc64(w1m & below) + popc64(w2m & below);
-    const long long d = gdbase + doff + popc64(opm & below) - popc64(clm & below);
+    long long d = (doff_f ? 0 : gdbase) + doff + popc64(opm & below) - popc64(clm & below);
+    uint32_t rid = 0;
+    if constexpr (kRec) {
+      const uint64_t nb = nl & below;
+      rid = rid_blk + popc64(nb);
+      if (nb) {  // depth since this record's start, inside the block
+        const uint64_t since = below & ~sb::low_bits(64 - clz64(nb));
+        d = popc64(opm & since) - popc64(clm & since);
+      }
+      a.rec_of[gbase + slot] = rid;
+    }
     a.idx[gbase + slot] = (uint32_t)(tile_base + local + p);
     a.aux[gbase + slot] = (uint32_t)(gsbase + soff + wb);
     a.tokrec[gbase + slot] = c | ((uint32_t)(uint16_t)clamp16(d) << 16);
-    a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + t);
+    a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + t + 2 * rid);
   };
   {
     // plain runs (escape positions get placeholder bytes, rewritten below;
@@ -565,12 +731,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       const BlockRec &r = s_blk[pos >> 6];
       const uint64_t below = sb::low_bits((int)(pos & 63));
       const uint32_t aux = r.soff + 4u * popc64(r.openq & below) + popc64(r.W & below);
-      const uint32_t t = r.toff + popc64(r.w1 & below) + popc64(r.w2 & below);
-      const int d = r.doff + popc64(r.op & below) - popc64(r.cl & below);
+      uint32_t t = r.toff + popc64(r.w1 & below) + popc64(r.w2 & below);
+      long long d = (r.pad ? 0 : db) + r.doff + popc64(r.op & below) - popc64(r.cl & below);
+      if constexpr (kRec) {
+        const RecBlk &x = s_rec[pos >> 6];
+        const uint64_t nb = x.nl & below;
+        const uint32_t rid = x.rid + popc64(nb);
+        if (nb) {
+          const uint64_t since = below & ~sb::low_bits(64 - clz64(nb));
+          d = popc64(r.op & since) - popc64(r.cl & since);
+        }
+        t += 2 * rid;  // every record owns two root words
+        a.rec_of[gb2 + k] = rid;
+      }
       const uint32_t c = s_in[pos];
       dst[k] = tb + pos;
       dax[k] = sb32 + aux;
-      drc[k] = c | ((uint32_t)(uint16_t)clamp16(db + d) << 16);
+      drc[k] = c | ((uint32_t)(uint16_t)clamp16(d) << 16);
       dtp[k] = tb32 + t;
       if (c == '"' && k + 1 < total && !pay_direct) {
         // string length = next entry's string offset - this one - 4 (the
@@ -589,6 +766,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
   }
   if (threadIdx.x == 0) a.tile_flags[tile] = (idx_direct || pay_direct) ? 1u : 0u;
+  if constexpr (kRec) {
+    // the record each newline ends: where the next one starts, and the
+    // token / tape / string-buffer prefixes at its end
+    for (uint64_t q = nl; q; q &= q - 1) {
+      const int r = ctz64(q);
+      const uint64_t below = sb::low_bits(r);
+      const uint32_t rid = rid_blk + popc64(nl & below);
+      a.rec_start[rid + 1] = (uint32_t)(blk + r + 1);
+      a.rec_kend[rid] = (uint32_t)(gb2 + off + popc64(fin & below));
+      a.rec_tend[rid] = (uint32_t)(1 + s_tbase + toff + popc64(w1m & below) + popc64(w2m & below) + 2 * rid);
+      a.rec_send[rid] = (uint32_t)(gsb2 + soff + 4u * popc64(openq & below) + popc64(W & below));
+    }
+  }
   __syncthreads();  // length fields staged before the payload copy-out
   if (!pay_direct && stotal) {
     uint8_t *dst = a.strings + gsb2;
@@ -631,8 +821,13 @@ size_t stage1_records(uint64_t len) {
 }
 
 cudaError_t stage1_configure() {
-  static const cudaError_t configured =
-      cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  static const cudaError_t configured = [] {
+    cudaError_t e = cudaFuncSetAttribute(k_stage1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemBytes);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_stage1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBytesRec);
+  }();
   return configured;
 }
 
@@ -648,16 +843,43 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
   const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
-  k_carry_fn<<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn);
-  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr);
-  k_stage1<<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
+  if (a.records) {
+    k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, a.nl_count);
+    k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
+                                                 a.nl_count, a.nl_base, a.nl_total);
+    k_rec_init<<<1184, 256, 0, stream>>>(a);
+    k_stage1<true><<<(unsigned)a.ntiles, kThreads, kSmemBytesRec, stream>>>(a);
+  } else {
+    k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+    k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
+                                                 nullptr, nullptr, nullptr);
+    k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_records_count(const Stage1Args &args_in, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, a.nl_count);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
+                                               a.nl_count, a.nl_base, a.nl_total);
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_records_main(const Stage1Args &args_in, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  const cudaError_t configured = stage1_configure();
+  if (configured != cudaSuccess) return configured;
+  k_rec_init<<<1184, 256, 0, stream>>>(a);
+  k_stage1<true><<<(unsigned)a.ntiles, kThreads, kSmemBytesRec, stream>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t stage1_shard_phase0(const Stage1Args &args_in, Sum0 *out, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  k_carry_fn<<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn);
-  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, nullptr, a.ntiles, nullptr, 0, out);
+  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, nullptr, a.ntiles, nullptr, 0, out, nullptr,
+                                               nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -666,8 +888,9 @@ cudaError_t stage1_shard_phase1(const Stage1Args &args_in, const Sum0 *gathered,
   const Stage1Args a = with_tiles(args_in);
   const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
-  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, gathered, g, nullptr);
-  k_stage1<<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, gathered, g, nullptr,
+                                               nullptr, nullptr, nullptr);
+  k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,14 @@ struct Stage1Args {
   uint64_t *tape_words;           // 1 + sum of token widths
   int64_t *depth_total;           // depth change over the range
   uint64_t begin, end;            // byte range [begin, end): a shard, or [0, len)
+  // record (NDJSON) mode: '\n'-separated records parsed independently
+  bool records;
+  uint32_t *nl_count, *nl_base;   // per tile: newlines, newlines before it (K0)
+  uint64_t *nl_total;             // newlines of the range
+  uint32_t *rec_start;            // per record: first byte (rec_start[0] = 0)
+  uint32_t *rec_kend, *rec_tend, *rec_send;  // per '\n': token / tape / string prefix at it
+  uint32_t *rec_utf8, *rec_serr;  // per record: first UTF-8 / string error position (~0 = none)
+  uint32_t *rec_of;               // per index entry: its record
   uint64_t ntiles;                // filled by the launchers
 };
 
@@ -42,6 +50,11 @@ size_t stage1_records(uint64_t len);
 
 constexpr int kStage1Launches = 3;  // K0a carry functions, K0b carry scan, K1
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
+
+// record (NDJSON) mode, split so the caller can size the per-record arrays
+// from the newline count: K0 (carries + newline counts), then K1
+cudaError_t stage1_records_count(const Stage1Args &args, cudaStream_t stream);
+cudaError_t stage1_records_main(const Stage1Args &args, cudaStream_t stream);
 
 struct Sum0;
 // sharded stage 1 (shard.h): phase 0 = K0a + the shard's composed carry

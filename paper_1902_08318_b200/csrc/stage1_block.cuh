@@ -157,6 +157,32 @@ JT_HD uint32_t block_function(const Masks &m, uint64_t esc0, uint64_t tog) {
   return f;
 }
 
+// '\n' bytes (0x0A = 0000 1010): record separators in NDJSON mode
+JT_HD uint64_t newline_mask(const uint64_t P[8]) {
+  return ~P[7] & ~P[6] & ~P[5] & ~P[4] & P[3] & ~P[2] & P[1] & ~P[0];
+}
+
+// Record (NDJSON) mode: a '\n' ends its record, so the in-string carry out of
+// a block with a newline is the quote parity after its last newline, whatever
+// came in (a backslash run cannot cross the newline either).
+JT_HD uint32_t block_function_rec(const Masks &m, uint64_t esc0, uint64_t tog, uint64_t nl) {
+  uint32_t f = block_function(m, esc0, tog);
+  if (!nl) return f;
+  const int r = 63 - clz64(nl);
+  const uint64_t after = r >= 63 ? 0ULL : (~0ULL << (r + 1));
+  const uint32_t so = popc64(m.qt & ~esc0 & after) & 1;  // bits > r do not see the carry
+  const uint32_t ws63 = (uint32_t)(m.ws >> 63), st63 = (uint32_t)(m.st >> 63);
+  const uint32_t uq63 = (uint32_t)(((m.qt & ~esc0) >> 63) & (r < 63 ? 1u : 0u));
+  const uint32_t sep = ws63 | uq63 | (st63 & (so ^ 1));
+  uint32_t g = 0;
+#pragma unroll
+  for (uint32_t x = 0; x < 4; x++) {
+    const uint32_t oo = (f >> (8 * x)) & 1;  // odd-run carry as before
+    g |= (oo | (so << 1) | (sep << 2)) << (8 * x);
+  }
+  return g;
+}
+
 // g after f (f applied first), 5 integer ops
 JT_HD uint32_t compose(uint32_t g_later, uint32_t f_earlier) {
   uint32_t v = f_earlier & 0x03030303u;
@@ -180,6 +206,22 @@ JT_HD uint64_t prefix_xor(uint64_t x) {
   x ^= x << 32;
   return x;
 }
+
+// In-string mask with resets: bits after a newline see only the quotes
+// after it; the newline itself is outside every string.
+JT_HD uint64_t instr_records(uint64_t uq, uint32_t in_str, uint64_t nl) {
+  const uint64_t x = prefix_xor(uq);
+  uint64_t instr = x ^ (in_str ? ~0ULL : 0ULL);
+  while (nl) {
+    const int r = ctz64(nl);
+    nl &= nl - 1;
+    const uint64_t seg = ~0ULL << r;  // bits >= r
+    const uint64_t base = ((x >> r) & 1) ? ~0ULL : 0ULL;  // x at r (the newline is no quote)
+    instr = (instr & ~seg) | ((x ^ base) & seg);
+  }
+  return instr;
+}
+
 
 // final structural mask of a block once its carry-in state is known
 // (string_mask blocks.h:79-85 + finalize_structurals blocks.h:155-168)

@@ -385,7 +385,15 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
       if (c == '"') {
         const uint32_t p = a.idx[i];
         const unsigned long long end = i + 1 < S ? a.idx[i + 1] : vw.next_pos;
-        fail = str_err >= p && str_err < end;  // the failing string holds the minimum
+        uint32_t sbase = 0;  // record mode: offsets within the record's string buffer
+        if (a.records) {
+          const uint32_t r = a.rec_of[i];
+          const uint32_t se = a.rec_serr[r];
+          fail = se != ~0u && se >= p && se < end;
+          sbase = r ? a.rec_send[r - 1] : 0u;
+        } else {
+          fail = str_err >= p && str_err < end;  // the failing string holds the minimum
+        }
         if (!fail) {
           const uint32_t so = a.aux[i];
           // stage 1 wrote the length unless the next token is in another
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
             f[2] = (uint8_t)(len >> 16);
             f[3] = (uint8_t)(len >> 24);
           }
-          a.tape[a.tape_idx[i]] = tape_word('"', vw.string_base + so);
+          a.tape[a.tape_idx[i]] = tape_word('"', vw.string_base + so - sbase);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
         const uint32_t p = a.idx[i];
@@ -636,8 +644,10 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
   return psv(a, T.base, L);
 }
 
-template <bool kShard>
+// kMode: 0 one document, 1 a byte-range shard (shard.h), 2 NDJSON records
+template <int kMode>
 __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
+  constexpr bool kShard = kMode == 1, kRecs = kMode == 2;
   __shared__ __align__(16) uint32_t s_tok[kK3Tile];
   __shared__ int16_t s_l1[256];
   __shared__ int16_t s_l2[16];
@@ -733,9 +743,18 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     if (i0 < S) do {
     const uint32_t *recs = s_tok + threadIdx.x * kK3Tok;
     uint32_t t = a.tape_idx[i0];  // local tape index (document index = tb + t)
+    // record mode: the chunk's current record, its root word (payloads are
+    // record-relative) and how many of the previous tokens belong to it
+    uint32_t rcur = 0, rtb = 0;
+    int64_t rbefore = (int64_t)i0 + before;
+    if (kRecs) {
+      rcur = a.rec_of[i0];
+      rtb = rcur ? a.rec_tend[rcur - 1] + 1 : 0u;
+      rbefore = (i0 >= 1 && a.rec_of[i0 - 1] == rcur) ? ((i0 >= 2 && a.rec_of[i0 - 2] == rcur) ? 2 : 1) : 0;
+    }
     // entry state from the two previous tokens (A.5 arrival rules)
     int mode = M_V;
-    if ((int64_t)i0 + before > 0) {
+    if (rbefore > 0) {
       uint32_t v1 = rec_at((int64_t)i0 - 1, tbase);
       uint32_t c1 = v1 & 0xFF;
       if (c1 == '{') mode = M_OF;
@@ -745,7 +764,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
         mode = scope_obj((int64_t)i0 - 1) ? M_K : M_V;
       } else if (c1 == '"') {
         mode = M_A;
-        if ((int64_t)i0 + before >= 2) {
+        if (rbefore >= 2) {
           uint32_t v2 = rec_at((int64_t)i0 - 2, tbase);
           uint32_t c2 = v2 & 0xFF;
           if (c2 == '{') mode = M_C;
@@ -764,10 +783,27 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     uint32_t far_tape = 0;  // document tape index
     bool far_obj = false;
     int err = 0;
+    bool dead = false;  // record mode: the current record already failed
     uint64_t i = i0;
     int depth_after = 0;
     for (int k = 0; k < kK3Tok; k++) {
       if (i >= i1) break;
+      if (kRecs) {
+        const uint32_t r = a.rec_of[i];
+        if (r != rcur) {  // a new record: a new root value
+          rcur = r;
+          rtb = a.rec_tend[r - 1] + 1;
+          t = a.tape_idx[i];
+          mode = M_V;
+          sp = 0;
+          far_level = -100;
+          dead = false;
+        }
+        if (dead) {
+          i++;
+          continue;
+        }
+      }
       const uint32_t v = recs[k];
       const uint32_t c = v & 0xFF;
       const bool fail = (v >> 8) & 1;
@@ -860,8 +896,8 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
         if (close && have_top) {
           if (top_local) sp--;
           else far_level = -100;
-          a.tape[t] = tape_word((uint8_t)c, top_tape);
-          const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1);
+          a.tape[t] = tape_word((uint8_t)c, top_tape - rtb);
+          const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1 - rtb);
           if (!kShard || top_tape > tb) {
             a.tape[top_tape - tb] = ow;
           } else {  // the opener lives in an earlier shard: patched after the last exchange
@@ -874,10 +910,26 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
           mode = M_A;
         }
       } while (again && !err);
+      if (kRecs) {
+        if (err) {  // first error of this record; skip to the next record
+          atomicMin(&a.rec_err[rcur], ((unsigned long long)i << 8) | (unsigned)err);
+          err = 0;
+          dead = true;
+          i++;
+          continue;
+        }
+        t += tok_width(c);
+        i++;
+        // the record's last token: it must close the root value
+        if ((i >= S || a.rec_of[i] != rcur) && !(mode == M_A && depth_after == 0))
+          a.rec_end_err[rcur] = kTapeError;
+        continue;
+      }
       if (err) break;
       t += tok_width(c);
       i++;
     }
+    if (kRecs) break;
     if (err) {
       report(ctrl, token_base + i, err);
       break;
@@ -939,6 +991,64 @@ __global__ void k_init(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *
     z.code = -1;
     z.offset = -1;
     *ctrl = z;
+  }
+}
+
+// ---- NDJSON records ---------------------------------------------------------
+
+__device__ __forceinline__ uint64_t n_records(const Stage2Args &a) {
+  const uint64_t nl = a.ctrl->n_newlines;
+  // a record after the last '\n' exists unless the input ends with it
+  return nl + ((a.len > 0 && a.in[a.len - 1] != '\n') ? 1 : 0);
+}
+
+__global__ void k_records_init(Stage2Args a) {
+  const uint64_t n = a.ctrl->n_newlines + 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
+    a.rec_err[k] = ~0ULL;
+    a.rec_end_err[k] = 0;
+  }
+}
+
+// one thread per record: code and record-relative offset as jt_parse of the
+// record alone (App. A.1 order: UTF-8, EMPTY, first grammar error in walk
+// order, OK), and on success its root words
+__global__ void k_final_records(Stage2Args a) {
+  const Ctrl *c = a.ctrl;
+  const uint64_t n = n_records(a), nl = c->n_newlines, S = c->S;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
+    const uint64_t start = a.rec_start[r];
+    const uint64_t end = r < nl ? (uint64_t)a.rec_start[r + 1] - 1 : a.len;
+    const uint64_t k0 = r ? a.rec_kend[r - 1] : 0, k1 = r < nl ? a.rec_kend[r] : S;
+    RecordResult out{};
+    out.offset = -1;
+    if (a.rec_utf8[r] != ~0u) {
+      out.code = kUtf8Error;
+      out.offset = (long long)(a.rec_utf8[r] - start);
+    } else if (k1 == k0) {
+      out.code = kEmpty;
+    } else if (a.rec_err[r] != ~0ULL) {
+      const uint64_t i = a.rec_err[r] >> 8;
+      out.code = (int)(a.rec_err[r] & 0xFF);
+      out.offset = out.code == kStringError ? (long long)(a.rec_serr[r] - start) : (long long)(a.idx[i] - start);
+    } else if (a.rec_end_err[r]) {
+      out.code = (int)a.rec_end_err[r];
+      out.offset = (long long)(end - start);
+    } else {
+      const uint64_t tb = r ? (uint64_t)a.rec_tend[r - 1] + 1 : 0;
+      const uint64_t te = r < nl ? (uint64_t)a.rec_tend[r] : c->tape_words + 2 * r;
+      const uint64_t sb = r ? a.rec_send[r - 1] : 0, se = r < nl ? a.rec_send[r] : c->string_bytes;
+      a.tape[tb] = tape_word(kTagRoot, te - tb);
+      a.tape[te] = tape_word(kTagRoot, 0);
+      out.code = kOk;
+      out.tape_begin = tb;
+      out.tape_words = te - tb + 1;
+      out.string_begin = sb;
+      out.string_bytes = se - sb;
+    }
+    a.results[r] = out;
   }
 }
 
@@ -1210,8 +1320,27 @@ static void launch_struct(const Stage2Args &a, cudaStream_t stream) {
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
   uint64_t nt = (a.cap_tokens + kK3Tile - 1) / kK3Tile;
   unsigned g3 = (unsigned)(nt < (uint64_t)sms * 4 ? nt : (uint64_t)sms * 4);
-  if (a.sh) k_struct<true><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
-  else k_struct<false><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  if (a.records) k_struct<2><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  else if (a.sh) k_struct<1><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+  else k_struct<0><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+}
+
+cudaError_t records_init_launch(const Stage2Args &a, cudaStream_t stream) {
+  k_records_init<<<1184, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches) {
+  const unsigned g2 = grid_tokens(a);
+  k_scalars<<<g2, 256, 0, stream>>>(a);
+  k_numbers<<<g2, 256, 0, stream>>>(a);
+  k_slow<<<8, 64, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
+  launch_stack(a, stream);
+  launch_struct(a, stream);
+  k_final_records<<<1184, 256, 0, stream>>>(a);
+  *launches = 7;
+  return cudaGetLastError();
 }
 
 cudaError_t shard_sum1_launch(const Stage2Args &a, Sum1 *out, cudaStream_t stream) {

@@ -34,11 +34,23 @@ struct Ctrl {
   uint64_t string_bytes;        // string buffer size (stage 1)
   unsigned long long str_err;   // min string error position (~0 = none)
   int64_t depth_total;          // depth change over the (shard's) tokens
+  uint64_t n_newlines;          // record mode: '\n' bytes (K0)
   // results written by the finalize kernel
   int32_t code;
   int32_t pad2;
   long long offset;
   uint64_t tape_len;            // E + 1 on success
+};
+
+// one NDJSON record's result (include/jsontape_b200.h jt_b200_record)
+struct RecordResult {
+  int32_t code;
+  int32_t reserved;
+  long long offset;        // relative to the record start, -1 if none
+  uint64_t tape_begin;     // tape index of the record's root word
+  uint64_t tape_words;     // root .. root close, 0 on error
+  uint64_t string_begin;   // string-buffer offset of the record's strings
+  uint64_t string_bytes;
 };
 
 struct Stage2Args {
@@ -67,6 +79,12 @@ struct Stage2Args {
   Shard *sh;
   uint64_t *bound;      // kBoundMax: containers open at the shard start (kind << 56 | tape)
   Sum3 *sum3;           // phase-3 summary (error, cross-shard bracket patches)
+  // record (NDJSON) mode (records == true): see stage1.h
+  bool records;
+  const uint32_t *rec_of, *rec_start, *rec_kend, *rec_tend, *rec_send, *rec_utf8, *rec_serr;
+  unsigned long long *rec_err;  // per record: (token << 8) | code, ~0 = none
+  uint32_t *rec_end_err;        // per record: error at the record's end (0 = none)
+  RecordResult *results;        // per record (k_final_records)
 };
 
 // words of look-back records / tree nodes needed for up to `cap` tokens
@@ -81,6 +99,11 @@ Stage2Sizes stage2_sizes(uint64_t cap_tokens);
 // `ev` (optional, 5 events) is recorded after each of the 5 kernels.
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
                           cudaEvent_t *ev = nullptr);
+
+// Record mode: per-record error slots, then the whole stage 2 with
+// per-record grammar, and one result per record.
+cudaError_t records_init_launch(const Stage2Args &a, cudaStream_t stream);
+cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches);
 
 // Sharded stage 2 (shard.h).  phase 2: bases from the gathered Sum1s, then
 // scalars / numbers / depth tree and this shard's open containers (Sum2);

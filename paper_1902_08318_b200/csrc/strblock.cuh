@@ -274,13 +274,16 @@ JT_HD int escape_overhang(At at, uint64_t blk, const EscClass &c) {
 // without escapes.  ov_in / vin = input / weight bytes of an escape begun in
 // the previous block; c must be restrict_from(ov_in).  *err gets the
 // minimum invalid-escape position.
+// errmask (optional) collects every invalid-escape position of the block
+// (record mode: each record needs its own first error).
 template <class Byte>
 JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const EscClass &c, int ov_in,
-                              int vin, uint64_t *err) {
+                              int vin, uint64_t *err, uint64_t *errmask = nullptr) {
   uint64_t cov = low_bits(ov_in) | c.sim | c.tr, virt = low_bits(vin);
   if (c.bad) {
     const uint64_t x = blk + (uint64_t)ctz64(c.bad);
     if (x < *err) *err = x;
+    if (errmask) *errmask |= c.bad;
   }
   uint64_t rest = c.u;
   while (rest) {
@@ -291,6 +294,7 @@ JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const E
     int end = p + 1;
     if (L == 0) {
       if (blk + (uint64_t)p < *err) *err = blk + (uint64_t)p;
+      if (errmask) *errmask |= 1ULL << p;
     } else {
       end = p + L;
       cov |= low_bits(end) & ~low_bits(p);

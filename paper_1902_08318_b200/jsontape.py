@@ -35,7 +35,8 @@ EXPORTS = [
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
-    "jt_b200_shard_download", "jt_b200_copy_in_range",
+    "jt_b200_shard_download", "jt_b200_copy_in_range", "jt_b200_parse_records",
+    "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download",
 ]
 KERNELS = ["init", "stage1", "tokens", "slow", "tree", "struct", "final"]
 
@@ -97,6 +98,11 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_extent.argtypes = [vp, C.POINTER(C.c_ulonglong)]
     L.jt_b200_shard_download.argtypes = [vp, vp, vp]
     L.jt_b200_copy_in_range.argtypes = [vp, vp, sz, sz]
+    L.jt_b200_parse_records.argtypes = [vp, sz, C.POINTER(sz)]
+    L.jt_b200_records.argtypes = [vp]
+    L.jt_b200_records.restype = vp
+    L.jt_b200_records_size.argtypes = [vp, C.POINTER(C.c_ulonglong)]
+    L.jt_b200_records_download.argtypes = [vp, vp, vp]
     _lib = L
     return L
 
@@ -249,6 +255,37 @@ class Parser:
         n = C.c_size_t()
         p = self._lib.jt_b200_device_index(self._h, C.byref(n))
         return p, n.value
+
+    def parse_records(self, n: int, download: bool = True):
+        """Parse the n resident bytes as NDJSON records (jt_b200_parse_records).
+        Returns [(name, offset, tape words or None, strings or None)] per record."""
+        cnt = C.c_size_t()
+        if self._lib.jt_b200_parse_records(self._h, n, C.byref(cnt)) != 0:
+            raise RuntimeError(self.last_error())
+        k = cnt.value
+        rec = np.dtype([("code", "<i4"), ("reserved", "<i4"), ("offset", "<i8"), ("tape_begin", "<u8"),
+                        ("tape_words", "<u8"), ("string_begin", "<u8"), ("string_bytes", "<u8")])
+        arr = np.frombuffer(C.string_at(self._lib.jt_b200_records(self._h), k * rec.itemsize),
+                            dtype=rec) if k else np.zeros(0, rec)
+        tape = strings = None
+        if download:
+            sz = (C.c_ulonglong * 2)()
+            self._lib.jt_b200_records_size(self._h, sz)
+            tape = np.zeros(max(1, sz[0]), np.uint64)
+            sb = C.create_string_buffer(max(1, sz[1]))
+            if self._lib.jt_b200_records_download(self._h, tape.ctypes.data, sb) != 0:
+                raise RuntimeError(self.last_error())
+            strings = sb.raw[:sz[1]]
+        out = []
+        for r in arr:
+            name = ERROR_NAMES[int(r["code"])]
+            if download and name == "OK":
+                tb, tw = int(r["tape_begin"]), int(r["tape_words"])
+                sb0, sn = int(r["string_begin"]), int(r["string_bytes"])
+                out.append((name, int(r["offset"]), tape[tb:tb + tw], strings[sb0:sb0 + sn]))
+            else:
+                out.append((name, int(r["offset"]), None, None))
+        return out
 
     def set_stream(self, stream_handle: int | None):
         self._lib.jt_b200_set_stream(self._h, stream_handle)
