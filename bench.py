@@ -291,6 +291,117 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
     dist.destroy_process_group()
 
 
+def record_ranges(data: bytes, world: int) -> list[tuple[int, int]]:
+    """Split an NDJSON buffer on record boundaries: rank g starts after the
+    first '\n' at or after g/world of the bytes."""
+    n = len(data)
+    cuts = [0]
+    for g in range(1, world):
+        k = data.find(b"\n", g * n // world)
+        cuts.append(n if k < 0 else k + 1)
+    cuts.append(n)
+    return [(cuts[g], cuts[g + 1]) for g in range(world)]
+
+
+def run_records(args, rank: int, world: int, local: int, torch, dist):
+    """C3: NDJSON records, each parsed as jt_parse(record) would, in one pass
+    per GPU (jt_b200_parse_records).  N > 1: one buffer of N x size bytes cut
+    on record boundaries; ranks need no exchange but an all_gather of their
+    record counts (global record numbering)."""
+    from paper_1902_08318_b200 import Parser
+    from tools.gen import generate
+    size = args.size or (64 << 20)
+    data = generate(3, size * world)
+    b, e = record_ranges(data, world)[rank]
+    mine = data[b:e]
+    n = len(mine)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    p = Parser()
+    p.set_stream(stream.cuda_stream)
+    host = torch.frombuffer(bytearray(mine), dtype=torch.uint8).pin_memory()
+    p.copy_in(host.data_ptr(), n)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    res = p.parse_records(n, download=False)
+    nrec = len(res)
+    bad = sum(1 for r in res if r[0] != "OK")
+    counts = torch.tensor([nrec], dtype=torch.int64, device="cuda")
+    if dist:
+        allc = torch.empty(world, dtype=torch.int64, device="cuda")
+        dist.all_gather_into_tensor(allc, counts)
+        first_record = int(allc[:rank].sum().item())
+    else:
+        first_record = 0
+    cnt = C.c_size_t()
+    for _ in range(args.warmup):
+        flush.zero_()
+        assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
+    launches = p.last_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        clk.wait_first()
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0  # one host sync inside
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    tot_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dist, "cuda")
+    total_bytes = len(data)
+    value = total_bytes * args.steps / (tot_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    sz = (C.c_ulonglong * 2)()
+    p._lib.jt_b200_records_size(p._h, sz)
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world == 1:
+            try:
+                from oracle.pyoracle import Reference
+                ref = Reference()
+                recs = mine.split(b"\n")[:20000]
+                t0 = time.perf_counter()
+                for r in recs:
+                    ref.parse_code(r)
+                dt = time.perf_counter() - t0
+                sb = sum(len(r) + 1 for r in recs)
+                cpu = {"value": sb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                       "sample": f"first {len(recs)} records, one reference jt_parse each, 1 thread"}
+            except Exception as ex:
+                cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": str(ex)}
+        per_step = tot_ms / args.steps
+        B2 = n + 8 * int(sz[0]) + int(sz[1])
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"C3: NDJSON, lognormal records (mean 256 B), {world} x {size} bytes, "
+                                   "each record parsed as jt_parse(record)",
+                       "bytes": total_bytes, "records_rank0": nrec, "failed_records_rank0": bad,
+                       "first_record_rank0": first_record,
+                       "l2": "flushed before every step (256 MiB memset, outside the events)",
+                       "parallelism": f"{world} GPUs, record-boundary split" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "kernel": "record-mode parse of rank 0's records",
+                         "achieved": B2 / (per_step / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": B2 / (per_step / 1e3) / 1e9 / peak, "traffic": None,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": None,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -317,6 +428,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.config == 3:
+        return run_records(args, rank, world, local, torch, dist)
     if world > 1 or args.shard:
         return run_sharded(args, rank, world, local, torch, dist)
 

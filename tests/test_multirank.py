@@ -103,3 +103,16 @@ def test_shard_layout_cpu():
         assert all(lo[k][1] == lo[k + 1][0] for k in range(G - 1))
     with pytest.raises(ValueError):
         layout(TILE, 2)
+
+
+def test_record_ranges():
+    """C3 across ranks: cuts fall right after a '\\n', cover the buffer, and
+    every record lands on exactly one rank"""
+    import bench
+    data = b"\n".join(b"[%d]" % k * (k % 7 + 1) for k in range(5000)) + b"\n"
+    for world in (1, 2, 3, 8):
+        rr = bench.record_ranges(data, world)
+        assert rr[0][0] == 0 and rr[-1][1] == len(data)
+        assert all(rr[k][1] == rr[k + 1][0] for k in range(world - 1))
+        assert all(b == 0 or data[b - 1:b] == b"\n" for b, _ in rr)
+        assert sum(data[b:e].count(b"\n") for b, e in rr) == data.count(b"\n")
