@@ -358,6 +358,22 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   }
 }
 
+// 4 consecutive tokens per thread (1024 per CTA pass): the token records and
+// their index / string-offset / tape-index words arrive as 16-byte vector
+// loads, all issued before any is used; the next token's index and string
+// offset come from the neighbouring lane.
+constexpr int kScTok = 4;
+
+__device__ __forceinline__ void ld4(const uint32_t *p, uint64_t i, uint64_t S, uint32_t v[4]) {
+  if (i + 4 <= S) {
+    const uint4 x = *(const uint4 *)(p + i);
+    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; k++) v[k] = i + k < S ? p[i + k] : 0u;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   __shared__ int s_wmin[8];
   Ctrl *ctrl = a.ctrl;
@@ -367,24 +383,46 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   const View vw = view_of(a);
   const InAt at{a.in};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t stride = (uint64_t)gridDim.x * 256;
-  for (uint64_t base = (uint64_t)blockIdx.x * 256; base < S; base += stride) {
-    const uint64_t i = base + threadIdx.x;
-    const bool live = i < S;
-    const uint32_t rec = live ? a.tok[i] : 0u;
+  constexpr uint64_t kPass = 256 * kScTok;
+  const uint64_t stride = (uint64_t)gridDim.x * kPass;
+  for (uint64_t base = (uint64_t)blockIdx.x * kPass; base < S; base += stride) {
+    const uint64_t i0 = base + (uint64_t)threadIdx.x * kScTok;
+    uint32_t rec[4], pos[4], so[4], ti[4];
+    ld4(a.tok, i0, S, rec);
+    ld4(a.idx, i0, S, pos);
+    ld4(a.aux, i0, S, so);
+    ld4(a.tape_idx, i0, S, ti);
+    // the token after this thread's four: the next lane's first, or memory
+    uint32_t npos = __shfl_down_sync(0xffffffffu, pos[0], 1);
+    uint32_t nso = __shfl_down_sync(0xffffffffu, so[0], 1);
+    if (lane == 31 && i0 + 4 < S) {
+      npos = a.idx[i0 + 4];
+      nso = a.aux[i0 + 4];
+    }
     // depth min-tree levels 1 (16 tokens), 2 (256), 3 (4096)
-    int m = live ? (int)(int16_t)(rec >> 16) : 0x7FFF;
+    int m = 0x7FFF;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (live && (i & 15) == 0) a.m1[i >> 4] = (int16_t)m;
-    m = min(m, __shfl_xor_sync(0xffffffffu, m, 16));
-    if (lane == 0) s_wmin[warp] = m;
-    if (live) {
-      const uint32_t c = rec & 0xFF;
+    for (int k = 0; k < 4; k++)
+      if (i0 + k < S) m = min(m, (int)(int16_t)(rec[k] >> 16));
+    m = min(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = min(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if ((lane & 3) == 0 && i0 < S) a.m1[i0 >> 4] = (int16_t)m;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_wmin[warp] = m;  // 128 tokens
+    uint32_t nummask = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t i = i0 + k;
+      if (i >= S) break;
+      const uint32_t c = rec[k] & 0xFF;
+      if (c == '-' || (c - '0') < 10u) nummask |= 1u << k;
       uint32_t fail = 0;
       if (c == '"') {
-        const uint32_t p = a.idx[i];
-        const unsigned long long end = i + 1 < S ? a.idx[i + 1] : vw.next_pos;
+        const uint32_t p = pos[k];
+        const uint32_t p_next = k < 3 ? pos[k + 1] : npos;
+        const uint32_t so_next = k < 3 ? so[k + 1] : nso;
+        const unsigned long long end = i + 1 < S ? p_next : vw.next_pos;
         uint32_t sbase = 0;  // record mode: offsets within the record's string buffer
         if (a.records) {
           const uint32_t r = a.rec_of[i];
@@ -395,47 +433,51 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
           fail = str_err >= p && str_err < end;  // the failing string holds the minimum
         }
         if (!fail) {
-          const uint32_t so = a.aux[i];
           // stage 1 wrote the length unless the next token is in another
           // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
           const uint64_t lt = (p - vw.begin) >> 14;
           if (end > a.len || lt != ((end - vw.begin) >> 14) || a.tile_flags[lt]) {
-            const uint32_t nx = i + 1 < S ? a.aux[i + 1] : (uint32_t)vw.next_aux;
-            const uint32_t len = nx - so - 4;
-            uint8_t *f = a.strings + so;
+            const uint32_t nx = i + 1 < S ? so_next : (uint32_t)vw.next_aux;
+            const uint32_t len = nx - so[k] - 4;
+            uint8_t *f = a.strings + so[k];
             f[0] = (uint8_t)len;
             f[1] = (uint8_t)(len >> 8);
             f[2] = (uint8_t)(len >> 16);
             f[3] = (uint8_t)(len >> 24);
           }
-          a.tape[a.tape_idx[i]] = tape_word('"', vw.string_base + so - sbase);
+          a.tape[ti[k]] = tape_word('"', vw.string_base + so[k] - sbase);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
-        const uint32_t p = a.idx[i];
-        fail = !str::atom_ok(at, a.len, p, c);
-        if (!fail) a.tape[a.tape_idx[i]] = (uint64_t)c << 56;
+        fail = !str::atom_ok(at, a.len, pos[k], c);
+        if (!fail) a.tape[ti[k]] = (uint64_t)c << 56;
       }
-      if (fail) a.tok[i] = rec | 0x100u;
+      if (fail) a.tok[i] = rec[k] | 0x100u;
     }
-    // number tokens go to a compacted list: parsed by full warps in k_numbers
+    // number tokens go to a compacted list: parsed by one thread each in k_numbers
     {
-      const uint32_t c = rec & 0xFF;
-      const bool isnum = live && (c == '-' || (c - '0') < 10u);
-      const uint32_t bal = __ballot_sync(0xffffffffu, isnum);
-      if (bal) {
-        uint32_t basep = 0;
-        if (lane == __ffs(bal) - 1) basep = atomicAdd(&ctrl->num_count, __popc(bal));
-        basep = __shfl_sync(0xffffffffu, basep, __ffs(bal) - 1);
-        if (isnum) a.numlist[basep + __popc(bal & ((1u << lane) - 1))] = (uint32_t)i;
+      const uint32_t n = __popc(nummask);
+      uint32_t incl = n;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t basep = 0;
+      if (tot) {
+        if (lane == 31) basep = atomicAdd(&ctrl->num_count, tot);
+        basep = __shfl_sync(0xffffffffu, basep, 31) + incl - n;
+        for (uint32_t q = nummask; q; q &= q - 1) a.numlist[basep++] = (uint32_t)(i0 + __ffs(q) - 1);
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int mm = s_wmin[0];
-#pragma unroll
-      for (int k = 1; k < 8; k++) mm = min(mm, s_wmin[k]);
-      a.m2[base >> 8] = (int16_t)mm;
-      atomicMax(&a.m3[base >> 12], 0x7FFF - mm);
+    if (threadIdx.x < 4) {  // m2 = 256 tokens = 2 warps
+      const int mm = min(s_wmin[2 * threadIdx.x], s_wmin[2 * threadIdx.x + 1]);
+      const uint64_t g2 = (base >> 8) + threadIdx.x;
+      if ((g2 << 8) < S) {
+        a.m2[g2] = (int16_t)mm;
+        atomicMax(&a.m3[g2 >> 4], 0x7FFF - mm);
+      }
     }
     __syncthreads();
   }
