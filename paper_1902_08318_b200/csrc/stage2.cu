@@ -158,116 +158,17 @@ __device__ __forceinline__ uint64_t stack_apply(const StackT &t, uint64_t S) {
 
 constexpr uint64_t kV = 1ULL << 63;
 
-__device__ __forceinline__ void stk_publish_agg(uint64_t *rec, uint64_t tile, const StackT &t) {
-  lb_store(rec + 4 * tile, kV | (t.P & 0xFFFFFFFFULL) | ((uint64_t)(t.k & 0x7FFFFFFF) << 32));
-  lb_store(rec + 4 * tile + 1, kV | (t.P >> 32) | ((uint64_t)t.m << 32));
-}
-
-__device__ __forceinline__ void stk_publish_incl(uint64_t *rec, uint64_t tile, uint64_t S) {
-  lb_store(rec + 4 * tile + 2, kV | (S & 0xFFFFFFFFULL));
-  lb_store(rec + 4 * tile + 3, kV | (S >> 32));
-}
-
-__device__ __forceinline__ void stk_issue(const uint64_t *rec, int64_t tile, uint64_t r[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; k++) r[k] = lb_load(rec + 4 * tile + k);
-}
-
-// 2 = inclusive (S), 1 = aggregate (t), 0 = not ready; r = the 4 record words
-__device__ __forceinline__ int stk_decode(const uint64_t r[4], StackT &t, uint64_t &S) {
-  uint64_t x = r[2], y = r[3];
-  if ((x & y) >> 63) {
-    S = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
-    return 2;
-  }
-  x = r[0], y = r[1];
-  if ((x & y) >> 63) {
-    t.P = (x & 0xFFFFFFFFULL) | ((y & 0xFFFFFFFFULL) << 32);
-    t.k = (uint32_t)((x >> 32) & 0x7FFFFFFF);
-    t.m = (uint32_t)((y >> 32) & 0x7FFFFFFF);
-    return 1;
-  }
-  return 0;
-}
-
-// incoming stack register of tile `tile` > 0 (one full warp); each lane
-// reads kLbPer predecessors per round (lookback.cuh)
-__device__ uint64_t stk_lookback(const uint64_t *rec, int64_t tile) {
-  const int lane = threadIdx.x & 31;
-  StackT G{0, 0, 0};
-  int64_t base = tile - 1;
-  for (;;) {
-    StackT t[kLbPer];
-    uint64_t Sv[kLbPer];
-    int st[kLbPer];
-    uint64_t r[kLbPer][4];
-#pragma unroll
-    for (int j = 0; j < kLbPer; j++) {  // whole window in flight, then wait
-      int64_t pred = base - (int64_t)kLbPer * lane - j;
-      if (pred >= 0) stk_issue(rec, pred, r[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < kLbPer; j++) {
-      int64_t pred = base - (int64_t)kLbPer * lane - j;
-      t[j] = StackT{0, 0, 0};
-      Sv[j] = 0;
-      st[j] = 2;
-      if (pred >= 0) {
-        while ((st[j] = stk_decode(r[j], t[j], Sv[j])) == 0) {
-          __nanosleep(32);
-          stk_issue(rec, pred, r[j]);
-        }
-      }
-    }
-    // per lane, farthest to nearest: resolved stack or composed transfer
-    StackT fn{0, 0, 0};
-    uint64_t sv = 0;
-    bool resolved = false;
-#pragma unroll
-    for (int j = kLbPer - 1; j >= 0; --j) {
-      if (st[j] == 2) {
-        resolved = true;
-        sv = Sv[j];
-        fn = StackT{0, 0, 0};
-      } else if (resolved) {
-        sv = stack_apply(t[j], sv);
-      } else {
-        fn = stack_compose(t[j], fn);
-      }
-    }
-    uint32_t incl = __ballot_sync(0xffffffffu, resolved);
-    if (incl) {
-      int kk = __ffs(incl) - 1;
-      uint64_t s0 = __shfl_sync(0xffffffffu, sv, kk);
-      for (int l = kk - 1; l >= 0; --l) {
-        StackT u;
-        u.P = __shfl_sync(0xffffffffu, fn.P, l);
-        u.k = __shfl_sync(0xffffffffu, fn.k, l);
-        u.m = __shfl_sync(0xffffffffu, fn.m, l);
-        s0 = stack_apply(u, s0);
-      }
-      return stack_apply(G, s0);
-    }
-    StackT H{0, 0, 0};
-    for (int l = 31; l >= 0; --l) {
-      StackT u;
-      u.P = __shfl_sync(0xffffffffu, fn.P, l);
-      u.k = __shfl_sync(0xffffffffu, fn.k, l);
-      u.m = __shfl_sync(0xffffffffu, fn.m, l);
-      H = stack_compose(u, H);
-    }
-    G = stack_compose(G, H);
-    base -= 32 * kLbPer;
-  }
-}
-
 // ---- K2K: container-kind stack scan -----------------------------------------
 // 4096 tokens per CTA (16 per thread); per token the kind of its innermost
 // open container (scopebits, 16 bits per thread) and the max depth.
 constexpr int kStkTok = 16;
 
+// kPass 0: each tile's stack transfer (reduce); kPass 1: scope bits from the
+// tile's carry-in (scan).  k_stack_scan runs between them: no chained
+// look-back, so no CTA waits on another.  Records: stk_rec[4t] = P,
+// [4t+1] = k | m << 32, [4t+2] = carry-in register.
+template <int kPass>
 __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
-  __shared__ uint32_t s_tile;
   __shared__ StackT s_wt[8];
   __shared__ uint64_t s_wS[8];
   Ctrl *ctrl = a.ctrl;
@@ -276,12 +177,7 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
   const View vw = view_of(a);
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->stk_tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    __syncthreads();
-    if (tile >= ntiles) return;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t i0 = (tile * 256 + threadIdx.x) * kStkTok;
     uint32_t recs[kStkTok];
     if (i0 + kStkTok <= S) {
@@ -317,31 +213,32 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
       o.m = __shfl_up_sync(0xffffffffu, inc.m, d);
       if (lane >= d) inc = stack_compose(inc, o);
     }
+    if (lane == 31) s_wt[warp] = inc;
+    if (kPass == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax + (int)vw.depth_base);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        StackT agg = s_wt[0];
+        for (int k = 1; k < 8; k++) agg = stack_compose(s_wt[k], agg);
+        a.stk_rec[4 * tile] = agg.P;
+        a.stk_rec[4 * tile + 1] = (uint64_t)agg.k | ((uint64_t)agg.m << 32);
+      }
+      __syncthreads();
+      continue;
+    }
     StackT ex;
     ex.P = __shfl_up_sync(0xffffffffu, inc.P, 1);
     ex.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
     ex.m = __shfl_up_sync(0xffffffffu, inc.m, 1);
     if (lane == 0) ex = StackT{0, 0, 0};
-    if (lane == 31) s_wt[warp] = inc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax + (int)vw.depth_base);
     __syncthreads();
-    if (warp == 0) {
-      StackT agg = s_wt[0];
-      for (int k = 1; k < 8; k++) agg = stack_compose(s_wt[k], agg);
-      uint64_t S0 = vw.S0;  // containers open at the shard start (0 unsharded)
-      if (tile > 0) {
-        if (lane == 0) stk_publish_agg(a.stk_rec, tile, agg);
-        S0 = stk_lookback(a.stk_rec, (int64_t)tile);
-      }
-      if (lane == 0) {
-        stk_publish_incl(a.stk_rec, tile, stack_apply(agg, S0));
-        uint64_t sw = S0;
-        for (int k = 0; k < 8; k++) {
-          s_wS[k] = sw;
-          sw = stack_apply(s_wt[k], sw);
-        }
+    if (threadIdx.x == 0) {
+      uint64_t sw = a.stk_rec[4 * tile + 2];  // carry-in (k_stack_scan)
+      for (int k = 0; k < 8; k++) {
+        s_wS[k] = sw;
+        sw = stack_apply(s_wt[k], sw);
       }
     }
     __syncthreads();
@@ -355,6 +252,49 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
       else if (c == '}' || c == ']') St >>= 1;
     }
     if (i0 < S) ((uint16_t *)a.scopebits)[i0 / kStkTok] = (uint16_t)bits;
+    __syncthreads();
+  }
+}
+
+// carry-in register of every k_stack tile: one CTA, each thread a contiguous
+// chunk of tiles; starts from the shard's incoming stack (0 unsharded)
+constexpr int kStkScan = 1024;
+__global__ void __launch_bounds__(kStkScan) k_stack_scan(Stage2Args a) {
+  __shared__ StackT s_w[kStkScan / 32];
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->utf8_pos != ~0ULL) return;
+  const uint64_t S = ctrl->S;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
+  const uint64_t per = (ntiles + kStkScan - 1) / kStkScan;
+  const uint64_t lo = threadIdx.x * per, hi = lo + per < ntiles ? lo + per : ntiles;
+  auto tile_t = [&](uint64_t t) {
+    const uint64_t km = a.stk_rec[4 * t + 1];
+    return StackT{a.stk_rec[4 * t], (uint32_t)km, (uint32_t)(km >> 32)};
+  };
+  StackT acc{0, 0, 0};
+  for (uint64_t t = lo; t < hi; t++) acc = stack_compose(tile_t(t), acc);
+  StackT inc = acc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    StackT o;
+    o.P = __shfl_up_sync(0xffffffffu, inc.P, d);
+    o.k = __shfl_up_sync(0xffffffffu, inc.k, d);
+    o.m = __shfl_up_sync(0xffffffffu, inc.m, d);
+    if (lane >= d) inc = stack_compose(inc, o);
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  uint64_t St = view_of(a).S0;
+  for (int k = 0; k < warp; k++) St = stack_apply(s_w[k], St);
+  StackT ex;
+  ex.P = __shfl_up_sync(0xffffffffu, inc.P, 1);
+  ex.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
+  ex.m = __shfl_up_sync(0xffffffffu, inc.m, 1);
+  if (lane > 0) St = stack_apply(ex, St);
+  for (uint64_t t = lo; t < hi; t++) {
+    a.stk_rec[4 * t + 2] = St;
+    St = stack_apply(tile_t(t), St);
   }
 }
 
@@ -1355,7 +1295,9 @@ static void launch_stack(const Stage2Args &a, cudaStream_t stream) {
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
   uint64_t nst = (a.cap_tokens + 4095) / 4096;
   unsigned gs = (unsigned)(nst < (uint64_t)sms * 4 ? nst : (uint64_t)sms * 4);
-  k_stack<<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
+  k_stack<0><<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
+  k_stack_scan<<<1, kStkScan, 0, stream>>>(a);
+  k_stack<1><<<gs < 1 ? 1 : gs, 256, 0, stream>>>(a);
 }
 
 static void launch_struct(const Stage2Args &a, cudaStream_t stream) {
@@ -1381,7 +1323,7 @@ cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int 
   launch_stack(a, stream);
   launch_struct(a, stream);
   k_final_records<<<1184, 256, 0, stream>>>(a);
-  *launches = 7;
+  *launches = 9;
   return cudaGetLastError();
 }
 
@@ -1409,7 +1351,7 @@ cudaError_t shard_phase3_launch(const Stage2Args &a, const Sum2 *gathered, cudaS
   launch_stack(a, stream);
   launch_struct(a, stream);
   k_final_shard<<<1, 1, 0, stream>>>(a);
-  *launches = 4;
+  *launches = 6;
   return cudaGetLastError();
 }
 
@@ -1438,7 +1380,7 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[4], stream);
-  *launches = 7;
+  *launches = 9;
   return cudaGetLastError();
 }
 
