@@ -1,2 +1,5 @@
-mkdir -p gpurun_out
-ncu --set full --import-source on --clock-control none -k regex:"k_scalars|k_struct|k_stack|k_numbers" -s 4 -c 4 -o gpurun_out/k2 -f python bench.py --config 1 --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu.log 2>&1; tail -1 gpurun_out/ncu.log
+for r in 1 2; do
+for v in A B; do
+if [ $v = A ]; then export JT_B200_LIB=$PWD/exp/libA.so; else unset JT_B200_LIB; fi
+python bench.py --config 1 --steps 20 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['kernel_ms']['struct'],4))"
+done; done

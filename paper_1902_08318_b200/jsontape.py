@@ -18,6 +18,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libjsontape_b200.so")
+# A/B builds: JT_B200_LIB points at another build of the same library
+LIB_PATH = os.environ.get("JT_B200_LIB", LIB_PATH)
 
 OK, UTF8_ERROR, STRING_ERROR, NUMBER_ERROR, TAPE_ERROR, DEPTH_ERROR, CAPACITY, EMPTY = range(8)
 ERROR_NAMES = ["OK", "UTF8_ERROR", "STRING_ERROR", "NUMBER_ERROR", "TAPE_ERROR", "DEPTH_ERROR",
