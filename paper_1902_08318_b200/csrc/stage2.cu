@@ -38,6 +38,14 @@ constexpr int kWarps2 = kS2Threads / 32;
 struct InAt {
   const uint8_t *in;
   __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
+  // eight bytes from i: two aligned 8-byte loads (the padded input is
+  // readable well past len)
+  __device__ __forceinline__ uint64_t load8(uint64_t i) const {
+    const uint64_t *q = (const uint64_t *)(in + (i & ~7ULL));
+    const uint64_t lo = q[0], hi = q[1];
+    const uint32_t sh = (uint32_t)(i & 7) * 8;
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+  }
 };
 
 // A token's bytes from a 40-byte register window [base, base+40), base =

@@ -11,7 +11,16 @@ using namespace jt;
 // returns 0 fail, 1 int, 2 float; *bits the word; *slow whether the exact
 // fallback was needed
 extern "C" int jt_cpu_number(const uint8_t *buf, uint64_t len, uint64_t *bits, int *slow) {
-  auto at = [&](uint64_t i) -> uint32_t { return i < len ? buf[i] : 0; };
+  struct At {
+    const uint8_t *buf;
+    uint64_t len;
+    uint32_t operator()(uint64_t i) const { return i < len ? buf[i] : 0; }
+    uint64_t load8(uint64_t i) const {
+      uint64_t v = 0;
+      for (int k = 0; k < 8; k++) v |= (uint64_t)(*this)(i + k) << (8 * k);
+      return v;
+    }
+  } at{buf, len};
   num::NumResult r = num::parse_number(at, len, 0);
   *slow = 0;
   if (r.kind == num::kNumSlow) {

@@ -171,6 +171,35 @@ def test_numbers_vs_strtod(number_lib, oracle):
             assert (k == 1) == is_int and b.value == bits, t
 
 
+def test_numbers_digit_runs(number_lib, oracle):
+    """8-digit SWAR steps (numparse.cuh): runs around the 8/16/19-digit
+    boundaries, leading fraction zeros across chunks, int64 limits"""
+    rng = random.Random(29)
+    cases = [b"9223372036854775807", b"9223372036854775808", b"-9223372036854775808",
+             b"-9223372036854775809", b"12345678", b"123456789012345678", b"1234567890123456789",
+             b"12345678901234567890", b"0.00000000000000000001", b"0.000000001234567890123",
+             b"0.00000000", b"0.0000000012345678e-5", b"1.0000000000000000000000001"]
+    for _ in range(20000):
+        ni = rng.choice([0, 1, 7, 8, 9, 11, 12, 16, 17, 19, 20, 25])
+        nf = rng.choice([0, 1, 7, 8, 9, 15, 16, 17, 24, 30])
+        lz = rng.choice([0, 0, 3, 8, 9, 16, 20])
+        ip = (str(rng.randrange(1, 10)) + "".join(rng.choice("0123456789") for _ in range(ni - 1))) if ni else "0"
+        fp = "0" * lz + "".join(rng.choice("0123456789") for _ in range(nf))
+        t = ip + ("." + fp if fp else "")
+        if rng.random() < 0.3:
+            t += "e" + rng.choice(["", "-", "+"]) + str(rng.randrange(0, 330))
+        if rng.random() < 0.3:
+            t = "-" + t
+        cases.append(t.encode())
+    for t in cases:
+        ok, is_int, bits = oracle.number(t)
+        b, slow = C.c_uint64(), C.c_int()
+        k = number_lib.jt_cpu_number(t + b"\0" * 64, len(t), C.byref(b), C.byref(slow))
+        assert (k != 0) == ok, t
+        if ok:
+            assert (k == 1) == is_int and b.value == bits, t
+
+
 def test_glibc_subnormal_quirk(number_lib, oracle):
     # (2724151024255084 + 3/4) * 2^-1074: correctly rounded is ...085, glibc
     # strtod (the reference's slow_float) returns ...084; we match glibc.
