@@ -677,6 +677,35 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     // plain runs (escape positions get placeholder bytes, rewritten below;
     // the first vin bits belong to the previous block's escape)
     uint64_t cm = W & ~sb::low_bits(vin);
+    // warp-uniform choice by the slowest lane's estimated cost (a warp runs
+    // the union of its lanes' paths): ~6 instructions per byte for the byte
+    // loop, ~35 per run plus a word copy per 4 bytes for the run loop
+    const int nruns = popc64(cm & ~(cm << 1));
+    int cost_byte = 6 * popc64(cm | openq), cost_run = 35 * nruns + popc64(cm) / 2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cost_byte = max(cost_byte, __shfl_xor_sync(0xffffffffu, cost_byte, o));
+      cost_run = max(cost_run, __shfl_xor_sync(0xffffffffu, cost_run, o));
+    }
+    if (cost_byte < cost_run) {
+      // fragmented (escape-dense) block: byte by byte, destinations counted
+      // as the bits go by (an opening quote adds its 4-byte length field)
+      uint64_t bits = cm | openq;
+      uint32_t wdst = 4u * popc64(openq & sb::low_bits(vin)) + popc64(W & sb::low_bits(vin));
+      while (bits) {
+        const int k = ctz64(bits);
+        bits &= bits - 1;
+        if ((openq >> k) & 1) {
+          wdst += 4;
+        } else {
+          const uint8_t b = s_in[local + k];
+          if (pay_direct) a.strings[gsbase + soff + wdst] = b;
+          else s_pay[soff + wdst] = b;
+          wdst++;
+        }
+      }
+      cm = 0;
+    }
     while (cm) {  // string runs, 4-byte gaps before each run opened here
       const int a0 = ctz64(cm);
       const uint64_t sh = cm >> a0;
