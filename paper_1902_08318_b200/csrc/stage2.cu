@@ -603,6 +603,64 @@ struct TileTree {
   int64_t base;
 };
 
+// 16-bit masks "depth <= L" of one group from vector loads (the records
+// hold depth_before in their high half; the tree levels are int16)
+__device__ __forceinline__ uint32_t tok_mask_le(const uint32_t *g16, int L) {
+  const uint4 *q = (const uint4 *)g16;
+  uint32_t m = 0;
+#pragma unroll
+  for (int h = 0; h < 4; h++) {
+    const uint4 x = q[h];
+    m |= (uint32_t)(tok_depth(x.x) <= L) << (4 * h);
+    m |= (uint32_t)(tok_depth(x.y) <= L) << (4 * h + 1);
+    m |= (uint32_t)(tok_depth(x.z) <= L) << (4 * h + 2);
+    m |= (uint32_t)(tok_depth(x.w) <= L) << (4 * h + 3);
+  }
+  return m;
+}
+
+__device__ __forceinline__ uint32_t i16_mask_le(const int16_t *g16, int L) {
+  const uint4 *q = (const uint4 *)g16;
+  uint32_t m = 0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const uint4 x = q[h];
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      m |= (uint32_t)((int)(int16_t)(w[k] & 0xFFFF) <= L) << (8 * h + 2 * k);
+      m |= (uint32_t)((int)(int16_t)(w[k] >> 16) <= L) << (8 * h + 2 * k + 1);
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ int last_bit(uint32_t m) { return 31 - __clz(m); }
+
+// Deep documents (containers span many groups): one masked step per tree
+// level instead of scanning entries one at a time.
+__device__ int64_t psv_tile_masked(const Stage2Args &a, const TileTree &T, int64_t i, int L) {
+  const int64_t x = i - 1 - T.base;
+  if (x >= 0) {
+    const int g = (int)(x >> 4), G = g >> 4;
+    uint32_t m = tok_mask_le(T.tok + g * 16, L) & ((2u << (x & 15)) - 1);
+    if (m) return T.base + g * 16 + last_bit(m);
+    int h = -1;
+    const uint32_t mh = i16_mask_le(T.l1 + G * 16, L) & ((1u << (g & 15)) - 1);
+    if (mh) {
+      h = G * 16 + last_bit(mh);
+    } else {
+      const uint32_t m2 = i16_mask_le(T.l2, L) & ((1u << G) - 1);
+      if (m2) {
+        const int H = last_bit(m2);
+        h = H * 16 + last_bit(i16_mask_le(T.l1 + H * 16, L));
+      }
+    }
+    if (h >= 0) return T.base + h * 16 + last_bit(tok_mask_le(T.tok + h * 16, L));
+  }
+  return psv(a, T.base, L);
+}
+
 // nearest j < i (j >= tile base) with depth_before <= L inside the tile, or
 // the global search below the tile
 __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, int L) {
@@ -634,18 +692,21 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
   return psv(a, T.base, L);
 }
 
-// kMode: 0 one document, 1 a byte-range shard (shard.h), 2 NDJSON records
-template <int kMode>
+// kMode: 0 one document, 1 a byte-range shard (shard.h), 2 NDJSON records.
+// kDeep: the instance for documents deeper than 64 (masked tree search); for
+// one document both instances are launched and the other one returns.
+template <int kMode, bool kDeep = false>
 __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   constexpr bool kShard = kMode == 1, kRecs = kMode == 2;
   __shared__ __align__(16) uint32_t s_tok[kK3Tile];
-  __shared__ int16_t s_l1[256];
-  __shared__ int16_t s_l2[16];
+  __shared__ __align__(16) int16_t s_l1[256];
+  __shared__ __align__(16) int16_t s_l2[16];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
   const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
+  const bool deep = !shallow;
   // this shard's place in the document, as scalars (a View captured by the
   // lambdas below would live in local memory)
   // (tape indices fit 32 bits: tape_idx is u32)
@@ -863,7 +924,8 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
               top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
             } else {
               if (far_level != D - 1) {
-                int64_t j = psv_tile(a, T, (int64_t)i, D - 1 - db);
+                int64_t j = deep ? psv_tile_masked(a, T, (int64_t)i, D - 1 - db)
+                                 : psv_tile(a, T, (int64_t)i, D - 1 - db);
                 if (j >= 0) {
                   far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
                   far_tape = tb + tape_of(a, j);
