@@ -508,6 +508,19 @@ def main():
     kern_bytes = {"stage1": B1, "tokens": Btok, "struct": 4 * S + 8 * T}
     dom = max(kern_bytes, key=lambda k: kt.get(k, 0.0))
     ach = kern_bytes[dom] / (kt[dom] / 1e3) / 1e9
+    # DRAM traffic of the dominant kernel per launch, from the committed
+    # `ncu --set full` capture of this workload (profiles/), when it matches
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_c1.json")) as f:
+            prof = json.load(f)
+        kname = {"stage1": "k_stage1<0>", "tokens": "k_scalars", "struct": "k_struct<0, 0>"}[dom]
+        e = next(v for k, v in prof.items() if k.endswith(kname))
+        if args.config == CONFIG and not args.size:
+            traffic = (float(e["dram__bytes_read.sum"]) + float(e["dram__bytes_write.sum"])) * 1e6
+            traffic_src = f"profiles/r01_ncu_full_c1.json {kname} dram read+write per launch"
+    except Exception:
+        pass
 
     # e2e through the public C ABI: pinned host input -> jt_parse -> host document
     e2e_ms = []
@@ -548,7 +561,8 @@ def main():
             "stage1_gbs": n / (s1_ms / 1e3) / 1e9,
             "kernel_ms": kt,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": None, "peak_source": peak_src},
+                         "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes": kern_bytes[dom], "peak_source": peak_src},
             "roofline_stage1": {"achieved": B1 / (s1_ms / 1e3) / 1e9, "frac": B1 / (s1_ms / 1e3) / 1e9 / peak,
                                 "bytes": B1},
             "roofline_full": {"achieved": B2 / (tot_ms / args.steps / 1e3) / 1e9,
