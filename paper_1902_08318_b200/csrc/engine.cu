@@ -185,6 +185,13 @@ struct jt_parser {
   jt::Shard *h_shard = nullptr;  // pinned
   DevBuf shard;                  // Shard + open-container stack
   uint64_t shard_len = 0;        // document length
+  // streamed jt_parse (parse_stream): copy stream, per-chunk events, chunk
+  // tile counters and carry states, stage-1 control block snapshot
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t ev_start = nullptr, ev_s1 = nullptr;
+  DevBuf stream_words;
+  jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
   std::vector<jt::RecordResult> h_records;
@@ -256,11 +263,14 @@ bool ensure_stage2(jt_parser *p, uint64_t len) {
   return ok;
 }
 
+// layout_tiles: tiles the record arrays are laid out for (the range's own
+// count unless a streamed document shares one layout across its pieces)
 jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0,
-                       uint64_t end = ~0ULL) {
+                       uint64_t end = ~0ULL, uint64_t layout_tiles = 0) {
   jt::Stage1Args a{};
   a.begin = begin;
   a.end = end == ~0ULL ? len : end;
+  a.last_tile = ~0ULL;
   jt::Ctrl *c = p->ctrl.as<jt::Ctrl>();
   a.in = p->in.as<uint8_t>();
   a.len = len;
@@ -270,7 +280,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0
   a.tokrec = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
   a.tile_flags = p->tile_flags.as<uint32_t>();
-  uint64_t nt = jt::stage1_records(a.end - a.begin);
+  uint64_t nt = layout_tiles ? layout_tiles : jt::stage1_records(a.end - a.begin);
   a.fn = (uint32_t *)p->s1rec.as<uint64_t>();  // 2 x ntiles u32 in the ntiles-word channel-1 area
   a.carry = a.fn + nt;
   a.rec_count = p->s1rec.as<uint64_t>() + nt;
@@ -458,6 +468,141 @@ jt_document *download(jt_parser *p) {
   return d;
 }
 
+// ---- streamed jt_parse --------------------------------
+// The host input goes up in kStreamChunk pieces on a copy stream; stage 1 of
+// each piece starts as soon as it has landed (K0b carries the carry state
+// from the previous piece, K1's count look-back spans pieces through the
+// document's tile numbering), so the upload hides stage 1.  The string
+// buffer is complete after stage 1 and comes back while stage 2 runs.
+constexpr uint64_t kStreamChunk = 4ULL << 20;  // multiple of kStage1Tile
+constexpr uint64_t kStreamMin = 8ULL << 20;    // shorter documents: one upload
+
+bool ensure_stream(jt_parser *p, uint64_t nch) {
+  if (!p->copy_stream &&
+      cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    p->copy_stream = nullptr;
+    return false;
+  }
+  if (!p->h_ctrl_s1 && cudaMallocHost((void **)&p->h_ctrl_s1, sizeof(jt::Ctrl)) != cudaSuccess) {
+    cudaGetLastError();
+    p->h_ctrl_s1 = nullptr;
+    return false;
+  }
+  auto mk = [](cudaEvent_t *e) {
+    return *e || cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  };
+  if (!mk(&p->ev_start) || !mk(&p->ev_s1)) return false;
+  while (p->chunk_ev.size() < nch) {
+    cudaEvent_t e = nullptr;
+    if (!mk(&e)) return false;
+    p->chunk_ev.push_back(e);
+  }
+  return p->stream_words.ensure(nch * 2 * sizeof(uint32_t) + 64);  // tile counters + carry states
+}
+
+jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
+  if (out) *out = nullptr;
+  const int which = p->cur ^ 1;
+  const uint64_t nch = (len + kStreamChunk - 1) / kStreamChunk;
+  const uint64_t ntiles = jt::stage1_records(len);
+  if (!ensure_input(p, len) || !ensure_stage1(p, len, which) || !ensure_stage2(p, len) ||
+      !ensure_stream(p, nch)) {
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  cudaStream_t cs = p->copy_stream;
+  uint32_t *counters = p->stream_words.as<uint32_t>(), *states = counters + nch;
+  p->launches = 0;
+  jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
+  const uint64_t s1w = ntiles * 9;
+  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
+  bool ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
+                                       p->s2rec.as<uint64_t>(), s2w, p->stream),
+                    "init") &&
+            cuda_ok(p, cudaMemsetAsync(counters, 0, nch * sizeof(uint32_t), p->stream), "counters") &&
+            cuda_ok(p, cudaEventRecord(p->ev_start, p->stream), "event") &&
+            cuda_ok(p, cudaStreamWaitEvent(cs, p->ev_start, 0), "wait");
+  p->launches = 1;
+  // uploads: zero tail first (the last piece's stage 1 reads it), then the pieces
+  uint8_t *in = p->in.as<uint8_t>();
+  ok = ok && cuda_ok(p, cudaMemsetAsync(in + len, 0, input_capacity(len) - len, cs), "tail");
+  for (uint64_t c = 0; ok && c < nch; c++) {
+    const uint64_t b = c * kStreamChunk, e = std::min(len, b + kStreamChunk);
+    ok = cuda_ok(p, cudaMemcpyAsync(in + b, data + b, e - b, cudaMemcpyHostToDevice, cs), "H2D") &&
+         cuda_ok(p, cudaEventRecord(p->chunk_ev[c], cs), "event");
+  }
+  // stage 1 piece by piece, each after its upload
+  for (uint64_t c = 0; ok && c < nch; c++) {
+    const uint64_t b = c * kStreamChunk, e = std::min(len, b + kStreamChunk);
+    jt::Stage1Args a = s1_args(p, len, which, b, e, ntiles);
+    a.rec_tile0 = b / jt::kStage1Tile;
+    a.last_tile = ntiles - 1;
+    a.fn += a.rec_tile0;
+    a.carry += a.rec_tile0;
+    a.tile_counter = counters + c;
+    a.init_state = c ? states + c - 1 : nullptr;
+    a.out_state = states + c;
+    ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
+         cuda_ok(p, jt::stage1_chunk_launch(a, p->stream), "stage1 chunk");
+    p->launches += jt::kStage1Launches;
+  }
+  ok = ok && cuda_ok(p, jt::stage1_lengths_launch(s1_args(p, len, which, 0, len, ntiles), ntiles, p->stream),
+                     "lengths") &&
+       cuda_ok(p, cudaMemcpyAsync(p->h_ctrl_s1, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl D2H") &&
+       cuda_ok(p, cudaEventRecord(p->ev_s1, p->stream), "event");
+  p->launches += 1;
+  int n2 = 0;
+  ok = ok && cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n2), "stage2") &&
+       cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                  p->stream),
+               "ctrl D2H");
+  p->launches += n2;
+  if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_s1), "sync")) {
+    cudaStreamSynchronize(p->stream);
+    cudaStreamSynchronize(cs);
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  // stage 1 is done: the string buffer is final; fetch it while stage 2 runs
+  jt_document *d = nullptr;
+  const jt::Ctrl c1 = *p->h_ctrl_s1;
+  if (out && c1.utf8_pos == ~0ULL) {
+    d = new (std::nothrow) jt_document;
+    if (d && !d->alloc(c1.tape_words + 1, c1.string_bytes)) {
+      delete d;
+      d = nullptr;
+    }
+    if (d && c1.string_bytes &&
+        !cuda_ok(p, cudaMemcpyAsync(d->strings.data(), p->strings.p, c1.string_bytes,
+                                    cudaMemcpyDeviceToHost, cs),
+                 "strings D2H")) {
+      delete d;
+      d = nullptr;
+    }
+  }
+  jt_error e = finish(p, which, true, off);  // waits for stage 2
+  cudaStreamSynchronize(cs);
+  if (e != JT_OK || !out) {
+    delete d;
+    return e;
+  }
+  if (!d || d->tape.size() != p->last_tape_len ||
+      !cuda_ok(p, cudaMemcpyAsync(d->tape.data(), p->tape.p, p->last_tape_len * 8,
+                                  cudaMemcpyDeviceToHost, p->stream),
+               "tape D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
+    delete d;
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  p->in_len = len;
+  *out = d;
+  return e;
+}
+
 jt_error parse_resident(jt_parser *p, uint64_t len, jt_document **out, long long *off) {
   if (out) *out = nullptr;
   if (len >= (1ULL << 32)) {  // indexer.cpp:33-34
@@ -520,6 +665,14 @@ void jt_parser_free(jt_parser *p) {
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
   if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
   if (p->h_shard) cudaFreeHost(p->h_shard);
+  if (p->copy_stream) {
+    cudaStreamSynchronize(p->copy_stream);
+    cudaStreamDestroy(p->copy_stream);
+  }
+  for (cudaEvent_t e : p->chunk_ev) cudaEventDestroy(e);
+  if (p->ev_start) cudaEventDestroy(p->ev_start);
+  if (p->ev_s1) cudaEventDestroy(p->ev_s1);
+  if (p->h_ctrl_s1) cudaFreeHost(p->h_ctrl_s1);
   delete p;
 }
 
@@ -537,6 +690,7 @@ jt_error jt_parse(jt_parser *p, const char *data, size_t len, jt_document **out,
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
+  if ((uint64_t)len >= kStreamMin) return parse_stream(p, data, len, out, error_offset);
   if (!upload(p, data, len)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;

@@ -207,7 +207,9 @@ __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn,
                                                              uint64_t ntiles, const Sum0 *gathered,
                                                              uint32_t g, Sum0 *total,
                                                              const uint32_t *nl_count,
-                                                             uint32_t *nl_base, uint64_t *nl_total) {
+                                                             uint32_t *nl_base, uint64_t *nl_total,
+                                                             const uint32_t *init_state = nullptr,
+                                                             uint32_t *out_state = nullptr) {
   __shared__ uint32_t s_agg[kScanThreads / 32];
   __shared__ uint32_t s_has[kScanThreads / 32];
   __shared__ uint32_t s_nlw[kScanThreads / 32];
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn,
   }
   // exclusive prefix state of this thread: earlier shards, earlier warps,
   // then earlier lanes
-  uint32_t state = s1::kInitState;
+  uint32_t state = init_state ? *init_state : s1::kInitState;
   if (gathered)
     for (uint32_t h = 0; h < g; h++) state = s1::apply(gathered[h].fn, state);
   for (int k = 0; k < warp; k++)
@@ -277,6 +279,7 @@ __global__ void __launch_bounds__(kScanThreads) k_carry_scan(const uint32_t *fn,
         state = s1::apply(v[j], state);
       }
   }
+  if (out_state && hi == ntiles && lo < hi) *out_state = state;  // the thread with the last tile
   if (nl_count == nullptr) return;
   // record mode: exclusive prefix of the tiles' newline counts (record ids)
   uint32_t mine = 0;
@@ -616,21 +619,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const uint64_t tdepth = kRec ? ((dtf ? kSegFlag : 0ULL) | ((uint64_t)(long long)dtotal & kSegMask))
                                 : ((unsigned long long)(long long)dtotal & kQuadMask);
   const Quad tot{{total, stotal, ttotal, tdepth}};
+  const int64_t gt = (int64_t)a.rec_tile0 + tile;  // tile in the document's records
+  const int64_t last_tile = a.last_tile == ~0ULL ? (int64_t)a.ntiles - 1 : (int64_t)a.last_tile;
   auto resolve_counts = [&]() {  // warp 0
     Quad base{{0, 0, 0, 0}};
-    if (tile > 0) base = quad_lookback<kRec>(a.rec_count, tile);
+    if (gt > 0) base = quad_lookback<kRec>(a.rec_count, gt);
     if (lane == 0) {
       JT_TL(tile, 5);
       Quad inc;
 #pragma unroll
       for (int k = 0; k < 3; k++) inc.v[k] = (base.v[k] + tot.v[k]) & kQuadMask;
       inc.v[3] = kRec ? seg_combine(base.v[3], tot.v[3]) : ((base.v[3] + tot.v[3]) & kQuadMask);
-      quad_publish(a.rec_count, tile, 1, inc);
+      quad_publish(a.rec_count, gt, 1, inc);
       s_base = base.v[0];
       s_sbase = base.v[1];
       s_tbase = base.v[2];
       s_dbase = kRec ? seg_value(base.v[3]) : sext63(base.v[3]);
-      if (tile == (int64_t)a.ntiles - 1) {
+      if (gt == last_tile) {
         *a.total = inc.v[0];
         *a.total_strings = inc.v[1];
         *a.tape_words = 1 + inc.v[2];
@@ -638,9 +643,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
     }
   };
-  if (threadIdx.x == 0 && tile > 0) {
+  if (threadIdx.x == 0 && gt > 0) {
     JT_TL(tile, 4);
-    quad_publish(a.rec_count, tile, 0, tot);
+    quad_publish(a.rec_count, gt, 0, tot);
   }
   if (direct && warp == 0) resolve_counts();
   if (threadIdx.x == 0) JT_TL(tile, 6);
@@ -794,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
     }
   }
-  if (threadIdx.x == 0) a.tile_flags[tile] = (idx_direct || pay_direct) ? 1u : 0u;
+  if (threadIdx.x == 0) a.tile_flags[gt] = (idx_direct || pay_direct) ? 1u : 0u;
   if constexpr (kRec) {
     // the record each newline ends: where the next one starts, and the
     // token / tape / string-buffer prefixes at its end
@@ -884,6 +889,47 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
                                                  nullptr, nullptr, nullptr);
     k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
   }
+  return cudaGetLastError();
+}
+
+// Length fields K1 leaves to stage 2 (a string whose next token is in another
+// tile, or any string of a spilled tile), written right after stage 1 so the
+// string buffer is final before the tape exists (streamed jt_parse).  One
+// thread per tile; counts from the tiles' inclusive look-back records.
+__global__ void k_tile_lengths(Stage1Args a, uint64_t ntiles) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const uint64_t S = *a.total, SB = *a.total_strings;
+  auto incl = [&](uint64_t k) { return a.rec_count[8 * k + 4] & kQuadMask; };
+  const uint64_t hi = incl(t), lo = t ? incl(t - 1) : 0;
+  if (hi == lo) return;
+  const uint64_t from = a.tile_flags[t] ? lo : hi - 1;
+  for (uint64_t k = from; k < hi; k++) {
+    if ((a.tokrec[k] & 0xFF) != '"') continue;
+    const uint32_t so = a.aux[k];
+    const uint32_t nx = k + 1 < S ? a.aux[k + 1] : (uint32_t)SB;
+    const uint32_t len = nx - so - 4;
+    uint8_t *f = a.strings + so;
+    f[0] = (uint8_t)len;
+    f[1] = (uint8_t)(len >> 8);
+    f[2] = (uint8_t)(len >> 16);
+    f[3] = (uint8_t)(len >> 24);
+  }
+}
+
+cudaError_t stage1_lengths_launch(const Stage1Args &a, uint64_t ntiles, cudaStream_t stream) {
+  k_tile_lengths<<<(unsigned)((ntiles + 255) / 256), 256, 0, stream>>>(a, ntiles);
+  return cudaGetLastError();
+}
+
+cudaError_t stage1_chunk_launch(const Stage1Args &args_in, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  const cudaError_t configured = stage1_configure();
+  if (configured != cudaSuccess) return configured;
+  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr, nullptr,
+                                               nullptr, nullptr, a.init_state, a.out_state);
+  k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError();
 }
 

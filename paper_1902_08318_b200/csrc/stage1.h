@@ -34,6 +34,13 @@ struct Stage1Args {
   uint64_t *tape_words;           // 1 + sum of token widths
   int64_t *depth_total;           // depth change over the range
   uint64_t begin, end;            // byte range [begin, end): a shard, or [0, len)
+  // streaming (one document in chunks): the range's first tile in the
+  // document's look-back records / tile flags, and the document's last tile
+  // (writes the totals); 0 and ~0 = the range is the whole record space
+  uint64_t rec_tile0;
+  uint64_t last_tile;
+  const uint32_t *init_state;     // carry state before the range (nullptr = initial)
+  uint32_t *out_state;            // carry state after the range (optional)
   // record (NDJSON) mode: '\n'-separated records parsed independently
   bool records;
   uint32_t *nl_count, *nl_base;   // per tile: newlines, newlines before it (K0)
@@ -50,6 +57,11 @@ size_t stage1_records(uint64_t len);
 
 constexpr int kStage1Launches = 3;  // K0a carry functions, K0b carry scan, K1
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
+// one chunk of a streamed document (rec_tile0 / last_tile / init_state /
+// out_state set): K0a, K0b, K1
+cudaError_t stage1_chunk_launch(const Stage1Args &args, cudaStream_t stream);
+// after a streamed stage 1: the string length fields K1 left to stage 2
+cudaError_t stage1_lengths_launch(const Stage1Args &args, uint64_t ntiles, cudaStream_t stream);
 
 // record (NDJSON) mode, split so the caller can size the per-record arrays
 // from the newline count: K0 (carries + newline counts), then K1

@@ -155,3 +155,21 @@ def test_error_sweep(parser, oracle):
         err = 1 + seed % 5
         data = generate(4, 1 << 14, seed=seed, err=err)
         check_same(parser, oracle, data, f"C4 err {err} seed {seed}")
+
+
+def test_streamed_jt_parse(parser, oracle):
+    """jt_parse of documents >= 8 MiB streams the host input in 4 MiB pieces
+    (engine.cu parse_stream): stage 1 per piece as it lands, the string
+    buffer fetched during stage 2.  Same results as the single-upload path."""
+    from tools.gen import generate
+    docs = [(generate(1, 20 << 20, seed=3), "C1 20 MiB"), (generate(2, 12 << 20, seed=4), "C2 12 MiB"),
+            (generate(4, 18 << 20, seed=5), "C4 18 MiB")]
+    base = generate(0, 9 << 20, seed=6)
+    # errors late in the document, in the last piece, and a string across a piece boundary
+    docs.append((base[:-3] + b"x]", "tail error"))
+    k = 4 << 20
+    docs.append((base[:k + 5] + b"\xff" + base[k + 6:], "utf-8 error in piece 1"))
+    s = b'["' + b"a" * ((8 << 20) + 100) + b'"]'
+    docs.append((s, "string across pieces"))
+    for data, where in docs:
+        check_same(parser, oracle, data, where)
