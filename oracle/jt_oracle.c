@@ -119,6 +119,30 @@ int jto_stage1(const uint8_t *data, size_t len, jto_result *r) {
   return JTO_OK;
 }
 
+/* jt_minify (capi.cpp:154-167): full parse, then minify_pass
+ * (indexer.cpp:58-75): keep in-string bytes (opening quote included),
+ * unescaped quotes (the closing one) and every non-whitespace byte. */
+int jto_minify(const uint8_t *data, size_t len, uint8_t *out, size_t *out_len, long long *offset) {
+  jto_result r;
+  int code = jto_parse(data, len, &r);
+  *offset = r.offset;
+  jto_free(&r);
+  *out_len = 0;
+  if (code != JTO_OK) return code;
+  size_t n = 0;
+  int run_odd = 0, in_string = 0;
+  for (size_t i = 0; i < len; i++) {
+    uint8_t c = data[i];
+    int escaped = run_odd;
+    run_odd = c == '\\' ? !run_odd : 0;
+    int uq = c == '"' && !escaped;
+    if (uq) in_string = !in_string;
+    if (in_string || uq || !is_ws(c)) out[n++] = c;
+  }
+  *out_len = n;
+  return JTO_OK;
+}
+
 /* ------------------------------------------------------------- strings */
 
 static int hex_value(uint8_t c) { /* stringparse.cpp:30-38 */

@@ -61,6 +61,8 @@ int jto_stage1(const uint8_t *data, size_t len, jto_result *r);
 /* full parse (capi.cpp:73-93 semantics); allocations freed by jto_free */
 int jto_parse(const uint8_t *data, size_t len, jto_result *r);
 void jto_free(jto_result *r);
+/* jt_minify: parse, then minify_pass; out >= len bytes */
+int jto_minify(const uint8_t *data, size_t len, uint8_t *out, size_t *out_len, long long *offset);
 
 /* single-token helpers, for the number/string unit vectors */
 int jto_parse_number(const uint8_t *buf, size_t len, size_t offset,

@@ -82,6 +82,8 @@ class Oracle:
         L.jto_parse.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_JtoResult)]
         L.jto_stage1.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_JtoResult)]
         L.jto_free.argtypes = [C.POINTER(_JtoResult)]
+        L.jto_minify.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(C.c_size_t),
+                                 C.POINTER(C.c_longlong)]
         L.jto_utf8_error_offset.argtypes = [C.c_char_p, C.c_size_t]
         L.jto_utf8_error_offset.restype = C.c_longlong
         L.jto_parse_number.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t,
@@ -89,6 +91,13 @@ class Oracle:
         L.jto_parse_string.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t,
                                        C.c_char_p, C.POINTER(C.c_uint32),
                                        C.POINTER(C.c_longlong)]
+
+    def minify(self, data: bytes):
+        """(error name, offset, minified bytes or None) as jt_minify"""
+        out = C.create_string_buffer(len(data) + 1)
+        n, off = C.c_size_t(), C.c_longlong()
+        code = self.lib.jto_minify(data, len(data), out, C.byref(n), C.byref(off))
+        return ERROR_NAMES[code], off.value, (out.raw[:n.value] if code == 0 else None)
 
     def parse(self, data: bytes) -> ParseResult:
         r = _JtoResult()
@@ -170,6 +179,16 @@ class Reference:
         off = C.c_longlong(-7)
         code = self.lib.jt_parse(self.p, data, len(data), None, C.byref(off))
         return code, off.value
+
+    def minify(self, data: bytes):
+        """the reference's jt_minify (capi.cpp:154-167)"""
+        L = self.lib
+        L.jt_minify.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, C.c_char_p,
+                                C.POINTER(C.c_size_t), C.POINTER(C.c_longlong)]
+        out = C.create_string_buffer(len(data) + 1)
+        n, off = C.c_size_t(), C.c_longlong(-7)
+        code = L.jt_minify(self.p, data, len(data), out, C.byref(n), C.byref(off))
+        return ERROR_NAMES[code], off.value, (out.raw[:n.value] if code == 0 else None)
 
     def stage1(self, data: bytes) -> ParseResult:
         off = C.c_longlong(-7)

@@ -194,6 +194,7 @@ struct jt_parser {
   jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
+  DevBuf minbuf;  // jt_minify: look-back records, counter, total, output
   std::vector<jt::RecordResult> h_records;
   // optional per-kernel timing: ev[0] before init, then one per launch
   bool prof = false;
@@ -864,15 +865,46 @@ char *jt_document_distinct(const jt_document *doc, const char *path) {
 
 void jt_string_free(char *s) { free(s); }
 
+// capi.cpp:154-167: full parse, then minify_pass (indexer.cpp:58-75) on the
+// GPU (k_minify) over the same resident input and its K0 carry-ins
 jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t *dst_len,
                    long long *error_offset) {
-  (void)p;
-  (void)data;
-  (void)len;
-  (void)dst;
-  (void)dst_len;
-  set_off(error_offset, -1);
-  return JT_CAPACITY;  // GPU minify is §8f "next"; not in round 1
+  if ((uint64_t)len >= (1ULL << 32)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  if (!upload(p, data, len)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  jt_error e = parse_resident(p, len, nullptr, error_offset);
+  if (e != JT_OK) return e;
+  const uint64_t ntiles = jt::stage1_records(len);
+  const size_t rec_bytes = round_up(ntiles * 8 + 16, 256);
+  if (!p->minbuf.ensure(rec_bytes + len + 256)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  jt::MinifyArgs a{};
+  a.in = p->in.as<uint8_t>();
+  a.len = len;
+  a.carry = s1_args(p, len, p->cur).carry;
+  a.rec = p->minbuf.as<uint64_t>();
+  a.tile_counter = (uint32_t *)(a.rec + ntiles);
+  a.total = a.rec + ntiles + 1;
+  a.out = p->minbuf.as<uint8_t>() + rec_bytes;
+  a.ntiles = ntiles;
+  uint64_t total = 0;
+  if (!cuda_ok(p, cudaMemsetAsync(p->minbuf.p, 0, (ntiles + 2) * 8, p->stream), "memset") ||
+      !cuda_ok(p, jt::minify_launch(a, p->stream), "minify") ||
+      !cuda_ok(p, cudaMemcpyAsync(&total, a.total, 8, cudaMemcpyDeviceToHost, p->stream), "D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync") ||
+      (total && !cuda_ok(p, cudaMemcpy(dst, a.out, total, cudaMemcpyDeviceToHost), "D2H"))) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  if (dst_len) *dst_len = total;
+  return JT_OK;
 }
 
 jt_error jt_compute_stats(jt_parser *p, const char *data, size_t len, jt_stats *out,

@@ -833,7 +833,121 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   if (threadIdx.x == 0) JT_TL(tile, 7);
 }
 
+// ---- jt_minify (capi.cpp:154-167, minify_pass indexer.cpp:58-75) -----------
+// After a successful parse: keep in-string bytes, unescaped quotes and every
+// non-whitespace byte.  One CTA per 16 KiB tile; the carry-in is K0b's from
+// the parse; kept bytes are staged in shared memory and written coalesced at
+// the tile's output offset (decoupled look-back over the kept counts).
+__global__ void __launch_bounds__(kThreads) k_minify(MinifyArgs a) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp_f[kWarps], s_warp_state[kWarps], s_warp_cnt[kWarps];
+  __shared__ unsigned long long s_base;
+  extern __shared__ __align__(16) uint8_t smem[];  // input tile | kept bytes
+  uint8_t *s_out = smem + kStage1Tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const uint64_t blk = (uint64_t)tile * kStage1Tile + (uint64_t)threadIdx.x * 64;
+  const uint32_t local = threadIdx.x * 64;
+  uint32_t w[16];
+  ld256(a.in + blk, w);
+  ld256(a.in + blk + 32, w + 8);
+  {
+    uint4 *d = (uint4 *)(smem + local);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    d[3] = make_uint4(w[12], w[13], w[14], w[15]);
+  }
+  s1::Masks m;
+  s1::classify64(w, m);
+  const uint64_t esc0 = s1::escaped_no_carry(m.bs), tog = s1::carry_toggle(m.bs);
+  uint32_t inc = s1::block_function(m, esc0, tog);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc = s1::compose(inc, o);
+  }
+  const uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 31) s_warp_f[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = a.carry[tile];
+    for (int k = 0; k < kWarps; k++) {
+      s_warp_state[k] = c;
+      c = s1::apply(s_warp_f[k], c);
+    }
+  }
+  __syncthreads();
+  uint32_t state = s_warp_state[warp];
+  if (lane > 0) state = s1::apply(excl, state);
+  const int64_t rem = (int64_t)a.len - (int64_t)blk;
+  const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
+  const uint64_t esc = (state & 1) ? (esc0 ^ tog) : esc0;
+  const uint64_t uq = m.qt & ~esc;
+  const uint64_t instr = s1::prefix_xor(uq) ^ ((state & 2) ? ~0ULL : 0ULL);
+  const uint64_t keep = (instr | uq | ~m.ws) & valid;
+  const uint32_t cnt = popc64(keep);
+  uint32_t ci = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, ci, d);
+    if (lane >= d) ci += o;
+  }
+  if (lane == 31) s_warp_cnt[warp] = ci;
+  __syncthreads();
+  uint32_t off = ci - cnt, total = 0;
+  for (int k = 0; k < kWarps; k++) {
+    off += k < warp ? s_warp_cnt[k] : 0;
+    total += s_warp_cnt[k];
+  }
+  // kept runs into the staging buffer
+  for (uint64_t cm = keep; cm;) {
+    const int a0 = ctz64(cm);
+    const uint64_t sh = cm >> a0;
+    const int n = ~sh == 0 ? 64 - a0 : ctz64(~sh);
+    smem_copy(smem, kStage1Tile + off + popc64(keep & sb::low_bits(a0)), local + a0, n);
+    cm &= ~(sb::low_bits(n) << a0);
+  }
+  if (warp == 0) {
+    unsigned long long base = 0;
+    if (tile > 0) {
+      if (lane == 0) lb_store(a.rec + tile, kFlagAgg | total);
+      base = lb_sum_exclusive(a.rec, tile);
+    }
+    if (lane == 0) {
+      lb_store(a.rec + tile, kFlagIncl | (base + total));
+      s_base = base;
+      if (tile == (int64_t)a.ntiles - 1) *a.total = base + total;
+    }
+  }
+  __syncthreads();
+  if (total) {
+    uint8_t *dst = a.out + s_base;
+    const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3) < total
+                              ? (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3)
+                              : total;
+    if (threadIdx.x < head) dst[threadIdx.x] = s_out[threadIdx.x];
+    const uint32_t nw = (total - head) / 4;
+    uint32_t *dw = (uint32_t *)(dst + head);
+    const uint32_t *sp = (const uint32_t *)s_out;
+    const uint32_t sh = head * 8;
+    for (uint32_t k = threadIdx.x; k < nw; k += kThreads) dw[k] = __funnelshift_r(sp[k], sp[k + 1], sh);
+    for (uint32_t k = head + 4 * nw + threadIdx.x; k < total; k += kThreads) dst[k] = s_out[k];
+  }
+}
+
 }  // namespace
+
+cudaError_t minify_launch(const MinifyArgs &args, cudaStream_t stream) {
+  constexpr int kSmemMin = 2 * kStage1Tile + 16;
+  static const cudaError_t configured =
+      cudaFuncSetAttribute(k_minify, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMin);
+  if (configured != cudaSuccess) return configured;
+  k_minify<<<(unsigned)args.ntiles, kThreads, kSmemMin, stream>>>(args);
+  return cudaGetLastError();
+}
 
 #ifdef JT_TIMELINE
 // copy (and clear) the K1 timeline; instrumented builds only

@@ -68,6 +68,20 @@ cudaError_t stage1_lengths_launch(const Stage1Args &args, uint64_t ntiles, cudaS
 cudaError_t stage1_records_count(const Stage1Args &args, cudaStream_t stream);
 cudaError_t stage1_records_main(const Stage1Args &args, cudaStream_t stream);
 
+// jt_minify after a successful parse of the same resident input (the
+// carry-ins are K0b's); rec and tile_counter zeroed, ntiles words / 1 word
+struct MinifyArgs {
+  const uint8_t *in;
+  uint64_t len;
+  const uint32_t *carry;
+  uint8_t *out;
+  uint64_t *rec;
+  uint32_t *tile_counter;
+  uint64_t *total;
+  uint64_t ntiles;
+};
+cudaError_t minify_launch(const MinifyArgs &args, cudaStream_t stream);
+
 struct Sum0;
 // sharded stage 1 (shard.h): phase 0 = K0a + the shard's composed carry
 // function; phase 1 = carry-in from all shards' functions, K0b, K1

@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_extent.argtypes = [vp, C.POINTER(C.c_ulonglong)]
     L.jt_b200_shard_download.argtypes = [vp, vp, vp]
     L.jt_b200_copy_in_range.argtypes = [vp, vp, sz, sz]
+    L.jt_minify.argtypes = [vp, C.c_char_p, sz, C.c_char_p, C.POINTER(sz), C.POINTER(ll)]
     L.jt_b200_parse_records.argtypes = [vp, sz, C.POINTER(sz)]
     L.jt_b200_records.argtypes = [vp]
     L.jt_b200_records.restype = vp
@@ -257,6 +258,13 @@ class Parser:
         n = C.c_size_t()
         p = self._lib.jt_b200_device_index(self._h, C.byref(n))
         return p, n.value
+
+    def minify(self, data: bytes):
+        """jt_minify: (error name, offset, minified bytes or None)"""
+        out = C.create_string_buffer(len(data) + 1)
+        n, off = C.c_size_t(), C.c_longlong(-7)
+        code = self._lib.jt_minify(self._h, data, len(data), out, C.byref(n), C.byref(off))
+        return ERROR_NAMES[code], off.value, (out.raw[:n.value] if code == 0 else None)
 
     def parse_records(self, n: int, download: bool = True):
         """Parse the n resident bytes as NDJSON records (jt_b200_parse_records).

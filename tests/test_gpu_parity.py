@@ -173,3 +173,18 @@ def test_streamed_jt_parse(parser, oracle):
     docs.append((s, "string across pieces"))
     for data, where in docs:
         check_same(parser, oracle, data, where)
+
+
+def test_minify(parser, oracle):
+    """jt_minify on the GPU (k_minify) vs the oracle (pinned to the
+    reference's jt_minify in test_oracle_vs_ref.py)"""
+    from tools.gen import generate
+    rng = random.Random(43)
+    docs = [b' { "a" : [ 1 , 2 ] } ', b'{"a b": "c \\" d"}', b"[]", b"", b'["a \t b"]', b"[1,]",
+            generate(1, 4 << 20), generate(4, 2 << 20), generate(0, 1 << 20), generate(2, 1 << 20),
+            generate(1, 9 << 20, seed=8)]
+    for _ in range(300):
+        d = _rand_json(rng).encode()
+        docs += [d, _mutate(rng, d)]
+    for d in docs:
+        assert parser.minify(d) == oracle.minify(d), d[:120]

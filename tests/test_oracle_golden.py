@@ -116,3 +116,11 @@ def test_golden_fixtures(oracle):
         if r.code == 0:
             assert hashlib.sha256(r.tape).hexdigest() == row["tape_sha"]
             assert hashlib.sha256(r.strings).hexdigest() == row["strings_sha"]
+
+
+def test_minify_kat(oracle):
+    """test_capi.cpp:107-118 and test_indexer.cpp:134-141"""
+    assert oracle.minify(b' { "a" : [ 1 , 2 ] } ') == ("OK", -1, b'{"a":[1,2]}')
+    assert oracle.minify(b' [ "a b" , "c\\" d" ] ') == ("OK", -1, b'["a b","c\\" d"]')
+    name, off, out = oracle.minify(b"[1,]")
+    assert name == "TAPE_ERROR" and off == 3 and out is None

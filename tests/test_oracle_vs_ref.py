@@ -59,3 +59,17 @@ def test_configs(oracle, ref):
         _same(oracle, ref, rec)
     for seed in range(1, 100):
         _same(oracle, ref, generate(4, 1 << 13, seed=seed, err=1 + seed % 5))
+
+
+def test_minify(oracle, ref):
+    """jt_minify (capi.cpp:154-167, minify_pass indexer.cpp:58-75): the
+    oracle's restatement against the reference on valid and invalid input"""
+    from tools.gen import generate
+    rng = random.Random(41)
+    docs = [b' { "a" : [ 1 , "x y\\" z" ] } ', b"[1,]", b'{"k": "\\\\", "v": [true, null]}\n', b"",
+            generate(1, 1 << 18), generate(4, 1 << 17), generate(0, 1 << 16)]
+    for _ in range(1500):
+        d = _rand_json(rng).encode()
+        docs += [d, _mutate(rng, d)]
+    for d in docs:
+        assert oracle.minify(d) == ref.minify(d), d[:120]
