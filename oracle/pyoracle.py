@@ -99,6 +99,28 @@ class Oracle:
         code = self.lib.jto_minify(data, len(data), out, C.byref(n), C.byref(off))
         return ERROR_NAMES[code], off.value, (out.raw[:n.value] if code == 0 else None)
 
+    def stats(self, data: bytes):
+        """jt_compute_stats restated over the oracle's tape (stats.cpp:5-47)"""
+        r = self.parse(data)
+        if r.code != 0:
+            return ERROR_NAMES[r.code], r.offset, None
+        import numpy as np
+        t = r.tape_array()
+        s = dict(integers=0, floats=0, strings=0, non_ascii_bytes=sum(b >= 0x80 for b in data),
+                 objects=0, arrays=0, nulls=0, trues=0, falses=0)
+        tags = {ord("l"): "integers", ord("d"): "floats", ord('"'): "strings", ord("{"): "objects",
+                ord("["): "arrays", ord("n"): "nulls", ord("t"): "trues", ord("f"): "falses"}
+        i = 0
+        while i < len(t):
+            tag = int(t[i]) >> 56
+            if tag in tags:
+                s[tags[tag]] += 1
+            i += 2 if tag in (ord("l"), ord("d")) else 1
+        s["structurals"] = len(r.index_list())
+        s["bytes"] = len(data)
+        s["bytes_per_structural"] = len(data) / s["structurals"] if s["structurals"] else 0.0
+        return "OK", -1, s
+
     def parse(self, data: bytes) -> ParseResult:
         r = _JtoResult()
         self.lib.jto_parse(data, len(data), C.byref(r))
@@ -179,6 +201,17 @@ class Reference:
         off = C.c_longlong(-7)
         code = self.lib.jt_parse(self.p, data, len(data), None, C.byref(off))
         return code, off.value
+
+    def stats(self, data: bytes):
+        """the reference's jt_compute_stats (capi.cpp:169-191)"""
+        from paper_1902_08318_b200.jsontape import JtStats
+        L = self.lib
+        L.jt_compute_stats.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, C.c_void_p,
+                                       C.POINTER(C.c_longlong)]
+        st = JtStats()
+        off = C.c_longlong(-7)
+        code = L.jt_compute_stats(self.p, data, len(data), C.addressof(st), C.byref(off))
+        return ERROR_NAMES[code], off.value, (st.as_dict() if code == 0 else None)
 
     def minify(self, data: bytes):
         """the reference's jt_minify (capi.cpp:154-167)"""

@@ -56,6 +56,12 @@ def build(verbose: bool = False, force: bool = False, defines: tuple = (), lib: 
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
         os.replace(tmp, lib)
+    # every symbol the library references must resolve (a kernel launcher
+    # left in an anonymous namespace links fine but fails at dlopen)
+    r = subprocess.run(["nm", "-C", "--undefined-only", lib], capture_output=True, text=True)
+    bad = [l for l in r.stdout.splitlines() if " jt::" in l]
+    if bad:
+        raise RuntimeError("unresolved symbols in " + lib + ":\n" + "\n".join(bad))
     return lib
 
 

@@ -907,31 +907,47 @@ jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t
   return JT_OK;
 }
 
+// capi.cpp:169-191 / stats.cpp:5-47: parse, then the counts as device
+// reductions over the token records, tape tags and input (k_stats)
 jt_error jt_compute_stats(jt_parser *p, const char *data, size_t len, jt_stats *out,
                           long long *error_offset) {
-  jt_document *doc = nullptr;
-  jt_error e = jt_parse(p, data, len, &doc, error_offset);
-  if (e != JT_OK) return e;
-  jt_stats s{};
-  const auto &t = doc->tape;
-  for (size_t i = 1; i + 1 < t.size(); i++) {
-    switch ((uint8_t)(t[i] >> 56)) {
-      case 'l': s.integers++; i++; break;
-      case 'd': s.floats++; i++; break;
-      case '"': s.strings++; break;
-      case '{': s.objects++; break;
-      case '[': s.arrays++; break;
-      case 'n': s.nulls++; break;
-      case 't': s.trues++; break;
-      case 'f': s.falses++; break;
-    }
+  if ((uint64_t)len >= (1ULL << 32)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
   }
-  for (size_t i = 0; i < len; i++) s.non_ascii_bytes += ((uint8_t)data[i]) >= 0x80;
+  if (!upload(p, data, len)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  jt_error e = parse_resident(p, len, nullptr, error_offset);
+  if (e != JT_OK) return e;
+  if (!p->minbuf.ensure(256)) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  unsigned long long *cnt = p->minbuf.as<unsigned long long>();
+  unsigned long long h[9] = {0};
+  if (!cuda_ok(p, cudaMemsetAsync(cnt, 0, sizeof(h), p->stream), "memset") ||
+      !cuda_ok(p, jt::stats_launch(s2_args(p, len, p->cur), cnt, p->stream), "stats") ||
+      !cuda_ok(p, cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, p->stream), "D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
+    set_off(error_offset, -1);
+    return JT_CAPACITY;
+  }
+  jt_stats s{};
+  s.integers = h[0];
+  s.floats = h[1];
+  s.strings = h[2];
+  s.non_ascii_bytes = h[3];
+  s.objects = h[4];
+  s.arrays = h[5];
+  s.nulls = h[6];
+  s.trues = h[7];
+  s.falses = h[8];
   s.structurals = p->index_count;
   s.bytes = len;
   s.bytes_per_structural = s.structurals ? (double)len / (double)s.structurals : 0.0;
-  jt_document_free(doc);
-  *out = s;
+  if (out) *out = s;
   return JT_OK;
 }
 

@@ -1046,6 +1046,41 @@ __global__ void k_init(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *
   }
 }
 
+// ---- jt_compute_stats (stats.cpp:5-47, capi.cpp:169-191) --------------------
+// After a successful parse: node counts from the token records (a number's
+// int/float from its tape tag) and the input's non-ASCII bytes, as warp-
+// aggregated atomics.  cnt: integers, floats, strings, non_ascii, objects,
+// arrays, nulls, trues, falses (jt_stats order).
+__global__ void __launch_bounds__(256) k_stats(Stage2Args a, unsigned long long *cnt) {
+  const uint64_t S = a.ctrl->S;
+  const int lane = threadIdx.x & 31;
+  unsigned long long loc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S; i += stride) {
+    const uint32_t c = a.tok[i] & 0xFF;
+    switch (c) {
+      case '"': loc[2]++; break;
+      case '{': loc[4]++; break;
+      case '[': loc[5]++; break;
+      case 'n': loc[6]++; break;
+      case 't': loc[7]++; break;
+      case 'f': loc[8]++; break;
+      default:
+        if (c == '-' || (c - '0') < 10u) loc[(a.tape[a.tape_idx[i]] >> 56) == 'l' ? 0 : 1]++;
+    }
+  }
+  const uint64_t words = (a.len + 3) / 4;  // the zero tail counts nothing
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < words; k += stride)
+    loc[3] += __popc(((const uint32_t *)a.in)[k] & 0x80808080u);
+#pragma unroll
+  for (int q = 0; q < 9; q++) {
+    unsigned long long v = loc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(cnt + q, v);
+  }
+}
+
 // ---- NDJSON records ---------------------------------------------------------
 
 __device__ __forceinline__ uint64_t n_records(const Stage2Args &a) {
@@ -1377,6 +1412,12 @@ static void launch_struct(const Stage2Args &a, cudaStream_t stream) {
   if (a.records) k_struct<2><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
   else if (a.sh) k_struct<1><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
   else k_struct<0><<<g3 < 1 ? 1 : g3, 256, 0, stream>>>(a);
+}
+
+cudaError_t stats_launch(const Stage2Args &a, unsigned long long *cnt, cudaStream_t stream) {
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  k_stats<<<sms * 4, 256, 0, stream>>>(a, cnt);
+  return cudaGetLastError();
 }
 
 cudaError_t records_init_launch(const Stage2Args &a, cudaStream_t stream) {

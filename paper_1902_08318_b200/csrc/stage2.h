@@ -117,6 +117,11 @@ cudaError_t shard_phase3_launch(const Stage2Args &a, const Sum2 *gathered, cudaS
 // global first error and the bracket patches that land in this shard
 cudaError_t shard_finish_launch(const Stage2Args &a, const Sum3 *gathered, cudaStream_t stream);
 
+// jt_compute_stats after a successful parse: 9 counters in jt_stats order
+// (integers, floats, strings, non_ascii_bytes, objects, arrays, nulls, trues,
+// falses), zeroed by the caller
+cudaError_t stats_launch(const Stage2Args &a, unsigned long long *cnt, cudaStream_t stream);
+
 // Reset kernel for the control block + look-back records.
 cudaError_t init_launch(Ctrl *ctrl, uint64_t *s1rec, uint64_t s1words, uint64_t *s2rec,
                         uint64_t s2words, cudaStream_t stream);

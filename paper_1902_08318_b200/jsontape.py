@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_download.argtypes = [vp, vp, vp]
     L.jt_b200_copy_in_range.argtypes = [vp, vp, sz, sz]
     L.jt_minify.argtypes = [vp, C.c_char_p, sz, C.c_char_p, C.POINTER(sz), C.POINTER(ll)]
+    L.jt_compute_stats.argtypes = [vp, C.c_char_p, sz, vp, C.POINTER(ll)]
     L.jt_b200_parse_records.argtypes = [vp, sz, C.POINTER(sz)]
     L.jt_b200_records.argtypes = [vp]
     L.jt_b200_records.restype = vp
@@ -108,6 +109,16 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_records_download.argtypes = [vp, vp, vp]
     _lib = L
     return L
+
+
+class JtStats(C.Structure):
+    """jt_stats (jsontape.h:71-84)"""
+    _fields_ = [(n, C.c_uint64) for n in ("integers", "floats", "strings", "non_ascii_bytes", "objects",
+                                           "arrays", "nulls", "trues", "falses", "structurals", "bytes")] + \
+               [("bytes_per_structural", C.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
 
 
 def error_name(code: int) -> str:
@@ -265,6 +276,13 @@ class Parser:
         n, off = C.c_size_t(), C.c_longlong(-7)
         code = self._lib.jt_minify(self._h, data, len(data), out, C.byref(n), C.byref(off))
         return ERROR_NAMES[code], off.value, (out.raw[:n.value] if code == 0 else None)
+
+    def stats(self, data: bytes):
+        """jt_compute_stats: (error name, offset, dict or None)"""
+        st = JtStats()
+        off = C.c_longlong(-7)
+        code = self._lib.jt_compute_stats(self._h, data, len(data), C.addressof(st), C.byref(off))
+        return ERROR_NAMES[code], off.value, (st.as_dict() if code == 0 else None)
 
     def parse_records(self, n: int, download: bool = True):
         """Parse the n resident bytes as NDJSON records (jt_b200_parse_records).

@@ -188,3 +188,16 @@ def test_minify(parser, oracle):
         docs += [d, _mutate(rng, d)]
     for d in docs:
         assert parser.minify(d) == oracle.minify(d), d[:120]
+
+
+def test_stats(parser, oracle):
+    """jt_compute_stats on the GPU (k_stats) vs the oracle's restatement
+    (pinned to the reference in test_oracle_vs_ref.py)"""
+    from tools.gen import generate
+    rng = random.Random(53)
+    docs = [generate(c, 1 << 20) for c in (0, 1, 2, 4)] + [b"[1,]", b"", b'["\xc3\xa9", -0, 1e5]']
+    for _ in range(200):
+        d = _rand_json(rng).encode()
+        docs += [d, _mutate(rng, d)]
+    for d in docs:
+        assert parser.stats(d) == oracle.stats(d), d[:120]

@@ -73,3 +73,16 @@ def test_minify(oracle, ref):
         docs += [d, _mutate(rng, d)]
     for d in docs:
         assert oracle.minify(d) == ref.minify(d), d[:120]
+
+
+def test_stats(oracle, ref):
+    """jt_compute_stats restatement (oracle) against the reference"""
+    from tools.gen import generate
+    rng = random.Random(47)
+    docs = [generate(0, 1 << 16), generate(1, 1 << 17), b"[1, 2.5, \"x\", {}, [], null, true, false]",
+            b"[1,]", b""]
+    for _ in range(300):
+        d = _rand_json(rng).encode()
+        docs += [d, _mutate(rng, d)]
+    for d in docs:
+        assert oracle.stats(d) == ref.stats(d), d[:120]
