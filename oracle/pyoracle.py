@@ -232,6 +232,23 @@ class Reference:
             out.index = C.string_at(self.lib.jt_index_positions(self.p), 4 * n) if n else b""
         return out
 
+    def distinct(self, data: bytes, paths):
+        """the reference's jt_document_distinct for each path (None if the parse fails)"""
+        L = self.lib
+        L.jt_document_distinct.argtypes = [C.c_void_p, C.c_char_p]
+        L.jt_document_distinct.restype = C.c_void_p
+        doc = C.c_void_p()
+        off = C.c_longlong(-7)
+        if self.lib.jt_parse(self.p, data, len(data), C.byref(doc), C.byref(off)) != 0:
+            return None
+        out = []
+        for path in paths:
+            sp = L.jt_document_distinct(doc, path)
+            out.append(C.string_at(sp))
+            L.jt_string_free(sp)
+        L.jt_document_free(doc)
+        return out
+
     def parse(self, data: bytes) -> ParseResult:
         """Full parse; tape words and strings recovered from the reference's
         own document dump is lossy, so the tape is read through the

@@ -17,8 +17,10 @@
 
 #include <algorithm>
 #include <charconv>
+#include <functional>
 #include <map>
 #include <mutex>
+#include <set>
 #include <new>
 #include <string>
 #include <vector>
@@ -857,10 +859,109 @@ char *jt_document_dump(const jt_document *doc) {
   return s;
 }
 
+// Sorted distinct scalars at a dotted key path (capi.cpp:143-151,
+// document.cpp:134-192): the first key matches at any depth, later keys must
+// follow directly, arrays are looked through.  Host-side walk of the
+// document's tape (a non-hot export).
 char *jt_document_distinct(const jt_document *doc, const char *path) {
-  (void)doc;
-  (void)path;
-  return nullptr;  // navigation/query is out of the hot-path scope
+  std::string out;
+  if (doc && path && *path && doc->tape.size() > 2) {
+    std::vector<std::string> keys;
+    for (const char *a = path;;) {
+      const char *dot = strchr(a, '.');
+      keys.emplace_back(a, dot ? (size_t)(dot - a) : strlen(a));
+      if (!dot) break;
+      a = dot + 1;
+    }
+    const uint64_t *t = doc->tape.data();
+    const uint8_t *sb = doc->strings.data();
+    auto tag = [&](uint64_t i) { return (uint8_t)(t[i] >> 56); };
+    auto pay = [&](uint64_t i) { return t[i] & ((1ULL << 56) - 1); };
+    auto next = [&](uint64_t i) -> uint64_t {  // index after the value at i
+      const uint8_t g = tag(i);
+      return (g == '{' || g == '[') ? pay(i) : (g == 'l' || g == 'd') ? i + 2 : i + 1;
+    };
+    auto str = [&](uint64_t i) {
+      uint32_t n;
+      memcpy(&n, sb + pay(i), 4);
+      return std::string((const char *)sb + pay(i) + 4, n);
+    };
+    // (kind, bits, bytes) ordered as scalar_value (document.h:71-90)
+    struct Val {
+      int k;
+      uint64_t bits;
+      std::string bytes;
+      bool operator<(const Val &o) const {
+        if (k != o.k) return k < o.k;
+        return k == 5 ? bytes < o.bytes : bits < o.bits;
+      }
+    };
+    std::set<Val> vals;
+    auto scalar = [&](uint64_t i) {
+      const uint8_t g = tag(i);
+      if (g == 'n') vals.insert({0, 0, {}});
+      else if (g == 'f') vals.insert({1, 0, {}});
+      else if (g == 't') vals.insert({2, 0, {}});
+      else if (g == 'l') vals.insert({3, t[i + 1], {}});
+      else if (g == 'd') vals.insert({4, t[i + 1], {}});
+      else if (g == '"') vals.insert({5, 0, str(i)});
+    };
+    // children of the container at i: (key index or 0, value index)
+    auto each = [&](uint64_t i, auto &&fn) {
+      const bool obj = tag(i) == '{';
+      for (uint64_t c = i + 1, stop = pay(i) - 1; c < stop;) {
+        const uint64_t v = obj ? c + 1 : c;
+        fn(obj ? c : 0, v);
+        c = next(v);
+      }
+    };
+    std::function<void(uint64_t, size_t)> follow = [&](uint64_t i, size_t k) {
+      const uint8_t g = tag(i);
+      if (k == keys.size()) {
+        if (g != '{' && g != '[') scalar(i);
+        return;
+      }
+      if (g == '{')
+        each(i, [&](uint64_t key, uint64_t v) {
+          if (str(key) == keys[k]) follow(v, k + 1);
+        });
+      else if (g == '[')
+        each(i, [&](uint64_t, uint64_t v) { follow(v, k); });
+    };
+    std::function<void(uint64_t)> search = [&](uint64_t i) {
+      const uint8_t g = tag(i);
+      if (g == '{')
+        each(i, [&](uint64_t key, uint64_t v) {
+          if (str(key) == keys[0]) follow(v, 1);
+          search(v);
+        });
+      else if (g == '[')
+        each(i, [&](uint64_t, uint64_t v) { search(v); });
+    };
+    search(1);  // document_root (document.cpp:99)
+    char buf[64];
+    for (const Val &v : vals) {
+      switch (v.k) {
+        case 0: out += "null"; break;
+        case 1: out += "false"; break;
+        case 2: out += "true"; break;
+        case 3: out.append(buf, std::to_chars(buf, buf + sizeof(buf), (int64_t)v.bits).ptr); break;
+        case 4: {
+          double d;
+          memcpy(&d, &v.bits, 8);
+          out.append(buf, std::to_chars(buf, buf + sizeof(buf), d).ptr);
+          break;
+        }
+        default: out += '"' + v.bytes + '"';
+      }
+      out += '\n';
+    }
+  }
+  char *r = (char *)malloc(out.size() + 1);
+  if (!r) return nullptr;
+  memcpy(r, out.data(), out.size());
+  r[out.size()] = 0;
+  return r;
 }
 
 void jt_string_free(char *s) { free(s); }

@@ -151,6 +151,16 @@ class Document:
         sp, sn = self._raw()[2:4]
         return C.string_at(sp, sn) if sn else b""
 
+    def distinct(self, path: bytes) -> bytes:
+        """jt_document_distinct: sorted distinct scalars at a dotted key path"""
+        L = self._lib
+        L.jt_document_distinct.argtypes = [C.c_void_p, C.c_char_p]
+        L.jt_document_distinct.restype = C.c_void_p
+        sp = L.jt_document_distinct(self._h, path)
+        out = C.string_at(sp)
+        L.jt_string_free(sp)
+        return out
+
     def dump(self) -> str:
         s = self._lib.jt_document_dump(self._h)
         out = C.string_at(s).decode("utf-8", "replace")

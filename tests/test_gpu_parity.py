@@ -201,3 +201,28 @@ def test_stats(parser, oracle):
         docs += [d, _mutate(rng, d)]
     for d in docs:
         assert parser.stats(d) == oracle.stats(d), d[:120]
+
+
+def test_document_distinct(parser):
+    """jt_document_distinct on GPU-parsed documents vs the reference's own
+    (oracle/_ref) on the same input"""
+    import os
+    from oracle.pyoracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    from tools.gen import generate
+    ref = Reference()
+    docs = [generate(0, 1 << 18), generate(1, 1 << 18), generate(3, 1 << 16).split(b"\n")[0],
+            b'{"a": {"b": [1, 2, 2, -3, 1.5, "x", null, true, {"b": 7}]}, "b": {"a": {"b": false}}}',
+            b'[{"k": 1}, {"k": "1"}, {"k": [1.0, 1e300, -0.0, 0]}, {"k": {"k": 9}}]', b"5"]
+    rng = random.Random(59)
+    for _ in range(150):
+        docs.append(_rand_json(rng).encode())
+    paths = [b"", b"a", b"b", b"a.b", b"k", b"k.k", b"x.y.z", b"id", b"name", b"b.a.b", b"k0", b"k1.k2", b"k0.k0.k0", b"k3"]
+    for d in docs:
+        want = ref.distinct(d, paths)
+        if want is None:
+            continue
+        r = parser.parse(d)
+        got = [r.document.distinct(p) for p in paths]
+        assert got == want, d[:200]
