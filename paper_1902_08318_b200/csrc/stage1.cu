@@ -682,7 +682,43 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     // plain runs (escape positions get placeholder bytes, rewritten below;
     // the first vin bits belong to the previous block's escape)
     uint64_t cm = W & ~sb::low_bits(vin);
-    // warp-uniform choice by the slowest lane's estimated cost (a warp runs
+    if (!pay_direct) {
+      // warp-cooperative copy into the staging buffer: 16 steps, each lane one
+      // 4-byte word of the warp's 2 KiB; the owning block's masks come by
+      // shuffle and the destination is the popcount formula (an opening
+      // quote's 4 bytes are skipped, filled by the copy-out)
+      const uint32_t *s_in32 = (const uint32_t *)s_in;
+      const uint32_t wbase = (uint32_t)warp * 32;  // first block (thread) of the warp
+      // block pairs with string bytes (warp-uniform; none at all on numeric text)
+      const uint32_t live = __ballot_sync(0xffffffffu, cm != 0);
+      uint32_t pairs = 0;
+#pragma unroll
+      for (int j = 0; j < 16; j++) pairs |= ((live >> (2 * j)) & 3u) ? (1u << j) : 0u;
+      while (pairs) {
+        const int j = __ffs(pairs) - 1;
+        pairs &= pairs - 1;
+        const int owner = 2 * j + (lane >> 4);
+        const uint64_t Ro = __shfl_sync(0xffffffffu, cm, owner);
+        const uint64_t Wo = __shfl_sync(0xffffffffu, W, owner);
+        const uint64_t Oo = __shfl_sync(0xffffffffu, openq, owner);
+        const uint32_t so = __shfl_sync(0xffffffffu, soff, owner);
+        const int o = (lane & 15) * 4;
+        const uint32_t k4 = (uint32_t)(Ro >> o) & 0xF;
+        if (k4) {
+          const uint64_t below = sb::low_bits(o);
+          uint32_t d = so + 4u * popc64(Oo & below) + popc64(Wo & below);
+          const uint32_t word = s_in32[(wbase + owner) * 16 + (lane & 15)];
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            if ((k4 >> k) & 1) s_pay[d] = (uint8_t)(word >> (8 * k));
+            d += (uint32_t)((Wo >> (o + k)) & 1) + 4u * (uint32_t)((Oo >> (o + k)) & 1);
+          }
+        }
+      }
+      __syncwarp();  // before the escape fix-ups overwrite placeholder bytes
+      cm = 0;
+    }
+    // direct (spilled) tiles: warp-uniform choice by the slowest lane's estimated cost (a warp runs
     // the union of its lanes' paths): ~6 instructions per byte for the byte
     // loop, ~35 per run plus a word copy per 4 bytes for the run loop
     const int nruns = popc64(cm & ~(cm << 1));
