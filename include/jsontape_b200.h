@@ -72,7 +72,8 @@ typedef struct {
   uint64_t string_bytes;
 } jt_b200_record;
 int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records);
-const void *jt_b200_records(const jt_parser *p); /* host jt_b200_record[n_records] */
+const void *jt_b200_records(jt_parser *p);        /* host jt_b200_record[n_records], copied on first use */
+const void *jt_b200_device_records(const jt_parser *p); /* the same on the device */
 void jt_b200_records_size(const jt_parser *p, unsigned long long *out);
 int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
 

@@ -198,6 +198,10 @@ struct jt_parser {
   DevBuf recs, nlbuf;
   DevBuf minbuf;  // jt_minify: look-back records, counter, total, output
   std::vector<jt::RecordResult> h_records;
+  bool h_records_valid = false;
+  const jt::RecordResult *rec_results = nullptr;
+  uint64_t rec_n = 0;
+  uint8_t rec_last_byte = 0;
   // optional per-kernel timing: ev[0] before init, then one per launch
   bool prof = false;
   cudaEvent_t ev[8] = {};
@@ -1208,6 +1212,9 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
       !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
                                   p->stream),
                "ctrl D2H") ||
+      (len && !cuda_ok(p, cudaMemcpyAsync(&p->rec_last_byte, p->in.as<uint8_t>() + len - 1, 1,
+                                          cudaMemcpyDeviceToHost, p->stream),
+                       "last byte")) ||
       !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
     return -1;
   const uint64_t nl = p->h_ctrl->n_newlines, nr = nl + 2;
@@ -1260,19 +1267,12 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
       !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
     return -1;
   p->launches = 1 + 2 + 2 + 1 + n2;
-  uint8_t last = 0;
-  if (len) cudaMemcpy(&last, p->in.as<uint8_t>() + len - 1, 1, cudaMemcpyDeviceToHost);
-  const uint64_t n = nl + ((len > 0 && last != '\n') ? 1 : 0);
-  try {
-    p->h_records.resize(n);
-  } catch (...) {
-    p->err = "parse_records: host results";
-    return -1;
-  }
-  if (n && !cuda_ok(p, cudaMemcpy(p->h_records.data(), res, n * sizeof(jt::RecordResult),
-                                  cudaMemcpyDeviceToHost),
-                    "results D2H"))
-    return -1;
+  // the input's last byte decides whether a record follows the last '\n'
+  // (read from the pinned control copy: no extra sync)
+  const uint64_t n = nl + ((len > 0 && p->rec_last_byte != '\n') ? 1 : 0);
+  p->rec_results = res;
+  p->rec_n = n;
+  p->h_records_valid = false;  // results stay on the device until asked for
   // the device tape / string buffer hold all records back to back
   p->last_tape_len = n ? p->h_ctrl->tape_words + 2 * (n - 1) + 1 : 0;
   p->last_string_bytes = p->h_ctrl->string_bytes;
@@ -1280,7 +1280,26 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   return 0;
 }
 
-const void *jt_b200_records(const jt_parser *p) { return p->h_records.data(); }
+// host copy of the last jt_b200_parse_records results (made on first use)
+const void *jt_b200_records(jt_parser *p) {
+  if (!p->h_records_valid) {
+    try {
+      p->h_records.resize(p->rec_n);
+    } catch (...) {
+      return nullptr;
+    }
+    if (p->rec_n && cudaMemcpy(p->h_records.data(), p->rec_results, p->rec_n * sizeof(jt::RecordResult),
+                               cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    p->h_records_valid = true;
+  }
+  return p->h_records.data();
+}
+
+// device pointer to the last jt_b200_parse_records results (jt_b200_record[n])
+const void *jt_b200_device_records(const jt_parser *p) { return p->rec_results; }
 
 // Copy all records' tape words and string bytes (jt_b200_record ranges) to host.
 int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {

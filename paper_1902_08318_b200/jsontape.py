@@ -38,7 +38,7 @@ EXPORTS = [
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
     "jt_b200_shard_download", "jt_b200_copy_in_range", "jt_b200_parse_records",
-    "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download",
+    "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download", "jt_b200_device_records",
 ]
 KERNELS = ["init", "stage1", "tokens", "slow", "tree", "struct", "final"]
 
