@@ -1221,7 +1221,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   const size_t cap_tok = (size_t)len + 16;
   // carve: start (nr+1), kend, tend, send, utf8, serr, end_err (nr each), rec_of (cap_tok),
   // err (nr u64), results (nr)
-  const size_t u32s = (nr + 1) + 6 * nr + cap_tok + 64;
+  const size_t u32s = (nr + 1) + 6 * nr + cap_tok + 64 + 4;
   const size_t bytes = round_up(u32s * 4, 256) + nr * 8 + nr * sizeof(jt::RecordResult) + 512;
   if (!p->recs.ensure(bytes)) {
     p->err = "parse_records: record arrays";
@@ -1242,6 +1242,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   q += nr;
   uint32_t *end_err = q;
   q += nr;
+  q = (uint32_t *)(((uintptr_t)q + 15) & ~(uintptr_t)15);  // rec_of is read as uint4 (k_struct)
   a1.rec_of = q;
   unsigned long long *err = (unsigned long long *)(p->recs.as<uint8_t>() + round_up(u32s * 4, 256));
   jt::RecordResult *res = (jt::RecordResult *)(err + nr);

@@ -798,8 +798,22 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     // record-relative) and how many of the previous tokens belong to it
     uint32_t rcur = 0, rtb = 0;
     int64_t rbefore = (int64_t)i0 + before;
+    // record mode: the chunk's record ids (and the next chunk's first) up front
+    uint32_t rids[kK3Tok + 1];
     if (kRecs) {
-      rcur = a.rec_of[i0];
+      if (i0 + kK3Tok <= S) {
+        const uint4 *rp = (const uint4 *)(a.rec_of + i0);
+#pragma unroll
+        for (int q = 0; q < kK3Tok / 4; q++) {
+          const uint4 r = rp[q];
+          rids[4 * q] = r.x, rids[4 * q + 1] = r.y, rids[4 * q + 2] = r.z, rids[4 * q + 3] = r.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kK3Tok; k++) rids[k] = i0 + k < S ? a.rec_of[i0 + k] : ~0u;
+      }
+      rids[kK3Tok] = i0 + kK3Tok < S ? a.rec_of[i0 + kK3Tok] : ~0u;
+      rcur = rids[0];
       rtb = rcur ? a.rec_tend[rcur - 1] + 1 : 0u;
       rbefore = (i0 >= 1 && a.rec_of[i0 - 1] == rcur) ? ((i0 >= 2 && a.rec_of[i0 - 2] == rcur) ? 2 : 1) : 0;
     }
@@ -840,7 +854,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     for (int k = 0; k < kK3Tok; k++) {
       if (i >= i1) break;
       if (kRecs) {
-        const uint32_t r = a.rec_of[i];
+        const uint32_t r = rids[k];
         if (r != rcur) {  // a new record: a new root value
           rcur = r;
           rtb = a.rec_tend[r - 1] + 1;
@@ -973,7 +987,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
         t += tok_width(c);
         i++;
         // the record's last token: it must close the root value
-        if ((i >= S || a.rec_of[i] != rcur) && !(mode == M_A && depth_after == 0))
+        if ((i >= S || rids[k + 1] != rcur) && !(mode == M_A && depth_after == 0))
           a.rec_end_err[rcur] = kTapeError;
         continue;
       }
