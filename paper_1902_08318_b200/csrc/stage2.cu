@@ -226,6 +226,11 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
       if (lane == 0 && dmax > 0) atomicMax(&ctrl->max_depth, dmax + (int)vw.depth_base);
+      // a shard starts inside depth_base open containers: the 64-kind
+      // register is exact only if that depth fits too (closers at the shard
+      // start pop below the carried-in kinds)
+      if (tile == blockIdx.x && threadIdx.x == 0 && blockIdx.x == 0 && vw.depth_base > 0)
+        atomicMax(&ctrl->max_depth, (int)min(vw.depth_base, (int64_t)1 << 20));
       __syncthreads();
       if (threadIdx.x == 0) {
         StackT agg = s_wt[0];

@@ -99,3 +99,22 @@ def test_shards_cut_positions(oracle):
         head = b'{"a": [' + b"7," * ((TILE - 12 - shift) // 2)
         doc = head + b'"x\\ud83d\\ude00y", {"b": [true, false, null, -1.5e3]}, "\\\\"]}'
         check_sharded(oracle, doc + b" " * 10, 2, f"cut shift {shift}")
+
+
+def test_shards_deep_then_shallow(oracle):
+    """A shard that starts hundreds of levels deep, closes them, then holds
+    shallow objects: its own openers are shallow but the carried-in stack is
+    not (max depth must include the shard's starting depth)."""
+    import os
+    deep = '{"a":' * 150 + "[" * 150
+    body = "1" + "]" * 150 + "}" * 149
+    tail = ', "k": {"x": 1, "y": [1, 2, {"z": "w"}], "v": {"p": true}}' * 600 + "}"
+    doc = (deep + "0," * ((TILE - len(deep)) // 2 + 40) + body + tail).encode()
+    for G in (2, 3):
+        check_sharded(oracle, doc, G, "deep then shallow")
+    here = os.path.join(os.path.dirname(__file__), "golden", "fuzz")
+    for name in sorted(os.listdir(here)):  # fuzz finds (tools/fuzz_gpu.py)
+        data = open(os.path.join(here, name), "rb").read()
+        for G in (2, 3, 5):
+            if G <= (len(data) + TILE - 1) // TILE:
+                check_sharded(oracle, data, G, name)
