@@ -318,7 +318,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_warp_nl[kWarps];
   __shared__ uint32_t s_warp_tdf[kWarps];
   __shared__ uint32_t s_warp_f[kWarps];
-  __shared__ uint32_t s_warp_state[kWarps];
   __shared__ uint32_t s_warp_cnt[kWarps];
   __shared__ uint32_t s_warp_sw[kWarps];
   __shared__ uint32_t s_warp_tw[kWarps];
@@ -437,17 +436,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
   }
 
-  // warp carry states from the tile's carry-in (K0 pre-pass, no look-back)
-  if (threadIdx.x == 0) {
-    uint32_t c = carry_in;
-    for (int k = 0; k < kWarps; k++) {
-      s_warp_state[k] = c;
-      c = s1::apply(s_warp_f[k], c);
-    }
-  }
-  __syncthreads();
-
-  uint32_t state = s_warp_state[warp];
+  // this warp's carry state: the tile's carry-in (K0 pre-pass, no look-back)
+  // through the earlier warps' functions, folded by every warp itself (no
+  // second barrier)
+  uint32_t state = carry_in;
+  for (int k = 0; k < warp; k++) state = s1::apply(s_warp_f[k], state);
   if (lane > 0) state = s1::apply(excl, state);
   int64_t rem = (int64_t)a.len - (int64_t)blk;
   const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
