@@ -32,6 +32,9 @@ jt_error jt_b200_parse_resident(jt_parser *p, size_t len, long long *error_offse
  * return immediately; jt_b200_finish waits and returns the result. */
 jt_error jt_b200_parse_async(jt_parser *p, size_t len);
 jt_error jt_b200_finish(jt_parser *p, long long *error_offset);
+/* jt_stage1 over the resident input without waiting (UTF-8 check + index,
+ * the k_index path); jt_b200_finish completes it like jt_stage1 would. */
+jt_error jt_b200_stage1_async(jt_parser *p, size_t len);
 
 /* Device views of the last results (valid until the next call). */
 const uint32_t *jt_b200_device_index(const jt_parser *p, size_t *count);

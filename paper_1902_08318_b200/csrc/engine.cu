@@ -171,8 +171,10 @@ struct jt_parser {
   int launches = 0;
   std::string err;
   uint64_t s1_str_err = ~0ULL, s1_string_bytes = 0, s1_tape_words = 0;  // retained with the index
+  bool s1_full = false;  // the retained index came with K1's stage-2 arrays
   uint64_t pending_len = 0;
   int pending_idx = -1;
+  bool pending_full = true;
   // captured launch sequences for repeated resident parses (one per index buffer)
   struct Graph {
     cudaGraphExec_t exec = nullptr;
@@ -180,7 +182,7 @@ struct jt_parser {
     cudaStream_t stream = nullptr;
     uint64_t sig = 0;
     int launches = 0;
-  } graph[2];
+  } graph[2], graph_s1[2];  // full parse / jt_stage1 (index only), per index buffer
   // byte-range shard of a document (shard.h), between jt_b200_shard_begin
   // and jt_b200_shard_finish
   bool shard_on = false;
@@ -352,8 +354,8 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full);
 // Full parses without profiling replay a CUDA graph of the 9 launches + the
 // control-block D2H (captured on first use for this length/stream/buffers).
 bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
-  if (!full || p->prof) return enqueue_direct(p, len, which, full);
-  auto &g = p->graph[which];
+  if (p->prof) return enqueue_direct(p, len, which, full);
+  auto &g = full ? p->graph[which] : p->graph_s1[which];
   const uint64_t sig = buffers_sig(p, which);
   if (!(g.exec && g.len == len && g.stream == p->stream && g.sig == sig)) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -399,8 +401,13 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
     return false;
   p->launches++;
   if (p->prof) cudaEventRecord(p->ev[1], p->stream);
-  if (!cuda_ok(p, jt::stage1_launch(s1_args(p, len, which), p->stream), "stage1")) return false;
-  p->launches += jt::kStage1Launches;
+  if (full) {
+    if (!cuda_ok(p, jt::stage1_launch(s1_args(p, len, which), p->stream), "stage1")) return false;
+    p->launches += jt::kStage1Launches;
+  } else {  // jt_stage1: the index alone (k_index); stage 2 rebuilds the rest
+    if (!cuda_ok(p, jt::index_launch(s1_args(p, len, which), p->stream), "index")) return false;
+    p->launches += jt::kIndexLaunches;
+  }
   if (p->prof) cudaEventRecord(p->ev[2], p->stream);
   if (full) {
     int n = 0;
@@ -435,6 +442,7 @@ jt_error finish(jt_parser *p, int which, bool full, long long *off) {
     p->s1_str_err = c.str_err;
     p->s1_string_bytes = c.string_bytes;
     p->s1_tape_words = c.tape_words;
+    p->s1_full = full;  // index-only stage 1: no stage-2 arrays yet
     p->h_index_valid = false;
   }
   set_off(off, c.offset);
@@ -669,6 +677,8 @@ void jt_parser_free(jt_parser *p) {
   cudaStreamSynchronize(p->stream);
   for (auto &g : p->graph)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto &g : p->graph_s1)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
   if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
   if (p->h_shard) cudaFreeHost(p->h_shard);
@@ -735,6 +745,25 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   if (!ensure_stage2(p, len)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
+  }
+  if (p->have_index && !p->s1_full) {
+    // the last jt_stage1 built the index alone (k_index): K1 rebuilds the
+    // same index with the string payload and token arrays, then stage 2
+    // (after a UTF-8-failed jt_stage1 the reference would run on its stale
+    // index; this reports the retained input's own verdict)
+    if (!ensure_stage1(p, len, p->cur) || !enqueue(p, len, p->cur, true)) {
+      set_off(error_offset, -1);
+      return JT_CAPACITY;
+    }
+    jt_error e = finish(p, p->cur, true, error_offset);
+    if (e == JT_OK && out) {
+      *out = download(p);
+      if (!*out) {
+        set_off(error_offset, -1);
+        return JT_CAPACITY;
+      }
+    }
+    return e;
   }
   // re-run stage 2 over the retained input, index and string payload:
   // reset the records, then restore the stage-1 results into the control block
@@ -1140,6 +1169,18 @@ jt_error jt_b200_parse_async(jt_parser *p, size_t len) {
     return JT_CAPACITY;
   p->pending_len = len;
   p->pending_idx = which;
+  p->pending_full = true;
+  return JT_OK;
+}
+
+jt_error jt_b200_stage1_async(jt_parser *p, size_t len) {
+  if ((uint64_t)len >= (1ULL << 32)) return JT_CAPACITY;
+  p->in_len = len;
+  int which = p->cur ^ 1;
+  if (!ensure_stage1(p, len, which) || !enqueue(p, len, which, false)) return JT_CAPACITY;
+  p->pending_len = len;
+  p->pending_idx = which;
+  p->pending_full = false;
   return JT_OK;
 }
 
@@ -1150,7 +1191,7 @@ jt_error jt_b200_finish(jt_parser *p, long long *error_offset) {
   }
   int which = p->pending_idx;
   p->pending_idx = -1;
-  return finish(p, which, true, error_offset);
+  return finish(p, which, p->pending_full, error_offset);
 }
 
 const uint32_t *jt_b200_device_index(const jt_parser *p, size_t *count) {

@@ -862,6 +862,269 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   if (threadIdx.x == 0) JT_TL(tile, 7);
 }
 
+// ---- index-only stage 1 (jt_stage1: build_structural_index, indexer.cpp:29-56)
+// The reference's stage 1 is UTF-8 validation + the structural index; K1
+// also produces what stage 2 needs (string payload, token records, tape
+// indices).  k_index does only the former, in ONE pass over the input: no
+// carry pre-pass.  A tile's structural count depends on its entry state
+// (odd backslash run, in string, previous separator), so every tile counts
+// its positions for all four (odd, in_string) entry states and publishes
+//   IdxAgg = (carry transfer function f, counts c[4], sep delta d[4])
+// -- d[x]: one more position when a separator precedes the tile (bit 0 of
+// the tile becomes a pseudo-structural start).  IdxAgg composes
+// associatively, so one decoupled look-back over the predecessors' IdxAggs
+// yields both the tile's entry state and its index base; the tile then picks
+// the final mask of its actual entry state (kept in registers).
+struct IdxAgg {
+  uint32_t f;     // 4 bytes: state_out (odd | ins << 1 | sep << 2) for x = odd | ins << 1
+  uint32_t c[4];  // positions for entry x (separator-free entry)
+  uint32_t d;     // bit x: +1 position with a separator before the tile
+  bool id;        // the neutral element (no tiles)
+};
+
+__device__ __forceinline__ uint32_t pick4(const uint32_t c[4], uint32_t x) {
+  const uint32_t lo = (x & 1) ? c[1] : c[0], hi = (x & 1) ? c[3] : c[2];
+  return (x & 2) ? hi : lo;
+}
+
+// `e` (earlier tiles) followed by `l` (later tiles)
+__device__ __forceinline__ IdxAgg idx_combine(const IdxAgg &e, const IdxAgg &l) {
+  if (e.id) return l;
+  if (l.id) return e;
+  IdxAgg r;
+  r.id = false;
+  r.f = s1::compose(l.f, e.f);
+  r.d = e.d;
+#pragma unroll
+  for (uint32_t x = 0; x < 4; x++) {
+    const uint32_t y = (e.f >> (8 * x)) & 7;
+    r.c[x] = e.c[x] + pick4(l.c, y & 3) + ((y >> 2) & (l.d >> (y & 3)) & 1u);
+  }
+  return r;
+}
+
+__device__ __forceinline__ IdxAgg idx_shfl_down(const IdxAgg &v, int d) {
+  IdxAgg o;
+  o.f = __shfl_down_sync(0xffffffffu, v.f, d);
+#pragma unroll
+  for (int k = 0; k < 4; k++) o.c[k] = __shfl_down_sync(0xffffffffu, v.c[k], d);
+  o.d = __shfl_down_sync(0xffffffffu, v.d, d);
+  o.id = __shfl_down_sync(0xffffffffu, (uint32_t)v.id, d) != 0;
+  return o;
+}
+
+// record layout per tile: agg words 2t, 2t+1 and the inclusive word at
+// 2 * ntiles + t; bit 63 = written.  agg0 = c0 | f << 16 | d << 48,
+// agg1 = c1 | c2 << 16 | c3 << 32 (a tile's counts are <= 16384);
+// incl = base | state << 48.
+constexpr uint64_t kIdxValid = 1ULL << 63;
+
+// Look-back of tile `tile` (> 0) by one full warp: entry state and base.
+__device__ __forceinline__ void idx_lookback(const uint64_t *agg, const uint64_t *incl, int64_t tile,
+                                             uint32_t &state, uint64_t &base) {
+  const int lane = threadIdx.x & 31;
+  IdxAgg acc;
+  acc.id = true;
+  int64_t j0 = tile - 1;
+  for (;;) {
+    const int64_t j = j0 - lane;
+    IdxAgg v;
+    v.id = true;
+    uint64_t iv = kIdxValid | ((uint64_t)s1::kInitState << 48);  // before tile 0
+    bool have = j < 0;
+    while (!have) {
+      iv = lb_load(incl + j);
+      if (iv & kIdxValid) {
+        have = true;
+        break;
+      }
+      const uint64_t a0 = lb_load(agg + 2 * j), a1 = lb_load(agg + 2 * j + 1);
+      if (a0 & a1 & kIdxValid) {
+        v.id = false;
+        v.c[0] = (uint32_t)(a0 & 0xFFFF);
+        v.f = (uint32_t)(a0 >> 16);
+        v.d = (uint32_t)(a0 >> 48) & 15u;
+        v.c[1] = (uint32_t)(a1 & 0xFFFF);
+        v.c[2] = (uint32_t)((a1 >> 16) & 0xFFFF);
+        v.c[3] = (uint32_t)((a1 >> 32) & 0xFFFF);
+        break;
+      }
+      __nanosleep(32);
+    }
+    const uint32_t hits = __ballot_sync(0xffffffffu, have);
+    const int k = hits ? __ffs(hits) - 1 : 32;
+    if (lane >= k) v.id = true;  // lanes from the first inclusive tile back: not needed
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      IdxAgg o = idx_shfl_down(v, d);
+      if (lane + d < 32) v = idx_combine(o, v);
+    }
+    // lane 0: the window's tiles after the inclusive one, in order
+    if (lane == 0) acc = idx_combine(v, acc);
+    if (hits) {
+      const uint64_t ik = __shfl_sync(0xffffffffu, iv, k);
+      if (lane == 0) {
+        const uint32_t s = (uint32_t)(ik >> 48) & 7u;
+        uint64_t b = ik & ((1ULL << 48) - 1);
+        if (acc.id) {
+          state = s;
+        } else {
+          b += pick4(acc.c, s & 3) + ((s >> 2) & (acc.d >> (s & 3)) & 1u);
+          state = (acc.f >> (8 * (s & 3))) & 7u;
+        }
+        base = b;
+      }
+      return;
+    }
+    j0 -= 32;
+  }
+}
+
+// final structural mask of a block for entry state s (s1::final_mask with the
+// odd-run variants of uq and its prefix XOR shared across the four states)
+__device__ __forceinline__ uint64_t idx_fin(const s1::Masks &m, uint64_t uq0, uint64_t uq1,
+                                            uint64_t px0, uint64_t px1, uint32_t s,
+                                            uint64_t valid) {
+  const uint64_t uq = (s & 1) ? uq1 : uq0;
+  const uint64_t instr = ((s & 1) ? px1 : px0) ^ ((s & 2) ? ~0ULL : 0ULL);
+  const uint64_t s1v = (m.st & ~instr) | uq;
+  const uint64_t pseudo = (((s1v | m.ws) << 1) | (uint64_t)(s >> 2)) & ~m.ws & ~instr;
+  return (s1v | pseudo) & ~(uq & ~instr) & valid;
+}
+
+__global__ void __launch_bounds__(kThreads) k_index(Stage1Args a) {
+  __shared__ uint32_t s_tile, s_warp_f[kWarps], s_d, s_sel;
+  __shared__ unsigned long long s_warp_cnt[kWarps], s_base;
+  __shared__ uint16_t s_pos[kStageIdx];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
+  const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
+  uint32_t w[16];
+  ld256(a.in + blk, w);
+  ld256(a.in + blk + 32, w + 8);
+  s1::Masks m;
+  s1::classify64(w, m);
+  const uint64_t esc0 = s1::escaped_no_carry(m.bs), tog = s1::carry_toggle(m.bs);
+  uint32_t inc = s1::block_function(m, esc0, tog);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc = s1::compose(inc, o);
+  }
+  const uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 31) s_warp_f[warp] = inc;
+  // UTF-8 validity (as K1)
+  uint32_t prev = __shfl_up_sync(0xffffffffu, w[15], 1);
+  if (lane == 0) prev = blk >= 4 ? *(const uint32_t *)(a.in + blk - 4) : 0u;
+  if ((m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3 &&
+      s1::utf8_block_error(m.P, prev, blk + 64 >= a.len)) {
+    const uint8_t *in = a.in;
+    const uint64_t len = a.len;
+    auto at = [in, len](uint64_t i) -> uint32_t { return i < len ? in[i] : 0u; };
+    uint64_t lo = blk >= 3 ? blk - 3 : 0, hi = blk + 64 < len ? blk + 64 : len;
+    for (uint64_t i = lo; i < hi; i++)
+      if (s1::utf8_flagged(at, i, len)) {
+        atomicMin(a.utf8_pos, (unsigned long long)i);
+        break;
+      }
+  }
+  const int64_t rem = (int64_t)a.len - (int64_t)blk;
+  const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
+  const uint64_t uq0 = m.qt & ~esc0, tq = m.qt & tog;
+  const uint64_t uq1 = uq0 ^ tq;
+  const uint64_t px0 = s1::prefix_xor(uq0), px1 = px0 ^ (0ULL - tq);
+  __syncthreads();
+  // G: tile entry -> this block's entry (identity for block 0, whose
+  // separator carry is the tile's: the d bits)
+  uint32_t wf = lane < kWarps ? s_warp_f[lane] : 0u;
+#pragma unroll
+  for (int d = 1; d < kWarps; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, wf, d);
+    if (lane >= d) wf = s1::compose(wf, o);
+  }
+  const uint32_t tile_f = __shfl_sync(0xffffffffu, wf, kWarps - 1);
+  const uint32_t wpre = __shfl_sync(0xffffffffu, wf, warp > 0 ? warp - 1 : 0);
+  uint32_t G;
+  if (warp == 0)
+    G = lane == 0 ? 0x03020100u : excl;
+  else
+    G = lane == 0 ? wpre : s1::compose(excl, wpre);
+  uint64_t fin[4];
+#pragma unroll
+  for (int x = 0; x < 4; x++) fin[x] = idx_fin(m, uq0, uq1, px0, px1, (G >> (8 * x)) & 7u, valid);
+  if (threadIdx.x == 0) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int x = 0; x < 4; x++)
+      d |= (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, (uint32_t)x | 4u, valid) ^ fin[x]) & 1) << x;
+    s_d = d;
+  }
+  const uint64_t cnt = (uint64_t)popc64(fin[0]) | ((uint64_t)popc64(fin[1]) << 16) |
+                       ((uint64_t)popc64(fin[2]) << 32) | ((uint64_t)popc64(fin[3]) << 48);
+  uint64_t ci = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t o = __shfl_up_sync(0xffffffffu, ci, d);
+    if (lane >= d) ci += o;
+  }
+  if (lane == 31) s_warp_cnt[warp] = ci;
+  __syncthreads();
+  uint64_t wc = lane < kWarps ? s_warp_cnt[lane] : 0ULL;
+#pragma unroll
+  for (int d = 1; d < kWarps; d <<= 1) {
+    uint64_t o = __shfl_up_sync(0xffffffffu, wc, d);
+    if (lane >= d) wc += o;
+  }
+  const uint64_t tile_c = __shfl_sync(0xffffffffu, wc, kWarps - 1);
+  const uint64_t cpre = warp > 0 ? __shfl_sync(0xffffffffu, wc, warp > 0 ? warp - 1 : 0) : 0ULL;
+  const uint64_t off4 = cpre + ci - cnt;
+  if (warp == 0) {
+    const uint32_t d = s_d;
+    uint64_t *agg = a.rec_count, *incl = a.rec_count + 2 * a.ntiles;
+    uint32_t state = s1::kInitState;
+    uint64_t base = 0;
+    if (tile > 0) {
+      if (lane == 0) {
+        lb_store(agg + 2 * tile, kIdxValid | (tile_c & 0xFFFF) | ((uint64_t)tile_f << 16) |
+                                     ((uint64_t)d << 48));
+        lb_store(agg + 2 * tile + 1, kIdxValid | (tile_c >> 16));
+      }
+      idx_lookback(agg, incl, tile, state, base);
+    }
+    if (lane == 0) {
+      const uint32_t x = state & 3, sep = (state >> 2) & (d >> x) & 1u;
+      const uint64_t out = base + ((tile_c >> (16 * x)) & 0xFFFF) + sep;
+      lb_store(incl + tile, kIdxValid | ((uint64_t)((tile_f >> (8 * x)) & 7u) << 48) | out);
+      if (tile == (int64_t)a.ntiles - 1) *a.total = out;
+      s_base = base;
+      s_sel = x | (sep << 2);
+    }
+  }
+  __syncthreads();
+  const uint32_t sel = s_sel, x = sel & 3, sep = sel >> 2;
+  uint64_t f = x == 0 ? fin[0] : x == 1 ? fin[1] : x == 2 ? fin[2] : fin[3];
+  if (threadIdx.x == 0) f |= sep;
+  const uint32_t off = (uint32_t)((off4 >> (16 * x)) & 0xFFFF) + (threadIdx.x ? sep : 0u);
+  const uint32_t total = (uint32_t)((tile_c >> (16 * x)) & 0xFFFF) + sep;
+  const uint64_t base = s_base;
+  if (total > (uint32_t)kStageIdx) {  // CTA-uniform
+    uint32_t slot = off;
+    for (uint64_t fm = f; fm; fm &= fm - 1) a.idx[base + slot++] = (uint32_t)(blk + ctz64(fm));
+    return;
+  }
+  {
+    uint32_t slot = off;
+    for (uint64_t fm = f; fm; fm &= fm - 1) s_pos[slot++] = (uint16_t)(threadIdx.x * 64 + ctz64(fm));
+  }
+  __syncthreads();
+  uint32_t *dst = a.idx + base;
+  const uint32_t tb = (uint32_t)tile_base;
+  for (uint32_t k = threadIdx.x; k < total; k += kThreads) dst[k] = tb + s_pos[k];
+}
+
 // ---- jt_minify (capi.cpp:154-167, minify_pass indexer.cpp:58-75) -----------
 // After a successful parse: keep in-string bytes, unescaped quotes and every
 // non-whitespace byte.  One CTA per 16 KiB tile; the carry-in is K0b's from
@@ -1073,6 +1336,12 @@ cudaError_t stage1_chunk_launch(const Stage1Args &args_in, cudaStream_t stream) 
   k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr, nullptr,
                                                nullptr, nullptr, a.init_state, a.out_state);
   k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t index_launch(const Stage1Args &args_in, cudaStream_t stream) {
+  const Stage1Args a = with_tiles(args_in);
+  k_index<<<(unsigned)a.ntiles, kThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -68,6 +68,11 @@ cudaError_t stage1_lengths_launch(const Stage1Args &args, uint64_t ntiles, cudaS
 cudaError_t stage1_records_count(const Stage1Args &args, cudaStream_t stream);
 cudaError_t stage1_records_main(const Stage1Args &args, cudaStream_t stream);
 
+// index-only stage 1 (jt_stage1): K0a, K0b, k_index -> idx, total, utf8_pos
+// (rec_count used as ntiles u62 look-back words, zeroed)
+constexpr int kIndexLaunches = 1;
+cudaError_t index_launch(const Stage1Args &args, cudaStream_t stream);
+
 // jt_minify after a successful parse of the same resident input (the
 // carry-ins are K0b's); rec and tile_counter zeroed, ntiles words / 1 word
 struct MinifyArgs {

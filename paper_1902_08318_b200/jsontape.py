@@ -32,7 +32,7 @@ EXPORTS = [
     "jt_document_equal", "jt_document_dump", "jt_document_distinct", "jt_string_free",
     "jt_minify", "jt_compute_stats", "jt_oracle_validate", "jt_generate", "jt_error_name",
     "jt_b200_input_buffer", "jt_b200_stage1_resident", "jt_b200_parse_resident",
-    "jt_b200_parse_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
+    "jt_b200_parse_async", "jt_b200_stage1_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
     "jt_b200_device_strings", "jt_b200_download", "jt_b200_set_stream",
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_shard_summary_bytes",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_stage1_resident.argtypes = [vp, sz, C.POINTER(ll)]
     L.jt_b200_parse_resident.argtypes = [vp, sz, C.POINTER(ll)]
     L.jt_b200_parse_async.argtypes = [vp, sz]
+    L.jt_b200_stage1_async.argtypes = [vp, sz]
     L.jt_b200_finish.argtypes = [vp, C.POINTER(ll)]
     L.jt_b200_device_index.argtypes = [vp, C.POINTER(sz)]
     L.jt_b200_device_index.restype = vp
@@ -254,6 +255,9 @@ class Parser:
 
     def parse_async(self, n: int) -> int:
         return self._lib.jt_b200_parse_async(self._h, n)
+
+    def stage1_async(self, n: int) -> int:
+        return self._lib.jt_b200_stage1_async(self._h, n)
 
     def finish(self) -> Result:
         off = C.c_longlong(-7)
