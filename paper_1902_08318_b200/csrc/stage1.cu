@@ -920,6 +920,11 @@ __device__ __forceinline__ IdxAgg idx_shfl_down(const IdxAgg &v, int d) {
 constexpr uint64_t kIdxValid = 1ULL << 63;
 
 // Look-back of tile `tile` (> 0) by one full warp: entry state and base.
+// Each round covers 128 predecessors (4 per lane, nearest first), all 12
+// record words of a lane loaded together: one L2 round trip per round.  A
+// persistent k_index resolves tiles in waves of ~G = #CTAs, so a tile may
+// sit up to G tiles past the last inclusive record.
+constexpr int kLbPer = 4;
 __device__ __forceinline__ void idx_lookback(const uint64_t *agg, const uint64_t *incl, int64_t tile,
                                              uint32_t &state, uint64_t &base) {
   const int lane = threadIdx.x & 31;
@@ -927,42 +932,73 @@ __device__ __forceinline__ void idx_lookback(const uint64_t *agg, const uint64_t
   acc.id = true;
   int64_t j0 = tile - 1;
   for (;;) {
-    const int64_t j = j0 - lane;
+    uint64_t iv[kLbPer], a0[kLbPer], a1[kLbPer];
+    int kq;
+    for (;;) {
+#pragma unroll
+      for (int q = 0; q < kLbPer; q++) {
+        const int64_t j = j0 - kLbPer * lane - q;
+        if (j >= 0) {
+          iv[q] = lb_load(incl + j);
+          a0[q] = lb_load(agg + 2 * j);
+          a1[q] = lb_load(agg + 2 * j + 1);
+        } else {  // before tile 0: the initial state, base 0
+          iv[q] = kIdxValid | ((uint64_t)s1::kInitState << 48);
+          a0[q] = a1[q] = 0;
+        }
+      }
+      // nearest inclusive record of this lane, and whether every nearer
+      // tile has published its aggregate
+      kq = kLbPer;
+      bool ok = true;
+#pragma unroll
+      for (int q = kLbPer - 1; q >= 0; q--) {
+        if (iv[q] & kIdxValid) {
+          kq = q;
+          ok = true;
+        } else if (!(a0[q] & a1[q] & kIdxValid)) {
+          ok = false;
+        }
+      }
+      const uint32_t hits = __ballot_sync(0xffffffffu, kq < kLbPer);
+      const int L = hits ? __ffs(hits) - 1 : 32;
+      const bool need = lane <= L;
+      if (__all_sync(0xffffffffu, ok || !need)) break;
+      JT_TLADD(tile, 12, lane == 0);
+      __nanosleep(64);
+    }
+    const uint32_t hits = __ballot_sync(0xffffffffu, kq < kLbPer);
+    const int L = hits ? __ffs(hits) - 1 : 32;
+    // this lane's tiles after the inclusive one, earliest first
     IdxAgg v;
     v.id = true;
-    uint64_t iv = kIdxValid | ((uint64_t)s1::kInitState << 48);  // before tile 0
-    bool have = j < 0;
-    while (!have) {
-      iv = lb_load(incl + j);
-      if (iv & kIdxValid) {
-        have = true;
-        break;
+    if (lane <= L) {
+#pragma unroll
+      for (int q = kLbPer - 1; q >= 0; q--) {
+        if (lane == L && q >= kq) continue;
+        IdxAgg t;
+        t.id = false;
+        t.c[0] = (uint32_t)(a0[q] & 0xFFFF);
+        t.f = (uint32_t)(a0[q] >> 16);
+        t.d = (uint32_t)(a0[q] >> 48) & 15u;
+        t.c[1] = (uint32_t)(a1[q] & 0xFFFF);
+        t.c[2] = (uint32_t)((a1[q] >> 16) & 0xFFFF);
+        t.c[3] = (uint32_t)((a1[q] >> 32) & 0xFFFF);
+        v = idx_combine(v, t);
       }
-      const uint64_t a0 = lb_load(agg + 2 * j), a1 = lb_load(agg + 2 * j + 1);
-      if (a0 & a1 & kIdxValid) {
-        v.id = false;
-        v.c[0] = (uint32_t)(a0 & 0xFFFF);
-        v.f = (uint32_t)(a0 >> 16);
-        v.d = (uint32_t)(a0 >> 48) & 15u;
-        v.c[1] = (uint32_t)(a1 & 0xFFFF);
-        v.c[2] = (uint32_t)((a1 >> 16) & 0xFFFF);
-        v.c[3] = (uint32_t)((a1 >> 32) & 0xFFFF);
-        break;
-      }
-      __nanosleep(32);
     }
-    const uint32_t hits = __ballot_sync(0xffffffffu, have);
-    const int k = hits ? __ffs(hits) - 1 : 32;
-    if (lane >= k) v.id = true;  // lanes from the first inclusive tile back: not needed
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       IdxAgg o = idx_shfl_down(v, d);
       if (lane + d < 32) v = idx_combine(o, v);
     }
-    // lane 0: the window's tiles after the inclusive one, in order
     if (lane == 0) acc = idx_combine(v, acc);
     if (hits) {
-      const uint64_t ik = __shfl_sync(0xffffffffu, iv, k);
+      uint64_t mine = iv[0];
+#pragma unroll
+      for (int q = 1; q < kLbPer; q++)
+        if (kq == q) mine = iv[q];
+      const uint64_t ik = __shfl_sync(0xffffffffu, mine, L);
       if (lane == 0) {
         const uint32_t s = (uint32_t)(ik >> 48) & 7u;
         uint64_t b = ik & ((1ULL << 48) - 1);
@@ -976,7 +1012,8 @@ __device__ __forceinline__ void idx_lookback(const uint64_t *agg, const uint64_t
       }
       return;
     }
-    j0 -= 32;
+    JT_TLADD(tile, 11, lane == 0);
+    j0 -= 32 * kLbPer;
   }
 }
 
@@ -992,137 +1029,296 @@ __device__ __forceinline__ uint64_t idx_fin(const s1::Masks &m, uint64_t uq0, ui
   return (s1v | pseudo) & ~(uq & ~instr) & valid;
 }
 
-__global__ void __launch_bounds__(kThreads) k_index(Stage1Args a) {
-  __shared__ uint32_t s_tile, s_warp_f[kWarps], s_d, s_sel;
-  __shared__ unsigned long long s_warp_cnt[kWarps], s_base;
-  __shared__ uint16_t s_pos[kStageIdx];
+// Persistent, warp-specialised k_index.  8 compute warps own a 16 KiB tile
+// (64 bytes per thread, as K1) and publish its IdxAgg as soon as it is
+// counted; a 9th warp (the look-back warp) resolves the look-backs of the
+// CTA's tiles in order.  Counted tiles wait in a ring of kIdxRing slots
+// (final masks per entry state + slot offsets) until their look-back is
+// done; the compute warps extract every resolved tile after each tile they
+// count and block only when the ring is full.  So a tile's compute never
+// waits on an earlier tile's look-back, aggregates appear in claim order,
+// and look-backs find their predecessors published (the first persistent
+// version, which waited on the previous tile's look-back before counting
+// the next, fed look-back latency back into aggregate latency: 10 us
+// look-backs, 7 us behind the predecessors' aggregates).
+// Hand-off through shared-memory sequence numbers: `ready` (compute ->
+// look-back warp, ring slot filled) and `done` (look-back warp -> compute,
+// entry state + base written).
+constexpr int kIdxCompute = kThreads;       // 256 compute threads
+constexpr int kIdxThreads = kThreads + 32;  // + look-back warp
+constexpr int kIdxMinBlocks = 3;
+constexpr int kIdxRing = 4;
+
+template <int kId, int kN>
+__device__ __forceinline__ void bar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+
+struct IdxSlot {
+  uint64_t fin[4][kIdxCompute];  // final masks per entry state (per block)
+  uint64_t off[kIdxCompute];     // 4 x 16-bit tile-relative slot per entry state
+  unsigned long long tc;         // tile counts (4 x 16 bit)
+  unsigned long long base;       // from the look-back warp
+  uint32_t tile, tf, d, sel;
+};
+
+struct IdxSmem {
+  IdxSlot slot[kIdxRing];
+  unsigned long long wc[kWarps];
+  uint32_t wf[kWarps];
+  uint32_t claim, snap;
+  volatile uint32_t ready, done;  // sequence numbers
+  volatile uint32_t end_seq;      // no tile at this sequence number: the CTA is done
+  alignas(16) uint32_t pos[kStageIdx + 8];  // absolute positions, shifted to the output's 16-byte phase
+};
+
+__global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args a) {
+  extern __shared__ __align__(16) uint8_t idx_smem_raw[];
+  IdxSmem &S = *reinterpret_cast<IdxSmem *>(idx_smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const uint64_t tile_base = (uint64_t)tile * kStage1Tile;
-  const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
-  uint32_t w[16];
-  ld256(a.in + blk, w);
-  ld256(a.in + blk + 32, w + 8);
-  s1::Masks m;
-  s1::classify64(w, m);
-  const uint64_t esc0 = s1::escaped_no_carry(m.bs), tog = s1::carry_toggle(m.bs);
-  uint32_t inc = s1::block_function(m, esc0, tog);
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc = s1::compose(inc, o);
-  }
-  const uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 31) s_warp_f[warp] = inc;
-  // UTF-8 validity (as K1)
-  uint32_t prev = __shfl_up_sync(0xffffffffu, w[15], 1);
-  if (lane == 0) prev = blk >= 4 ? *(const uint32_t *)(a.in + blk - 4) : 0u;
-  if ((m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3 &&
-      s1::utf8_block_error(m.P, prev, blk + 64 >= a.len)) {
-    const uint8_t *in = a.in;
-    const uint64_t len = a.len;
-    auto at = [in, len](uint64_t i) -> uint32_t { return i < len ? in[i] : 0u; };
-    uint64_t lo = blk >= 3 ? blk - 3 : 0, hi = blk + 64 < len ? blk + 64 : len;
-    for (uint64_t i = lo; i < hi; i++)
-      if (s1::utf8_flagged(at, i, len)) {
-        atomicMin(a.utf8_pos, (unsigned long long)i);
-        break;
-      }
-  }
-  const int64_t rem = (int64_t)a.len - (int64_t)blk;
-  const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
-  const uint64_t uq0 = m.qt & ~esc0, tq = m.qt & tog;
-  const uint64_t uq1 = uq0 ^ tq;
-  const uint64_t px0 = s1::prefix_xor(uq0), px1 = px0 ^ (0ULL - tq);
-  __syncthreads();
-  // G: tile entry -> this block's entry (identity for block 0, whose
-  // separator carry is the tile's: the d bits)
-  uint32_t wf = lane < kWarps ? s_warp_f[lane] : 0u;
-#pragma unroll
-  for (int d = 1; d < kWarps; d <<= 1) {
-    uint32_t o = __shfl_up_sync(0xffffffffu, wf, d);
-    if (lane >= d) wf = s1::compose(wf, o);
-  }
-  const uint32_t tile_f = __shfl_sync(0xffffffffu, wf, kWarps - 1);
-  const uint32_t wpre = __shfl_sync(0xffffffffu, wf, warp > 0 ? warp - 1 : 0);
-  uint32_t G;
-  if (warp == 0)
-    G = lane == 0 ? 0x03020100u : excl;
-  else
-    G = lane == 0 ? wpre : s1::compose(excl, wpre);
-  uint64_t fin[4];
-#pragma unroll
-  for (int x = 0; x < 4; x++) fin[x] = idx_fin(m, uq0, uq1, px0, px1, (G >> (8 * x)) & 7u, valid);
+  const uint32_t ntiles = (uint32_t)a.ntiles;
   if (threadIdx.x == 0) {
-    uint32_t d = 0;
-#pragma unroll
-    for (int x = 0; x < 4; x++)
-      d |= (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, (uint32_t)x | 4u, valid) ^ fin[x]) & 1) << x;
-    s_d = d;
+    S.claim = atomicAdd(a.tile_counter, 1u);
+    S.ready = 0;
+    S.done = 0;
+    S.end_seq = ~0u;
   }
-  const uint64_t cnt = (uint64_t)popc64(fin[0]) | ((uint64_t)popc64(fin[1]) << 16) |
-                       ((uint64_t)popc64(fin[2]) << 32) | ((uint64_t)popc64(fin[3]) << 48);
-  uint64_t ci = cnt;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint64_t o = __shfl_up_sync(0xffffffffu, ci, d);
-    if (lane >= d) ci += o;
-  }
-  if (lane == 31) s_warp_cnt[warp] = ci;
   __syncthreads();
-  uint64_t wc = lane < kWarps ? s_warp_cnt[lane] : 0ULL;
-#pragma unroll
-  for (int d = 1; d < kWarps; d <<= 1) {
-    uint64_t o = __shfl_up_sync(0xffffffffu, wc, d);
-    if (lane >= d) wc += o;
-  }
-  const uint64_t tile_c = __shfl_sync(0xffffffffu, wc, kWarps - 1);
-  const uint64_t cpre = warp > 0 ? __shfl_sync(0xffffffffu, wc, warp > 0 ? warp - 1 : 0) : 0ULL;
-  const uint64_t off4 = cpre + ci - cnt;
-  if (warp == 0) {
-    const uint32_t d = s_d;
-    uint64_t *agg = a.rec_count, *incl = a.rec_count + 2 * a.ntiles;
-    uint32_t state = s1::kInitState;
-    uint64_t base = 0;
-    if (tile > 0) {
+
+  if (warp == kWarps) {  // ---- look-back warp
+    const uint64_t *agg = a.rec_count;
+    uint64_t *incl = a.rec_count + 2 * a.ntiles;
+    for (uint32_t seq = 0;; seq++) {
+      IdxSlot &R = S.slot[seq % kIdxRing];
+      while (S.ready <= seq) __nanosleep(32);
+      if (seq == S.end_seq) return;
+      const uint32_t tile = R.tile;
+      if (lane == 0) JT_TL(tile, 2);
+      const uint64_t tile_c = R.tc;
+      const uint32_t tile_f = R.tf, d = R.d;
+      uint32_t state = s1::kInitState;
+      uint64_t base = 0;
+      if (tile > 0) idx_lookback(agg, incl, tile, state, base);
       if (lane == 0) {
+        const uint32_t x = state & 3, sep = (state >> 2) & (d >> x) & 1u;
+        const uint64_t out = base + ((tile_c >> (16 * x)) & 0xFFFF) + sep;
+        lb_store(incl + tile, kIdxValid | ((uint64_t)((tile_f >> (8 * x)) & 7u) << 48) | out);
+        if (tile == ntiles - 1) *a.total = out;
+        R.base = base;
+        R.sel = x | (sep << 2);
+        JT_TL(tile, 3);
+        __threadfence_block();
+        S.done = seq + 1;
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---- compute warps
+  const bool vec_ok = ((uintptr_t)a.idx & 15) == 0;
+  // positions of a resolved tile: entry state and base from the look-back
+  // warp, final mask from its ring slot, staged then written as 16-byte
+  // vectors
+  auto extract = [&](uint32_t seq) {
+    IdxSlot &R = S.slot[seq % kIdxRing];
+    bar_sync<1, kIdxCompute>();  // S.pos free, R.sel / R.base visible
+    const uint32_t ptile = R.tile;
+    if (threadIdx.x == 0) JT_TL(ptile, 5);
+    const uint32_t sel = R.sel, x = sel & 3, sep = sel >> 2;
+    const uint64_t base = R.base;
+    const uint64_t tc = R.tc;
+    uint64_t f = R.fin[x][threadIdx.x];
+    if (threadIdx.x == 0) f |= sep;
+    const uint32_t off = (uint32_t)((R.off[threadIdx.x] >> (16 * x)) & 0xFFFF) + (threadIdx.x ? sep : 0u);
+    const uint32_t total = (uint32_t)((tc >> (16 * x)) & 0xFFFF) + sep;
+    const uint32_t blk = ptile * (uint32_t)kStage1Tile + threadIdx.x * 64u;
+    if (total > (uint32_t)kStageIdx) {  // CTA-uniform: direct stores
+      uint32_t slot = off;
+      for (uint64_t fm = f; fm; fm &= fm - 1) a.idx[base + slot++] = blk + (uint32_t)ctz64(fm);
+      return;
+    }
+    const uint32_t shift = vec_ok ? (uint32_t)(base & 3) : 0u;
+    uint32_t slot = off + shift;
+    uint32_t lo = (uint32_t)f, hi = (uint32_t)(f >> 32);
+    while (lo) {
+      S.pos[slot++] = blk + (uint32_t)(__ffs(lo) - 1);
+      lo &= lo - 1;
+    }
+    while (hi) {
+      S.pos[slot++] = blk + 32u + (uint32_t)(__ffs(hi) - 1);
+      hi &= hi - 1;
+    }
+    bar_sync<1, kIdxCompute>();
+    uint32_t *dst = a.idx + (base - shift);  // 16-byte aligned when vec_ok
+    const uint32_t end = total + shift;
+    if (vec_ok) {
+      for (uint32_t q = threadIdx.x; 4 * q < end; q += kIdxCompute) {
+        const uint32_t j = 4 * q;
+        if (j >= shift && j + 4 <= end) {
+          *reinterpret_cast<uint4 *>(dst + j) = *reinterpret_cast<const uint4 *>(&S.pos[j]);
+        } else {
+          for (uint32_t k = j; k < j + 4; k++)
+            if (k >= shift && k < end) dst[k] = S.pos[k];
+        }
+      }
+    } else {
+      for (uint32_t k = threadIdx.x; k < total; k += kIdxCompute) dst[k] = S.pos[k];
+    }
+    if (threadIdx.x == 0) JT_TL(ptile, 6);
+  };
+  // block until the look-back of pending tile `seq` is done
+  auto wait_done = [&](uint32_t seq) {
+    if (threadIdx.x == 0) {
+      JT_TL(S.slot[seq % kIdxRing].tile, 4);
+      while (S.done <= seq) __nanosleep(64);
+    }
+  };
+
+  uint32_t tile = S.claim;
+  uint32_t w[16];
+  if (tile < ntiles) {
+    const uint64_t blk = (uint64_t)tile * kStage1Tile + (uint64_t)threadIdx.x * 64;
+    ld256(a.in + blk, w);
+    ld256(a.in + blk + 32, w + 8);
+  }
+  uint32_t head = 0, tail = 0;  // pending tiles: sequence numbers [head, tail)
+  for (;;) {
+    if (tile >= ntiles) {
+      if (threadIdx.x == 0) {
+        S.end_seq = tail;
+        __threadfence_block();
+        S.ready = tail + 1;
+      }
+      while (head < tail) {
+        wait_done(head);
+        extract(head++);
+      }
+      return;
+    }
+    if (tail - head == kIdxRing) {  // ring full: the oldest must go first
+      wait_done(head);
+      extract(head++);
+    }
+    IdxSlot &R = S.slot[tail % kIdxRing];
+    const uint64_t blk = (uint64_t)tile * kStage1Tile + (uint64_t)threadIdx.x * 64;
+    if (threadIdx.x == 0) {
+      JT_TL(tile, 0);
+#ifdef JT_TIMELINE
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      JT_TLV(tile, 8, smid | ((uint64_t)blockIdx.x << 16));
+#endif
+    }
+    s1::Masks m;
+    s1::classify64(w, m);
+    const uint64_t esc0 = s1::escaped_no_carry(m.bs), tog = s1::carry_toggle(m.bs);
+    uint32_t inc = s1::block_function(m, esc0, tog);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc = s1::compose(inc, o);
+    }
+    const uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 31) S.wf[warp] = inc;
+    // UTF-8 validity (as K1)
+    uint32_t prev = __shfl_up_sync(0xffffffffu, w[15], 1);
+    if (lane == 0) prev = blk >= 4 ? *(const uint32_t *)(a.in + blk - 4) : 0u;
+    if ((m.P[7] | (uint64_t)(prev & 0x80808000u)) != 0 && blk < a.len + 3 &&
+        s1::utf8_block_error(m.P, prev, blk + 64 >= a.len)) {
+      const uint8_t *in = a.in;
+      const uint64_t len = a.len;
+      auto at = [in, len](uint64_t k) -> uint32_t { return k < len ? in[k] : 0u; };
+      uint64_t lo = blk >= 3 ? blk - 3 : 0, hi = blk + 64 < len ? blk + 64 : len;
+      for (uint64_t k = lo; k < hi; k++)
+        if (s1::utf8_flagged(at, k, len)) {
+          atomicMin(a.utf8_pos, (unsigned long long)k);
+          break;
+        }
+    }
+    const int64_t rem = (int64_t)a.len - (int64_t)blk;
+    const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
+    const uint64_t uq0 = m.qt & ~esc0, tq = m.qt & tog;
+    const uint64_t uq1 = uq0 ^ tq;
+    const uint64_t px0 = s1::prefix_xor(uq0), px1 = px0 ^ (0ULL - tq);
+    bar_sync<1, kIdxCompute>();
+    // G: tile entry -> this block's entry
+    uint32_t wf = lane < kWarps ? S.wf[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < kWarps; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, wf, d);
+      if (lane >= d) wf = s1::compose(wf, o);
+    }
+    const uint32_t tile_f = __shfl_sync(0xffffffffu, wf, kWarps - 1);
+    const uint32_t wpre = __shfl_sync(0xffffffffu, wf, warp > 0 ? warp - 1 : 0);
+    uint32_t G;
+    if (warp == 0)
+      G = lane == 0 ? 0x03020100u : excl;
+    else
+      G = lane == 0 ? wpre : s1::compose(excl, wpre);
+    uint64_t fin[4];
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+      fin[x] = idx_fin(m, uq0, uq1, px0, px1, (G >> (8 * x)) & 7u, valid);
+      R.fin[x][threadIdx.x] = fin[x];
+    }
+    uint32_t dsep = 0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+        dsep |= (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, (uint32_t)x | 4u, valid) ^ fin[x]) & 1) << x;
+    }
+    const uint64_t cnt = (uint64_t)popc64(fin[0]) | ((uint64_t)popc64(fin[1]) << 16) |
+                         ((uint64_t)popc64(fin[2]) << 32) | ((uint64_t)popc64(fin[3]) << 48);
+    uint64_t ci = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t o = __shfl_up_sync(0xffffffffu, ci, d);
+      if (lane >= d) ci += o;
+    }
+    if (lane == 31) S.wc[warp] = ci;
+    if (threadIdx.x == 0) {  // claimed late: claim order ~ aggregate order
+      S.claim = atomicAdd(a.tile_counter, 1u);
+      JT_TL(S.claim, 7);
+      S.snap = S.done;       // look-backs finished so far (extracted below)
+    }
+    bar_sync<1, kIdxCompute>();
+    const uint32_t next = S.claim;
+    const uint32_t snap = S.snap;
+    uint64_t wc = lane < kWarps ? S.wc[lane] : 0ULL;
+#pragma unroll
+    for (int d = 1; d < kWarps; d <<= 1) {
+      uint64_t o = __shfl_up_sync(0xffffffffu, wc, d);
+      if (lane >= d) wc += o;
+    }
+    const uint64_t cpre = warp > 0 ? __shfl_sync(0xffffffffu, wc, warp > 0 ? warp - 1 : 0) : 0ULL;
+    const uint64_t tile_c = __shfl_sync(0xffffffffu, wc, kWarps - 1);
+    R.off[threadIdx.x] = cpre + ci - cnt;
+    if (threadIdx.x == 0) {
+      // publish the aggregate, then hand the slot to the look-back warp
+      if (tile > 0) {
+        uint64_t *agg = a.rec_count;
         lb_store(agg + 2 * tile, kIdxValid | (tile_c & 0xFFFF) | ((uint64_t)tile_f << 16) |
-                                     ((uint64_t)d << 48));
+                                     ((uint64_t)dsep << 48));
         lb_store(agg + 2 * tile + 1, kIdxValid | (tile_c >> 16));
       }
-      idx_lookback(agg, incl, tile, state, base);
+      R.tc = tile_c;
+      R.tf = tile_f;
+      R.d = dsep;
+      R.tile = tile;
+      JT_TL(tile, 1);
+      __threadfence_block();
+      S.ready = tail + 1;
     }
-    if (lane == 0) {
-      const uint32_t x = state & 3, sep = (state >> 2) & (d >> x) & 1u;
-      const uint64_t out = base + ((tile_c >> (16 * x)) & 0xFFFF) + sep;
-      lb_store(incl + tile, kIdxValid | ((uint64_t)((tile_f >> (8 * x)) & 7u) << 48) | out);
-      if (tile == (int64_t)a.ntiles - 1) *a.total = out;
-      s_base = base;
-      s_sel = x | (sep << 2);
+    tail++;
+    // next tile's bytes in flight while resolved tiles are written out
+    if (next < ntiles) {
+      const uint64_t nb = (uint64_t)next * kStage1Tile + (uint64_t)threadIdx.x * 64;
+      ld256(a.in + nb, w);
+      ld256(a.in + nb + 32, w + 8);
     }
+    while (head < snap) extract(head++);
+    tile = next;
   }
-  __syncthreads();
-  const uint32_t sel = s_sel, x = sel & 3, sep = sel >> 2;
-  uint64_t f = x == 0 ? fin[0] : x == 1 ? fin[1] : x == 2 ? fin[2] : fin[3];
-  if (threadIdx.x == 0) f |= sep;
-  const uint32_t off = (uint32_t)((off4 >> (16 * x)) & 0xFFFF) + (threadIdx.x ? sep : 0u);
-  const uint32_t total = (uint32_t)((tile_c >> (16 * x)) & 0xFFFF) + sep;
-  const uint64_t base = s_base;
-  if (total > (uint32_t)kStageIdx) {  // CTA-uniform
-    uint32_t slot = off;
-    for (uint64_t fm = f; fm; fm &= fm - 1) a.idx[base + slot++] = (uint32_t)(blk + ctz64(fm));
-    return;
-  }
-  {
-    uint32_t slot = off;
-    for (uint64_t fm = f; fm; fm &= fm - 1) s_pos[slot++] = (uint16_t)(threadIdx.x * 64 + ctz64(fm));
-  }
-  __syncthreads();
-  uint32_t *dst = a.idx + base;
-  const uint32_t tb = (uint32_t)tile_base;
-  for (uint32_t k = threadIdx.x; k < total; k += kThreads) dst[k] = tb + s_pos[k];
 }
 
 // ---- jt_minify (capi.cpp:154-167, minify_pass indexer.cpp:58-75) -----------
@@ -1341,7 +1537,16 @@ cudaError_t stage1_chunk_launch(const Stage1Args &args_in, cudaStream_t stream) 
 
 cudaError_t index_launch(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  k_index<<<(unsigned)a.ntiles, kThreads, 0, stream>>>(a);
+  static const unsigned grid_max = [] {
+    int dev = 0, sms = 148, occ = kIdxMinBlocks;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_index, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(IdxSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_index, kIdxThreads, sizeof(IdxSmem));
+    return (unsigned)(sms * (occ > 0 ? occ : 1));
+  }();
+  const unsigned grid = a.ntiles < grid_max ? (unsigned)a.ntiles : grid_max;
+  k_index<<<grid, kIdxThreads, sizeof(IdxSmem), stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -97,3 +97,16 @@ def test_stage1_then_parse_interleaved(parser, oracle):
 def test_stage1_empty_and_whitespace(parser, oracle):
     for data in (b"", b" ", b"\n\t ", b"1", b'"', b"\\", b"\xff"):
         check_stage1(parser, oracle, data, repr(data))
+
+
+def test_stage1_many_tiles_per_cta(parser, oracle):
+    """documents with far more tiles than resident CTAs (the persistent
+    k_index loops over tiles, overlapping each tile's look-back with the
+    next tile), incl. tiles past the 4096-entry staging capacity"""
+    from tools.gen import generate
+    for cfg, size in ((1, 40 << 20), (4, 24 << 20), (2, 20 << 20), (0, 9 << 20)):
+        check_stage1(parser, oracle, generate(cfg, size, seed=11 + cfg), f"C{cfg} {size}")
+    dense = b"[" + b"1," * (4 << 20) + b"1]"
+    check_stage1(parser, oracle, dense, "dense")
+    mixed = b"[" + b",".join([b"1," * 3000 + b'"' + b"x" * 20000 + b'"'] * 300) + b"]"
+    check_stage1(parser, oracle, mixed, "mixed")
