@@ -1059,14 +1059,14 @@ struct IdxSlot {
   uint64_t off[kIdxCompute];     // 4 x 16-bit tile-relative slot per entry state
   unsigned long long tc;         // tile counts (4 x 16 bit)
   unsigned long long base;       // from the look-back warp
-  uint32_t tile, tf, d, sel;
+  uint32_t tile, tf, d, sel, two;
 };
 
 struct IdxSmem {
   IdxSlot slot[kIdxRing];
   unsigned long long wc[kWarps];
   uint32_t wf[kWarps];
-  uint32_t claim, snap;
+  uint32_t claim, snap, two;
   volatile uint32_t ready, done;  // sequence numbers
   volatile uint32_t end_seq;      // no tile at this sequence number: the CTA is done
   alignas(16) uint32_t pos[kStageIdx + 8];  // absolute positions, shifted to the output's 16-byte phase
@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
     const uint32_t sel = R.sel, x = sel & 3, sep = sel >> 2;
     const uint64_t base = R.base;
     const uint64_t tc = R.tc;
-    uint64_t f = R.fin[x][threadIdx.x];
+    uint64_t f = R.fin[R.two ? x : (x & 2)][threadIdx.x];
     if (threadIdx.x == 0) f |= sep;
     const uint32_t off = (uint32_t)((R.off[threadIdx.x] >> (16 * x)) & 0xFFFF) + (threadIdx.x ? sep : 0u);
     const uint32_t total = (uint32_t)((tc >> (16 * x)) & 0xFFFF) + sep;
@@ -1220,6 +1220,11 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
     }
     const uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
     if (lane == 31) S.wf[warp] = inc;
+    const uint64_t uq0 = m.qt & ~esc0, tq = m.qt & tog;
+    // the odd-backslash carry into the tile changes nothing unless block 0's
+    // first non-backslash byte is a quote (or block 0 is all backslashes):
+    // otherwise only the two in-string entry states are counted
+    if (threadIdx.x == 0) S.two = (tq != 0 || m.bs == ~0ULL) ? 1u : 0u;
     // UTF-8 validity (as K1)
     uint32_t prev = __shfl_up_sync(0xffffffffu, w[15], 1);
     if (lane == 0) prev = blk >= 4 ? *(const uint32_t *)(a.in + blk - 4) : 0u;
@@ -1237,10 +1242,10 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
     }
     const int64_t rem = (int64_t)a.len - (int64_t)blk;
     const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
-    const uint64_t uq0 = m.qt & ~esc0, tq = m.qt & tog;
     const uint64_t uq1 = uq0 ^ tq;
     const uint64_t px0 = s1::prefix_xor(uq0), px1 = px0 ^ (0ULL - tq);
     bar_sync<1, kIdxCompute>();
+    const bool four = S.two != 0;  // CTA-uniform
     // G: tile entry -> this block's entry
     uint32_t wf = lane < kWarps ? S.wf[lane] : 0u;
 #pragma unroll
@@ -1255,20 +1260,29 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
       G = lane == 0 ? 0x03020100u : excl;
     else
       G = lane == 0 ? wpre : s1::compose(excl, wpre);
-    uint64_t fin[4];
-#pragma unroll
-    for (int x = 0; x < 4; x++) {
-      fin[x] = idx_fin(m, uq0, uq1, px0, px1, (G >> (8 * x)) & 7u, valid);
-      R.fin[x][threadIdx.x] = fin[x];
+    const uint64_t fin0 = idx_fin(m, uq0, uq1, px0, px1, G & 7u, valid);
+    const uint64_t fin2 = idx_fin(m, uq0, uq1, px0, px1, (G >> 16) & 7u, valid);
+    R.fin[0][threadIdx.x] = fin0;
+    R.fin[2][threadIdx.x] = fin2;
+    uint64_t fin1 = fin0, fin3 = fin2;
+    uint32_t c1 = popc64(fin0), c3 = popc64(fin2);
+    const uint32_t c0 = c1, c2 = c3;
+    if (four) {
+      fin1 = idx_fin(m, uq0, uq1, px0, px1, (G >> 8) & 7u, valid);
+      fin3 = idx_fin(m, uq0, uq1, px0, px1, (G >> 24) & 7u, valid);
+      R.fin[1][threadIdx.x] = fin1;
+      R.fin[3][threadIdx.x] = fin3;
+      c1 = popc64(fin1);
+      c3 = popc64(fin3);
     }
     uint32_t dsep = 0;
     if (threadIdx.x == 0) {
-#pragma unroll
-      for (int x = 0; x < 4; x++)
-        dsep |= (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, (uint32_t)x | 4u, valid) ^ fin[x]) & 1) << x;
+      dsep = (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 4u, valid) ^ fin0) & 1) |
+             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 5u, valid) ^ fin1) & 1) << 1) |
+             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 6u, valid) ^ fin2) & 1) << 2) |
+             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 7u, valid) ^ fin3) & 1) << 3);
     }
-    const uint64_t cnt = (uint64_t)popc64(fin[0]) | ((uint64_t)popc64(fin[1]) << 16) |
-                         ((uint64_t)popc64(fin[2]) << 32) | ((uint64_t)popc64(fin[3]) << 48);
+    const uint64_t cnt = (uint64_t)c0 | ((uint64_t)c1 << 16) | ((uint64_t)c2 << 32) | ((uint64_t)c3 << 48);
     uint64_t ci = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1304,6 +1318,7 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
       R.tc = tile_c;
       R.tf = tile_f;
       R.d = dsep;
+      R.two = four ? 1u : 0u;
       R.tile = tile;
       JT_TL(tile, 1);
       __threadfence_block();
