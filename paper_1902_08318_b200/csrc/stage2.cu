@@ -697,6 +697,157 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
   return psv(a, T.base, L);
 }
 
+// Token-parallel grammar check for one document no deeper than 64 (the
+// scope bits are exact): the state in which token i arrives follows from the
+// two tokens before it and their innermost containers' kinds (SURVEY.md
+// App. A.5; the goto machine of tape_builder.cpp:140-258 restated as
+// adjacent-token transitions), so every token is checked on its own.  A
+// closer finds its opener as the previous token with depth_before <= D - 1
+// (psv) and writes both bracket words.  Errors: atomicMin of (token, code);
+// only the first one is reported, so checks of tokens after an error (whose
+// arrival state assumed a valid prefix) are harmless.
+__device__ __forceinline__ bool scope_bit(const Stage2Args &a, uint64_t j) {
+  return (a.scopebits[j >> 5] >> (j & 31)) & 1;
+}
+
+// token classes and the transition table of struct_tokens
+enum : uint32_t { C_OBR = 0, C_ABR, C_OCL, C_ACL, C_COM, C_COL, C_STR, C_ATOM, C_NUM, C_BAD, kNCls };
+__device__ __forceinline__ uint32_t token_class(uint32_t c) {
+  switch (c) {
+    case '{': return C_OBR;
+    case '[': return C_ABR;
+    case '}': return C_OCL;
+    case ']': return C_ACL;
+    case ',': return C_COM;
+    case ':': return C_COL;
+    case '"': return C_STR;
+    case 't': case 'f': case 'n': return C_ATOM;
+    default: return (c == '-' || (c - '0') < 10u) ? C_NUM : C_BAD;
+  }
+}
+// entry for (arrival state, class): bits 0-2 error, 3-5 error when the token
+// failed its own parse, 6-8 state after, 9 closes a container, 10 opens one
+// (depth check), 11 comma after a value (next state from the scope bit),
+// 12 closer after a value (kind from the scope bit)
+constexpr uint32_t kTrClose = 1u << 9, kTrOpen = 1u << 10, kTrComma = 1u << 11, kTrKind = 1u << 12;
+__host__ __device__ constexpr uint32_t tr_entry(int mode, uint32_t cl) {
+  // value position (M_V, and M_AF / M_OF fall-throughs)
+  return (mode == M_OF && cl == C_OCL) || (mode == M_AF && cl == C_ACL)
+             ? (kTrClose | (M_A << 6))
+         : (mode == M_V || mode == M_AF)
+             ? (cl == C_OBR ? (kTrOpen | (M_OF << 6))
+                : cl == C_ABR ? (kTrOpen | (M_AF << 6))
+                : cl == C_STR ? ((kStringError << 3) | (M_A << 6))
+                : cl == C_ATOM ? ((kTapeError << 3) | (M_A << 6))
+                : cl == C_NUM ? ((kNumberError << 3) | (M_A << 6))
+                              : (kTapeError | (kTapeError << 3)))
+         : (mode == M_K || mode == M_OF)
+             ? (cl == C_STR ? ((kStringError << 3) | (M_C << 6)) : (kTapeError | (kTapeError << 3)))
+         : mode == M_C ? (cl == C_COL ? (M_V << 6) : (kTapeError | (kTapeError << 3)))
+                       // M_A
+                       : (cl == C_COM ? kTrComma
+                          : (cl == C_OCL || cl == C_ACL) ? (kTrClose | kTrKind | (M_A << 6))
+                                                         : (kTapeError | (kTapeError << 3)));
+}
+
+// state in which a token arrives after a token of class cl1 whose innermost
+// container is an object (sc1); a key string (M_C) is decided by the caller
+__host__ __device__ constexpr int arrival_state(uint32_t cl1, uint32_t sc1) {
+  return cl1 == C_OBR ? M_OF : cl1 == C_ABR ? M_AF : cl1 == C_COL ? M_V : cl1 == C_COM ? (sc1 ? M_K : M_V) : M_A;
+}
+
+template <class Tree>
+__device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, uint64_t S, const Tree &T,
+                                              uint64_t tbase, uint64_t tend, const uint16_t *s_tr,
+                                              const uint8_t *s_cls, const uint8_t *s_arr) {
+  const int lane = threadIdx.x & 31;
+  auto rec = [&](uint64_t j) -> uint32_t { return j >= tbase ? T.tok[j - tbase] : a.tok[j]; };
+  // one warp per 32 consecutive tokens (lane = token), so the two previous
+  // tokens, the scope bits and most bracket partners are a shuffle away
+  for (uint64_t cb = tbase + 32 * (threadIdx.x >> 5); cb < tend; cb += blockDim.x) {
+    const uint64_t i = cb + lane;
+    const bool live = i < tend;
+    const uint32_t v = live ? T.tok[i - tbase] : (uint32_t)'x';
+    const uint32_t c = v & 0xFF;
+    const uint32_t cl = s_cls[c];
+    const bool fail = (v >> 8) & 1;
+    const int D = tok_depth(v);
+    const uint32_t sw = a.scopebits[cb >> 5];             // bit l: token cb + l in an object
+    const uint32_t swp = cb ? a.scopebits[(cb >> 5) - 1] : 0u;
+    const uint64_t sw2 = ((uint64_t)sw << 32) | swp;     // bit 32 + l - k: token i - k
+    const uint32_t sc0 = (sw >> lane) & 1, sc1 = (uint32_t)(sw2 >> (31 + lane)) & 1,
+                   sc2 = (uint32_t)(sw2 >> (30 + lane)) & 1;
+    uint32_t cl1 = __shfl_up_sync(0xffffffffu, cl, 1), cl2 = __shfl_up_sync(0xffffffffu, cl, 2);
+    if (lane < 2) {
+      if (lane == 0) cl1 = i >= 1 ? s_cls[rec(i - 1) & 0xFF] : C_BAD;
+      cl2 = i >= 2 ? s_cls[rec(i - 2) & 0xFF] : C_BAD;
+    }
+    const uint32_t ti = live ? a.tape_idx[i] : 0u;
+    // arrival state from the two previous tokens (App. A.5)
+    const bool key1 = cl1 == C_STR && (cl2 == C_OBR || (cl2 == C_COM && sc2));  // i-1 was a key
+    int mode = key1 ? M_C : (int)s_arr[2 * cl1 + sc1];
+    if (i == 0) mode = M_V;
+    const uint32_t e = s_tr[mode * kNCls + cl];
+    int err = (int)((fail ? e >> 3 : e) & 7);
+    if ((e & kTrOpen) && D >= kMaxDepth && !err) err = kDepthError;
+    if (mode == M_A && D <= 0) err = kTapeError;
+    if ((e & kTrKind) && sc0 != (cl == C_OCL ? 1u : 0u)) err = kTapeError;
+    const int after = (e & kTrComma) ? (sc0 ? M_K : M_V) : (int)((e >> 6) & 7);
+    // bracket partners: the opener is the previous token with depth <= D - 1;
+    // inside the warp by ballots (one per distinct depth), else the tile tree
+    const bool need = live && (e & kTrClose) && !err;
+    int64_t j = -1;
+    uint32_t pending = __ballot_sync(0xffffffffu, need);
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const int L = __shfl_sync(0xffffffffu, D - 1, leader);
+      const uint32_t m = __ballot_sync(0xffffffffu, live && D <= L);
+      const bool mine = need && D - 1 == L;
+      if (mine) {
+        const uint32_t below = m & ((1u << lane) - 1u);
+        j = below ? (int64_t)(cb + 31 - __clz(below)) : -2;  // -2: before this warp
+      }
+      pending &= ~__ballot_sync(0xffffffffu, mine);
+    }
+    const int src = j >= 0 ? (int)(j - cb) : lane;
+    const uint32_t tj_w = __shfl_sync(0xffffffffu, ti, src);
+    // openers before this warp's tokens: the previous chunks of the tile by
+    // ballots as well (up to 8), then the tile tree
+    uint64_t pb = cb;
+    for (int step = 0; step < 8; step++) {
+      uint32_t rem = __ballot_sync(0xffffffffu, need && j == -2);
+      if (!rem || pb == tbase) break;
+      pb -= 32;
+      const int dl = tok_depth(T.tok[pb - tbase + lane]);
+      while (rem) {
+        const int leader = __ffs(rem) - 1;
+        const int L = __shfl_sync(0xffffffffu, D - 1, leader);
+        const uint32_t m = __ballot_sync(0xffffffffu, dl <= L);
+        const bool mine = need && j == -2 && D - 1 == L;
+        if (mine && m) j = (int64_t)(pb + 31 - __clz(m));
+        rem &= ~__ballot_sync(0xffffffffu, mine);
+      }
+    }
+    if (need) {
+      uint32_t tj = tj_w;
+      if (j == -2) j = psv_tile_masked(a, T, (int64_t)pb, D - 1);
+      if (j >= 0 && (j < (int64_t)cb)) tj = a.tape_idx[j];
+      if (j < 0) {
+        err = kTapeError;
+      } else {
+        a.tape[ti] = tape_word((uint8_t)c, tj);
+        a.tape[tj] = tape_word(cl == C_OCL ? '{' : '[', ti + 1);
+      }
+    }
+    if (err && live) {
+      report(ctrl, i, err);
+    } else if (live && i == S - 1) {  // the root value must be complete
+      const int depth_after = D + (cl <= C_ABR ? 1 : cl <= C_ACL ? -1 : 0);
+      if (!(after == M_A && depth_after == 0)) report(ctrl, S, kTapeError);
+    }
+  }
+}
+
 // kMode: 0 one document, 1 a byte-range shard (shard.h), 2 NDJSON records.
 // kDeep: the instance for documents deeper than 64 (masked tree search); for
 // one document both instances are launched and the other one returns.
@@ -706,12 +857,22 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   __shared__ __align__(16) uint32_t s_tok[kK3Tile];
   __shared__ __align__(16) int16_t s_l1[256];
   __shared__ __align__(16) int16_t s_l2[16];
+  __shared__ uint16_t s_tr[6 * kNCls];
+  __shared__ uint8_t s_cls[256];
+  __shared__ uint8_t s_arr[2 * kNCls];
+  if (kMode == 0) {
+    s_cls[threadIdx.x] = (uint8_t)token_class(threadIdx.x);
+    if (threadIdx.x < 2 * kNCls) s_arr[threadIdx.x] = (uint8_t)arrival_state(threadIdx.x >> 1, threadIdx.x & 1);
+    if (threadIdx.x < 6 * kNCls) s_tr[threadIdx.x] = (uint16_t)tr_entry(threadIdx.x / kNCls, threadIdx.x % kNCls);
+    __syncthreads();
+  }
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = ctrl->S;
   const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
   const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
   const bool deep = !shallow;
+
   // this shard's place in the document, as scalars (a View captured by the
   // lambdas below would live in local memory)
   // (tape indices fit 32 bits: tape_idx is u32)
@@ -794,6 +955,11 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     }
     __syncthreads();
     const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase};
+    if (kMode == 0 && shallow) {  // token-parallel grammar check
+      struct_tokens(a, ctrl, S, T, tbase, min(tbase + kK3Tile, S), s_tr, s_cls, s_arr);
+      __syncthreads();
+      continue;
+    }
     const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
     const uint64_t i1 = min(i0 + kK3Tok, S);
     if (i0 < S) do {
