@@ -11,6 +11,10 @@
 // There is no CPU fallback: without a CUDA device jt_parser_new returns NULL
 // and nothing else can be called.
 #include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -131,10 +135,19 @@ struct jt_document {
   void *block = nullptr;
   size_t block_cap = 0;
   bool pinned = false;
+  // streamed jt_parse: the string buffer has its own block (sized before
+  // the parse knows it), the tape the first one
+  void *sblock = nullptr;
+  size_t sblock_cap = 0;
+  bool spinned = false;
+  static void release(void *b, size_t cap, bool pin) {
+    if (!b) return;
+    if (pin) PinnedPool::get().give(b, cap);
+    else free(b);
+  }
   ~jt_document() {
-    if (!block) return;
-    if (pinned) PinnedPool::get().give(block, block_cap);
-    else free(block);
+    release(block, block_cap, pinned);
+    release(sblock, sblock_cap, spinned);
   }
   bool alloc(size_t words, size_t bytes) {
     const size_t tb = (words * 8 + 63) & ~(size_t)63;
@@ -142,6 +155,19 @@ struct jt_document {
     if (!block) return false;
     tape = Span<uint64_t>{(uint64_t *)block, words};
     strings = Span<uint8_t>{(uint8_t *)block + tb, bytes};
+    return true;
+  }
+  // string buffer of up to `cap` bytes (its size is set once known)
+  bool alloc_strings(size_t cap) {
+    sblock = PinnedPool::get().take(cap + 64, &sblock_cap, &spinned);
+    if (!sblock) return false;
+    strings = Span<uint8_t>{(uint8_t *)sblock, 0};
+    return true;
+  }
+  bool alloc_tape(size_t words) {
+    block = PinnedPool::get().take(words * 8 + 64, &block_cap, &pinned);
+    if (!block) return false;
+    tape = Span<uint64_t>{(uint64_t *)block, words};
     return true;
   }
 };
@@ -192,7 +218,11 @@ struct jt_parser {
   // streamed jt_parse (parse_stream): copy stream, per-chunk events, chunk
   // tile counters and carry states, stage-1 control block snapshot
   cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> chunk_ev;
+  cudaStream_t d2h_stream = nullptr;  // string pieces back while the input goes up
+  std::vector<cudaEvent_t> chunk_ev, piece_ev;
+  cudaEvent_t ev_d2h = nullptr;
+  uint64_t *h_piece_sb = nullptr;     // pinned, host-mapped: string bytes up to each piece's end
+  uint64_t h_piece_cap = 0;
   cudaEvent_t ev_start = nullptr, ev_s1 = nullptr;
   DevBuf stream_words;
   jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
@@ -507,16 +537,43 @@ bool ensure_stream(jt_parser *p, uint64_t nch) {
   auto mk = [](cudaEvent_t *e) {
     return *e || cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   };
-  if (!mk(&p->ev_start) || !mk(&p->ev_s1)) return false;
+  if (!mk(&p->ev_start) || !mk(&p->ev_s1) || !mk(&p->ev_d2h)) return false;
   while (p->chunk_ev.size() < nch) {
     cudaEvent_t e = nullptr;
     if (!mk(&e)) return false;
     p->chunk_ev.push_back(e);
   }
+  while (p->piece_ev.size() < nch) {
+    cudaEvent_t e = nullptr;
+    if (!mk(&e)) return false;
+    p->piece_ev.push_back(e);
+  }
+  if (!p->d2h_stream &&
+      cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    p->d2h_stream = nullptr;
+    return false;
+  }
+  if (p->h_piece_cap < nch) {
+    if (p->h_piece_sb) cudaFreeHost(p->h_piece_sb);
+    p->h_piece_sb = nullptr;
+    p->h_piece_cap = 0;
+    if (cudaMallocHost((void **)&p->h_piece_sb, nch * sizeof(uint64_t)) != cudaSuccess) {
+      cudaGetLastError();
+      p->h_piece_sb = nullptr;
+      return false;
+    }
+    p->h_piece_cap = nch;
+  }
   return p->stream_words.ensure(nch * 2 * sizeof(uint32_t) + 64);  // tile counters + carry states
 }
 
 jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
+  static const bool trace = getenv("JT_TRACE") != nullptr;
+  auto now_us = []() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = trace ? now_us() : 0;
   if (out) *out = nullptr;
   const int which = p->cur ^ 1;
   const uint64_t nch = (len + kStreamChunk - 1) / kStreamChunk;
@@ -558,12 +615,53 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     a.tile_counter = counters + c;
     a.init_state = c ? states + c - 1 : nullptr;
     a.out_state = states + c;
+    a.sb_out = p->h_piece_sb + c;
     ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
-         cuda_ok(p, jt::stage1_chunk_launch(a, p->stream), "stage1 chunk");
+         cuda_ok(p, jt::stage1_chunk_launch(a, p->stream), "stage1 chunk") &&
+         cuda_ok(p, cudaEventRecord(p->piece_ev[c], p->stream), "event");
     p->launches += jt::kStage1Launches;
   }
-  ok = ok && cuda_ok(p, jt::stage1_lengths_launch(s1_args(p, len, which, 0, len, ntiles), ntiles, p->stream),
-                     "lengths") &&
+  if (trace) fprintf(stderr, " enqueued %.0f us\n", now_us() - t0);
+  // the string bytes of each piece go back as soon as its stage 1 is done,
+  // while later pieces are still uploading (the copy engines run both
+  // directions at once); the string-buffer size is not known yet, so the
+  // host block is sized for 5/4 of the input and the rare document with a
+  // larger buffer is fetched whole after stage 1
+  jt_document *d = nullptr;
+  bool early = false;
+  uint64_t sb_done = 0;
+  if (ok && out) {
+    d = new (std::nothrow) jt_document;
+    early = d && d->alloc_strings(len + len / 4 + 64);
+    for (uint64_t c = 0; early && c < nch; c++) {
+      if (!cuda_ok(p, cudaEventSynchronize(p->piece_ev[c]), "sync")) {
+        early = false;
+        break;
+      }
+      if (trace && (c < 2 || c + 2 >= nch || c % 4 == 0)) fprintf(stderr, " piece %d done %.0f us\n", (int)c, now_us() - t0);
+      const uint64_t e = p->h_piece_sb[c];
+      if (e > d->sblock_cap - 64 || e < sb_done) {  // too large: fetched whole below
+        early = false;
+        break;
+      }
+      if (e > sb_done &&
+          !cuda_ok(p, cudaMemcpyAsync(d->strings.p + sb_done, p->strings.as<uint8_t>() + sb_done, e - sb_done,
+                                      cudaMemcpyDeviceToHost, p->d2h_stream),
+                   "strings piece D2H")) {
+        early = false;
+        break;
+      }
+      sb_done = e;
+    }
+    // length fields left to k_tile_lengths are patched into the host copy
+    // too, after the last piece is down
+    ok = cuda_ok(p, cudaEventRecord(p->ev_d2h, p->d2h_stream), "event") &&
+         cuda_ok(p, cudaStreamWaitEvent(p->stream, p->ev_d2h, 0), "wait");
+  }
+  const double t2 = trace ? now_us() : 0;
+  jt::Stage1Args la = s1_args(p, len, which, 0, len, ntiles);
+  if (early) la.strings_host = d->strings.p;
+  ok = ok && cuda_ok(p, jt::stage1_lengths_launch(la, ntiles, p->stream), "lengths") &&
        cuda_ok(p, cudaMemcpyAsync(p->h_ctrl_s1, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
                                   p->stream),
                "ctrl D2H") &&
@@ -578,13 +676,27 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_s1), "sync")) {
     cudaStreamSynchronize(p->stream);
     cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(p->d2h_stream);
+    delete d;
     set_off(off, -1);
     return JT_CAPACITY;
   }
-  // stage 1 is done: the string buffer is final; fetch it while stage 2 runs
-  jt_document *d = nullptr;
+  const double t3 = trace ? now_us() : 0;
+  // stage 1 is done: the string buffer is final (and, if it came back piece
+  // by piece, already on the host); otherwise fetch it while stage 2 runs
   const jt::Ctrl c1 = *p->h_ctrl_s1;
-  if (out && c1.utf8_pos == ~0ULL) {
+  if (d && (!early || (c1.utf8_pos == ~0ULL && sb_done != c1.string_bytes))) {
+    delete d;  // not (completely) fetched piece by piece: the whole buffer below
+    d = nullptr;
+    early = false;
+  }
+  if (out && c1.utf8_pos == ~0ULL && d && early) {
+    d->strings.n = c1.string_bytes;
+    if (!d->alloc_tape(c1.tape_words + 1)) {
+      delete d;
+      d = nullptr;
+    }
+  } else if (out && c1.utf8_pos == ~0ULL) {
     d = new (std::nothrow) jt_document;
     if (d && !d->alloc(c1.tape_words + 1, c1.string_bytes)) {
       delete d;
@@ -600,6 +712,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   }
   jt_error e = finish(p, which, true, off);  // waits for stage 2
   cudaStreamSynchronize(cs);
+  const double t4 = trace ? now_us() : 0;
   if (e != JT_OK || !out) {
     delete d;
     return e;
@@ -615,6 +728,9 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   }
   p->in_len = len;
   *out = d;
+  if (trace)
+    fprintf(stderr, "parse_stream: pieces+D2H enqueued %.0f us, stage 1 done %.0f, stage 2 done %.0f, tape down %.0f (early %d)\n",
+            t2 - t0, t3 - t0, t4 - t0, now_us() - t0, (int)early);
   return e;
 }
 
@@ -686,6 +802,13 @@ void jt_parser_free(jt_parser *p) {
     cudaStreamSynchronize(p->copy_stream);
     cudaStreamDestroy(p->copy_stream);
   }
+  if (p->d2h_stream) {
+    cudaStreamSynchronize(p->d2h_stream);
+    cudaStreamDestroy(p->d2h_stream);
+  }
+  for (cudaEvent_t e : p->piece_ev) cudaEventDestroy(e);
+  if (p->ev_d2h) cudaEventDestroy(p->ev_d2h);
+  if (p->h_piece_sb) cudaFreeHost(p->h_piece_sb);
   for (cudaEvent_t e : p->chunk_ev) cudaEventDestroy(e);
   if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->ev_s1) cudaEventDestroy(p->ev_s1);

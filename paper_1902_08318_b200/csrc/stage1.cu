@@ -628,6 +628,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       s_sbase = base.v[1];
       s_tbase = base.v[2];
       s_dbase = kRec ? seg_value(base.v[3]) : sext63(base.v[3]);
+      if (a.sb_out && tile == (int64_t)a.ntiles - 1) *a.sb_out = inc.v[1];  // host-mapped
       if (gt == last_tile) {
         *a.total = inc.v[0];
         *a.total_strings = inc.v[1];
@@ -1531,6 +1532,13 @@ __global__ void k_tile_lengths(Stage1Args a, uint64_t ntiles) {
     f[1] = (uint8_t)(len >> 8);
     f[2] = (uint8_t)(len >> 16);
     f[3] = (uint8_t)(len >> 24);
+    if (a.strings_host) {  // the host copy already holds the rest of the buffer
+      uint8_t *h = a.strings_host + so;
+      h[0] = (uint8_t)len;
+      h[1] = (uint8_t)(len >> 8);
+      h[2] = (uint8_t)(len >> 16);
+      h[3] = (uint8_t)(len >> 24);
+    }
   }
 }
 

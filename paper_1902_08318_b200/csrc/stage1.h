@@ -41,6 +41,11 @@ struct Stage1Args {
   uint64_t last_tile;
   const uint32_t *init_state;     // carry state before the range (nullptr = initial)
   uint32_t *out_state;            // carry state after the range (optional)
+  // streamed jt_parse: string-buffer bytes up to the end of the range,
+  // written to host-mapped memory by the range's last tile (optional), and
+  // the host copy of the string buffer that k_tile_lengths also patches
+  uint64_t *sb_out;
+  uint8_t *strings_host;
   // record (NDJSON) mode: '\n'-separated records parsed independently
   bool records;
   uint32_t *nl_count, *nl_base;   // per tile: newlines, newlines before it (K0)
