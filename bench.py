@@ -42,6 +42,7 @@ METRIC = "JSON parsed GB/s (stage1 & full tape) at 1/2/4/8 B200; % of HBM roofli
 WORKLOAD = ("C1: 64 MiB single document, pretty-printed (2-space, LF), random tree "
             "branching 1-10 depth<=8, 30% non-ASCII string chars, 10% strings with escapes")
 CONFIG = 1
+PROFILE = "r01b_ncu_full_c1.json"  # ncu --set full capture of the current kernels (traffic)
 SIZE = 64 << 20
 
 
@@ -510,15 +511,16 @@ def main():
     ach = kern_bytes[dom] / (kt[dom] / 1e3) / 1e9
     # DRAM traffic of the dominant kernel per launch, from the committed
     # `ncu --set full` capture of this workload (profiles/), when it matches
-    traffic, traffic_src = None, None
+    traffic, traffic_src, alu_pct = None, None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_c1.json")) as f:
+        with open(os.path.join(ROOT, "profiles", PROFILE)) as f:
             prof = json.load(f)
         kname = {"stage1": "k_stage1<0>", "tokens": "k_scalars", "struct": "k_struct<0, 0>"}[dom]
         e = next(v for k, v in prof.items() if k.endswith(kname))
         if args.config == CONFIG and not args.size:
             traffic = (float(e["dram__bytes_read.sum"]) + float(e["dram__bytes_write.sum"])) * 1e6
-            traffic_src = f"profiles/r01_ncu_full_c1.json {kname} dram read+write per launch"
+            traffic_src = f"profiles/{PROFILE} {kname} dram read+write per launch"
+        alu_pct = float(e["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"])
     except Exception:
         pass
 
@@ -580,9 +582,12 @@ def main():
             "kernel_ms": kt,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes": kern_bytes[dom], "peak_source": peak_src},
+                         "algorithmic_bytes": kern_bytes[dom], "peak_source": peak_src,
+                         # the integer ALU pipe (LOP3/SHF/IADD3/PRMT, 16 lanes per SMSP
+                         # per clock) is what binds these kernels, not HBM
+                         "alu_pipe_pct_of_peak": alu_pct},
             "roofline_stage1": {"achieved": B1 / (s1i / 1e3) / 1e9, "frac": B1 / (s1i / 1e3) / 1e9 / peak,
-                                "bytes": B1, "path": "jt_stage1 (k_carry_fn, k_carry_scan, k_index)"},
+                                "bytes": B1, "path": "jt_stage1 (k_init, k_index, k_stage1_final)"},
             "roofline_full": {"achieved": B2 / (tot_ms / args.steps / 1e3) / 1e9,
                               "frac": B2 / (tot_ms / args.steps / 1e3) / 1e9 / peak, "bytes": B2},
             "cpu_baseline": cpu,
