@@ -29,16 +29,19 @@ JT_HD void transpose32(const uint32_t w[8], uint32_t p[8]) {
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int m = 0; m < 4; m++) {
+    // t and t << k never overlap in a delta swap, so t ^ (t << k) = t * (1 + 2^k):
+    // the multiply goes to the FMA pipe, which the rest of stage 1 leaves idle
+    // (the ALU pipe, LOP3/SHF, is what binds these kernels)
     uint32_t a = w[2 * m], b = w[2 * m + 1], t;
     t = (a ^ (a >> 7)) & 0x00AA00AAu;
-    a = a ^ t ^ (t << 7);
+    a ^= t * 129u;
     t = (b ^ (b >> 7)) & 0x00AA00AAu;
-    b = b ^ t ^ (t << 7);
+    b ^= t * 129u;
     t = (a ^ (a >> 14)) & 0x0000CCCCu;
-    a = a ^ t ^ (t << 14);
+    a ^= t * 16385u;
     t = (b ^ (b >> 14)) & 0x0000CCCCu;
-    b = b ^ t ^ (t << 14);
-    t = (a ^ (b << 4)) & 0xF0F0F0F0u;
+    b ^= t * 16385u;
+    t = (a ^ (b * 16u)) & 0xF0F0F0F0u;
     a ^= t;
     b ^= t >> 4;
     lo[m] = a;  // byte p (0..3): plane p bits of bytes 8m..8m+7
