@@ -403,6 +403,79 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
         dist.destroy_process_group()
 
 
+def run_select(args, rank: int, world: int, local: int, torch, dist):
+    """Parse + select (the paper's parse-then-query use):
+    distinct_values at a key path that occurs in the document.  Device:
+    resident parse + jt_b200_distinct (selection on the GPU, values and string
+    bytes gathered, host sort of the selected values); the same text as
+    jt_document_distinct on the downloaded document (checked).  CPU baseline:
+    the reference's jt_parse + jt_document_distinct on one core.  Every rank
+    runs its own replica (no collective)."""
+    import re
+    from paper_1902_08318_b200 import Parser
+    from tools.gen import generate
+    size = args.size or (SIZE if args.config == CONFIG else None)
+    data = generate(args.config, size)
+    n = len(data)
+    keys = [m.group(1) for m in re.finditer(rb'"([^"\\.]{1,24})"\s*:', data[:1 << 20])]
+    path = keys[0] if keys else b"a"
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    p = Parser()
+    p.set_stream(stream.cuda_stream)
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    p.copy_in(host.data_ptr(), n)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    assert p.parse_resident(n).name == "OK"
+    want = p.download().distinct(path)
+    assert p.distinct(path) == want
+    for _ in range(args.warmup):
+        p.parse_resident(n)
+        p.distinct(path)
+    if dist:
+        dist.barrier()
+    ts = []
+    with ClockSampler(local) as clk:
+        clk.wait_first()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = p.parse_resident(n)
+            out = p.distinct(path)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+            assert r.name == "OK" and out == want
+    tot_ms = max_over_ranks(sum(ts) * 1e3, dist, "cuda")
+    value = job_throughput(n, args.steps, world, tot_ms)
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            try:
+                from oracle.pyoracle import Reference
+                ref = Reference()
+                best = None
+                for _ in range(2):
+                    t0 = time.perf_counter()
+                    got = ref.distinct(data, [path])
+                    dt = time.perf_counter() - t0
+                    best = dt if best is None else min(best, dt)
+                assert got is not None and got[0] == want
+                cpu = {"value": n / best / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                       "sample": "full document, reference jt_parse + jt_document_distinct, best of 2, 1 thread"}
+            except Exception as e:
+                cpu = {"unavailable": e.__class__.__name__}
+        print(json.dumps({
+            "metric": "JSON parse + select (distinct_values) GB/s", "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"config {args.config} + distinct_values at path {path.decode('utf-8', 'replace')!r}",
+                       "bytes": n, "distinct_values": want.count(b"\n"),
+                       "timing": "host wall clock around resident parse + jt_b200_distinct (synchronous)",
+                       "l2": "flushed before every step"},
+            "cpu_baseline": cpu, "clocks": clk.summary()}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,6 +486,8 @@ def main():
     ap.add_argument("--size", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="byte-range shard path even at N = 1")
+    ap.add_argument("--select", action="store_true",
+                    help="parse + select: distinct_values at a key path (SURVEY.md §8f rank 4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -429,6 +504,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.select:
+        return run_select(args, rank, world, local, torch, dist)
     if args.config == 3:
         return run_records(args, rank, world, local, torch, dist)
     if world > 1 or args.shard:

@@ -111,6 +111,13 @@ int jt_b200_device(const jt_parser *p);
 /* Last CUDA error string seen by the parser ("" if none). */
 const char *jt_b200_last_error(const jt_parser *p);
 
+/* distinct_values over the last successful parse, on the device ("parse +
+ * select"; document.cpp:134-192): the same text as
+ * jt_document_distinct on the downloaded document (sorted distinct scalars at
+ * a dotted key path, one per line).  Free with jt_string_free; NULL without a
+ * successful parse or on a device error. */
+char *jt_b200_distinct(jt_parser *p, const char *path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@
 // There is no CPU fallback: without a CUDA device jt_parser_new returns NULL
 // and nothing else can be called.
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 
 #include <chrono>
 #include <cstdio>
@@ -225,6 +226,7 @@ struct jt_parser {
   uint64_t h_piece_cap = 0;
   cudaEvent_t ev_start = nullptr, ev_s1 = nullptr;
   DevBuf stream_words;
+  DevBuf qbuf, qstr;  // distinct_values query: keys, matches, values, lengths, offsets, scan | strings
   jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
@@ -1015,6 +1017,67 @@ char *jt_document_dump(const jt_document *doc) {
   return s;
 }
 
+}  // extern "C"
+
+namespace {
+
+// (kind, bits, bytes) ordered as scalar_value (document.h:71-90)
+struct DVal {
+  int k;
+  uint64_t bits;
+  std::string bytes;
+  bool operator<(const DVal &o) const {
+    if (k != o.k) return k < o.k;
+    return k == 5 ? bytes < o.bytes : bits < o.bits;
+  }
+};
+
+// one value per line, as the reference prints scalar_value (document.cpp:108-131)
+std::string format_distinct(const std::set<DVal> &vals) {
+  std::string out;
+  char buf[64];
+  for (const DVal &v : vals) {
+    switch (v.k) {
+      case 0: out += "null"; break;
+      case 1: out += "false"; break;
+      case 2: out += "true"; break;
+      case 3: out.append(buf, std::to_chars(buf, buf + sizeof(buf), (int64_t)v.bits).ptr); break;
+      case 4: {
+        double d;
+        memcpy(&d, &v.bits, 8);
+        out.append(buf, std::to_chars(buf, buf + sizeof(buf), d).ptr);
+        break;
+      }
+      default: out += '"' + v.bytes + '"';
+    }
+    out += '\n';
+  }
+  return out;
+}
+
+char *malloc_string(const std::string &out) {
+  char *r = (char *)malloc(out.size() + 1);
+  if (!r) return nullptr;
+  memcpy(r, out.data(), out.size());
+  r[out.size()] = 0;
+  return r;
+}
+
+std::vector<std::string> split_path(const char *path) {
+  std::vector<std::string> keys;
+  for (const char *a = path;;) {
+    const char *dot = strchr(a, '.');
+    keys.emplace_back(a, dot ? (size_t)(dot - a) : strlen(a));
+    if (!dot) break;
+    a = dot + 1;
+  }
+  return keys;
+}
+
+}  // namespace
+
+extern "C" {
+
 // Sorted distinct scalars at a dotted key path (capi.cpp:143-151,
 // document.cpp:134-192): the first key matches at any depth, later keys must
 // follow directly, arrays are looked through.  Host-side walk of the
@@ -1022,13 +1085,7 @@ char *jt_document_dump(const jt_document *doc) {
 char *jt_document_distinct(const jt_document *doc, const char *path) {
   std::string out;
   if (doc && path && *path && doc->tape.size() > 2) {
-    std::vector<std::string> keys;
-    for (const char *a = path;;) {
-      const char *dot = strchr(a, '.');
-      keys.emplace_back(a, dot ? (size_t)(dot - a) : strlen(a));
-      if (!dot) break;
-      a = dot + 1;
-    }
+    const std::vector<std::string> keys = split_path(path);
     const uint64_t *t = doc->tape.data();
     const uint8_t *sb = doc->strings.data();
     auto tag = [&](uint64_t i) { return (uint8_t)(t[i] >> 56); };
@@ -1042,17 +1099,7 @@ char *jt_document_distinct(const jt_document *doc, const char *path) {
       memcpy(&n, sb + pay(i), 4);
       return std::string((const char *)sb + pay(i) + 4, n);
     };
-    // (kind, bits, bytes) ordered as scalar_value (document.h:71-90)
-    struct Val {
-      int k;
-      uint64_t bits;
-      std::string bytes;
-      bool operator<(const Val &o) const {
-        if (k != o.k) return k < o.k;
-        return k == 5 ? bytes < o.bytes : bits < o.bits;
-      }
-    };
-    std::set<Val> vals;
+    std::set<DVal> vals;
     auto scalar = [&](uint64_t i) {
       const uint8_t g = tag(i);
       if (g == 'n') vals.insert({0, 0, {}});
@@ -1095,29 +1142,102 @@ char *jt_document_distinct(const jt_document *doc, const char *path) {
         each(i, [&](uint64_t, uint64_t v) { search(v); });
     };
     search(1);  // document_root (document.cpp:99)
-    char buf[64];
-    for (const Val &v : vals) {
-      switch (v.k) {
-        case 0: out += "null"; break;
-        case 1: out += "false"; break;
-        case 2: out += "true"; break;
-        case 3: out.append(buf, std::to_chars(buf, buf + sizeof(buf), (int64_t)v.bits).ptr); break;
-        case 4: {
-          double d;
-          memcpy(&d, &v.bits, 8);
-          out.append(buf, std::to_chars(buf, buf + sizeof(buf), d).ptr);
-          break;
-        }
-        default: out += '"' + v.bytes + '"';
-      }
-      out += '\n';
+    out = format_distinct(vals);
+  }
+  return malloc_string(out);
+}
+
+// distinct_values of the parser's last successful parse, on the device
+// (§8f rank 4, "parse + select"): k_distinct_match selects the scalars, the
+// values and their string bytes are gathered into a compact buffer (one D2H
+// each), and the host only sorts the selected values; same text as
+// jt_document_distinct on the downloaded document.  NULL without such a
+// parse or on a device error.
+char *jt_b200_distinct(jt_parser *p, const char *path) {
+  if (!p || !p->last_ok || !path) return nullptr;
+  std::set<DVal> vals;
+  if (!*path) return malloc_string(std::string());
+  const std::vector<std::string> keys = split_path(path);
+  if (keys.size() > (size_t)jt::kDistinctMaxKeys) {
+    p->err = "distinct: too many keys";
+    return nullptr;
+  }
+  const uint64_t S = p->index_count, len = p->in_len;
+  jt::DistinctQuery q{};
+  std::string kb;
+  q.nkeys = (int)keys.size();
+  for (size_t k = 0; k < keys.size(); k++) {
+    q.key_off[k] = (uint32_t)kb.size();
+    kb += keys[k];
+  }
+  q.key_off[keys.size()] = (uint32_t)kb.size();
+  // qbuf: count | keys | match[S] | vals[S] | len[S] | off[S] | scan temp
+  const size_t a_keys = 256, a_match = round_up(a_keys + kb.size() + 1, 256);
+  const size_t a_vals = round_up(a_match + 4 * S + 4, 256), a_len = round_up(a_vals + 16 * S, 256);
+  const size_t a_off = round_up(a_len + 4 * S + 4, 256), a_tmp = round_up(a_off + 4 * S + 4, 256);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(S + 1));
+  if (!p->qbuf.ensure(a_tmp + tmp_bytes + 256)) {
+    p->err = "distinct: out of memory";
+    return nullptr;
+  }
+  uint8_t *qb = p->qbuf.as<uint8_t>();
+  uint32_t *d_count = (uint32_t *)qb, *d_match = (uint32_t *)(qb + a_match), *d_len = (uint32_t *)(qb + a_len),
+           *d_off = (uint32_t *)(qb + a_off);
+  jt::DistinctVal *d_vals = (jt::DistinctVal *)(qb + a_vals);
+  q.key_bytes = qb + a_keys;
+  const jt::Stage2Args a = s2_args(p, len, p->cur);
+  uint32_t count = 0;
+  if (!cuda_ok(p, cudaMemsetAsync(d_count, 0, 4, p->stream), "memset") ||
+      (kb.size() && !cuda_ok(p, cudaMemcpyAsync(qb + a_keys, kb.data(), kb.size(), cudaMemcpyHostToDevice, p->stream),
+                             "keys H2D")) ||
+      !cuda_ok(p, jt::distinct_match_launch(a, q, d_match, d_count, p->stream), "distinct match") ||
+      !cuda_ok(p, cudaMemcpyAsync(&count, d_count, 4, cudaMemcpyDeviceToHost, p->stream), "count D2H") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
+    return nullptr;
+  std::vector<jt::DistinctVal> hv(count);
+  std::vector<uint32_t> last(2, 0);
+  std::vector<uint8_t> hs;
+  if (count) {
+    size_t tb = tmp_bytes;
+    if (!cuda_ok(p, jt::distinct_values_launch(a, d_match, count, d_vals, d_len, p->stream), "distinct values") ||
+        !cuda_ok(p, cudaMemsetAsync(d_len + count, 0, 4, p->stream), "memset") ||
+        !cuda_ok(p, cub::DeviceScan::ExclusiveSum(qb + a_tmp, tb, d_len, d_off, (int)count + 1, p->stream),
+                 "scan") ||
+        !cuda_ok(p, cudaMemcpyAsync(hv.data(), d_vals, 16 * (size_t)count, cudaMemcpyDeviceToHost, p->stream),
+                 "values D2H") ||
+        !cuda_ok(p, cudaMemcpyAsync(last.data(), d_off + count, 4, cudaMemcpyDeviceToHost, p->stream), "D2H") ||
+        !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
+      return nullptr;
+    const uint32_t total = last[0];
+    if (total) {
+      if (!p->qstr.ensure(total) ||
+          !cuda_ok(p, jt::distinct_strings_launch(a, d_vals, d_off, count, p->qstr.as<uint8_t>(), p->stream),
+                   "distinct strings"))
+        return nullptr;
+      hs.resize(total);
+      std::vector<uint32_t> ho(count);
+      if (!cuda_ok(p, cudaMemcpyAsync(hs.data(), p->qstr.p, total, cudaMemcpyDeviceToHost, p->stream), "D2H") ||
+          !cuda_ok(p, cudaMemcpyAsync(ho.data(), d_off, 4 * (size_t)count, cudaMemcpyDeviceToHost, p->stream),
+                   "D2H") ||
+          !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
+        return nullptr;
+      for (uint32_t k = 0; k < count; k++)
+        if (hv[k].tag == '"') hv[k].bits = ho[k];
     }
   }
-  char *r = (char *)malloc(out.size() + 1);
-  if (!r) return nullptr;
-  memcpy(r, out.data(), out.size());
-  r[out.size()] = 0;
-  return r;
+  for (const jt::DistinctVal &r : hv) {
+    switch (r.tag) {
+      case 'n': vals.insert({0, 0, {}}); break;
+      case 'f': vals.insert({1, 0, {}}); break;
+      case 't': vals.insert({2, 0, {}}); break;
+      case 'l': vals.insert({3, r.bits, {}}); break;
+      case 'd': vals.insert({4, r.bits, {}}); break;
+      case '"': vals.insert({5, 0, std::string((const char *)hs.data() + r.bits, r.len)}); break;
+      default: break;
+    }
+  }
+  return malloc_string(format_distinct(vals));
 }
 
 void jt_string_free(char *s) { free(s); }

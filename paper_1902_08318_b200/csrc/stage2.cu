@@ -1656,6 +1656,109 @@ cudaError_t shard_finish_launch(const Stage2Args &a, const Sum3 *gathered, cudaS
   return cudaGetLastError();
 }
 
+// ---- distinct_values over the device-resident parse (§8f rank 4) ----------
+// document.cpp:134-192: a scalar is selected when, walking up from it, the
+// object keys met (arrays are looked through between keys, not below the
+// last one) end with the path's keys; the first key may sit at any depth.
+// One thread per token: the innermost step needs ':' + key before the token,
+// every further container is found by the previous-smaller-depth query on
+// the stage-2 min tree (psv), so the walk is a few loads per level.
+__device__ __forceinline__ bool key_is(const Stage2Args &a, const DistinctQuery &q, uint64_t key, int k) {
+  if ((a.tok[key] & 0xFF) != '"') return false;
+  const uint8_t *s = a.strings + a.aux[key];
+  const uint32_t n = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16) | ((uint32_t)s[3] << 24);
+  const uint32_t b = q.key_off[k], e = q.key_off[k + 1];
+  if (n != e - b) return false;
+  for (uint32_t j = 0; j < n; j++)
+    if (s[4 + j] != q.key_bytes[b + j]) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_distinct_match(Stage2Args a, DistinctQuery q, uint32_t *match,
+                                                        uint32_t *count) {
+  const uint64_t S = a.ctrl->S;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S; i += stride) {
+    const uint32_t v = a.tok[i];
+    const uint32_t c = v & 0xFF;
+    const bool scalar = c == '"' || c == 't' || c == 'f' || c == 'n' || c == '-' || (c - '0') < 10u;
+    int d = tok_depth(v);
+    if (!scalar || d <= 0 || i < 2 || (a.tok[i - 1] & 0xFF) != ':') continue;
+    if (!key_is(a, q, i - 2, q.nkeys - 1)) continue;
+    int k = q.nkeys - 2;
+    int64_t cur = psv(a, (int64_t)i, d - 1);  // the object holding the last key
+    d--;
+    bool ok = true;
+    while (k >= 0) {
+      if (cur < 1 || d <= 0) {  // the root: keys left over
+        ok = false;
+        break;
+      }
+      if ((a.tok[cur - 1] & 0xFF) == ':') {  // a member value: its key must be the next one
+        if (cur < 2 || !key_is(a, q, (uint64_t)cur - 2, k)) {
+          ok = false;
+          break;
+        }
+        k--;
+      }  // else an array element: looked through
+      if (k < 0) break;
+      cur = psv(a, cur, d - 1);
+      d--;
+    }
+    if (ok) match[atomicAdd(count, 1u)] = (uint32_t)i;
+  }
+}
+
+__global__ void k_distinct_values(Stage2Args a, const uint32_t *match, uint32_t count, DistinctVal *vals,
+                                  uint32_t *len) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const uint32_t t = a.tape_idx[match[k]];
+  const uint64_t w = a.tape[t];
+  DistinctVal r{};
+  r.tag = (uint32_t)(w >> 56);
+  if (r.tag == 'l' || r.tag == 'd') {
+    r.bits = a.tape[t + 1];
+  } else if (r.tag == '"') {
+    const uint8_t *s = a.strings + (w & kPayloadMask);
+    r.len = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16) | ((uint32_t)s[3] << 24);
+    r.bits = w & kPayloadMask;  // source offset until the scan
+  }
+  vals[k] = r;
+  len[k] = r.len;
+}
+
+// one warp per string
+__global__ void k_distinct_strings(Stage2Args a, const DistinctVal *vals, const uint32_t *off, uint32_t count,
+                                   uint8_t *out) {
+  const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= count) return;
+  const DistinctVal r = vals[k];
+  if (r.tag != '"') return;
+  const uint8_t *s = a.strings + r.bits + 4;
+  for (uint32_t j = lane; j < r.len; j += 32) out[off[k] + j] = s[j];
+}
+
+cudaError_t distinct_match_launch(const Stage2Args &a, const DistinctQuery &q, uint32_t *match,
+                                  uint32_t *count, cudaStream_t stream) {
+  const int sms = a.num_sms > 0 ? a.num_sms : 148;
+  k_distinct_match<<<sms * 8, 256, 0, stream>>>(a, q, match, count);
+  return cudaGetLastError();
+}
+
+cudaError_t distinct_values_launch(const Stage2Args &a, const uint32_t *match, uint32_t count,
+                                   DistinctVal *vals, uint32_t *len, cudaStream_t stream) {
+  if (count) k_distinct_values<<<(count + 255) / 256, 256, 0, stream>>>(a, match, count, vals, len);
+  return cudaGetLastError();
+}
+
+cudaError_t distinct_strings_launch(const Stage2Args &a, const DistinctVal *vals, const uint32_t *off,
+                                    uint32_t count, uint8_t *out, cudaStream_t stream) {
+  if (count) k_distinct_strings<<<(unsigned)(((uint64_t)count * 32 + 255) / 256), 256, 0, stream>>>(a, vals, off, count, out);
+  return cudaGetLastError();
+}
+
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
                           cudaEvent_t *ev) {
   const Stage2Sizes z = stage2_sizes(a.cap_tokens);

@@ -87,6 +87,29 @@ struct Stage2Args {
   RecordResult *results;        // per record (k_final_records)
 };
 
+// distinct_values query over the device-resident result of the last parse
+// (document.cpp:134-192): matched scalar tokens, then their values.
+constexpr int kDistinctMaxKeys = 32;
+struct DistinctQuery {
+  const uint8_t *key_bytes;   // the path's keys, concatenated
+  uint32_t key_off[kDistinctMaxKeys + 1];
+  int nkeys;
+};
+struct DistinctVal {          // one matched scalar
+  uint64_t bits;              // int64 / float64 bits; string: byte offset in the compact buffer
+  uint32_t len;               // string bytes
+  uint32_t tag;               // tape tag
+};
+// k_distinct_match: S tokens -> match[] (token indices, unordered), *count
+cudaError_t distinct_match_launch(const Stage2Args &a, const DistinctQuery &q, uint32_t *match,
+                                  uint32_t *count, cudaStream_t stream);
+// values of count matches; string lengths into len[] (for the caller's scan)
+cudaError_t distinct_values_launch(const Stage2Args &a, const uint32_t *match, uint32_t count,
+                                   DistinctVal *vals, uint32_t *len, cudaStream_t stream);
+// string bytes of the matches to out at the scanned offsets off[]
+cudaError_t distinct_strings_launch(const Stage2Args &a, const DistinctVal *vals, const uint32_t *off,
+                                    uint32_t count, uint8_t *out, cudaStream_t stream);
+
 // words of look-back records / tree nodes needed for up to `cap` tokens
 struct Stage2Sizes {
   uint64_t chunks, tiles, n1, n2, n3, nhi;

@@ -35,7 +35,7 @@ EXPORTS = [
     "jt_b200_parse_async", "jt_b200_stage1_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
     "jt_b200_device_strings", "jt_b200_download", "jt_b200_set_stream",
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
-    "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_shard_summary_bytes",
+    "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_distinct", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
     "jt_b200_shard_download", "jt_b200_copy_in_range", "jt_b200_parse_records",
     "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download", "jt_b200_device_records",
@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_device.argtypes = [vp]
     L.jt_b200_last_error.argtypes = [vp]
     L.jt_b200_last_error.restype = C.c_char_p
+    L.jt_b200_distinct.argtypes = [vp, C.c_char_p]
+    L.jt_b200_distinct.restype = vp
     L.jt_b200_profile.argtypes = [vp, C.c_int]
     L.jt_b200_kernel_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     L.jt_b200_copy_in.argtypes = [vp, vp, sz]
@@ -327,6 +329,16 @@ class Parser:
                 out.append((name, int(r["offset"]), tape[tb:tb + tw], strings[sb0:sb0 + sn]))
             else:
                 out.append((name, int(r["offset"]), None, None))
+        return out
+
+    def distinct(self, path: bytes) -> bytes | None:
+        """jt_b200_distinct: distinct_values over the last successful parse,
+        selected on the device (same text as Document.distinct)"""
+        sp = self._lib.jt_b200_distinct(self._h, path)
+        if not sp:
+            return None
+        out = C.string_at(sp)
+        self._lib.jt_string_free(sp)
         return out
 
     def set_stream(self, stream_handle: int | None):

@@ -226,3 +226,28 @@ def test_document_distinct(parser):
         r = parser.parse(d)
         got = [r.document.distinct(p) for p in paths]
         assert got == want, d[:200]
+        # the same query selected on the device (jt_b200_distinct)
+        assert [parser.distinct(p) for p in paths] == want, d[:200]
+
+
+def test_device_distinct_large(parser):
+    """jt_b200_distinct on full-size synthetic documents (deep trees, many
+    matches, long strings) against the host walk of the downloaded document,
+    which test_document_distinct pins to the reference"""
+    from tools.gen import generate
+    for cfg, size in ((0, 1 << 20), (1, 8 << 20), (2, 4 << 20), (4, 8 << 20)):
+        d = generate(cfg, size, seed=5 + cfg)
+        r = parser.parse(d)
+        assert r.name == "OK"
+        import re
+        keys = [m.group(1) for m in re.finditer(rb'"([^"\\]{1,24})"\s*:', d[:200000])][:40]
+        paths = [b"x.y"] + keys[:6] + [a + b"." + b for a, b in zip(keys[:12], keys[1:13])]
+        paths += [keys[0] + b"." + keys[1] + b"." + keys[2]] if len(keys) > 2 else []
+        hits = 0
+        for p in paths:
+            want = r.document.distinct(p)
+            hits += want.count(b"\n")
+            assert parser.distinct(p) == want, (cfg, p)
+        assert cfg == 2 or hits > 0, cfg  # C2 has no keys
+    assert parser.parse(b"[1, ]").name != "OK"
+    assert parser.distinct(b"a") is None  # no successful parse to query
