@@ -1,12 +1,13 @@
 """Long-running differential fuzz of the GPU paths against the oracle.
 
-python tools/fuzz_gpu.py --seconds 600 [--seed N]
+python tests/fuzz_gpu.py --seconds 600 [--seed N]   (test infrastructure: it runs the oracle)
 
 Each round draws a document (generated configs C0..C4 at random sizes, random
 JSON, byte soups, and seeded mutations of all of them) and checks, against
 the oracle (tests/ pin the oracle to the reference):
   jt_parse (in-memory and, >= 8 MiB, the streamed path), emulated byte-range
-  shards (2..6), NDJSON records, jt_minify, jt_compute_stats.
+  shards (2..6), NDJSON records, jt_minify, jt_compute_stats, jt_stage1 (the
+  k_index path) and the device distinct_values query (against the host walk).
 Prints one line per failure (document saved under gpurun_out/fuzz_fail_*.bin)
 and a summary; exit status 1 if anything failed.
 """
@@ -60,7 +61,8 @@ def main():
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     t0 = time.time()
     n = fails = 0
-    counts = {"parse": 0, "shards": 0, "records": 0, "minify": 0, "stats": 0, "streamed": 0}
+    counts = {"parse": 0, "shards": 0, "records": 0, "minify": 0, "stats": 0, "streamed": 0, "stage1": 0,
+              "distinct": 0}
 
     def fail(what, d, detail):
         nonlocal fails
@@ -82,6 +84,20 @@ def main():
         if r.code == 0 and (not np.array_equal(g.document.tape, r.tape_array()) or g.document.strings != r.strings):
             fail("parse tape", d, "tape/strings differ")
             continue
+        if r.code == 0 and rng.random() < 0.3:  # device distinct_values on this parse
+            import re
+            keys = [m.group(1) for m in re.finditer(rb'"([^"\\\x00]{1,16})"\s*:', d[:1 << 16])][:8]
+            for path in [k for k in keys[:3]] + [a + b"." + b for a, b in zip(keys[:3], keys[1:4])]:
+                counts["distinct"] += 1
+                if p.distinct(path) != g.document.distinct(path):
+                    fail("distinct", d, path)
+                    break
+        if rng.random() < 0.3:  # jt_stage1 alone (k_index)
+            s1g, s1o = p.stage1(d), o.stage1(d)
+            counts["stage1"] += 1
+            if (s1g.name, s1g.offset) != (s1o.name, s1o.offset) or (
+                    s1o.code == 0 and not np.array_equal(p.index(), s1o.index_list())):
+                fail("stage1", d, (s1g.name, s1g.offset, s1o.name, s1o.offset))
         if rng.random() < 0.1 and len(d) > 0:  # a big streamed variant: the doc in a 9+ MiB array
             reps = max(1, (9 << 20) // max(1, len(d)) + 1)
             if r.code == 0 and reps * len(d) < (40 << 20):

@@ -113,7 +113,7 @@ def test_shards_deep_then_shallow(oracle):
     for G in (2, 3):
         check_sharded(oracle, doc, G, "deep then shallow")
     here = os.path.join(os.path.dirname(__file__), "golden", "fuzz")
-    for name in sorted(os.listdir(here)):  # fuzz finds (tools/fuzz_gpu.py)
+    for name in sorted(os.listdir(here)):  # fuzz finds (tests/fuzz_gpu.py)
         data = open(os.path.join(here, name), "rb").read()
         for G in (2, 3, 5):
             if G <= (len(data) + TILE - 1) // TILE:
