@@ -363,6 +363,19 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) s_wmin[warp] = m;  // 128 tokens
+    // every load that depends on the four positions goes out before any of
+    // them is used: the string's stage-1 tile flag, and the 8 bytes of an
+    // atom (atom_ok8), instead of a chain of dependent byte loads
+    uint32_t tflag[4];
+    uint64_t aw[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t c = rec[k] & 0xFF;
+      const bool live = i0 + k < S;
+      const uint64_t lt = ((uint64_t)pos[k] - vw.begin) >> 14;
+      tflag[k] = live && c == '"' && !a.records ? __ldg(a.tile_flags + lt) : 0u;
+      aw[k] = live && (c == 't' || c == 'f' || c == 'n') ? at.load8(pos[k]) : 0ULL;
+    }
     uint32_t nummask = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -389,7 +402,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
           // stage 1 wrote the length unless the next token is in another
           // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
           const uint64_t lt = (p - vw.begin) >> 14;
-          if (end > a.len || lt != ((end - vw.begin) >> 14) || a.tile_flags[lt]) {
+          if (end > a.len || lt != ((end - vw.begin) >> 14) || (a.records ? a.tile_flags[lt] : tflag[k])) {
             const uint32_t nx = i + 1 < S ? so_next : (uint32_t)vw.next_aux;
             const uint32_t len = nx - so[k] - 4;
             uint8_t *f = a.strings + so[k];
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
           a.tape[ti[k]] = tape_word('"', vw.string_base + so[k] - sbase);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
-        fail = !str::atom_ok(at, a.len, pos[k], c);
+        fail = !str::atom_ok8(aw[k], a.len, pos[k], c);
         if (!fail) a.tape[ti[k]] = (uint64_t)c << 56;
       }
       if (fail) a.tok[i] = rec[k] | 0x100u;

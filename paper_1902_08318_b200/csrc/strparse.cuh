@@ -171,5 +171,26 @@ JT_HD bool atom_ok(At at, uint64_t len, uint64_t p, uint32_t c) {
   return is_sep(t) || t == '"';
 }
 
+// atom_ok on the 8 bytes from p (little endian, w = bytes p..p+7): the
+// literal and its terminator in registers, no dependent byte loads
+JT_HD bool atom_ok8(uint64_t w, uint64_t len, uint64_t p, uint32_t c) {
+  uint64_t e;
+  uint32_t t;
+  if (c == 't') {
+    if ((uint32_t)w != 0x65757274u) return false;  // "true"
+    e = p + 4;
+    t = (uint32_t)(w >> 32) & 0xFF;
+  } else if (c == 'f') {
+    if ((w & 0xFFFFFFFFFFULL) != 0x65736c6166ULL) return false;  // "false"
+    e = p + 5;
+    t = (uint32_t)(w >> 40) & 0xFF;
+  } else {
+    if ((uint32_t)w != 0x6c6c756eu) return false;  // "null"
+    e = p + 4;
+    t = (uint32_t)(w >> 32) & 0xFF;
+  }
+  return e >= len || is_sep(t) || t == '"';
+}
+
 }  // namespace str
 }  // namespace jt

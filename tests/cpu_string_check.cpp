@@ -111,3 +111,21 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
   *str_err = serr == ~0ULL ? -1 : (long long)serr;
   return 0;
 }
+
+// atom_ok8 (register form used by k_scalars) against the byte-at-a-time
+// atom_ok, over every literal start in `data` (padded with zeros past len,
+// as the device input is); returns the number of disagreements
+extern "C" int jt_cpu_atoms(const uint8_t *data, uint64_t len) {
+  std::vector<uint8_t> pad(data, data + len);
+  pad.resize(len + 16, 0);
+  auto at = [&](uint64_t i) -> uint32_t { return pad[i]; };
+  int bad = 0;
+  for (uint64_t p = 0; p < len; p++) {
+    const uint32_t c = pad[p];
+    if (c != 't' && c != 'f' && c != 'n') continue;
+    uint64_t w = 0;
+    for (int k = 7; k >= 0; k--) w = (w << 8) | pad[p + k];
+    if (jt::str::atom_ok8(w, len, p, c) != jt::str::atom_ok(at, len, p, c)) bad++;
+  }
+  return bad;
+}

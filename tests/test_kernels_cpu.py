@@ -216,3 +216,16 @@ def test_glibc_subnormal_quirk(number_lib, oracle):
     b, slow = C.c_uint64(), C.c_int()
     number_lib.jt_cpu_number(t + b"\0" * 64, len(t), C.byref(b), C.byref(slow))
     assert ok and bits == 2724151024255084 and b.value == bits
+
+
+def test_atom_register_check(string_lib):
+    """k_scalars' atom_ok8 (8 bytes in registers) = atom_ok byte by byte"""
+    L = string_lib
+    L.jt_cpu_atoms.argtypes = [C.c_char_p, C.c_uint64]
+    rng = random.Random(17)
+    lits = [b"true", b"false", b"null", b"tru", b"nul", b"fals", b"truex", b"nulll", b"t", b"f", b"n"]
+    ends = [b"", b",", b"]", b"}", b" ", b"\n", b"\t", b"\r", b":", b"[", b"{", b'"', b"x", b"0", b"\x00"]
+    for _ in range(3000):
+        d = b"".join(rng.choice(lits) + rng.choice(ends) for _ in range(rng.randrange(1, 8)))
+        assert L.jt_cpu_atoms(d, len(d)) == 0, d
+        assert L.jt_cpu_atoms(d, max(0, len(d) - rng.randrange(0, 3))) == 0, d
