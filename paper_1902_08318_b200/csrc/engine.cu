@@ -220,6 +220,9 @@ struct jt_parser {
   // tile counters and carry states, stage-1 control block snapshot
   cudaStream_t copy_stream = nullptr;
   cudaStream_t d2h_stream = nullptr;  // string pieces back while the input goes up
+  cudaStream_t side_stream = nullptr;  // k_stack next to the scalar kernels (stage2_launch)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  jt::Stage2Fork fork{};
   std::vector<cudaEvent_t> chunk_ev, piece_ev;
   cudaEvent_t ev_d2h = nullptr;
   uint64_t *h_piece_sb = nullptr;     // pinned, host-mapped: string bytes up to each piece's end
@@ -383,6 +386,12 @@ uint64_t buffers_sig(jt_parser *p, int which) {
 
 bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full);
 
+const jt::Stage2Fork *stage2_fork(jt_parser *p) {
+  if (!p->side_stream) return nullptr;
+  p->fork = jt::Stage2Fork{p->side_stream, p->ev_fork, p->ev_join};
+  return &p->fork;
+}
+
 // Full parses without profiling replay a CUDA graph of the 9 launches + the
 // control-block D2H (captured on first use for this length/stream/buffers).
 bool enqueue(jt_parser *p, uint64_t len, int which, bool full) {
@@ -444,7 +453,7 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
   if (full) {
     int n = 0;
     if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n,
-                                      p->prof ? p->ev + 3 : nullptr),
+                                      p->prof ? p->ev + 3 : nullptr, stage2_fork(p)),
                  "stage2"))
       return false;
     p->launches += n;
@@ -670,7 +679,8 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
        cuda_ok(p, cudaEventRecord(p->ev_s1, p->stream), "event");
   p->launches += 1;
   int n2 = 0;
-  ok = ok && cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n2), "stage2") &&
+  ok = ok && cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n2, nullptr, stage2_fork(p)),
+                     "stage2") &&
        cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
                                   p->stream),
                "ctrl D2H");
@@ -786,6 +796,14 @@ jt_parser *jt_parser_new(void) {
     return nullptr;
   }
   p->stream = p->own_stream;
+  // optional: without the side stream stage 2 runs k_stack in line
+  if (cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    if (p->side_stream) cudaStreamDestroy(p->side_stream);
+    p->side_stream = nullptr;
+  }
   jt::stage1_configure();  // kernel attributes once, outside any capture
   return p;
 }
@@ -798,6 +816,12 @@ void jt_parser_free(jt_parser *p) {
   for (auto &g : p->graph_s1)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  if (p->side_stream) {
+    cudaStreamSynchronize(p->side_stream);
+    cudaStreamDestroy(p->side_stream);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
   if (p->h_shard) cudaFreeHost(p->h_shard);
   if (p->copy_stream) {
@@ -913,7 +937,8 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   *p->h_ctrl = c0;
   cudaMemcpyAsync(p->ctrl.p, p->h_ctrl, sizeof(jt::Ctrl), cudaMemcpyHostToDevice, p->stream);
   int n = 0;
-  if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, p->cur), p->stream, &n), "stage2") ||
+  if (!cuda_ok(p, jt::stage2_launch(s2_args(p, len, p->cur), p->stream, &n, nullptr, stage2_fork(p)),
+               "stage2") ||
       !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
                                   p->stream),
                "ctrl")) {

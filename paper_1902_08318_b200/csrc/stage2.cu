@@ -1773,13 +1773,20 @@ cudaError_t distinct_strings_launch(const Stage2Args &a, const DistinctVal *vals
 }
 
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
-                          cudaEvent_t *ev) {
+                          cudaEvent_t *ev, const Stage2Fork *fork) {
   const Stage2Sizes z = stage2_sizes(a.cap_tokens);
   const int sms = a.num_sms > 0 ? a.num_sms : 148;
   // K2: one thread per token, grid sized for the capacity bound, grid-stride
   uint64_t g = (a.cap_tokens + 255) / 256;
   unsigned g2 = (unsigned)(g < (uint64_t)sms * 16 ? g : (uint64_t)sms * 16);
   if (g2 < 1) g2 = 1;
+  const bool forked = fork && !ev;
+  if (forked) {  // k_stack reads only stage 1's token records
+    cudaEventRecord(fork->fork, stream);
+    cudaStreamWaitEvent(fork->side, fork->fork, 0);
+    launch_stack(a, fork->side);
+    cudaEventRecord(fork->join, fork->side);
+  }
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[0], stream);
@@ -1787,7 +1794,8 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[1], stream);
   k_tree<<<1, 1024, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
-  launch_stack(a, stream);  // container kinds (scope bits) for k_struct
+  if (forked) cudaStreamWaitEvent(stream, fork->join, 0);
+  else launch_stack(a, stream);  // container kinds (scope bits) for k_struct
   launch_struct(a, stream);
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);

@@ -120,8 +120,15 @@ Stage2Sizes stage2_sizes(uint64_t cap_tokens);
 // Enqueue the whole stage 2 (tokens, slow numbers, tree, structure,
 // finalize); returns the number of kernel launches via *launches.
 // `ev` (optional, 5 events) is recorded after each of the 5 kernels.
+// `fork` (optional, without `ev`): {side stream, fork event, join event} --
+// the container-kind stack (k_stack) runs on the side stream next to the
+// scalar / number / tree kernels, which it does not depend on.
+struct Stage2Fork {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
-                          cudaEvent_t *ev = nullptr);
+                          cudaEvent_t *ev = nullptr, const Stage2Fork *fork = nullptr);
 
 // Record mode: per-record error slots, then the whole stage 2 with
 // per-record grammar, and one result per record.
