@@ -677,35 +677,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     // the first vin bits belong to the previous block's escape)
     uint64_t cm = W & ~sb::low_bits(vin);
     if (!pay_direct) {
-      // warp-cooperative copy into the staging buffer: 16 steps, each lane one
-      // 4-byte word of the warp's 2 KiB; the owning block's masks come by
-      // shuffle and the destination is the popcount formula (an opening
-      // quote's 4 bytes are skipped, filled by the copy-out)
-      const uint32_t *s_in32 = (const uint32_t *)s_in;
-      const uint32_t wbase = (uint32_t)warp * 32;  // first block (thread) of the warp
-      // block pairs with string bytes (warp-uniform; none at all on numeric text)
-      const uint32_t live = __ballot_sync(0xffffffffu, cm != 0);
-      uint32_t pairs = 0;
+      // each lane copies its own block into the staging buffer, bytes in
+      // order with a running destination (+1 per weight bit, +4 per opening
+      // quote: the length field, filled by the copy-out); fully unrolled and
+      // predicated, 16-byte chunks without string bytes skipped
+      if (cm) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(s_in + local);
+        uint32_t d = soff;
 #pragma unroll
-      for (int j = 0; j < 16; j++) pairs |= ((live >> (2 * j)) & 3u) ? (1u << j) : 0u;
-      while (pairs) {
-        const int j = __ffs(pairs) - 1;
-        pairs &= pairs - 1;
-        const int owner = 2 * j + (lane >> 4);
-        const uint64_t Ro = __shfl_sync(0xffffffffu, cm, owner);
-        const uint64_t Wo = __shfl_sync(0xffffffffu, W, owner);
-        const uint64_t Oo = __shfl_sync(0xffffffffu, openq, owner);
-        const uint32_t so = __shfl_sync(0xffffffffu, soff, owner);
-        const int o = (lane & 15) * 4;
-        const uint32_t k4 = (uint32_t)(Ro >> o) & 0xF;
-        if (k4) {
-          const uint64_t below = sb::low_bits(o);
-          uint32_t d = so + 4u * popc64(Oo & below) + popc64(Wo & below);
-          const uint32_t word = s_in32[(wbase + owner) * 16 + (lane & 15)];
+        for (int c = 0; c < 4; c++) {
+          const uint32_t cmw = (uint32_t)(cm >> (16 * c)) & 0xFFFFu;
+          const uint32_t ww = (uint32_t)(W >> (16 * c)) & 0xFFFFu;
+          const uint32_t ow = (uint32_t)(openq >> (16 * c)) & 0xFFFFu;
+          if (cmw == 0) {
+            d += (uint32_t)__popc(ww) + 4u * (uint32_t)__popc(ow);
+            continue;
+          }
+          const uint4 v = src[c];
+          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int k = 0; k < 4; k++) {
-            if ((k4 >> k) & 1) s_pay[d] = (uint8_t)(word >> (8 * k));
-            d += (uint32_t)((Wo >> (o + k)) & 1) + 4u * (uint32_t)((Oo >> (o + k)) & 1);
+          for (int b = 0; b < 16; b++) {
+            if ((cmw >> b) & 1) s_pay[d] = (uint8_t)(wd[b >> 2] >> (8 * (b & 3)));
+            d += ((ww >> b) & 1) + 4u * ((ow >> b) & 1);
           }
         }
       }
