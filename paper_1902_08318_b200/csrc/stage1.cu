@@ -1508,14 +1508,17 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
 // string buffer is final before the tape exists (streamed jt_parse).  One
 // thread per tile; counts from the tiles' inclusive look-back records.
 __global__ void k_tile_lengths(Stage1Args a, uint64_t ntiles) {
-  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  // one warp per tile: a spilled tile (string-dense text) leaves all its
+  // lengths, up to thousands of tokens
+  const uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   if (t >= ntiles) return;
   const uint64_t S = *a.total, SB = *a.total_strings;
   auto incl = [&](uint64_t k) { return a.rec_count[8 * k + 4] & kQuadMask; };
   const uint64_t hi = incl(t), lo = t ? incl(t - 1) : 0;
   if (hi == lo) return;
   const uint64_t from = a.tile_flags[t] ? lo : hi - 1;
-  for (uint64_t k = from; k < hi; k++) {
+  for (uint64_t k = from + lane; k < hi; k += 32) {
     if ((a.tokrec[k] & 0xFF) != '"') continue;
     const uint32_t so = a.aux[k];
     const uint32_t nx = k + 1 < S ? a.aux[k + 1] : (uint32_t)SB;
@@ -1536,7 +1539,7 @@ __global__ void k_tile_lengths(Stage1Args a, uint64_t ntiles) {
 }
 
 cudaError_t stage1_lengths_launch(const Stage1Args &a, uint64_t ntiles, cudaStream_t stream) {
-  k_tile_lengths<<<(unsigned)((ntiles + 255) / 256), 256, 0, stream>>>(a, ntiles);
+  k_tile_lengths<<<(unsigned)((ntiles * 32 + 255) / 256), 256, 0, stream>>>(a, ntiles);
   return cudaGetLastError();
 }
 
