@@ -48,29 +48,6 @@ struct InAt {
   }
 };
 
-// A token's bytes from a 40-byte register window [base, base+40), base =
-// token & ~7 (5 independent 8-byte loads instead of one dependent load per
-// byte); bytes past the window come from memory.
-struct WindowAt {
-  const uint8_t *in;
-  uint64_t base;
-  uint64_t w0, w1, w2, w3, w4;
-  __device__ __forceinline__ WindowAt(const uint8_t *src, uint64_t p) : in(src), base(p & ~7ULL) {
-    const uint64_t *q = (const uint64_t *)(src + base);
-    w0 = q[0];
-    w1 = q[1];
-    w2 = q[2];
-    w3 = q[3];
-    w4 = q[4];
-  }
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-    uint64_t k = i - base;
-    if (k >= 40) return in[i];
-    uint64_t w = k < 8 ? w0 : k < 16 ? w1 : k < 24 ? w2 : k < 32 ? w3 : w4;
-    return (uint32_t)(w >> (8 * (k & 7))) & 0xFF;
-  }
-};
-
 __device__ __forceinline__ int tok_width(uint32_t c) {
   if (c == ',' || c == ':') return 0;
   if (c == '-' || (c - '0') < 10u) return 2;
