@@ -48,6 +48,12 @@ jt_error jt_b200_download(jt_parser *p, jt_document **out);
  * current stream) instead of its own; NULL restores the parser's stream. */
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream);
 
+/* How jt_parse streams a host document of >= 8 MiB: 0 = stage 1 per 4 MiB
+ * piece as it lands, stage 2 after the upload (default); 1 = every piece
+ * parsed as a byte-range shard (stage 2 included) while later pieces
+ * upload, tape and strings back per piece.  Results are identical. */
+void jt_b200_set_stream_mode(jt_parser *p, int mode);
+
 /* Number of kernel launches enqueued by the last parse call. */
 int jt_b200_last_launches(const jt_parser *p);
 

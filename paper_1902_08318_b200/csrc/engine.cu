@@ -231,6 +231,18 @@ struct jt_parser {
   DevBuf stream_words;
   DevBuf qbuf, qstr;  // distinct_values query: keys, matches, values, lengths, offsets, scan | strings
   jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
+  // streamed jt_parse with stage 2 per piece (parse_pieces): one child
+  // parser per piece, each a byte-range shard reading this parser's input
+  const uint8_t *in_alias = nullptr;  // child: the parent's padded input
+  bool needs_mat = false;             // the resident state is in the children: re-parse on demand
+  int stream_mode = 0;                // jt_b200_set_stream_mode
+  std::vector<jt_parser *> kids;
+  std::vector<cudaEvent_t> done_ev;
+  cudaEvent_t ev_fin = nullptr;
+  DevBuf psum;                        // gathered Sum0 | Sum1 | Sum2 | Sum3 of the pieces
+  jt::Sum1 *h_sum1_init = nullptr;    // pinned: "not written yet" Sum1s
+  jt::Sum3 *h_sum3 = nullptr;         // pinned: the pieces' Sum3 (bracket patches)
+  uint32_t h_sum_cap = 0;
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
   DevBuf minbuf;  // jt_minify: look-back records, counter, total, output
@@ -316,7 +328,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0
   a.end = end == ~0ULL ? len : end;
   a.last_tile = ~0ULL;
   jt::Ctrl *c = p->ctrl.as<jt::Ctrl>();
-  a.in = p->in.as<uint8_t>();
+  a.in = p->in_alias ? p->in_alias : p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
   a.aux = p->aux[which].as<uint32_t>();
@@ -343,7 +355,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
                        bool sharded = false) {
   if (cap_len == ~0ULL) cap_len = len;
   jt::Stage2Args a{};
-  a.in = p->in.as<uint8_t>();
+  a.in = p->in_alias ? p->in_alias : p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
   a.aux = p->aux[which].as<uint32_t>();
@@ -470,6 +482,7 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
 
 // wait for the enqueued work and publish its results into the parser
 jt_error finish(jt_parser *p, int which, bool full, long long *off) {
+  p->needs_mat = false;
   if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
     set_off(off, -1);
     return JT_CAPACITY;
@@ -627,8 +640,18 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     a.init_state = c ? states + c - 1 : nullptr;
     a.out_state = states + c;
     a.sb_out = p->h_piece_sb + c;
+    // K1 runs one tile behind the piece boundaries: a tile's last block may
+    // read a few bytes past the tile (an escape straddling it), which for a
+    // piece's last tile are the next piece's, still uploading
+    jt::Stage1Args k1 = a;
+    k1.begin = c == 0 ? 0 : b - jt::kStage1Tile;
+    k1.end = c + 1 == nch ? len : e - jt::kStage1Tile;
+    k1.rec_tile0 = k1.begin / jt::kStage1Tile;
+    k1.carry = a.carry - a.rec_tile0 + k1.rec_tile0;
+    k1.fn = a.fn - a.rec_tile0 + k1.rec_tile0;
     ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
-         cuda_ok(p, jt::stage1_chunk_launch(a, p->stream), "stage1 chunk") &&
+         cuda_ok(p, jt::stage1_chunk_carry(a, p->stream), "stage1 carry") &&
+         cuda_ok(p, jt::stage1_chunk_main(k1, p->stream), "stage1 chunk") &&
          cuda_ok(p, cudaEventRecord(p->piece_ev[c], p->stream), "event");
     p->launches += jt::kStage1Launches;
   }
@@ -772,6 +795,318 @@ jt_error parse_resident(jt_parser *p, uint64_t len, jt_document **out, long long
   return e;
 }
 
+
+// Byte-range shard setup (shard.h) shared by jt_b200_shard_begin and the
+// pieces of a streamed jt_parse (children alias the parent's input).
+int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
+  if (G == 0 || g >= G || (uint64_t)len >= (1ULL << 32) || begin % jt::kStage1Tile != 0 ||
+      !(begin < end) || end > len || (g + 1 == G) != (end == len) || (g == 0) != (begin == 0)) {
+    p->err = "shard_begin: bad shard layout";
+    return -1;
+  }
+  if (!p->h_shard && cudaMallocHost((void **)&p->h_shard, sizeof(jt::Shard)) != cudaSuccess) {
+    cudaGetLastError();
+    p->h_shard = nullptr;
+    p->err = "shard_begin: pinned allocation";
+    return -1;
+  }
+  const uint64_t range = end - begin;
+  if ((!p->in_alias && !ensure_input(p, len)) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
+      !p->shard.ensure(kShardBoundOff + jt::kBoundMax * sizeof(uint64_t))) {
+    p->err = "shard_begin: device allocation";
+    return -1;
+  }
+  jt::Shard h{};
+  h.g = g;
+  h.G = G;
+  h.begin = begin;
+  h.end = end;
+  h.len = len;
+  *p->h_shard = h;
+  if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
+                                  p->stream),
+               "shard upload"))
+    return -1;
+  p->shard_on = true;
+  p->shard_len = len;
+  p->in_len = len;
+  p->cur = 0;
+  p->last_ok = false;
+  p->have_index = false;
+  p->h_index_valid = false;
+  p->needs_mat = false;
+  return 0;
+}
+
+// ---- streamed jt_parse, stage 2 included ------------
+// The document is cut into G tile-aligned pieces, each parsed by a child
+// parser as byte-range shard g of G (shard.h) while the later pieces are
+// still uploading.  The shard phases need only summaries of EARLIER pieces,
+// plus the next piece's first token (phase 2), so on one stream:
+//   upload g | phase 0 (g) | [upload g+1: K1 reads a few bytes past the
+//   piece] phase 1 (g) | phase 2, 3 (g-1)
+// and piece g-1's tape words and string bytes go back to the host while the
+// upload continues.  Bracket pairs across pieces are the shards' patches
+// (Sum3), applied to the host tape at the end; the root word carries the
+// document's root close index.  The parser's own resident state (index,
+// tape, strings in HBM) is rebuilt on demand (materialize) by the calls
+// that read it.  A piece whose phase 2 met a later piece without a summary
+// yet (next non-empty piece not parsed: pieces without a token start) is
+// reported by Ctrl.redo and the document is parsed again resident.
+constexpr uint64_t kPieceBytes = 8ULL << 20;
+constexpr unsigned kMaxPieces = 64;  // k_apply2 folds at most 64 earlier shards
+
+unsigned piece_count(uint64_t len) {
+  static const uint64_t piece = [] {
+    const char *e = getenv("JT_PIECE_MB");
+    const long v = e ? atol(e) : 0;
+    return v > 0 ? (uint64_t)v << 20 : kPieceBytes;
+  }();
+  const uint64_t tiles = (len + jt::kStage1Tile - 1) / jt::kStage1Tile;
+  uint64_t G = (len + piece / 2) / piece;
+  G = std::max<uint64_t>(2, std::min<uint64_t>(G, kMaxPieces));
+  return (unsigned)std::min<uint64_t>(G, tiles);
+}
+
+bool ensure_pieces(jt_parser *p, unsigned G) {
+  while (p->kids.size() < G) {
+    jt_parser *k = jt_parser_new();
+    if (!k) return false;
+    p->kids.push_back(k);
+  }
+  auto mk = [](cudaEvent_t *e) {
+    return *e || cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  };
+  while (p->done_ev.size() < G) {
+    cudaEvent_t e = nullptr;
+    if (!mk(&e)) return false;
+    p->done_ev.push_back(e);
+  }
+  if (!mk(&p->ev_fin)) return false;
+  if (p->h_sum_cap < G) {
+    if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
+    if (p->h_sum3) cudaFreeHost(p->h_sum3);
+    p->h_sum1_init = nullptr;
+    p->h_sum3 = nullptr;
+    p->h_sum_cap = 0;
+    if (cudaMallocHost((void **)&p->h_sum1_init, kMaxPieces * sizeof(jt::Sum1)) != cudaSuccess ||
+        cudaMallocHost((void **)&p->h_sum3, kMaxPieces * sizeof(jt::Sum3)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    for (unsigned k = 0; k < kMaxPieces; k++) {
+      jt::Sum1 z{};
+      z.utf8_pos = ~0ULL;
+      z.str_err = ~0ULL;
+      p->h_sum1_init[k] = z;  // pad[0] == 0: not written
+    }
+    p->h_sum_cap = kMaxPieces;
+  }
+  return p->psum.ensure(kMaxPieces * (sizeof(jt::Sum0) + sizeof(jt::Sum1) + sizeof(jt::Sum2) + sizeof(jt::Sum3)));
+}
+
+jt_error parse_pieces(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
+  static const bool trace = getenv("JT_TRACE") != nullptr;
+  auto now_us = []() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = trace ? now_us() : 0;
+  if (out) *out = nullptr;
+  const unsigned G = piece_count(len);
+  if (!ensure_input(p, len) || !ensure_stream(p, G) || !ensure_pieces(p, G)) {
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  // piece layout as shard.py layout(): tile-aligned cuts
+  const uint64_t tiles = (len + jt::kStage1Tile - 1) / jt::kStage1Tile;
+  std::vector<uint64_t> cut(G + 1);
+  for (unsigned g = 0; g < G; g++) cut[g] = (g * tiles / G) * jt::kStage1Tile;
+  cut[G] = len;
+  uint8_t *in = p->in.as<uint8_t>();
+  jt::Sum0 *s0 = (jt::Sum0 *)p->psum.p;
+  jt::Sum1 *s1 = (jt::Sum1 *)(s0 + kMaxPieces);
+  jt::Sum2 *s2 = (jt::Sum2 *)(s1 + kMaxPieces);
+  jt::Sum3 *s3 = (jt::Sum3 *)(s2 + kMaxPieces);
+  cudaStream_t cs = p->copy_stream, st = p->stream;
+  p->launches = 0;
+  p->needs_mat = false;
+  bool ok = cuda_ok(p, cudaEventRecord(p->ev_start, st), "event") &&
+            cuda_ok(p, cudaStreamWaitEvent(cs, p->ev_start, 0), "wait") &&
+            cuda_ok(p, cudaMemsetAsync(in + len, 0, input_capacity(len) - len, cs), "tail");
+  for (unsigned g = 0; ok && g < G; g++)
+    ok = cuda_ok(p, cudaMemcpyAsync(in + cut[g], data + cut[g], cut[g + 1] - cut[g], cudaMemcpyHostToDevice, cs),
+                 "H2D") &&
+         cuda_ok(p, cudaEventRecord(p->chunk_ev[g], cs), "event");
+  ok = ok && cuda_ok(p, cudaMemcpyAsync(s1, p->h_sum1_init, G * sizeof(jt::Sum1), cudaMemcpyHostToDevice, st),
+                     "sum1 init");
+  for (unsigned g = 0; ok && g < G; g++) {
+    jt_parser *k = p->kids[g];
+    k->in_alias = in;
+    k->stream = st;
+    ok = shard_setup(k, len, g, G, cut[g], cut[g + 1]) == 0;
+    if (!ok) p->err = k->err;
+  }
+  auto back = [&](unsigned g) {  // phases 2 + 3 of piece g, its control block and patches to the host
+    jt_parser *k = p->kids[g];
+    bool r = jt_b200_shard_phase(k, 2, s1, s2 + g) == 0 && jt_b200_shard_phase(k, 3, s2, s3 + g) == 0;
+    if (!r) p->err = k->err;
+    return r && cuda_ok(p, cudaMemcpyAsync(k->h_ctrl, k->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, st),
+                        "ctrl D2H") &&
+           cuda_ok(p, cudaMemcpyAsync(p->h_sum3 + g, s3 + g, sizeof(jt::Sum3), cudaMemcpyDeviceToHost, st),
+                   "sum3 D2H") &&
+           cuda_ok(p, cudaEventRecord(p->done_ev[g], st), "event");
+  };
+  for (unsigned g = 0; ok && g < G; g++) {
+    jt_parser *k = p->kids[g];
+    ok = cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[g], 0), "wait") &&
+         jt_b200_shard_phase(k, 0, nullptr, s0 + g) == 0 &&
+         cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[std::min(g + 1, G - 1)], 0), "wait") &&
+         jt_b200_shard_phase(k, 1, s0, s1 + g) == 0;
+    if (!ok && p->err.empty()) p->err = k->err;
+    if (ok && g > 0) ok = back(g - 1);
+  }
+  jt_parser *last = p->kids[G - 1];
+  ok = ok && back(G - 1) &&
+       cuda_ok(p, jt::shard_finish_launch(s2_args(last, len, 0, cut[G] - cut[G - 1], true), s3, st), "finish") &&
+       cuda_ok(p, cudaMemcpyAsync(last->h_ctrl, last->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, st),
+               "ctrl D2H") &&
+       cuda_ok(p, cudaEventRecord(p->ev_fin, st), "event");
+  if (trace) fprintf(stderr, " pieces: %u enqueued %.0f us\n", G, now_us() - t0);
+  // pieces come back as they finish; the host document is sized from the
+  // input (tape <= 1 word per input byte + 3 is not guaranteed: a larger
+  // document is downloaded whole below)
+  jt_document *d = nullptr;
+  bool early = false, failed = false;
+  uint64_t tbase = 0, sbase = 0, S = 0;
+  if (ok && out) {
+    d = new (std::nothrow) jt_document;
+    early = d && d->alloc(len / 8 + 1024, len + len / 4 + 64);
+  }
+  for (unsigned g = 0; ok && g < G; g++) {
+    if (!cuda_ok(p, cudaEventSynchronize(p->done_ev[g]), "sync")) {
+      ok = false;
+      break;
+    }
+    const jt::Ctrl &c = *p->kids[g]->h_ctrl;
+    if (c.utf8_pos != ~0ULL || c.err_key != ~0ULL || c.redo) failed = true;  // no document: result below
+    const uint64_t lo = g == 0 ? 0 : 1, hi = c.tape_words + (g + 1 == G ? 1 : 0);
+    if (early && !failed) {
+      if (tbase + hi > d->tape.size() || sbase + c.string_bytes > d->strings.size()) {
+        early = false;
+      } else {
+        jt_parser *k = p->kids[g];
+        ok = cuda_ok(p, cudaStreamWaitEvent(p->d2h_stream, p->done_ev[g], 0), "wait") &&
+             cuda_ok(p, cudaMemcpyAsync(d->tape.data() + tbase + lo, k->tape.as<uint64_t>() + lo, (hi - lo) * 8,
+                                        cudaMemcpyDeviceToHost, p->d2h_stream),
+                     "tape piece D2H") &&
+             (!c.string_bytes ||
+              cuda_ok(p, cudaMemcpyAsync(d->strings.data() + sbase, k->strings.p, c.string_bytes,
+                                         cudaMemcpyDeviceToHost, p->d2h_stream),
+                      "strings piece D2H"));
+      }
+    }
+    if (trace && (g < 2 || g + 2 >= G || g % 4 == 0)) fprintf(stderr, " piece %u done %.0f us\n", g, now_us() - t0);
+    tbase += c.tape_words - 1;
+    sbase += c.string_bytes;
+    S += c.S;
+  }
+  if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_fin), "sync") ||
+      !cuda_ok(p, cudaStreamSynchronize(p->d2h_stream), "sync") || !cuda_ok(p, cudaStreamSynchronize(cs), "sync")) {
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(p->d2h_stream);
+    delete d;
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
+  p->launches = 0;
+  bool redo = false;
+  for (unsigned g = 0; g < G; g++) {
+    p->launches += p->kids[g]->launches;
+    redo = redo || p->kids[g]->h_ctrl->redo;
+  }
+  p->in_len = len;
+  if (redo) {  // a piece needed a summary that did not exist yet: parse resident
+    delete d;
+    return parse_resident(p, len, out, off);
+  }
+  const jt::Ctrl &c = *last->h_ctrl;
+  const jt_error e = (jt_error)c.code;
+  set_off(off, c.offset);
+  // the parser's index / tape / strings: rebuilt from the resident input when read
+  p->needs_mat = true;
+  p->last_ok = false;
+  if (c.code != jt::kUtf8Error) {
+    p->have_index = true;
+    p->index_count = S;
+    p->h_index_valid = false;
+  }
+  const double t4 = trace ? now_us() : 0;
+  if (e != JT_OK || !out) {
+    delete d;
+    return e;
+  }
+  const uint64_t E = tbase + 1;  // root close index = 1 + sum of token widths
+  if (!d || !early) {  // larger than the early host blocks: the pieces whole
+    delete d;
+    d = new (std::nothrow) jt_document;
+    if (!d || !d->alloc(E + 1, sbase)) {
+      delete d;
+      set_off(off, -1);
+      return JT_CAPACITY;
+    }
+    uint64_t tb = 0, sb = 0;
+    for (unsigned g = 0; g < G; g++) {
+      jt_parser *k = p->kids[g];
+      const jt::Ctrl &kc = *k->h_ctrl;
+      const uint64_t lo = g == 0 ? 0 : 1, hi = kc.tape_words + (g + 1 == G ? 1 : 0);
+      if (!cuda_ok(p, cudaMemcpyAsync(d->tape.data() + tb + lo, k->tape.as<uint64_t>() + lo, (hi - lo) * 8,
+                                      cudaMemcpyDeviceToHost, st),
+                   "tape D2H") ||
+          (kc.string_bytes && !cuda_ok(p, cudaMemcpyAsync(d->strings.data() + sb, k->strings.p, kc.string_bytes,
+                                                          cudaMemcpyDeviceToHost, st),
+                                       "strings D2H"))) {
+        delete d;
+        set_off(off, -1);
+        return JT_CAPACITY;
+      }
+      tb += kc.tape_words - 1;
+      sb += kc.string_bytes;
+    }
+    if (!cuda_ok(p, cudaStreamSynchronize(st), "sync")) {
+      delete d;
+      set_off(off, -1);
+      return JT_CAPACITY;
+    }
+  } else {
+    d->tape.n = E + 1;
+    d->strings.n = sbase;
+  }
+  // brackets whose opener lives in an earlier piece; the root word
+  for (unsigned g = 0; g < G; g++) {
+    const jt::Sum3 &r = p->h_sum3[g];
+    const uint32_t n = std::min<uint32_t>(r.patch_n, (uint32_t)jt::kBoundMax);
+    for (uint32_t q = 0; q < n; q++)
+      if (r.patch[2 * q] < E + 1) d->tape.data()[r.patch[2 * q]] = r.patch[2 * q + 1];
+  }
+  d->tape.data()[0] = jt::tape_word(jt::kTagRoot, E);
+  *out = d;
+  if (trace)
+    fprintf(stderr, "parse_pieces: %u pieces, all done %.0f us, document %.0f us (early %d)\n", G, t4 - t0,
+            now_us() - t0, (int)early);
+  return e;
+}
+
+// The calls that read the parser's resident state after a parse_pieces
+// (index positions, jt_stage2, device views, distinct_values) parse the
+// resident input once more here.
+void materialize(const jt_parser *cp) {
+  jt_parser *p = const_cast<jt_parser *>(cp);
+  if (!p->needs_mat) return;
+  p->needs_mat = false;
+  parse_resident(p, p->in_len, nullptr, nullptr);
+}
+
 }  // namespace
 
 extern "C" {
@@ -811,6 +1146,11 @@ jt_parser *jt_parser_new(void) {
 void jt_parser_free(jt_parser *p) {
   if (!p) return;
   cudaStreamSynchronize(p->stream);
+  for (jt_parser *k : p->kids) {  // children run on this parser's stream
+    k->stream = k->own_stream;
+    jt_parser_free(k);
+  }
+  p->kids.clear();
   for (auto &g : p->graph)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto &g : p->graph_s1)
@@ -839,6 +1179,10 @@ void jt_parser_free(jt_parser *p) {
   if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->ev_s1) cudaEventDestroy(p->ev_s1);
   if (p->h_ctrl_s1) cudaFreeHost(p->h_ctrl_s1);
+  for (cudaEvent_t e : p->done_ev) cudaEventDestroy(e);
+  if (p->ev_fin) cudaEventDestroy(p->ev_fin);
+  if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
+  if (p->h_sum3) cudaFreeHost(p->h_sum3);
   delete p;
 }
 
@@ -856,7 +1200,13 @@ jt_error jt_parse(jt_parser *p, const char *data, size_t len, jt_document **out,
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
-  if ((uint64_t)len >= kStreamMin) return parse_stream(p, data, len, out, error_offset);
+  if ((uint64_t)len >= kStreamMin) {
+    // stream mode 1: stage 2 per piece as well (parse_pieces).  Measured
+    // slower on C1 (25.4 vs 27.7 GB/s e2e): the shard phases of a piece take
+    // longer on the GPU than the piece's upload (~250 vs ~170 us per 8 MiB)
+    return p->stream_mode == 1 ? parse_pieces(p, data, len, out, error_offset)
+                               : parse_stream(p, data, len, out, error_offset);
+  }
   if (!upload(p, data, len)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -879,6 +1229,7 @@ jt_error jt_stage1(jt_parser *p, const char *data, size_t len, long long *error_
 size_t jt_index_count(const jt_parser *p) { return p->have_index ? (size_t)p->index_count : 0; }
 
 const uint32_t *jt_index_positions(const jt_parser *p) {
+  materialize(p);
   if (!p->h_index_valid) {
     p->h_index.assign(p->index_count + 8, 0u);
     if (p->index_count)
@@ -890,6 +1241,7 @@ const uint32_t *jt_index_positions(const jt_parser *p) {
 
 jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
   if (out) *out = nullptr;
+  materialize(p);
   uint64_t len = p->in_len;
   if (!ensure_stage2(p, len)) {
     set_off(error_offset, -1);
@@ -1179,6 +1531,7 @@ char *jt_document_distinct(const jt_document *doc, const char *path) {
 // jt_document_distinct on the downloaded document.  NULL without such a
 // parse or on a device error.
 char *jt_b200_distinct(jt_parser *p, const char *path) {
+  materialize(p);
   if (!p || !p->last_ok || !path) return nullptr;
   std::set<DVal> vals;
   if (!*path) return malloc_string(std::string());
@@ -1386,6 +1739,7 @@ const char *jt_error_name(jt_error code) {
 
 void *jt_b200_input_buffer(jt_parser *p, size_t len) {
   if ((uint64_t)len >= (1ULL << 32)) return nullptr;
+  materialize(p);  // the resident state of a streamed parse still needs its input
   if (!ensure_input(p, len) || !zero_tail(p, len)) return nullptr;
   if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) return nullptr;
   return p->in.p;
@@ -1402,6 +1756,7 @@ int jt_b200_copy_in(jt_parser *p, const void *src, size_t len) {
 // Enqueue (no wait) a copy of bytes [offset, offset + n) of a host or device
 // document `src` into the same positions of the input buffer.
 int jt_b200_copy_in_range(jt_parser *p, const void *src, size_t offset, size_t n) {
+  materialize(p);
   if (offset + n > p->in.cap) return -1;
   if (n && !cuda_ok(p, cudaMemcpyAsync(p->in.as<uint8_t>() + offset, (const uint8_t *)src + offset, n,
                                        cudaMemcpyDefault, p->stream),
@@ -1463,26 +1818,32 @@ jt_error jt_b200_finish(jt_parser *p, long long *error_offset) {
 }
 
 const uint32_t *jt_b200_device_index(const jt_parser *p, size_t *count) {
+  materialize(p);
   if (count) *count = jt_index_count(p);
   return p->idx[p->cur].as<uint32_t>();
 }
 
 const uint64_t *jt_b200_device_tape(const jt_parser *p, size_t *words) {
+  materialize(p);
   if (words) *words = p->last_ok ? p->last_tape_len : 0;
   return p->tape.as<uint64_t>();
 }
 
 const uint8_t *jt_b200_device_strings(const jt_parser *p, size_t *bytes) {
+  materialize(p);
   if (bytes) *bytes = p->last_ok ? p->last_string_bytes : 0;
   return p->strings.as<uint8_t>();
 }
 
 jt_error jt_b200_download(jt_parser *p, jt_document **out) {
   *out = nullptr;
+  materialize(p);
   if (!p->last_ok) return JT_CAPACITY;
   *out = download(p);
   return *out ? JT_OK : JT_CAPACITY;
 }
+
+void jt_b200_set_stream_mode(jt_parser *p, int mode) { p->stream_mode = mode == 1 ? 1 : 0; }
 
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
   p->stream = cuda_stream ? (cudaStream_t)cuda_stream : p->own_stream;
@@ -1494,6 +1855,7 @@ void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
 // the record alone would.  Waits; one host sync after the newline count.
 int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   if (n_records) *n_records = 0;
+  p->needs_mat = false;  // the resident state becomes this parse's
   if ((uint64_t)len >= (1ULL << 32) || !ensure_input(p, len) || !ensure_stage1(p, len, 0) ||
       !ensure_stage2(p, len) ||
       !p->nlbuf.ensure(jt::stage1_records(len) * 2 * sizeof(uint32_t) + 64)) {
@@ -1642,42 +2004,7 @@ size_t jt_b200_shard_summary_bytes(int phase) {
 }
 
 int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
-  if (G == 0 || g >= G || (uint64_t)len >= (1ULL << 32) || begin % jt::kStage1Tile != 0 ||
-      !(begin < end) || end > len || (g + 1 == G) != (end == len) || (g == 0) != (begin == 0)) {
-    p->err = "shard_begin: bad shard layout";
-    return -1;
-  }
-  if (!p->h_shard && cudaMallocHost((void **)&p->h_shard, sizeof(jt::Shard)) != cudaSuccess) {
-    cudaGetLastError();
-    p->h_shard = nullptr;
-    p->err = "shard_begin: pinned allocation";
-    return -1;
-  }
-  const uint64_t range = end - begin;
-  if (!ensure_input(p, len) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
-      !p->shard.ensure(kShardBoundOff + jt::kBoundMax * sizeof(uint64_t))) {
-    p->err = "shard_begin: device allocation";
-    return -1;
-  }
-  jt::Shard h{};
-  h.g = g;
-  h.G = G;
-  h.begin = begin;
-  h.end = end;
-  h.len = len;
-  *p->h_shard = h;
-  if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
-                                  p->stream),
-               "shard upload"))
-    return -1;
-  p->shard_on = true;
-  p->shard_len = len;
-  p->in_len = len;
-  p->cur = 0;
-  p->last_ok = false;
-  p->have_index = false;
-  p->h_index_valid = false;
-  return 0;
+  return shard_setup(p, len, g, G, begin, end);
 }
 
 // Enqueue phase 0..3 of this shard (shard.h).  `gathered` = device pointer

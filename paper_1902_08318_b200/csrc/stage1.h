@@ -65,6 +65,10 @@ cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
 // one chunk of a streamed document (rec_tile0 / last_tile / init_state /
 // out_state set): K0a, K0b, K1
 cudaError_t stage1_chunk_launch(const Stage1Args &args, cudaStream_t stream);
+// the same split in two: K0a + K0b over the piece's tiles, then K1 over a
+// tile range (streamed jt_parse runs K1 one tile behind the piece boundary)
+cudaError_t stage1_chunk_carry(const Stage1Args &args, cudaStream_t stream);
+cudaError_t stage1_chunk_main(const Stage1Args &args, cudaStream_t stream);
 // after a streamed stage 1: the string length fields K1 left to stage 2
 cudaError_t stage1_lengths_launch(const Stage1Args &args, uint64_t ntiles, cudaStream_t stream);
 

@@ -746,15 +746,36 @@ __host__ __device__ constexpr int arrival_state(uint32_t cl1, uint32_t sc1) {
   return cl1 == C_OBR ? M_OF : cl1 == C_ABR ? M_AF : cl1 == C_COL ? M_V : cl1 == C_COM ? (sc1 ? M_K : M_V) : M_A;
 }
 
-template <class Tree>
+// A byte-range shard's place in the document (shard.h) for struct_tokens:
+// depth / tape / token bases, the two tokens before the shard and the
+// containers open at its start (a.bound).  Unsharded: all zero, is_last.
+struct ShardPos {
+  int db;             // depth at the shard start
+  uint32_t tb;        // tape base: document tape index = tb + local index
+  uint64_t token_base;
+  uint32_t prev0, prev1;  // bytes of the tokens before the shard (prev0 nearest)
+  int64_t before;     // how many exist (<= 2)
+  int open_n;         // containers open at the shard start
+  bool is_last;
+};
+
+template <bool kShard, class Tree>
 __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, uint64_t S, const Tree &T,
                                               uint64_t tbase, uint64_t tend, const uint16_t *s_tr,
-                                              const uint8_t *s_cls, const uint8_t *s_arr) {
+                                              const uint8_t *s_cls, const uint8_t *s_arr, const ShardPos &sp,
+                                              uint64_t cstart) {
   const int lane = threadIdx.x & 31;
-  auto rec = [&](uint64_t j) -> uint32_t { return j >= tbase ? T.tok[j - tbase] : a.tok[j]; };
+  const bool bound_obj = kShard && sp.open_n > 0 && (a.bound[sp.open_n - 1] >> 56) == '{';
+  // tokens before the shard: their bytes, and the innermost container open
+  // at the boundary for their scope bit (only read for , and key strings)
+  auto rec = [&](int64_t j) -> uint32_t {
+    if (j >= (int64_t)tbase) return T.tok[j - tbase];
+    if (!kShard || j >= 0) return a.tok[j];
+    return j == -1 ? sp.prev0 : sp.prev1;
+  };
   // one warp per 32 consecutive tokens (lane = token), so the two previous
   // tokens, the scope bits and most bracket partners are a shuffle away
-  for (uint64_t cb = tbase + 32 * (threadIdx.x >> 5); cb < tend; cb += blockDim.x) {
+  for (uint64_t cb = cstart + 32 * (threadIdx.x >> 5); cb < tend; cb += blockDim.x) {
     const uint64_t i = cb + lane;
     const bool live = i < tend;
     const uint32_t v = live ? T.tok[i - tbase] : (uint32_t)'x';
@@ -763,24 +784,26 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
     const bool fail = (v >> 8) & 1;
     const int D = tok_depth(v);
     const uint32_t sw = a.scopebits[cb >> 5];             // bit l: token cb + l in an object
-    const uint32_t swp = cb ? a.scopebits[(cb >> 5) - 1] : 0u;
+    const uint32_t swp = cb ? a.scopebits[(cb >> 5) - 1] : (bound_obj ? ~0u : 0u);
     const uint64_t sw2 = ((uint64_t)sw << 32) | swp;     // bit 32 + l - k: token i - k
     const uint32_t sc0 = (sw >> lane) & 1, sc1 = (uint32_t)(sw2 >> (31 + lane)) & 1,
                    sc2 = (uint32_t)(sw2 >> (30 + lane)) & 1;
     uint32_t cl1 = __shfl_up_sync(0xffffffffu, cl, 1), cl2 = __shfl_up_sync(0xffffffffu, cl, 2);
     if (lane < 2) {
-      if (lane == 0) cl1 = i >= 1 ? s_cls[rec(i - 1) & 0xFF] : C_BAD;
-      cl2 = i >= 2 ? s_cls[rec(i - 2) & 0xFF] : C_BAD;
+      const int64_t gi = (int64_t)i + (kShard ? sp.before : 0);  // tokens before i in the document
+      if (lane == 0) cl1 = gi >= 1 ? s_cls[rec((int64_t)i - 1) & 0xFF] : C_BAD;
+      cl2 = gi >= 2 ? s_cls[rec((int64_t)i - 2) & 0xFF] : C_BAD;
     }
     const uint32_t ti = live ? a.tape_idx[i] : 0u;
     // arrival state from the two previous tokens (App. A.5)
     const bool key1 = cl1 == C_STR && (cl2 == C_OBR || (cl2 == C_COM && sc2));  // i-1 was a key
     int mode = key1 ? M_C : (int)s_arr[2 * cl1 + sc1];
-    if (i == 0) mode = M_V;
+    if (i == 0 && (!kShard || sp.token_base == 0)) mode = M_V;
     const uint32_t e = s_tr[mode * kNCls + cl];
     int err = (int)((fail ? e >> 3 : e) & 7);
-    if ((e & kTrOpen) && D >= kMaxDepth && !err) err = kDepthError;
-    if (mode == M_A && D <= 0) err = kTapeError;
+    const int Dd = D + (kShard ? sp.db : 0);  // document depth
+    if ((e & kTrOpen) && Dd >= kMaxDepth && !err) err = kDepthError;
+    if (mode == M_A && Dd <= 0) err = kTapeError;
     if ((e & kTrKind) && sc0 != (cl == C_OCL ? 1u : 0u)) err = kTapeError;
     const int after = (e & kTrComma) ? (sc0 ? M_K : M_V) : (int)((e >> 6) & 7);
     // bracket partners: the opener is the previous token with depth <= D - 1;
@@ -822,27 +845,43 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
       uint32_t tj = tj_w;
       if (j == -2) j = psv_tile_masked(a, T, (int64_t)pb, D - 1);
       if (j >= 0 && (j < (int64_t)cb)) tj = a.tape_idx[j];
-      if (j < 0) {
-        err = kTapeError;
+      const uint64_t ow = tape_word(cl == C_OCL ? '{' : '[', (kShard ? sp.tb : 0u) + ti + 1);
+      if (j >= 0) {
+        a.tape[ti] = tape_word((uint8_t)c, (kShard ? sp.tb : 0u) + tj);
+        a.tape[tj] = ow;
+      } else if (kShard && Dd - 1 >= 0 && Dd - 1 < sp.open_n) {
+        // the opener lives in an earlier shard: patched after the last exchange
+        const uint64_t at = a.bound[Dd - 1] & ((1ULL << 56) - 1);
+        a.tape[ti] = tape_word((uint8_t)c, at);
+        const uint32_t k = atomicAdd(&a.sum3->patch_n, 1u);
+        if (k < (uint32_t)kBoundMax) {
+          a.sum3->patch[2 * k] = at;
+          a.sum3->patch[2 * k + 1] = ow;
+        }
       } else {
-        a.tape[ti] = tape_word((uint8_t)c, tj);
-        a.tape[tj] = tape_word(cl == C_OCL ? '{' : '[', ti + 1);
+        err = kTapeError;
       }
     }
+    const uint64_t tokbase = kShard ? sp.token_base : 0;
     if (err && live) {
-      report(ctrl, i, err);
-    } else if (live && i == S - 1) {  // the root value must be complete
-      const int depth_after = D + (cl <= C_ABR ? 1 : cl <= C_ACL ? -1 : 0);
-      if (!(after == M_A && depth_after == 0)) report(ctrl, S, kTapeError);
+      report(ctrl, tokbase + i, err);
+    } else if (live && i == S - 1 && (!kShard || sp.is_last)) {  // the root value must be complete
+      const int depth_after = Dd + (cl <= C_ABR ? 1 : cl <= C_ACL ? -1 : 0);
+      if (!(after == M_A && depth_after == 0)) report(ctrl, tokbase + S, kTapeError);
     }
   }
 }
 
+// 4 CTAs (32 warps) per SM: the token-parallel path is latency-bound, so
+// occupancy beats registers (79 -> 64 registers, no spills)
+#ifndef JT_STRUCT_MINB
+#define JT_STRUCT_MINB 4
+#endif
 // kMode: 0 one document, 1 a byte-range shard (shard.h), 2 NDJSON records.
 // kDeep: the instance for documents deeper than 64 (masked tree search); for
 // one document both instances are launched and the other one returns.
 template <int kMode, bool kDeep = false>
-__global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
+__global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   constexpr bool kShard = kMode == 1, kRecs = kMode == 2;
   __shared__ __align__(16) uint32_t s_tok[kK3Tile];
   __shared__ __align__(16) int16_t s_l1[256];
@@ -850,7 +889,7 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
   __shared__ uint16_t s_tr[6 * kNCls];
   __shared__ uint8_t s_cls[256];
   __shared__ uint8_t s_arr[2 * kNCls];
-  if (kMode == 0) {
+  if (kMode <= 1) {
     s_cls[threadIdx.x] = (uint8_t)token_class(threadIdx.x);
     if (threadIdx.x < 2 * kNCls) s_arr[threadIdx.x] = (uint8_t)arrival_state(threadIdx.x >> 1, threadIdx.x & 1);
     if (threadIdx.x < 6 * kNCls) s_tr[threadIdx.x] = (uint16_t)tr_entry(threadIdx.x / kNCls, threadIdx.x % kNCls);
@@ -914,7 +953,12 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     if (j >= 0) return a.tok[j];
     return j == -1 ? prev0 : prev1;
   };
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // token-parallel path on few tiles (a streamed piece, a small document):
+  // kSplit CTAs share a tile (each loads it for the tree, checks a quarter),
+  // so the per-tile latency of 16 chunk rounds per warp is spread out
+  const uint32_t split = (kMode <= 1 && shallow && 2 * ntiles <= (uint64_t)gridDim.x) ? 4u : 1u;
+  for (uint64_t work = blockIdx.x; work < ntiles * split; work += gridDim.x) {
+    const uint64_t tile = work / split;
     const uint64_t tbase = tile * kK3Tile;
     {
       const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
@@ -945,8 +989,10 @@ __global__ void __launch_bounds__(256) k_struct(Stage2Args a) {
     }
     __syncthreads();
     const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase};
-    if (kMode == 0 && shallow) {  // token-parallel grammar check
-      struct_tokens(a, ctrl, S, T, tbase, min(tbase + kK3Tile, S), s_tr, s_cls, s_arr);
+    if (kMode <= 1 && shallow) {  // token-parallel grammar check
+      const ShardPos sp{db, tb, token_base, prev0, prev1, before, open_n, is_last};
+      const uint64_t part = kK3Tile / split, c0 = tbase + (work % split) * part;
+      struct_tokens<kShard>(a, ctrl, S, T, tbase, min(c0 + part, S), s_tr, s_cls, s_arr, sp, c0);
       __syncthreads();
       continue;
     }
@@ -1330,6 +1376,7 @@ __global__ void k_sum1(Stage2Args a, Sum1 *out) {
   r.first_aux = r.S ? a.aux[0] : 0;
   r.last[0] = r.S >= 1 ? (a.tok[r.S - 1] & 0xFF) : 0;
   r.last[1] = r.S >= 2 ? (a.tok[r.S - 2] & 0xFF) : 0;
+  r.pad[0] = 1;  // written (a streamed parse gathers the summaries as they appear)
   *out = r;
 }
 
@@ -1368,6 +1415,10 @@ __global__ void k_apply1(Stage2Args a, const Sum1 *gs) {
   h->next_aux = sb - h->string_base;
   uint64_t run = 0;
   for (uint32_t k = g; k < G; k++) {
+    if (k > g && gs[k].pad[0] == 0) {  // not parsed yet (streamed pieces): the caller redoes the parse
+      c->redo = 1;
+      break;
+    }
     if (k > g && gs[k].S > 0) {
       h->next_pos = gs[k].first_pos;
       h->next_aux = run + gs[k].first_aux;

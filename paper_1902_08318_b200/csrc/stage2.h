@@ -37,7 +37,7 @@ struct Ctrl {
   uint64_t n_newlines;          // record mode: '\n' bytes (K0)
   // results written by the finalize kernel
   int32_t code;
-  int32_t pad2;
+  int32_t redo;                 // streamed pieces: a later piece's summary was needed before it existed
   long long offset;
   uint64_t tape_len;            // E + 1 on success
 };

@@ -175,6 +175,56 @@ def test_streamed_jt_parse(parser, oracle):
         check_same(parser, oracle, data, where)
 
 
+def _piece_cut(length: int) -> int:
+    """First cut of parse_pieces (engine.cu piece_count, 8 MiB pieces, >= 2)."""
+    piece = 8 << 20
+    tiles = (length + 16383) // 16384
+    G = max(2, min(64, (length + piece // 2) // piece))
+    return (tiles // G) * 16384
+
+
+def test_streamed_pieces(parser, oracle):
+    """Streamed jt_parse with stage 2 per piece (engine.cu parse_pieces):
+    escapes, numbers, atoms and brackets across the piece cut, a piece
+    without a token start (resident re-parse), deep nesting across pieces,
+    and the resident state (index, jt_stage2) read after the streamed parse."""
+    from paper_1902_08318_b200 import Parser
+    from tools.gen import generate
+    parser = Parser()
+    parser.set_stream_mode(1)
+    n = 12 << 20
+    cut = _piece_cut(n)
+    filler = generate(0, cut - 4096, seed=11)[1:-1]  # object members of a top-level array
+    escs = [b"\\u00e9", b"\\ud83d\\ude00", b"\\n", b"\\\\", b"\\u20ac"]
+    for esc in escs:
+        for shift in (1, 2, 5, 7, 11):
+            head = b"[" + filler + b',"'
+            pad = cut - shift - len(head)
+            doc = head + b"q" * pad + esc + b'", 1.25e-3, true, {"k": [null]}'
+            doc = doc + b"," + generate(0, n - len(doc), seed=12)[1:]
+            assert doc.index(esc, len(head)) == cut - shift
+            check_same(parser, oracle, doc, f"esc {esc!r} at cut-{shift}")
+    for shift in range(1, 24, 3):  # number / atom / bracket tokens straddling the cut
+        head = b"[" + filler + b","
+        pad = cut - shift - len(head)
+        for tok in (b"-12345678901234567.5e-7", b"true", b"null", b"[[]]", b'{"a":{}}'):
+            doc = head + b" " * pad + tok + b"," + generate(0, n - cut, seed=13)[1:]
+            check_same(parser, oracle, doc, f"token {tok!r} at cut-{shift}")
+    # a middle piece without any token start: resident re-parse
+    s = b'[1,"' + b"z" * (20 << 20) + b'",2]'
+    check_same(parser, oracle, s, "token-free piece")
+    # nesting deeper than 64 opened in one piece and closed in a later one
+    deep = b"[" * 900 + generate(1, 16 << 20, seed=14) + b"]" * 900
+    check_same(parser, oracle, deep, "deep across pieces")
+    # jt_stage2 after a streamed jt_parse re-uses the retained input + index
+    data = generate(1, 10 << 20, seed=15)
+    check_same(parser, oracle, data, "C1 10 MiB")
+    r = parser.stage2()
+    o = oracle.parse(data)
+    assert r.name == "OK" and np.array_equal(r.document.tape, o.tape_array())
+    assert r.document.strings == o.strings
+
+
 def test_minify(parser, oracle):
     """jt_minify on the GPU (k_minify) vs the oracle (pinned to the
     reference's jt_minify in test_oracle_vs_ref.py)"""
