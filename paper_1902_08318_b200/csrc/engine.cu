@@ -239,6 +239,7 @@ struct jt_parser {
   std::vector<jt_parser *> kids;
   std::vector<cudaEvent_t> done_ev;
   cudaEvent_t ev_fin = nullptr;
+  cudaStream_t s2_stream = nullptr;   // pieces' stage 2: high priority, ahead of later pieces' stage 1
   DevBuf psum;                        // gathered Sum0 | Sum1 | Sum2 | Sum3 of the pieces
   jt::Sum1 *h_sum1_init = nullptr;    // pinned: "not written yet" Sum1s
   jt::Sum3 *h_sum3 = nullptr;         // pinned: the pieces' Sum3 (bracket patches)
@@ -798,7 +799,8 @@ jt_error parse_resident(jt_parser *p, uint64_t len, jt_document **out, long long
 
 // Byte-range shard setup (shard.h) shared by jt_b200_shard_begin and the
 // pieces of a streamed jt_parse (children alias the parent's input).
-int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
+int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end,
+                bool streamed = false) {
   if (G == 0 || g >= G || (uint64_t)len >= (1ULL << 32) || begin % jt::kStage1Tile != 0 ||
       !(begin < end) || end > len || (g + 1 == G) != (end == len) || (g == 0) != (begin == 0)) {
     p->err = "shard_begin: bad shard layout";
@@ -822,6 +824,7 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
   h.begin = begin;
   h.end = end;
   h.len = len;
+  h.streamed = streamed ? 1u : 0u;
   *p->h_shard = h;
   if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
                                   p->stream),
@@ -883,6 +886,15 @@ bool ensure_pieces(jt_parser *p, unsigned G) {
     p->done_ev.push_back(e);
   }
   if (!mk(&p->ev_fin)) return false;
+  if (!p->s2_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&p->s2_stream, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      cudaGetLastError();
+      p->s2_stream = nullptr;
+      return false;
+    }
+  }
   if (p->h_sum_cap < G) {
     if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
     if (p->h_sum3) cudaFreeHost(p->h_sum3);
@@ -925,52 +937,69 @@ jt_error parse_pieces(jt_parser *p, const char *data, uint64_t len, jt_document 
   uint8_t *in = p->in.as<uint8_t>();
   jt::Sum0 *s0 = (jt::Sum0 *)p->psum.p;
   jt::Sum1 *s1 = (jt::Sum1 *)(s0 + kMaxPieces);
-  jt::Sum2 *s2 = (jt::Sum2 *)(s1 + kMaxPieces);
-  jt::Sum3 *s3 = (jt::Sum3 *)(s2 + kMaxPieces);
-  cudaStream_t cs = p->copy_stream, st = p->stream;
+  jt::Sum2 *sum2 = (jt::Sum2 *)(s1 + kMaxPieces);
+  jt::Sum3 *s3 = (jt::Sum3 *)(sum2 + kMaxPieces);
+  // stage 1 of the pieces on the parser's stream, stage 2 on a high-priority
+  // stream (its short kernels go ahead of the next pieces' stage-1 tiles)
+  cudaStream_t cs = p->copy_stream, st = p->stream, s2 = p->s2_stream;
   p->launches = 0;
   p->needs_mat = false;
+  // JT_TRACE: device timeline of the pieces (upload / stage 1 / stage 2 done)
+  std::vector<cudaEvent_t> tev;
+  if (trace) {
+    tev.resize(3 * G + 1);
+    for (auto &e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], st);
+  }
+  auto mark = [&](int k, cudaStream_t s_) {
+    if (trace) cudaEventRecord(tev[k], s_);
+  };
   bool ok = cuda_ok(p, cudaEventRecord(p->ev_start, st), "event") &&
             cuda_ok(p, cudaStreamWaitEvent(cs, p->ev_start, 0), "wait") &&
             cuda_ok(p, cudaMemsetAsync(in + len, 0, input_capacity(len) - len, cs), "tail");
-  for (unsigned g = 0; ok && g < G; g++)
+  for (unsigned g = 0; ok && g < G; g++) {
     ok = cuda_ok(p, cudaMemcpyAsync(in + cut[g], data + cut[g], cut[g + 1] - cut[g], cudaMemcpyHostToDevice, cs),
                  "H2D") &&
          cuda_ok(p, cudaEventRecord(p->chunk_ev[g], cs), "event");
+    mark(1 + g, cs);
+  }
   ok = ok && cuda_ok(p, cudaMemcpyAsync(s1, p->h_sum1_init, G * sizeof(jt::Sum1), cudaMemcpyHostToDevice, st),
                      "sum1 init");
   for (unsigned g = 0; ok && g < G; g++) {
     jt_parser *k = p->kids[g];
     k->in_alias = in;
     k->stream = st;
-    ok = shard_setup(k, len, g, G, cut[g], cut[g + 1]) == 0;
+    ok = shard_setup(k, len, g, G, cut[g], cut[g + 1], true) == 0;
     if (!ok) p->err = k->err;
   }
-  auto back = [&](unsigned g) {  // phases 2 + 3 of piece g, its control block and patches to the host
+  auto back = [&](unsigned g) {  // phases 2 + 3 of piece g (side stream), its control block and patches
     jt_parser *k = p->kids[g];
-    bool r = jt_b200_shard_phase(k, 2, s1, s2 + g) == 0 && jt_b200_shard_phase(k, 3, s2, s3 + g) == 0;
-    if (!r) p->err = k->err;
-    return r && cuda_ok(p, cudaMemcpyAsync(k->h_ctrl, k->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, st),
+    k->stream = s2;
+    bool r = cuda_ok(p, cudaStreamWaitEvent(s2, p->piece_ev[std::min(g + 1, G - 1)], 0), "wait") &&
+             jt_b200_shard_phase(k, 2, s1, sum2 + g) == 0 && jt_b200_shard_phase(k, 3, sum2, s3 + g) == 0;
+    if (!r && p->err.empty()) p->err = k->err;
+    return r && cuda_ok(p, cudaMemcpyAsync(k->h_ctrl, k->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, s2),
                         "ctrl D2H") &&
-           cuda_ok(p, cudaMemcpyAsync(p->h_sum3 + g, s3 + g, sizeof(jt::Sum3), cudaMemcpyDeviceToHost, st),
-                   "sum3 D2H") &&
-           cuda_ok(p, cudaEventRecord(p->done_ev[g], st), "event");
+           cuda_ok(p, cudaEventRecord(p->done_ev[g], s2), "event") && (mark(1 + 2 * G + g, s2), true);
   };
   for (unsigned g = 0; ok && g < G; g++) {
     jt_parser *k = p->kids[g];
     ok = cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[g], 0), "wait") &&
          jt_b200_shard_phase(k, 0, nullptr, s0 + g) == 0 &&
          cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[std::min(g + 1, G - 1)], 0), "wait") &&
-         jt_b200_shard_phase(k, 1, s0, s1 + g) == 0;
+         jt_b200_shard_phase(k, 1, s0, s1 + g) == 0 &&
+         cuda_ok(p, cudaEventRecord(p->piece_ev[g], st), "event");
+    mark(1 + G + g, st);
     if (!ok && p->err.empty()) p->err = k->err;
     if (ok && g > 0) ok = back(g - 1);
   }
   jt_parser *last = p->kids[G - 1];
   ok = ok && back(G - 1) &&
-       cuda_ok(p, jt::shard_finish_launch(s2_args(last, len, 0, cut[G] - cut[G - 1], true), s3, st), "finish") &&
-       cuda_ok(p, cudaMemcpyAsync(last->h_ctrl, last->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, st),
+       cuda_ok(p, jt::shard_finish_launch(s2_args(last, len, 0, cut[G] - cut[G - 1], true), s3, s2), "finish") &&
+       cuda_ok(p, cudaMemcpyAsync(last->h_ctrl, last->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, s2),
                "ctrl D2H") &&
-       cuda_ok(p, cudaEventRecord(p->ev_fin, st), "event");
+       cuda_ok(p, cudaMemcpyAsync(p->h_sum3, s3, G * sizeof(jt::Sum3), cudaMemcpyDeviceToHost, s2), "sum3 D2H") &&
+       cuda_ok(p, cudaEventRecord(p->ev_fin, s2), "event");
   if (trace) fprintf(stderr, " pieces: %u enqueued %.0f us\n", G, now_us() - t0);
   // pieces come back as they finish; the host document is sized from the
   // input (tape <= 1 word per input byte + 3 is not guaranteed: a larger
@@ -1010,14 +1039,24 @@ jt_error parse_pieces(jt_parser *p, const char *data, uint64_t len, jt_document 
     sbase += c.string_bytes;
     S += c.S;
   }
-  if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_fin), "sync") ||
+  if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_fin), "sync") || !cuda_ok(p, cudaStreamSynchronize(st), "sync") ||
       !cuda_ok(p, cudaStreamSynchronize(p->d2h_stream), "sync") || !cuda_ok(p, cudaStreamSynchronize(cs), "sync")) {
     cudaStreamSynchronize(st);
+    cudaStreamSynchronize(s2);
     cudaStreamSynchronize(cs);
     cudaStreamSynchronize(p->d2h_stream);
     delete d;
     set_off(off, -1);
     return JT_CAPACITY;
+  }
+  if (trace) {
+    for (unsigned g = 0; g < G; g++) {
+      float t[3];
+      for (int q = 0; q < 3; q++) cudaEventElapsedTime(&t[q], tev[0], tev[1 + q * G + g]);
+      fprintf(stderr, " piece %u: uploaded %.0f us, stage 1 %.0f, stage 2 %.0f\n", g, 1e3 * t[0], 1e3 * t[1],
+              1e3 * t[2]);
+    }
+    for (auto &e : tev) cudaEventDestroy(e);
   }
   p->launches = 0;
   bool redo = false;
@@ -1181,6 +1220,10 @@ void jt_parser_free(jt_parser *p) {
   if (p->h_ctrl_s1) cudaFreeHost(p->h_ctrl_s1);
   for (cudaEvent_t e : p->done_ev) cudaEventDestroy(e);
   if (p->ev_fin) cudaEventDestroy(p->ev_fin);
+  if (p->s2_stream) {
+    cudaStreamSynchronize(p->s2_stream);
+    cudaStreamDestroy(p->s2_stream);
+  }
   if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
   if (p->h_sum3) cudaFreeHost(p->h_sum3);
   delete p;

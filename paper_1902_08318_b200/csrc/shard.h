@@ -44,6 +44,9 @@ struct Shard {
   uint64_t S0;            // kinds as a shift register (bit 0 = innermost, 1 = object)
   int32_t open_n;         // how many (<= kBoundMax)
   uint32_t patch_n;       // cross-shard bracket patches recorded by k_struct
+  uint32_t streamed;      // pieces of one streamed parse: only summaries up to g + 1 are final
+                          // when phase 2 runs (later ones may be being written)
+  uint32_t pad_;
 };
 
 // phase summaries (all-gathered as raw bytes)

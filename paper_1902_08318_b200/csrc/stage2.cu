@@ -1389,7 +1389,10 @@ __global__ void k_apply1(Stage2Args a, const Sum1 *gs) {
   uint64_t tok = 0, tape = 0, str = 0, S = 0, T = 0, sb = 0;
   int64_t dep = 0;
   unsigned long long u8 = ~0ULL, se = ~0ULL;
-  for (uint32_t k = 0; k < G; k++) {
+  // streamed pieces: summaries past g + 1 may still be in flight (phase 1
+  // of later pieces runs concurrently); only earlier ones decide this shard
+  const uint32_t kmax = h->streamed && g + 2 < G ? g + 2 : G;
+  for (uint32_t k = 0; k < kmax; k++) {
     if (k == g) {
       h->token_base = tok;
       h->tape_base = tape;
@@ -1415,7 +1418,7 @@ __global__ void k_apply1(Stage2Args a, const Sum1 *gs) {
   h->next_aux = sb - h->string_base;
   uint64_t run = 0;
   for (uint32_t k = g; k < G; k++) {
-    if (k > g && gs[k].pad[0] == 0) {  // not parsed yet (streamed pieces): the caller redoes the parse
+    if (k > g && (k >= kmax || gs[k].pad[0] == 0)) {  // not parsed yet (streamed pieces): the caller redoes the parse
       c->redo = 1;
       break;
     }
