@@ -166,6 +166,8 @@ struct jt_document {
     return true;
   }
   bool alloc_tape(size_t words) {
+    release(block, block_cap, pinned);  // a block taken before the size was known
+    block = nullptr;
     block = PinnedPool::get().take(words * 8 + 64, &block_cap, &pinned);
     if (!block) return false;
     tape = Span<uint64_t>{(uint64_t *)block, words};
@@ -240,6 +242,13 @@ struct jt_parser {
   std::vector<cudaEvent_t> done_ev;
   cudaEvent_t ev_fin = nullptr;
   cudaStream_t s2_stream = nullptr;   // pieces' stage 2: high priority, ahead of later pieces' stage 1
+  // streamed jt_parse, stage 2 in two token ranges (parse_stream)
+  DevBuf rngbuf;                      // TokRange A, B | stage-1 token count at piece cA
+  DevBuf patchbuf;                    // range B's openers below range A's tape end
+  jt::TokRange *h_range = nullptr;    // pinned copies of the early ranges
+  unsigned long long *h_patch = nullptr;  // pinned copy of the patch list
+  cudaEvent_t ev_rng[5] = {};         // early range k done (its TokRange on the host); [4]: the last range
+  cudaStream_t ta_stream = nullptr;   // the early ranges' tape words back to the host
   DevBuf psum;                        // gathered Sum0 | Sum1 | Sum2 | Sum3 of the pieces
   jt::Sum1 *h_sum1_init = nullptr;    // pinned: "not written yet" Sum1s
   jt::Sum3 *h_sum3 = nullptr;         // pinned: the pieces' Sum3 (bracket patches)
@@ -593,6 +602,44 @@ bool ensure_stream(jt_parser *p, uint64_t nch) {
   return p->stream_words.ensure(nch * 2 * sizeof(uint32_t) + 64);  // tile counters + carry states
 }
 
+constexpr size_t kPatchWords = 2 + 2 * jt::kPatchMax;
+constexpr int kMaxRanges = 4;  // early stage-2 ranges of a streamed parse (+ the last one)
+
+bool ensure_ranges(jt_parser *p) {
+  if (!p->s2_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&p->s2_stream, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      cudaGetLastError();
+      p->s2_stream = nullptr;
+      return false;
+    }
+  }
+  if (!p->ta_stream && cudaStreamCreateWithFlags(&p->ta_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    p->ta_stream = nullptr;
+    return false;
+  }
+  for (cudaEvent_t &e : p->ev_rng)
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      e = nullptr;
+      return false;
+    }
+  if (!p->h_range && cudaMallocHost((void **)&p->h_range, kMaxRanges * sizeof(jt::TokRange)) != cudaSuccess) {
+    cudaGetLastError();
+    p->h_range = nullptr;
+    return false;
+  }
+  if (!p->h_patch && cudaMallocHost((void **)&p->h_patch, kPatchWords * 8) != cudaSuccess) {
+    cudaGetLastError();
+    p->h_patch = nullptr;
+    return false;
+  }
+  return p->rngbuf.ensure((kMaxRanges + 1) * sizeof(jt::TokRange) + kMaxRanges * 8 + 64) &&
+         p->patchbuf.ensure(kPatchWords * 8);
+}
+
 jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
   static const bool trace = getenv("JT_TRACE") != nullptr;
   auto now_us = []() {
@@ -608,6 +655,35 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     set_off(off, -1);
     return JT_CAPACITY;
   }
+  // stage 2 in token ranges: early range k covers the tokens of the pieces up
+  // to rcut[k] (rounded down to 4096 tokens) and runs on a high-priority
+  // stream while the later pieces upload; its tape words go back to the host
+  // during the upload; the last range finishes the document after the last
+  // piece.  Cuts at JT_RANGE_PCTS % of the pieces (default 30,55,80; "0": none).
+  static const std::vector<uint64_t> pcts = [] {
+    std::vector<uint64_t> v;
+    const char *e = getenv("JT_RANGE_PCTS");
+    std::string str = e ? e : "30,55,80";
+    size_t at = 0;
+    while (at < str.size() && (int)v.size() < kMaxRanges) {
+      const long x = atol(str.c_str() + at);
+      if (x > 0 && x < 100 && (v.empty() || (uint64_t)x > v.back())) v.push_back((uint64_t)x);
+      const size_t c = str.find(',', at);
+      if (c == std::string::npos) break;
+      at = c + 1;
+    }
+    return v;
+  }();
+  std::vector<int64_t> rcut;  // piece after whose stage 1 early range k starts
+  if (nch >= 3 && !pcts.empty() && ensure_ranges(p))
+    for (uint64_t q : pcts) {
+      const int64_t c = std::max<int64_t>(0, (int64_t)(nch * q / 100) - 1);
+      if (c + 1 < (int64_t)nch && (rcut.empty() || c > rcut.back())) rcut.push_back(c);
+    }
+  const int nR = (int)rcut.size();
+  const int64_t cA = nR ? rcut[0] : -1;  // >= 0: ranges on
+  jt::TokRange *dr = p->rngbuf.as<jt::TokRange>();
+  uint64_t *tokA = (uint64_t *)(dr + kMaxRanges + 1);  // token count at each cut
   cudaStream_t cs = p->copy_stream;
   uint32_t *counters = p->stream_words.as<uint32_t>(), *states = counters + nch;
   p->launches = 0;
@@ -650,11 +726,28 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     k1.rec_tile0 = k1.begin / jt::kStage1Tile;
     k1.carry = a.carry - a.rec_tile0 + k1.rec_tile0;
     k1.fn = a.fn - a.rec_tile0 + k1.rec_tile0;
+    int rk = -1;  // early range starting after this piece
+    for (int q = 0; q < nR; q++)
+      if (rcut[q] == (int64_t)c) rk = q;
+    if (rk >= 0) k1.tok_out = tokA + rk;
     ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
          cuda_ok(p, jt::stage1_chunk_carry(a, p->stream), "stage1 carry") &&
          cuda_ok(p, jt::stage1_chunk_main(k1, p->stream), "stage1 chunk") &&
          cuda_ok(p, cudaEventRecord(p->piece_ev[c], p->stream), "event");
     p->launches += jt::kStage1Launches;
+    if (ok && rk >= 0) {  // early range rk next to the later pieces' stage 1
+      jt::Stage2Args s2a = s2_args(p, len, which);
+      s2a.patch = p->patchbuf.as<unsigned long long>();
+      int nA = 0;
+      ok = cuda_ok(p, cudaStreamWaitEvent(p->s2_stream, p->piece_ev[c], 0), "wait") &&
+           cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->s2_stream, &nA),
+                   "range") &&
+           cuda_ok(p, cudaMemcpyAsync(p->h_range + rk, dr + rk, sizeof(jt::TokRange), cudaMemcpyDeviceToHost,
+                                      p->s2_stream),
+                   "range D2H") &&
+           cuda_ok(p, cudaEventRecord(p->ev_rng[rk], p->s2_stream), "event");
+      p->launches += nA;
+    }
   }
   if (trace) fprintf(stderr, " enqueued %.0f us\n", now_us() - t0);
   // the string bytes of each piece go back as soon as its stage 1 is done,
@@ -665,9 +758,39 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   jt_document *d = nullptr;
   bool early = false;
   uint64_t sb_done = 0;
+  // the early ranges' tape words [1, tapeA) go back as each range is done,
+  // into a host tape block sized from the input (a larger tape is fetched
+  // whole), on their own stream: the string pieces' stream is waited on by
+  // k_tile_lengths, these copies must not delay stage 1
+  uint64_t tapeA = 0, tape_cap = 0;
+  int r_next = 0;
+  bool r_stop = false;
+  auto tape_a = [&](bool block) {
+    while (r_next < nR && d && tape_cap) {
+      if (!block && cudaEventQuery(p->ev_rng[r_next]) != cudaSuccess) return;
+      if (!cuda_ok(p, cudaEventSynchronize(p->ev_rng[r_next]), "sync")) return;
+      const uint64_t lo = r_next ? p->h_range[r_next - 1].tape_end : 1, te = p->h_range[r_next].tape_end;
+      if (!r_stop && te >= lo && te <= tape_cap && lo == (tapeA ? tapeA : 1)) {
+        if (te > lo &&
+            !(cuda_ok(p, cudaStreamWaitEvent(p->ta_stream, p->ev_rng[r_next], 0), "wait") &&
+              cuda_ok(p, cudaMemcpyAsync(d->tape.p + lo, p->tape.as<uint64_t>() + lo, (te - lo) * 8,
+                                         cudaMemcpyDeviceToHost, p->ta_stream),
+                      "tape range D2H")))
+          r_stop = true;
+        else
+          tapeA = te;
+      } else {
+        r_stop = true;  // the rest comes back with the last range
+      }
+      if (trace) fprintf(stderr, " range %d done %.0f us: tape words %llu\n", r_next, now_us() - t0,
+                         (unsigned long long)te);
+      r_next++;
+    }
+  };
   if (ok && out) {
     d = new (std::nothrow) jt_document;
     early = d && d->alloc_strings(len + len / 4 + 64);
+    if (early && cA >= 0 && d->alloc_tape(len / 8 + 1024)) tape_cap = d->tape.n;
     for (uint64_t c = 0; early && c < nch; c++) {
       if (!cuda_ok(p, cudaEventSynchronize(p->piece_ev[c]), "sync")) {
         early = false;
@@ -687,6 +810,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
         break;
       }
       sb_done = e;
+      if ((int64_t)c > cA) tape_a(false);
     }
     // length fields left to k_tile_lengths are patched into the host copy
     // too, after the last piece is down
@@ -703,16 +827,39 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
        cuda_ok(p, cudaEventRecord(p->ev_s1, p->stream), "event");
   p->launches += 1;
   int n2 = 0;
-  ok = ok && cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n2, nullptr, stage2_fork(p)),
-                     "stage2") &&
-       cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
-                                  p->stream),
-               "ctrl D2H");
+  if (cA >= 0) {
+    // the last range: the rest of the document, on the early ranges' stream
+    // right after the last piece's stage 1 (it does not need the string
+    // pieces' copies k_tile_lengths waits for); openers below the early
+    // ranges' tape end as patches.  The parser's stream joins it (finish).
+    jt::Stage2Args s2b = s2_args(p, len, which);
+    s2b.patch = p->patchbuf.as<unsigned long long>();
+    cudaStream_t sb = p->s2_stream;
+    ok = ok && cuda_ok(p, cudaStreamWaitEvent(sb, p->piece_ev[nch - 1], 0), "wait") &&
+         cuda_ok(p, jt::range_b_launch(s2b, dr + nR - 1, dr + nR, sb, &n2, stage2_fork(p)), "range B") &&
+         cuda_ok(p, cudaMemcpyAsync(p->h_patch, p->patchbuf.p, kPatchWords * 8, cudaMemcpyDeviceToHost, sb),
+                 "patch D2H") &&
+         cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, sb),
+                 "ctrl D2H") &&
+         cuda_ok(p, cudaEventRecord(p->ev_rng[kMaxRanges], sb), "event") &&
+         cuda_ok(p, cudaStreamWaitEvent(p->stream, p->ev_rng[kMaxRanges], 0), "wait");
+  } else {
+    ok = ok && cuda_ok(p, jt::stage2_launch(s2_args(p, len, which), p->stream, &n2, nullptr, stage2_fork(p)),
+                       "stage2") &&
+         cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
+                                    p->stream),
+                 "ctrl D2H");
+  }
   p->launches += n2;
+  if (ok) tape_a(true);  // the early ranges' tape words not yet on their way
   if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_s1), "sync")) {
     cudaStreamSynchronize(p->stream);
     cudaStreamSynchronize(cs);
     cudaStreamSynchronize(p->d2h_stream);
+    if (cA >= 0) {
+      cudaStreamSynchronize(p->s2_stream);
+      cudaStreamSynchronize(p->ta_stream);
+    }
     delete d;
     set_off(off, -1);
     return JT_CAPACITY;
@@ -722,15 +869,24 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   // by piece, already on the host); otherwise fetch it while stage 2 runs
   const jt::Ctrl c1 = *p->h_ctrl_s1;
   if (d && (!early || (c1.utf8_pos == ~0ULL && sb_done != c1.string_bytes))) {
+    cudaStreamSynchronize(p->d2h_stream);  // no copy may still target its blocks
+    if (cA >= 0) cudaStreamSynchronize(p->ta_stream);
+    tapeA = 0;
     delete d;  // not (completely) fetched piece by piece: the whole buffer below
     d = nullptr;
     early = false;
   }
   if (out && c1.utf8_pos == ~0ULL && d && early) {
     d->strings.n = c1.string_bytes;
-    if (!d->alloc_tape(c1.tape_words + 1)) {
-      delete d;
-      d = nullptr;
+    if (tapeA && c1.tape_words + 1 <= tape_cap) {
+      d->tape.n = c1.tape_words + 1;  // range A's words are in it already
+    } else {
+      if (tapeA) cudaStreamSynchronize(p->ta_stream);  // before the block is recycled
+      tapeA = 0;
+      if (!d->alloc_tape(c1.tape_words + 1)) {
+        delete d;
+        d = nullptr;
+      }
     }
   } else if (out && c1.utf8_pos == ~0ULL) {
     d = new (std::nothrow) jt_document;
@@ -748,19 +904,27 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   }
   jt_error e = finish(p, which, true, off);  // waits for stage 2
   cudaStreamSynchronize(cs);
+  if (cA >= 0) cudaStreamSynchronize(p->ta_stream);  // the early ranges' tape words
   const double t4 = trace ? now_us() : 0;
   if (e != JT_OK || !out) {
     delete d;
     return e;
   }
-  if (!d || d->tape.size() != p->last_tape_len ||
-      !cuda_ok(p, cudaMemcpyAsync(d->tape.data(), p->tape.p, p->last_tape_len * 8,
-                                  cudaMemcpyDeviceToHost, p->stream),
+  const uint64_t t_lo = tapeA ? tapeA : 0;  // words below came back with range A
+  if (!d || d->tape.size() != p->last_tape_len || t_lo > p->last_tape_len ||
+      !cuda_ok(p, cudaMemcpyAsync(d->tape.data() + t_lo, p->tape.as<uint64_t>() + t_lo,
+                                  (p->last_tape_len - t_lo) * 8, cudaMemcpyDeviceToHost, p->stream),
                "tape D2H") ||
       !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
     delete d;
     set_off(off, -1);
     return JT_CAPACITY;
+  }
+  if (tapeA) {  // the root word and range B's openers of containers range A opened
+    d->tape.data()[0] = jt::tape_word(jt::kTagRoot, p->last_tape_len - 1);
+    const uint64_t n = std::min<uint64_t>(p->h_patch[0], jt::kPatchMax);
+    for (uint64_t q = 0; q < n; q++)
+      if (p->h_patch[2 + 2 * q] < p->last_tape_len) d->tape.data()[p->h_patch[2 + 2 * q]] = p->h_patch[3 + 2 * q];
   }
   p->in_len = len;
   *out = d;
@@ -1223,6 +1387,14 @@ void jt_parser_free(jt_parser *p) {
   if (p->s2_stream) {
     cudaStreamSynchronize(p->s2_stream);
     cudaStreamDestroy(p->s2_stream);
+  }
+  if (p->h_range) cudaFreeHost(p->h_range);
+  if (p->h_patch) cudaFreeHost(p->h_patch);
+  for (cudaEvent_t e : p->ev_rng)
+    if (e) cudaEventDestroy(e);
+  if (p->ta_stream) {
+    cudaStreamSynchronize(p->ta_stream);
+    cudaStreamDestroy(p->ta_stream);
   }
   if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
   if (p->h_sum3) cudaFreeHost(p->h_sum3);

@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       s_tbase = base.v[2];
       s_dbase = kRec ? seg_value(base.v[3]) : sext63(base.v[3]);
       if (a.sb_out && tile == (int64_t)a.ntiles - 1) *a.sb_out = inc.v[1];  // host-mapped
+      if (a.tok_out && tile == (int64_t)a.ntiles - 1) *a.tok_out = inc.v[0];
       if (gt == last_tile) {
         *a.total = inc.v[0];
         *a.total_strings = inc.v[1];

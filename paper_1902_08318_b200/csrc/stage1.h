@@ -45,6 +45,7 @@ struct Stage1Args {
   // written to host-mapped memory by the range's last tile (optional), and
   // the host copy of the string buffer that k_tile_lengths also patches
   uint64_t *sb_out;
+  uint64_t *tok_out;     // streamed pieces: index entries up to the range's last tile (device)
   uint8_t *strings_host;
   // record (NDJSON) mode: '\n'-separated records parsed independently
   bool records;

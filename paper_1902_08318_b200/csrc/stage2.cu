@@ -107,6 +107,32 @@ __device__ View view_of(const Stage2Args &a) {
   return v;
 }
 
+// Tokens of this launch: all of them, or a partial range (TokRange).
+struct Rng {
+  uint64_t lo, hi, avail;
+  bool fin;
+};
+__device__ __forceinline__ Rng rng_of(const Stage2Args &a, const Ctrl *c) {
+  if (!a.range) {
+    const uint64_t S = c->S;
+    return Rng{0, S, S, true};
+  }
+  return Rng{a.range->lo, a.range->hi, a.range->avail, a.range->fin != 0};
+}
+
+// an opener's tape word; below a partial range's patch_lim it is on the host
+// already and goes to the patch list too
+__device__ __forceinline__ void put_opener(const Stage2Args &a, uint64_t at, uint64_t w) {
+  a.tape[at] = w;
+  if (a.range && at < a.range->patch_lim) {
+    const unsigned long long k = atomicAdd(a.patch, 1ULL);
+    if (k < kPatchMax) {
+      a.patch[2 + 2 * k] = at;
+      a.patch[3 + 2 * k] = w;
+    }
+  }
+}
+
 // ---- K2: scalars, one thread per token ---------------------------------
 
 // Stack of container kinds as a 64-bit shift register: bit 0 = innermost
@@ -158,11 +184,12 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   __shared__ uint64_t s_wS[8];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint64_t S = ctrl->S;
+  const Rng R = rng_of(a, ctrl);
+  const uint64_t S = R.hi;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
   const View vw = view_of(a);
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (uint64_t tile = R.lo / (256 * kStkTok) + blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t i0 = (tile * 256 + threadIdx.x) * kStkTok;
     uint32_t recs[kStkTok];
     if (i0 + kStkTok <= S) {
@@ -206,7 +233,7 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
       // a shard starts inside depth_base open containers: the 64-kind
       // register is exact only if that depth fits too (closers at the shard
       // start pop below the carried-in kinds)
-      if (tile == blockIdx.x && threadIdx.x == 0 && blockIdx.x == 0 && vw.depth_base > 0)
+      if (threadIdx.x == 0 && blockIdx.x == 0 && tile == R.lo / (256 * kStkTok) && vw.depth_base > 0)
         atomicMax(&ctrl->max_depth, (int)min(vw.depth_base, (int64_t)1 << 20));
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -253,7 +280,7 @@ __global__ void __launch_bounds__(kStkScan) k_stack_scan(Stage2Args a) {
   __shared__ StackT s_w[kStkScan / 32];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint64_t S = ctrl->S;
+  const uint64_t S = rng_of(a, ctrl).hi;  // a partial range rescans all tiles below its end
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
   const uint64_t per = (ntiles + kStkScan - 1) / kStkScan;
@@ -308,24 +335,26 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
   __shared__ int s_wmin[8];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint64_t S = ctrl->S;
+  // tokens [R.lo, S); the next token is readable below R.avail
+  const Rng R = rng_of(a, ctrl);
+  const uint64_t S = R.hi, Sa = R.avail;
   const unsigned long long str_err = ctrl->str_err;
   const View vw = view_of(a);
   const InAt at{a.in};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr uint64_t kPass = 256 * kScTok;
   const uint64_t stride = (uint64_t)gridDim.x * kPass;
-  for (uint64_t base = (uint64_t)blockIdx.x * kPass; base < S; base += stride) {
+  for (uint64_t base = R.lo + (uint64_t)blockIdx.x * kPass; base < S; base += stride) {
     const uint64_t i0 = base + (uint64_t)threadIdx.x * kScTok;
     uint32_t rec[4], pos[4], so[4], ti[4];
     ld4(a.tok, i0, S, rec);
-    ld4(a.idx, i0, S, pos);
-    ld4(a.aux, i0, S, so);
+    ld4(a.idx, i0, Sa, pos);
+    ld4(a.aux, i0, Sa, so);
     ld4(a.tape_idx, i0, S, ti);
     // the token after this thread's four: the next lane's first, or memory
     uint32_t npos = __shfl_down_sync(0xffffffffu, pos[0], 1);
     uint32_t nso = __shfl_down_sync(0xffffffffu, so[0], 1);
-    if (lane == 31 && i0 + 4 < S) {
+    if (lane == 31 && i0 + 4 < Sa) {
       npos = a.idx[i0 + 4];
       nso = a.aux[i0 + 4];
     }
@@ -365,7 +394,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
         const uint32_t p = pos[k];
         const uint32_t p_next = k < 3 ? pos[k + 1] : npos;
         const uint32_t so_next = k < 3 ? so[k + 1] : nso;
-        const unsigned long long end = i + 1 < S ? p_next : vw.next_pos;
+        const unsigned long long end = i + 1 < Sa ? p_next : vw.next_pos;
         uint32_t sbase = 0;  // record mode: offsets within the record's string buffer
         if (a.records) {
           const uint32_t r = a.rec_of[i];
@@ -380,7 +409,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
           // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
           const uint64_t lt = (p - vw.begin) >> 14;
           if (end > a.len || lt != ((end - vw.begin) >> 14) || (a.records ? a.tile_flags[lt] : tflag[k])) {
-            const uint32_t nx = i + 1 < S ? so_next : (uint32_t)vw.next_aux;
+            const uint32_t nx = i + 1 < Sa ? so_next : (uint32_t)vw.next_aux;
             const uint32_t len = nx - so[k] - 4;
             uint8_t *f = a.strings + so[k];
             f[0] = (uint8_t)len;
@@ -431,9 +460,9 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
 __global__ void __launch_bounds__(256) k_numbers(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint32_t n = ctrl->num_count;
+  const uint32_t n = ctrl->num_count, k0 = a.range ? a.range->num_lo : 0u;
   const InAt at{a.in};
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+  for (uint32_t k = k0 + blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t i = a.numlist[k];
     const uint32_t p = a.idx[i];
     const uint32_t t = a.tape_idx[i];
@@ -457,9 +486,9 @@ __global__ void __launch_bounds__(256) k_numbers(Stage2Args a) {
 __global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint32_t n = ctrl->slow_count;
+  const uint32_t n = ctrl->slow_count, k0 = a.range ? a.range->slow_lo : 0u;
   const InAt at{a.in};
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+  for (uint32_t k = k0 + blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     uint32_t tokn = a.slow[2 * k], slot = a.slow[2 * k + 1];
     num::Decimal dec;
     uint64_t bits;
@@ -473,7 +502,7 @@ __global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
 __global__ void __launch_bounds__(1024) k_tree(Stage2Args a) {
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint64_t S = ctrl->S;
+  const uint64_t S = rng_of(a, ctrl).hi;  // a partial range rebuilds the levels below its end
   uint64_t n = (S + 4095) / 4096;  // level-3 entries
   uint64_t n4 = (n + 15) / 16;
   int16_t *l4 = a.mhi + a.hi_off[0];
@@ -848,7 +877,7 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
       const uint64_t ow = tape_word(cl == C_OCL ? '{' : '[', (kShard ? sp.tb : 0u) + ti + 1);
       if (j >= 0) {
         a.tape[ti] = tape_word((uint8_t)c, (kShard ? sp.tb : 0u) + tj);
-        a.tape[tj] = ow;
+        put_opener(a, tj, ow);
       } else if (kShard && Dd - 1 >= 0 && Dd - 1 < sp.open_n) {
         // the opener lives in an earlier shard: patched after the last exchange
         const uint64_t at = a.bound[Dd - 1] & ((1ULL << 56) - 1);
@@ -865,7 +894,7 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
     const uint64_t tokbase = kShard ? sp.token_base : 0;
     if (err && live) {
       report(ctrl, tokbase + i, err);
-    } else if (live && i == S - 1 && (!kShard || sp.is_last)) {  // the root value must be complete
+    } else if (live && i == S - 1 && sp.is_last) {  // the root value must be complete (last range)
       const int depth_after = Dd + (cl <= C_ABR ? 1 : cl <= C_ACL ? -1 : 0);
       if (!(after == M_A && depth_after == 0)) report(ctrl, tokbase + S, kTapeError);
     }
@@ -897,8 +926,9 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   }
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
-  const uint64_t S = ctrl->S;
-  const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile;
+  const Rng R = rng_of(a, ctrl);
+  const uint64_t S = R.hi;
+  const uint64_t ntiles = (S + kK3Tile - 1) / kK3Tile, tile0 = R.lo / kK3Tile;
   const bool shallow = ctrl->max_depth <= 64;  // scope bits exact (k_stack)
   const bool deep = !shallow;
 
@@ -906,7 +936,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   // lambdas below would live in local memory)
   // (tape indices fit 32 bits: tape_idx is u32)
   constexpr bool sharded = kShard;
-  bool is_last = true;
+  bool is_last = R.fin;
   int db = 0, open_n = 0;
   uint32_t tb = 0;
   uint64_t token_base = 0;
@@ -914,7 +944,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   int64_t before = 0;
   if (kShard) {
     const View vw = view_of(a);
-    is_last = vw.is_last;
+    is_last = vw.is_last && R.fin;
     db = (int)vw.depth_base;
     open_n = vw.open_n;
     tb = (uint32_t)vw.tape_base;
@@ -956,9 +986,9 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   // token-parallel path on few tiles (a streamed piece, a small document):
   // kSplit CTAs share a tile (each loads it for the tree, checks a quarter),
   // so the per-tile latency of 16 chunk rounds per warp is spread out
-  const uint32_t split = (kMode <= 1 && shallow && 2 * ntiles <= (uint64_t)gridDim.x) ? 4u : 1u;
-  for (uint64_t work = blockIdx.x; work < ntiles * split; work += gridDim.x) {
-    const uint64_t tile = work / split;
+  const uint32_t split = (kMode <= 1 && shallow && 2 * (ntiles - tile0) <= (uint64_t)gridDim.x) ? 4u : 1u;
+  for (uint64_t work = blockIdx.x; work < (ntiles - tile0) * split; work += gridDim.x) {
+    const uint64_t tile = tile0 + work / split;
     const uint64_t tbase = tile * kK3Tile;
     {
       const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
@@ -1172,7 +1202,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
           a.tape[t] = tape_word((uint8_t)c, top_tape - rtb);
           const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1 - rtb);
           if (!kShard || top_tape > tb) {
-            a.tape[top_tape - tb] = ow;
+            put_opener(a, top_tape - tb, ow);
           } else {  // the opener lives in an earlier shard: patched after the last exchange
             const uint32_t k = atomicAdd(&a.sum3->patch_n, 1u);
             if (k < (uint32_t)kBoundMax) {
@@ -1664,6 +1694,77 @@ cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int 
   launch_struct(a, stream);
   k_final_records<<<1184, 256, 0, stream>>>(a);
   *launches = 9;
+  return cudaGetLastError();
+}
+
+// ---- streamed jt_parse: stage 2 in two token ranges ------------------------
+__global__ void k_range_a(Stage2Args a, const uint64_t *known, const TokRange *prev, TokRange *r) {
+  const Ctrl *c = a.ctrl;
+  const uint64_t n = *known;  // index entries stage 1 has produced so far
+  const uint64_t lo = prev ? prev->hi : 0;
+  uint64_t hi = n > 0 ? (n - 1) / 4096 * 4096 : 0;  // token hi exists
+  if (hi < lo) hi = lo;
+  TokRange v{};
+  v.lo = lo;
+  v.hi = hi;
+  v.avail = n;
+  v.num_lo = prev ? c->num_count : 0u;
+  v.slow_lo = prev ? c->slow_count : 0u;
+  v.patch_lim = prev ? prev->tape_end : 0;
+  v.tape_end = hi > lo ? a.tape_idx[hi] : (prev ? prev->tape_end : 1);
+  *r = v;
+  if (!prev) a.patch[0] = 0;
+}
+
+__global__ void k_range_b(Stage2Args a, const TokRange *ra, TokRange *rb) {
+  const Ctrl *c = a.ctrl;
+  TokRange v{};
+  v.lo = ra->hi;
+  v.hi = v.avail = c->S;
+  v.num_lo = c->num_count;
+  v.slow_lo = c->slow_count;
+  v.fin = 1;
+  v.patch_lim = ra->tape_end;
+  *rb = v;
+}
+
+cudaError_t range_a_launch(const Stage2Args &a_in, const uint64_t *known, const TokRange *prev, TokRange *r,
+                           cudaStream_t stream, int *launches) {
+  Stage2Args a = a_in;
+  a.range = r;
+  const unsigned g2 = grid_tokens(a);
+  k_range_a<<<1, 1, 0, stream>>>(a, known, prev, r);
+  k_scalars<<<g2, 256, 0, stream>>>(a);
+  k_numbers<<<g2, 256, 0, stream>>>(a);
+  k_slow<<<8, 64, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
+  launch_stack(a, stream);
+  launch_struct(a, stream);
+  *launches = 9;
+  return cudaGetLastError();
+}
+
+cudaError_t range_b_launch(const Stage2Args &a_in, const TokRange *ra, TokRange *rb, cudaStream_t stream,
+                           int *launches, const Stage2Fork *fork) {
+  Stage2Args a = a_in;
+  a.range = rb;
+  const unsigned g2 = grid_tokens(a);
+  k_range_b<<<1, 1, 0, stream>>>(a, ra, rb);
+  if (fork) {  // k_stack next to the scalar / number / tree kernels (stage2_launch)
+    cudaEventRecord(fork->fork, stream);
+    cudaStreamWaitEvent(fork->side, fork->fork, 0);
+    launch_stack(a, fork->side);
+    cudaEventRecord(fork->join, fork->side);
+  }
+  k_scalars<<<g2, 256, 0, stream>>>(a);
+  k_numbers<<<g2, 256, 0, stream>>>(a);
+  k_slow<<<8, 64, 0, stream>>>(a);
+  k_tree<<<1, 1024, 0, stream>>>(a);
+  if (fork) cudaStreamWaitEvent(stream, fork->join, 0);
+  else launch_stack(a, stream);
+  launch_struct(a, stream);
+  k_final<<<1, 1, 0, stream>>>(a);
+  *launches = 10;
   return cudaGetLastError();
 }
 

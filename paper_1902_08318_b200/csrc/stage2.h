@@ -53,6 +53,21 @@ struct RecordResult {
   uint64_t string_bytes;
 };
 
+// A partial stage 2 over the tokens [lo, hi) (streamed jt_parse runs stage 2
+// on the document's first tokens while the rest is still uploading; a second
+// range finishes it).  lo and hi are multiples of 4096 (the k_stack / k_struct
+// tile and the min-tree level-3 group) except the final hi = S; `avail`
+// tokens exist (the token after hi is readable); numbers / slow floats from
+// list entry num_lo / slow_lo; opener words below patch_lim (already copied to
+// the host) written by this range are also recorded in Stage2Args.patch.
+struct TokRange {
+  uint64_t lo, hi, avail;
+  uint32_t num_lo, slow_lo;
+  uint64_t fin;        // 1: the document's last range (end-of-document checks)
+  uint64_t patch_lim;
+  uint64_t tape_end;   // first tape word not final after this range (range A)
+};
+
 struct Stage2Args {
   const uint8_t *in;
   uint64_t len;
@@ -85,6 +100,9 @@ struct Stage2Args {
   unsigned long long *rec_err;  // per record: (token << 8) | code, ~0 = none
   uint32_t *rec_end_err;        // per record: error at the record's end (0 = none)
   RecordResult *results;        // per record (k_final_records)
+  // partial stage 2 (nullptr: all tokens)
+  const TokRange *range;
+  unsigned long long *patch;    // [0] = count, then (tape index, word) pairs
 };
 
 // distinct_values query over the device-resident result of the last parse
@@ -129,6 +147,20 @@ struct Stage2Fork {
 };
 cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
                           cudaEvent_t *ev = nullptr, const Stage2Fork *fork = nullptr);
+
+// Streamed jt_parse, stage 2 in token ranges.  range_a_launch: the next
+// range = [prev.hi (or 0), hi) with hi the last multiple of 4096 below the
+// tokens stage 1 has produced so far (*known), written to `r` (with the tape
+// words it finalises up to r->tape_end); then the range's stage 2 (no root
+// words, no end checks).  range_b_launch: the last range = [prev.hi, S)
+// after the whole stage 1, then the document's finalize.  Openers a range
+// writes below its patch_lim (earlier ranges' words, already on their way to
+// the host) are recorded as patches.
+constexpr uint64_t kPatchMax = 8192;  // containers open at the range boundaries (<= kMaxDepth + 1 each)
+cudaError_t range_a_launch(const Stage2Args &a, const uint64_t *known, const TokRange *prev, TokRange *r,
+                           cudaStream_t stream, int *launches);
+cudaError_t range_b_launch(const Stage2Args &a, const TokRange *ra, TokRange *rb, cudaStream_t stream,
+                           int *launches, const Stage2Fork *fork = nullptr);
 
 // Record mode: per-record error slots, then the whole stage 2 with
 // per-record grammar, and one result per record.

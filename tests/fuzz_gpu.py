@@ -58,6 +58,8 @@ def main():
     args = ap.parse_args()
     rng = random.Random(args.seed)
     o, p = Oracle(), Parser()
+    pp = Parser()  # stream mode 1: pieces parsed as byte-range shards
+    pp.set_stream_mode(1)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     t0 = time.time()
     n = fails = 0
@@ -102,11 +104,16 @@ def main():
             reps = max(1, (9 << 20) // max(1, len(d)) + 1)
             if r.code == 0 and reps * len(d) < (40 << 20):
                 big = b"[" + b",".join([d] * reps) + b"]"
-                rb, gb = o.parse(big), p.parse(big)
-                counts["streamed"] += 1
-                if (gb.name, gb.offset) != (rb.name, rb.offset) or (
-                        rb.code == 0 and not np.array_equal(gb.document.tape, rb.tape_array())):
-                    fail("streamed", big, (gb.name, gb.offset, rb.name, rb.offset))
+                rb = o.parse(big)
+                for mode, q in (("streamed", p), ("streamed pieces", pp)):
+                    if mode == "streamed pieces" and rng.random() < 0.5:
+                        continue
+                    gb = q.parse(big)
+                    counts["streamed"] += 1
+                    if (gb.name, gb.offset) != (rb.name, rb.offset) or (
+                            rb.code == 0 and (not np.array_equal(gb.document.tape, rb.tape_array())
+                                              or gb.document.strings != rb.strings)):
+                        fail(mode, big, (gb.name, gb.offset, rb.name, rb.offset))
         tiles = (len(d) + 16383) // 16384
         if tiles >= 2 and rng.random() < 0.5:
             from paper_1902_08318_b200.shard import LocalShards

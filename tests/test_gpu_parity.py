@@ -175,6 +175,29 @@ def test_streamed_jt_parse(parser, oracle):
         check_same(parser, oracle, data, where)
 
 
+def test_streamed_stage2_ranges(parser, oracle):
+    """Streamed jt_parse (stream mode 0) runs stage 2 in token ranges: the
+    early ranges while later pieces upload (tape words back early), the last
+    one after the upload (engine.cu parse_stream, stage2.cu k_range_a/b).
+    Brackets whose opener lies in an earlier range (patches), nesting deeper
+    than 64 across ranges, numbers and hard floats in every range, errors in
+    early ranges, ranges without tokens, and a tape larger than the early
+    host block."""
+    from tools.gen import generate
+    docs = [(generate(2, 20 << 20, seed=21), "C2 numbers 20 MiB"),
+            (generate(0, 24 << 20, seed=22), "C0-style 24 MiB"),
+            (b"[" * 1000 + generate(1, 16 << 20, seed=23) + b"]" * 1000, "deep across ranges"),
+            (b"{\"a\":" * 60 + generate(4, 16 << 20, seed=24) + b"}" * 60, "objects across ranges")]
+    base = generate(1, 16 << 20, seed=25)
+    docs.append((base[:3 << 20] + b"}" + base[(3 << 20) + 1:], "error in the first range"))
+    docs.append((base[:(9 << 20) + 7] + b"\x01" + base[(9 << 20) + 8:], "control byte mid document"))
+    docs.append((b'["' + b"w" * (14 << 20) + b'", [1, 2.5e-310, "x"]]', "early ranges without tokens"))
+    docs.append((b"[" + b"1," * (6 << 20) + b"1]", "tape above the early block"))
+    docs.append((b"[" + b"1.7976931348623157e308,4.9e-324," * (300000) + b"0]", "hard floats"))
+    for data, where in docs:
+        check_same(parser, oracle, data, where)
+
+
 def _piece_cut(length: int) -> int:
     """First cut of parse_pieces (engine.cu piece_count, 8 MiB pieces, >= 2)."""
     piece = 8 << 20
