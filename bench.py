@@ -42,7 +42,7 @@ METRIC = "JSON parsed GB/s (stage1 & full tape) at 1/2/4/8 B200; % of HBM roofli
 WORKLOAD = ("C1: 64 MiB single document, pretty-printed (2-space, LF), random tree "
             "branching 1-10 depth<=8, 30% non-ASCII string chars, 10% strings with escapes")
 CONFIG = 1
-PROFILE = "r01c_ncu_full_c1.json"  # ncu --set full capture of the current kernels (traffic)
+PROFILE = "r01d_ncu_full_c1.json"  # ncu --set full capture of the current kernels (traffic)
 SIZE = 64 << 20
 
 
