@@ -693,6 +693,9 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   const int64_t cA = nR ? rcut[0] : -1;  // >= 0: ranges on
   jt::TokRange *dr = p->rngbuf.as<jt::TokRange>();
   uint64_t *tokA = (uint64_t *)(dr + kMaxRanges + 1);  // token count at each cut
+  cudaEvent_t tr_ev[2 * kMaxRanges + 3] = {};  // JT_TRACE: device times of the ranges
+  if (trace)
+    for (auto &e : tr_ev) cudaEventCreate(&e);
   cudaStream_t cs = p->copy_stream;
   uint32_t *counters = p->stream_words.as<uint32_t>(), *states = counters + nch;
   p->launches = 0;
@@ -704,6 +707,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
                     "init") &&
             cuda_ok(p, cudaMemsetAsync(counters, 0, nch * sizeof(uint32_t), p->stream), "counters") &&
             cuda_ok(p, cudaEventRecord(p->ev_start, p->stream), "event") &&
+            (!trace || cudaEventRecord(tr_ev[2 * kMaxRanges + 2], p->stream) == cudaSuccess) &&
             cuda_ok(p, cudaStreamWaitEvent(cs, p->ev_start, 0), "wait");
   p->launches = 1;
   // uploads: zero tail first (the last piece's stage 1 reads it), then the pieces
@@ -765,12 +769,12 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
       s2a.patch = p->patchbuf.as<unsigned long long>();
       int nA = 0;
       ok = cuda_ok(p, cudaStreamWaitEvent(p->s2_stream, p->piece_ev[c], 0), "wait") &&
-           cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->s2_stream, &nA),
+           (!trace || cudaEventRecord(tr_ev[2 * rk], p->s2_stream) == cudaSuccess) &&
+           cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->h_range + rk,
+                                         p->s2_stream, &nA),
                    "range") &&
-           cuda_ok(p, cudaMemcpyAsync(p->h_range + rk, dr + rk, sizeof(jt::TokRange), cudaMemcpyDeviceToHost,
-                                      p->s2_stream),
-                   "range D2H") &&
            cuda_ok(p, cudaEventRecord(p->ev_rng[rk], p->s2_stream), "event");
+      if (trace) cudaEventRecord(tr_ev[2 * rk + 1], p->s2_stream);
       p->launches += nA;
     }
   }
@@ -954,6 +958,13 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   }
   p->in_len = len;
   *out = d;
+  if (trace && nR) {
+    float t[2 * kMaxRanges];
+    for (int q = 0; q < 2 * nR; q++) cudaEventElapsedTime(&t[q], tr_ev[2 * kMaxRanges + 2], tr_ev[q]);
+    for (int q = 0; q < nR; q++) fprintf(stderr, " range %d on the device: started %.0f us, done %.0f us\n", q, 1e3 * t[2 * q], 1e3 * t[2 * q + 1]);
+  }
+  if (trace)
+    for (auto &e : tr_ev) cudaEventDestroy(e);
   if (trace)
     fprintf(stderr, "parse_stream: pieces+D2H enqueued %.0f us, stage 1 done %.0f, stage 2 done %.0f, tape down %.0f (early %d)\n",
             t2 - t0, t3 - t0, t4 - t0, now_us() - t0, (int)early);

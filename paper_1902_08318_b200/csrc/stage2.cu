@@ -1698,7 +1698,8 @@ cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int 
 }
 
 // ---- streamed jt_parse: stage 2 in two token ranges ------------------------
-__global__ void k_range_a(Stage2Args a, const uint64_t *known, const TokRange *prev, TokRange *r) {
+__global__ void k_range_a(Stage2Args a, const uint64_t *known, const TokRange *prev, TokRange *r,
+                          TokRange *host) {
   const Ctrl *c = a.ctrl;
   const uint64_t n = *known;  // index entries stage 1 has produced so far
   const uint64_t lo = prev ? prev->hi : 0;
@@ -1713,6 +1714,7 @@ __global__ void k_range_a(Stage2Args a, const uint64_t *known, const TokRange *p
   v.patch_lim = prev ? prev->tape_end : 0;
   v.tape_end = hi > lo ? a.tape_idx[hi] : (prev ? prev->tape_end : 1);
   *r = v;
+  if (host) *host = v;  // host-mapped: no copy queued behind the bulk D2H copies
   if (!prev) a.patch[0] = 0;
 }
 
@@ -1729,11 +1731,11 @@ __global__ void k_range_b(Stage2Args a, const TokRange *ra, TokRange *rb) {
 }
 
 cudaError_t range_a_launch(const Stage2Args &a_in, const uint64_t *known, const TokRange *prev, TokRange *r,
-                           cudaStream_t stream, int *launches) {
+                           TokRange *host, cudaStream_t stream, int *launches) {
   Stage2Args a = a_in;
   a.range = r;
   const unsigned g2 = grid_tokens(a);
-  k_range_a<<<1, 1, 0, stream>>>(a, known, prev, r);
+  k_range_a<<<1, 1, 0, stream>>>(a, known, prev, r, host);
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   k_slow<<<8, 64, 0, stream>>>(a);
