@@ -771,7 +771,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
       ok = cuda_ok(p, cudaStreamWaitEvent(p->s2_stream, p->piece_ev[c], 0), "wait") &&
            (!trace || cudaEventRecord(tr_ev[2 * rk], p->s2_stream) == cudaSuccess) &&
            cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->h_range + rk,
-                                         p->s2_stream, &nA),
+                                         p->s2_stream, &nA, stage2_fork(p)),
                    "range") &&
            cuda_ok(p, cudaEventRecord(p->ev_rng[rk], p->s2_stream), "event");
       if (trace) cudaEventRecord(tr_ev[2 * rk + 1], p->s2_stream);

@@ -1731,16 +1731,23 @@ __global__ void k_range_b(Stage2Args a, const TokRange *ra, TokRange *rb) {
 }
 
 cudaError_t range_a_launch(const Stage2Args &a_in, const uint64_t *known, const TokRange *prev, TokRange *r,
-                           TokRange *host, cudaStream_t stream, int *launches) {
+                           TokRange *host, cudaStream_t stream, int *launches, const Stage2Fork *fork) {
   Stage2Args a = a_in;
   a.range = r;
   const unsigned g2 = grid_tokens(a);
   k_range_a<<<1, 1, 0, stream>>>(a, known, prev, r, host);
+  if (fork) {  // k_stack next to the scalar / number / tree kernels
+    cudaEventRecord(fork->fork, stream);
+    cudaStreamWaitEvent(fork->side, fork->fork, 0);
+    launch_stack(a, fork->side);
+    cudaEventRecord(fork->join, fork->side);
+  }
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   k_slow<<<8, 64, 0, stream>>>(a);
   k_tree<<<1, 1024, 0, stream>>>(a);
-  launch_stack(a, stream);
+  if (fork) cudaStreamWaitEvent(stream, fork->join, 0);
+  else launch_stack(a, stream);
   launch_struct(a, stream);
   *launches = 9;
   return cudaGetLastError();

@@ -158,7 +158,8 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
 // the host) are recorded as patches.
 constexpr uint64_t kPatchMax = 8192;  // containers open at the range boundaries (<= kMaxDepth + 1 each)
 cudaError_t range_a_launch(const Stage2Args &a, const uint64_t *known, const TokRange *prev, TokRange *r,
-                           TokRange *host, cudaStream_t stream, int *launches);  // host: pinned copy (or null)
+                           TokRange *host, cudaStream_t stream, int *launches,
+                           const Stage2Fork *fork = nullptr);  // host: pinned copy (or null)
 cudaError_t range_b_launch(const Stage2Args &a, const TokRange *ra, TokRange *rb, cudaStream_t stream,
                            int *launches, const Stage2Fork *fork = nullptr);
 
