@@ -312,8 +312,11 @@ __global__ void k_rec_init(Stage1Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.rec_start[0] = 0;
 }
 
+#ifndef JT_K1_MINB
+#define JT_K1_MINB 3
+#endif
 template <bool kRec>
-__global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
+__global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_nl[kWarps];
   __shared__ uint32_t s_warp_tdf[kWarps];
