@@ -196,6 +196,10 @@ def test_streamed_stage2_ranges(parser, oracle):
     docs.append((b"[" + b"1.7976931348623157e308,4.9e-324," * (300000) + b"0]", "hard floats"))
     for data, where in docs:
         check_same(parser, oracle, data, where)
+    # jt_parse without a document (out == NULL): code and offset only
+    for data, where in docs[:2] + docs[4:6]:
+        g, o = parser.parse(data, want_document=False), oracle.parse(data)
+        assert (g.name, g.offset) == (o.name, o.offset) and g.document is None, where
 
 
 def _piece_cut(length: int) -> int:
