@@ -1926,14 +1926,19 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
     cudaEventRecord(fork->fork, stream);
     cudaStreamWaitEvent(fork->side, fork->fork, 0);
     launch_stack(a, fork->side);
-    cudaEventRecord(fork->join, fork->side);
   }
   k_scalars<<<g2, 256, 0, stream>>>(a);
+  if (forked) {  // the upper tree levels (from k_scalars' level 3) next to the numbers
+    cudaEventRecord(fork->fork, stream);
+    cudaStreamWaitEvent(fork->side, fork->fork, 0);
+    k_tree<<<1, 1024, 0, fork->side>>>(a);
+    cudaEventRecord(fork->join, fork->side);
+  }
   k_numbers<<<g2, 256, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[0], stream);
   k_slow<<<8, 64, 0, stream>>>(a);  // rare work; small grid keeps the local-memory reservation small
   if (ev) cudaEventRecord(ev[1], stream);
-  k_tree<<<1, 1024, 0, stream>>>(a);
+  if (!forked) k_tree<<<1, 1024, 0, stream>>>(a);
   if (ev) cudaEventRecord(ev[2], stream);
   if (forked) cudaStreamWaitEvent(stream, fork->join, 0);
   else launch_stack(a, stream);  // container kinds (scope bits) for k_struct
