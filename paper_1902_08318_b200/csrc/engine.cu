@@ -693,6 +693,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   const int64_t cA = nR ? rcut[0] : -1;  // >= 0: ranges on
   jt::TokRange *dr = p->rngbuf.as<jt::TokRange>();
   uint64_t *tokA = (uint64_t *)(dr + kMaxRanges + 1);  // token count at each cut
+  if (nR) memset((void *)p->h_range, 0, kMaxRanges * sizeof(jt::TokRange));  // nothing in flight writes it
   cudaEvent_t tr_ev[2 * kMaxRanges + 3] = {};  // JT_TRACE: device times of the ranges
   if (trace)
     for (auto &e : tr_ev) cudaEventCreate(&e);
@@ -794,10 +795,14 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   uint64_t tapeA = 0, tape_cap = 0;
   int r_next = 0;
   bool r_stop = false;
+  // A range publishes its tape end (host-mapped, written first thing by
+  // k_range_a), so its copy is queued behind its completion event while it
+  // still runs: no host polling delay between the range and its copy.
+  auto published = [&](int k) { return *(volatile uint64_t *)&p->h_range[k].tape_end != 0; };
   auto tape_a = [&](bool block) {
     while (r_next < nR && d && tape_cap) {
-      if (!block && cudaEventQuery(p->ev_rng[r_next]) != cudaSuccess) return;
-      if (!cuda_ok(p, cudaEventSynchronize(p->ev_rng[r_next]), "sync")) return;
+      if (!block && !published(r_next) && cudaEventQuery(p->ev_rng[r_next]) != cudaSuccess) return;
+      if (!published(r_next) && !cuda_ok(p, cudaEventSynchronize(p->ev_rng[r_next]), "sync")) return;
       const uint64_t lo = r_next ? p->h_range[r_next - 1].tape_end : 1, te = p->h_range[r_next].tape_end;
       if (!r_stop && te >= lo && te <= tape_cap && lo == (tapeA ? tapeA : 1)) {
         if (te > lo &&

@@ -1714,7 +1714,14 @@ __global__ void k_range_a(Stage2Args a, const uint64_t *known, const TokRange *p
   v.patch_lim = prev ? prev->tape_end : 0;
   v.tape_end = hi > lo ? a.tape_idx[hi] : (prev ? prev->tape_end : 1);
   *r = v;
-  if (host) *host = v;  // host-mapped: no copy queued behind the bulk D2H copies
+  if (host) {  // host-mapped (no copy queued behind the bulk D2H copies); tape_end
+    // last: the host polls it (nonzero) to queue the range's tape copy early
+    TokRange hv = v;
+    hv.tape_end = 0;
+    *host = hv;
+    __threadfence_system();
+    *(volatile uint64_t *)&host->tape_end = v.tape_end;
+  }
   if (!prev) a.patch[0] = 0;
 }
 
