@@ -46,7 +46,7 @@ struct Shard {
   uint32_t patch_n;       // cross-shard bracket patches recorded by k_struct
   uint32_t streamed;      // pieces of one streamed parse: only summaries up to g + 1 are final
                           // when phase 2 runs (later ones may be being written)
-  uint32_t pad_;
+  uint32_t last_tok;      // this shard holds the document's last token (end-of-input check)
 };
 
 // phase summaries (all-gathered as raw bytes)

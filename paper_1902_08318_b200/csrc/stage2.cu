@@ -70,7 +70,7 @@ __device__ __forceinline__ long long sext63(uint64_t v) { return (long long)(v <
 // unsharded.  Token / tape / string indices inside the kernels stay local;
 // the bases turn them into document values where they are written.
 struct View {
-  bool sharded, is_last;
+  bool sharded, is_last, last_tok;
   uint64_t begin, token_base, tape_base, string_base, S_total, next_pos, next_aux;
   int64_t depth_base;
   uint32_t prev[2], prev_n;
@@ -85,6 +85,7 @@ __device__ View view_of(const Stage2Args &a) {
     const Shard *h = a.sh;
     v.sharded = true;
     v.is_last = h->is_last != 0;
+    v.last_tok = h->last_tok != 0;
     v.begin = h->begin;
     v.token_base = h->token_base;
     v.tape_base = h->tape_base;
@@ -100,6 +101,7 @@ __device__ View view_of(const Stage2Args &a) {
     v.open_n = h->open_n;
   } else {
     v.is_last = true;
+    v.last_tok = true;
     v.S_total = c->S;
     v.next_pos = a.len + 1;
     v.next_aux = c->string_bytes;
@@ -944,7 +946,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   int64_t before = 0;
   if (kShard) {
     const View vw = view_of(a);
-    is_last = vw.is_last && R.fin;
+    is_last = vw.last_tok && R.fin;  // the end-of-input check: the shard with the last token
     db = (int)vw.depth_base;
     open_n = vw.open_n;
     tb = (uint32_t)vw.tape_base;
@@ -1459,6 +1461,9 @@ __global__ void k_apply1(Stage2Args a, const Sum1 *gs) {
     }
     run += gs[k].sb;
   }
+  // no later shard has a token: this one ends the document (a trailing
+  // shard can lie inside the last token, e.g. a number cut by the shard end)
+  h->last_tok = (gs[g].S > 0 && h->next_pos == h->len + 1) ? 1u : 0u;
   // the two tokens before the shard
   uint32_t n = 0;
   h->prev[0] = h->prev[1] = 0;

@@ -118,3 +118,22 @@ def test_shards_deep_then_shallow(oracle):
         for G in (2, 3, 5):
             if G <= (len(data) + TILE - 1) // TILE:
                 check_sharded(oracle, data, G, name)
+
+
+def test_shards_trailing_token_free(oracle):
+    """Shards after the document's last token (a trailing shard inside the
+    last number or string): the end-of-input check belongs to the shard that
+    holds the last token (fuzz find, tests/fuzz_gpu.py seed 99)."""
+    T = 16384
+    docs = []
+    for tail in (5, 100, T - 1):
+        head = b"[" + b"12," * ((2 * T - 8) // 3)
+        body = head + b"7" * (2 * T + tail - len(head))  # last number runs into the last shard
+        docs.append((body, f"unterminated, number into the last shard (+{tail})"))
+        docs.append((body + b"]", f"terminated (+{tail})"))
+    docs.append((b"[0." + b"1" * (3 * T), "one number across all shards, unterminated"))
+    docs.append((b"0." + b"1" * (3 * T), "root number across all shards"))
+    docs.append((b'["' + b"s" * (3 * T), "unterminated string across shards"))
+    for data, where in docs:
+        for G in (2, 3):
+            check_sharded(oracle, data, G, where)
