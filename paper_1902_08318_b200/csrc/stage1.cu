@@ -1547,17 +1547,6 @@ cudaError_t stage1_lengths_launch(const Stage1Args &a, uint64_t ntiles, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t stage1_chunk_launch(const Stage1Args &args_in, cudaStream_t stream) {
-  const Stage1Args a = with_tiles(args_in);
-  const cudaError_t configured = stage1_configure();
-  if (configured != cudaSuccess) return configured;
-  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
-  k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr, nullptr,
-                                               nullptr, nullptr, a.init_state, a.out_state);
-  k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
-  return cudaGetLastError();
-}
-
 cudaError_t stage1_chunk_carry(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
   k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);

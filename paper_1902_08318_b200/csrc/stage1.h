@@ -63,11 +63,10 @@ size_t stage1_records(uint64_t len);
 
 constexpr int kStage1Launches = 3;  // K0a carry functions, K0b carry scan, K1
 cudaError_t stage1_launch(const Stage1Args &args, cudaStream_t stream);
-// one chunk of a streamed document (rec_tile0 / last_tile / init_state /
-// out_state set): K0a, K0b, K1
-cudaError_t stage1_chunk_launch(const Stage1Args &args, cudaStream_t stream);
-// the same split in two: K0a + K0b over the piece's tiles, then K1 over a
-// tile range (streamed jt_parse runs K1 one tile behind the piece boundary)
+// one piece of a streamed document (rec_tile0 / last_tile / init_state /
+// out_state set) in two launches: K0a + K0b over the piece's tiles, then K1
+// over a tile range (streamed jt_parse runs K1 one tile behind the piece
+// boundary)
 cudaError_t stage1_chunk_carry(const Stage1Args &args, cudaStream_t stream);
 cudaError_t stage1_chunk_main(const Stage1Args &args, cudaStream_t stream);
 // after a streamed stage 1: the string length fields K1 left to stage 2
