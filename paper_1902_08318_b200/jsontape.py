@@ -302,15 +302,18 @@ class Parser:
         code = self._lib.jt_compute_stats(self._h, data, len(data), C.addressof(st), C.byref(off))
         return ERROR_NAMES[code], off.value, (st.as_dict() if code == 0 else None)
 
-    def parse_records(self, n: int, download: bool = True):
+    RECORD = np.dtype([("code", "<i4"), ("reserved", "<i4"), ("offset", "<i8"), ("tape_begin", "<u8"),
+                       ("tape_words", "<u8"), ("string_begin", "<u8"), ("string_bytes", "<u8")])
+
+    def parse_records_arrays(self, n: int, download: bool = True):
         """Parse the n resident bytes as NDJSON records (jt_b200_parse_records).
-        Returns [(name, offset, tape words or None, strings or None)] per record."""
+        Returns (records array of RECORD, tape words, string bytes); the last
+        two are None without `download`."""
         cnt = C.c_size_t()
         if self._lib.jt_b200_parse_records(self._h, n, C.byref(cnt)) != 0:
             raise RuntimeError(self.last_error())
         k = cnt.value
-        rec = np.dtype([("code", "<i4"), ("reserved", "<i4"), ("offset", "<i8"), ("tape_begin", "<u8"),
-                        ("tape_words", "<u8"), ("string_begin", "<u8"), ("string_bytes", "<u8")])
+        rec = self.RECORD
         arr = np.frombuffer(C.string_at(self._lib.jt_b200_records(self._h), k * rec.itemsize),
                             dtype=rec) if k else np.zeros(0, rec)
         tape = strings = None
@@ -318,10 +321,18 @@ class Parser:
             sz = (C.c_ulonglong * 2)()
             self._lib.jt_b200_records_size(self._h, sz)
             tape = np.zeros(max(1, sz[0]), np.uint64)
-            sb = C.create_string_buffer(max(1, sz[1]))
-            if self._lib.jt_b200_records_download(self._h, tape.ctypes.data, sb) != 0:
+            sbuf = np.zeros(max(1, sz[1]), np.uint8)
+            if self._lib.jt_b200_records_download(self._h, tape.ctypes.data, sbuf.ctypes.data) != 0:
                 raise RuntimeError(self.last_error())
-            strings = sb.raw[:sz[1]]
+            tape = tape[:sz[0]]
+            strings = sbuf[:sz[1]]
+        return arr, tape, strings
+
+    def parse_records(self, n: int, download: bool = True):
+        """Parse the n resident bytes as NDJSON records (jt_b200_parse_records).
+        Returns [(name, offset, tape words or None, strings or None)] per record."""
+        arr, tape, sarr = self.parse_records_arrays(n, download)
+        strings = sarr.tobytes() if sarr is not None else None
         out = []
         for r in arr:
             name = ERROR_NAMES[int(r["code"])]

@@ -124,3 +124,19 @@ def test_minify_kat(oracle):
     assert oracle.minify(b' [ "a b" , "c\\" d" ] ') == ("OK", -1, b'["a b","c\\" d"]')
     name, off, out = oracle.minify(b"[1,]")
     assert name == "TAPE_ERROR" and off == 3 and out is None
+
+
+def test_oracle_vs_large_fixture(oracle):
+    """The C restatement against the reference's full-size results
+    (tests/golden/large_outputs.json): C0 1 MiB, C1 64 MiB, C2 256 MiB, and the
+    generator's input digests (the GPU box regenerates these documents)."""
+    from tests.large_cases import document, load_fixture, sha
+    for row in load_fixture()["clean"]:
+        if row["config"] == 4:
+            continue  # 1 GiB: pinned on the GPU box only (tests/test_gpu_large.py)
+        d = document(row["config"])
+        assert sha(d) == row["input_sha"], row["name"]
+        r = oracle.parse(d)
+        assert (r.name, r.offset) == (row["code"], row["offset"]), row["name"]
+        assert sha(r.index) == row["index_sha"] and sha(r.tape) == row["tape_sha"]
+        assert sha(r.strings) == row["strings_sha"], row["name"]
