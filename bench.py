@@ -632,8 +632,6 @@ def main():
     s1i = statistics.median(s1i_ms)
 
     # e2e through the public C ABI: pinned host input -> jt_parse -> host document
-    # (JT_STREAM_MODE=1: the pieces mode of jt_b200_set_stream_mode, for A/B)
-    p.set_stream_mode(int(os.environ.get("JT_STREAM_MODE", "0")))
     e2e_ms = []
     for k in range(args.warmup + args.steps):
         e0 = torch.cuda.Event(enable_timing=True)

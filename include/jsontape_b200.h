@@ -44,15 +44,19 @@ const uint8_t *jt_b200_device_strings(const jt_parser *p, size_t *bytes);
 /* Materialise the last successful resident parse as a host document. */
 jt_error jt_b200_download(jt_parser *p, jt_document **out);
 
+/* Host views of a document's tape words and string buffer (the reference's
+ * parsed_document::tape / ::strings, proj/src/tape.h:49-58; valid until
+ * jt_document_free).  Used by the C++ entry points in jsontape.hpp. */
+const uint64_t *jt_b200_document_tape(const jt_document *doc, size_t *words);
+const uint8_t *jt_b200_document_strings(const jt_document *doc, size_t *bytes);
+/* A host document holding a copy of the given tape words and string buffer
+ * (free with jt_document_free); NULL on allocation failure.  Lets a C++
+ * parsed_document go through jt_document_dump / jt_document_distinct. */
+jt_document *jt_b200_document_from(const uint64_t *tape, size_t words, const uint8_t *strings, size_t bytes);
+
 /* Run the parser's work on a caller stream (a cudaStream_t, e.g. torch's
  * current stream) instead of its own; NULL restores the parser's stream. */
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream);
-
-/* How jt_parse streams a host document of >= 8 MiB: 0 = stage 1 per 4 MiB
- * piece as it lands, stage 2 after the upload (default); 1 = every piece
- * parsed as a byte-range shard (stage 2 included) while later pieces
- * upload, tape and strings back per piece.  Results are identical. */
-void jt_b200_set_stream_mode(jt_parser *p, int mode);
 
 /* Number of kernel launches enqueued by the last parse call. */
 int jt_b200_last_launches(const jt_parser *p);

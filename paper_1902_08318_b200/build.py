@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libjsontape_b200.so")
 SOURCES = ["stage1.cu", "stage2.cu", "engine.cu"]
-HEADERS = ["jt_common.cuh", "stage1_block.cuh", "lookback.cuh", "numparse.cuh", "strparse.cuh",
+HEADERS = ["jt_common.cuh", "shard.h", "stage1_block.cuh", "lookback.cuh", "numparse.cuh", "strparse.cuh",
            "strblock.cuh", "stage1.h", "stage2.h", "pow5_table.inc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

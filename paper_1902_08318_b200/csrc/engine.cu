@@ -11,7 +11,6 @@
 // There is no CPU fallback: without a CUDA device jt_parser_new returns NULL
 // and nothing else can be called.
 #include <cuda_runtime.h>
-#include <cub/cub.cuh>
 
 #include <chrono>
 #include <cstdio>
@@ -233,15 +232,7 @@ struct jt_parser {
   DevBuf stream_words;
   DevBuf qbuf, qstr;  // distinct_values query: keys, matches, values, lengths, offsets, scan | strings
   jt::Ctrl *h_ctrl_s1 = nullptr;  // pinned
-  // streamed jt_parse with stage 2 per piece (parse_pieces): one child
-  // parser per piece, each a byte-range shard reading this parser's input
-  const uint8_t *in_alias = nullptr;  // child: the parent's padded input
-  bool needs_mat = false;             // the resident state is in the children: re-parse on demand
-  int stream_mode = 0;                // jt_b200_set_stream_mode
-  std::vector<jt_parser *> kids;
-  std::vector<cudaEvent_t> done_ev;
-  cudaEvent_t ev_fin = nullptr;
-  cudaStream_t s2_stream = nullptr;   // pieces' stage 2: high priority, ahead of later pieces' stage 1
+  cudaStream_t s2_stream = nullptr;   // early stage-2 ranges: high priority, ahead of later pieces' stage 1
   // streamed jt_parse, stage 2 in two token ranges (parse_stream)
   DevBuf rngbuf;                      // TokRange A, B | stage-1 token count at piece cA
   DevBuf patchbuf;                    // range B's openers below range A's tape end
@@ -249,10 +240,6 @@ struct jt_parser {
   unsigned long long *h_patch = nullptr;  // pinned copy of the patch list
   cudaEvent_t ev_rng[5] = {};         // early range k done (its TokRange on the host); [4]: the last range
   cudaStream_t ta_stream = nullptr;   // the early ranges' tape words back to the host
-  DevBuf psum;                        // gathered Sum0 | Sum1 | Sum2 | Sum3 of the pieces
-  jt::Sum1 *h_sum1_init = nullptr;    // pinned: "not written yet" Sum1s
-  jt::Sum3 *h_sum3 = nullptr;         // pinned: the pieces' Sum3 (bracket patches)
-  uint32_t h_sum_cap = 0;
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
   DevBuf minbuf;  // jt_minify: look-back records, counter, total, output
@@ -268,6 +255,20 @@ struct jt_parser {
 };
 
 namespace {
+
+// Every call runs on the parser's device (a parser is bound to the device
+// current at jt_parser_new), whatever device the calling thread has selected.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const jt_parser *p) {
+    int d = -1;
+    if (p && cudaGetDevice(&d) == cudaSuccess && d != p->device && cudaSetDevice(p->device) == cudaSuccess)
+      prev = d;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 bool cuda_ok(jt_parser *p, cudaError_t e, const char *what) {
   if (e == cudaSuccess) return true;
@@ -338,7 +339,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0
   a.end = end == ~0ULL ? len : end;
   a.last_tile = ~0ULL;
   jt::Ctrl *c = p->ctrl.as<jt::Ctrl>();
-  a.in = p->in_alias ? p->in_alias : p->in.as<uint8_t>();
+  a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
   a.aux = p->aux[which].as<uint32_t>();
@@ -365,7 +366,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
                        bool sharded = false) {
   if (cap_len == ~0ULL) cap_len = len;
   jt::Stage2Args a{};
-  a.in = p->in_alias ? p->in_alias : p->in.as<uint8_t>();
+  a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
   a.aux = p->aux[which].as<uint32_t>();
@@ -492,7 +493,6 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
 
 // wait for the enqueued work and publish its results into the parser
 jt_error finish(jt_parser *p, int which, bool full, long long *off) {
-  p->needs_mat = false;
   if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) {
     set_off(off, -1);
     return JT_CAPACITY;
@@ -510,6 +510,14 @@ jt_error finish(jt_parser *p, int which, bool full, long long *off) {
     p->h_index_valid = false;
   }
   set_off(off, c.offset);
+  if (full && c.code == jt::kOk && (c.string_bytes >= (1ULL << 32) || c.tape_words >= (1ULL << 32))) {
+    // string offsets and tape indices travel as u32 between the kernels: a
+    // document whose string buffer or tape reaches 2^32 cannot be represented
+    // (only inputs > ~2.4 GiB can get there); fail like an allocation failure
+    // (capi.cpp:81-84) instead of returning wrapped offsets
+    set_off(off, -1);
+    return JT_CAPACITY;
+  }
   if (full && c.code == jt::kOk) {
     p->last_ok = true;
     p->last_tape_len = c.tape_len;
@@ -823,7 +831,10 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   };
   if (ok && out) {
     d = new (std::nothrow) jt_document;
-    early = d && d->alloc_strings(len + len / 4 + 64);
+    // the early path lets kernels (k_tile_lengths) write into the host block:
+    // only when it is page-locked (a pageable fallback block is filled by
+    // plain copies after stage 1 instead)
+    early = d && d->alloc_strings(len + len / 4 + 64) && d->spinned;
     if (early && cA >= 0 && d->alloc_tape(len / 8 + 1024)) tape_cap = d->tape.n;
     for (uint64_t c = 0; early && c < nch; c++) {
       if (!cuda_ok(p, cudaEventSynchronize(p->piece_ev[c]), "sync")) {
@@ -1003,10 +1014,8 @@ jt_error parse_resident(jt_parser *p, uint64_t len, jt_document **out, long long
 }
 
 
-// Byte-range shard setup (shard.h) shared by jt_b200_shard_begin and the
-// pieces of a streamed jt_parse (children alias the parent's input).
-int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end,
-                bool streamed = false) {
+// Byte-range shard setup (shard.h) for jt_b200_shard_begin.
+int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
   if (G == 0 || g >= G || (uint64_t)len >= (1ULL << 32) || begin % jt::kStage1Tile != 0 ||
       !(begin < end) || end > len || (g + 1 == G) != (end == len) || (g == 0) != (begin == 0)) {
     p->err = "shard_begin: bad shard layout";
@@ -1019,7 +1028,7 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
     return -1;
   }
   const uint64_t range = end - begin;
-  if ((!p->in_alias && !ensure_input(p, len)) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
+  if (!ensure_input(p, len) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
       !p->shard.ensure(kShardBoundOff + jt::kBoundMax * sizeof(uint64_t))) {
     p->err = "shard_begin: device allocation";
     return -1;
@@ -1030,7 +1039,7 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
   h.begin = begin;
   h.end = end;
   h.len = len;
-  h.streamed = streamed ? 1u : 0u;
+  h.streamed = 0u;
   *p->h_shard = h;
   if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
                                   p->stream),
@@ -1043,313 +1052,7 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
   p->last_ok = false;
   p->have_index = false;
   p->h_index_valid = false;
-  p->needs_mat = false;
   return 0;
-}
-
-// ---- streamed jt_parse, stage 2 included ------------
-// The document is cut into G tile-aligned pieces, each parsed by a child
-// parser as byte-range shard g of G (shard.h) while the later pieces are
-// still uploading.  The shard phases need only summaries of EARLIER pieces,
-// plus the next piece's first token (phase 2), so on one stream:
-//   upload g | phase 0 (g) | [upload g+1: K1 reads a few bytes past the
-//   piece] phase 1 (g) | phase 2, 3 (g-1)
-// and piece g-1's tape words and string bytes go back to the host while the
-// upload continues.  Bracket pairs across pieces are the shards' patches
-// (Sum3), applied to the host tape at the end; the root word carries the
-// document's root close index.  The parser's own resident state (index,
-// tape, strings in HBM) is rebuilt on demand (materialize) by the calls
-// that read it.  A piece whose phase 2 met a later piece without a summary
-// yet (next non-empty piece not parsed: pieces without a token start) is
-// reported by Ctrl.redo and the document is parsed again resident.
-constexpr uint64_t kPieceBytes = 8ULL << 20;
-constexpr unsigned kMaxPieces = 64;  // k_apply2 folds at most 64 earlier shards
-
-unsigned piece_count(uint64_t len) {
-  static const uint64_t piece = [] {
-    const char *e = getenv("JT_PIECE_MB");
-    const long v = e ? atol(e) : 0;
-    return v > 0 ? (uint64_t)v << 20 : kPieceBytes;
-  }();
-  const uint64_t tiles = (len + jt::kStage1Tile - 1) / jt::kStage1Tile;
-  uint64_t G = (len + piece / 2) / piece;
-  G = std::max<uint64_t>(2, std::min<uint64_t>(G, kMaxPieces));
-  return (unsigned)std::min<uint64_t>(G, tiles);
-}
-
-bool ensure_pieces(jt_parser *p, unsigned G) {
-  while (p->kids.size() < G) {
-    jt_parser *k = jt_parser_new();
-    if (!k) return false;
-    p->kids.push_back(k);
-  }
-  auto mk = [](cudaEvent_t *e) {
-    return *e || cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
-  };
-  while (p->done_ev.size() < G) {
-    cudaEvent_t e = nullptr;
-    if (!mk(&e)) return false;
-    p->done_ev.push_back(e);
-  }
-  if (!mk(&p->ev_fin)) return false;
-  if (!p->s2_stream) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&p->s2_stream, cudaStreamNonBlocking, hi) != cudaSuccess) {
-      cudaGetLastError();
-      p->s2_stream = nullptr;
-      return false;
-    }
-  }
-  if (p->h_sum_cap < G) {
-    if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
-    if (p->h_sum3) cudaFreeHost(p->h_sum3);
-    p->h_sum1_init = nullptr;
-    p->h_sum3 = nullptr;
-    p->h_sum_cap = 0;
-    if (cudaMallocHost((void **)&p->h_sum1_init, kMaxPieces * sizeof(jt::Sum1)) != cudaSuccess ||
-        cudaMallocHost((void **)&p->h_sum3, kMaxPieces * sizeof(jt::Sum3)) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    for (unsigned k = 0; k < kMaxPieces; k++) {
-      jt::Sum1 z{};
-      z.utf8_pos = ~0ULL;
-      z.str_err = ~0ULL;
-      p->h_sum1_init[k] = z;  // pad[0] == 0: not written
-    }
-    p->h_sum_cap = kMaxPieces;
-  }
-  return p->psum.ensure(kMaxPieces * (sizeof(jt::Sum0) + sizeof(jt::Sum1) + sizeof(jt::Sum2) + sizeof(jt::Sum3)));
-}
-
-jt_error parse_pieces(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
-  static const bool trace = getenv("JT_TRACE") != nullptr;
-  auto now_us = []() {
-    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
-  };
-  const double t0 = trace ? now_us() : 0;
-  if (out) *out = nullptr;
-  const unsigned G = piece_count(len);
-  if (!ensure_input(p, len) || !ensure_stream(p, G) || !ensure_pieces(p, G)) {
-    set_off(off, -1);
-    return JT_CAPACITY;
-  }
-  // piece layout as shard.py layout(): tile-aligned cuts
-  const uint64_t tiles = (len + jt::kStage1Tile - 1) / jt::kStage1Tile;
-  std::vector<uint64_t> cut(G + 1);
-  for (unsigned g = 0; g < G; g++) cut[g] = (g * tiles / G) * jt::kStage1Tile;
-  cut[G] = len;
-  uint8_t *in = p->in.as<uint8_t>();
-  jt::Sum0 *s0 = (jt::Sum0 *)p->psum.p;
-  jt::Sum1 *s1 = (jt::Sum1 *)(s0 + kMaxPieces);
-  jt::Sum2 *sum2 = (jt::Sum2 *)(s1 + kMaxPieces);
-  jt::Sum3 *s3 = (jt::Sum3 *)(sum2 + kMaxPieces);
-  // stage 1 of the pieces on the parser's stream, stage 2 on a high-priority
-  // stream (its short kernels go ahead of the next pieces' stage-1 tiles)
-  cudaStream_t cs = p->copy_stream, st = p->stream, s2 = p->s2_stream;
-  p->launches = 0;
-  p->needs_mat = false;
-  // JT_TRACE: device timeline of the pieces (upload / stage 1 / stage 2 done)
-  std::vector<cudaEvent_t> tev;
-  if (trace) {
-    tev.resize(3 * G + 1);
-    for (auto &e : tev) cudaEventCreate(&e);
-    cudaEventRecord(tev[0], st);
-  }
-  auto mark = [&](int k, cudaStream_t s_) {
-    if (trace) cudaEventRecord(tev[k], s_);
-  };
-  bool ok = cuda_ok(p, cudaEventRecord(p->ev_start, st), "event") &&
-            cuda_ok(p, cudaStreamWaitEvent(cs, p->ev_start, 0), "wait") &&
-            cuda_ok(p, cudaMemsetAsync(in + len, 0, input_capacity(len) - len, cs), "tail");
-  for (unsigned g = 0; ok && g < G; g++) {
-    ok = cuda_ok(p, cudaMemcpyAsync(in + cut[g], data + cut[g], cut[g + 1] - cut[g], cudaMemcpyHostToDevice, cs),
-                 "H2D") &&
-         cuda_ok(p, cudaEventRecord(p->chunk_ev[g], cs), "event");
-    mark(1 + g, cs);
-  }
-  ok = ok && cuda_ok(p, cudaMemcpyAsync(s1, p->h_sum1_init, G * sizeof(jt::Sum1), cudaMemcpyHostToDevice, st),
-                     "sum1 init");
-  for (unsigned g = 0; ok && g < G; g++) {
-    jt_parser *k = p->kids[g];
-    k->in_alias = in;
-    k->stream = st;
-    ok = shard_setup(k, len, g, G, cut[g], cut[g + 1], true) == 0;
-    if (!ok) p->err = k->err;
-  }
-  auto back = [&](unsigned g) {  // phases 2 + 3 of piece g (side stream), its control block and patches
-    jt_parser *k = p->kids[g];
-    k->stream = s2;
-    bool r = cuda_ok(p, cudaStreamWaitEvent(s2, p->piece_ev[std::min(g + 1, G - 1)], 0), "wait") &&
-             jt_b200_shard_phase(k, 2, s1, sum2 + g) == 0 && jt_b200_shard_phase(k, 3, sum2, s3 + g) == 0;
-    if (!r && p->err.empty()) p->err = k->err;
-    return r && cuda_ok(p, cudaMemcpyAsync(k->h_ctrl, k->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, s2),
-                        "ctrl D2H") &&
-           cuda_ok(p, cudaEventRecord(p->done_ev[g], s2), "event") && (mark(1 + 2 * G + g, s2), true);
-  };
-  for (unsigned g = 0; ok && g < G; g++) {
-    jt_parser *k = p->kids[g];
-    ok = cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[g], 0), "wait") &&
-         jt_b200_shard_phase(k, 0, nullptr, s0 + g) == 0 &&
-         cuda_ok(p, cudaStreamWaitEvent(st, p->chunk_ev[std::min(g + 1, G - 1)], 0), "wait") &&
-         jt_b200_shard_phase(k, 1, s0, s1 + g) == 0 &&
-         cuda_ok(p, cudaEventRecord(p->piece_ev[g], st), "event");
-    mark(1 + G + g, st);
-    if (!ok && p->err.empty()) p->err = k->err;
-    if (ok && g > 0) ok = back(g - 1);
-  }
-  jt_parser *last = p->kids[G - 1];
-  ok = ok && back(G - 1) &&
-       cuda_ok(p, jt::shard_finish_launch(s2_args(last, len, 0, cut[G] - cut[G - 1], true), s3, s2), "finish") &&
-       cuda_ok(p, cudaMemcpyAsync(last->h_ctrl, last->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost, s2),
-               "ctrl D2H") &&
-       cuda_ok(p, cudaMemcpyAsync(p->h_sum3, s3, G * sizeof(jt::Sum3), cudaMemcpyDeviceToHost, s2), "sum3 D2H") &&
-       cuda_ok(p, cudaEventRecord(p->ev_fin, s2), "event");
-  if (trace) fprintf(stderr, " pieces: %u enqueued %.0f us\n", G, now_us() - t0);
-  // pieces come back as they finish; the host document is sized from the
-  // input (tape <= 1 word per input byte + 3 is not guaranteed: a larger
-  // document is downloaded whole below)
-  jt_document *d = nullptr;
-  bool early = false, failed = false;
-  uint64_t tbase = 0, sbase = 0, S = 0;
-  if (ok && out) {
-    d = new (std::nothrow) jt_document;
-    early = d && d->alloc(len / 8 + 1024, len + len / 4 + 64);
-  }
-  for (unsigned g = 0; ok && g < G; g++) {
-    if (!cuda_ok(p, cudaEventSynchronize(p->done_ev[g]), "sync")) {
-      ok = false;
-      break;
-    }
-    const jt::Ctrl &c = *p->kids[g]->h_ctrl;
-    if (c.utf8_pos != ~0ULL || c.err_key != ~0ULL || c.redo) failed = true;  // no document: result below
-    const uint64_t lo = g == 0 ? 0 : 1, hi = c.tape_words + (g + 1 == G ? 1 : 0);
-    if (early && !failed) {
-      if (tbase + hi > d->tape.size() || sbase + c.string_bytes > d->strings.size()) {
-        early = false;
-      } else {
-        jt_parser *k = p->kids[g];
-        ok = cuda_ok(p, cudaStreamWaitEvent(p->d2h_stream, p->done_ev[g], 0), "wait") &&
-             cuda_ok(p, cudaMemcpyAsync(d->tape.data() + tbase + lo, k->tape.as<uint64_t>() + lo, (hi - lo) * 8,
-                                        cudaMemcpyDeviceToHost, p->d2h_stream),
-                     "tape piece D2H") &&
-             (!c.string_bytes ||
-              cuda_ok(p, cudaMemcpyAsync(d->strings.data() + sbase, k->strings.p, c.string_bytes,
-                                         cudaMemcpyDeviceToHost, p->d2h_stream),
-                      "strings piece D2H"));
-      }
-    }
-    if (trace && (g < 2 || g + 2 >= G || g % 4 == 0)) fprintf(stderr, " piece %u done %.0f us\n", g, now_us() - t0);
-    tbase += c.tape_words - 1;
-    sbase += c.string_bytes;
-    S += c.S;
-  }
-  if (!ok || !cuda_ok(p, cudaEventSynchronize(p->ev_fin), "sync") || !cuda_ok(p, cudaStreamSynchronize(st), "sync") ||
-      !cuda_ok(p, cudaStreamSynchronize(p->d2h_stream), "sync") || !cuda_ok(p, cudaStreamSynchronize(cs), "sync")) {
-    cudaStreamSynchronize(st);
-    cudaStreamSynchronize(s2);
-    cudaStreamSynchronize(cs);
-    cudaStreamSynchronize(p->d2h_stream);
-    delete d;
-    set_off(off, -1);
-    return JT_CAPACITY;
-  }
-  if (trace) {
-    for (unsigned g = 0; g < G; g++) {
-      float t[3];
-      for (int q = 0; q < 3; q++) cudaEventElapsedTime(&t[q], tev[0], tev[1 + q * G + g]);
-      fprintf(stderr, " piece %u: uploaded %.0f us, stage 1 %.0f, stage 2 %.0f\n", g, 1e3 * t[0], 1e3 * t[1],
-              1e3 * t[2]);
-    }
-    for (auto &e : tev) cudaEventDestroy(e);
-  }
-  p->launches = 0;
-  bool redo = false;
-  for (unsigned g = 0; g < G; g++) {
-    p->launches += p->kids[g]->launches;
-    redo = redo || p->kids[g]->h_ctrl->redo;
-  }
-  p->in_len = len;
-  if (redo) {  // a piece needed a summary that did not exist yet: parse resident
-    delete d;
-    return parse_resident(p, len, out, off);
-  }
-  const jt::Ctrl &c = *last->h_ctrl;
-  const jt_error e = (jt_error)c.code;
-  set_off(off, c.offset);
-  // the parser's index / tape / strings: rebuilt from the resident input when read
-  p->needs_mat = true;
-  p->last_ok = false;
-  if (c.code != jt::kUtf8Error) {
-    p->have_index = true;
-    p->index_count = S;
-    p->h_index_valid = false;
-  }
-  const double t4 = trace ? now_us() : 0;
-  if (e != JT_OK || !out) {
-    delete d;
-    return e;
-  }
-  const uint64_t E = tbase + 1;  // root close index = 1 + sum of token widths
-  if (!d || !early) {  // larger than the early host blocks: the pieces whole
-    delete d;
-    d = new (std::nothrow) jt_document;
-    if (!d || !d->alloc(E + 1, sbase)) {
-      delete d;
-      set_off(off, -1);
-      return JT_CAPACITY;
-    }
-    uint64_t tb = 0, sb = 0;
-    for (unsigned g = 0; g < G; g++) {
-      jt_parser *k = p->kids[g];
-      const jt::Ctrl &kc = *k->h_ctrl;
-      const uint64_t lo = g == 0 ? 0 : 1, hi = kc.tape_words + (g + 1 == G ? 1 : 0);
-      if (!cuda_ok(p, cudaMemcpyAsync(d->tape.data() + tb + lo, k->tape.as<uint64_t>() + lo, (hi - lo) * 8,
-                                      cudaMemcpyDeviceToHost, st),
-                   "tape D2H") ||
-          (kc.string_bytes && !cuda_ok(p, cudaMemcpyAsync(d->strings.data() + sb, k->strings.p, kc.string_bytes,
-                                                          cudaMemcpyDeviceToHost, st),
-                                       "strings D2H"))) {
-        delete d;
-        set_off(off, -1);
-        return JT_CAPACITY;
-      }
-      tb += kc.tape_words - 1;
-      sb += kc.string_bytes;
-    }
-    if (!cuda_ok(p, cudaStreamSynchronize(st), "sync")) {
-      delete d;
-      set_off(off, -1);
-      return JT_CAPACITY;
-    }
-  } else {
-    d->tape.n = E + 1;
-    d->strings.n = sbase;
-  }
-  // brackets whose opener lives in an earlier piece; the root word
-  for (unsigned g = 0; g < G; g++) {
-    const jt::Sum3 &r = p->h_sum3[g];
-    const uint32_t n = std::min<uint32_t>(r.patch_n, (uint32_t)jt::kBoundMax);
-    for (uint32_t q = 0; q < n; q++)
-      if (r.patch[2 * q] < E + 1) d->tape.data()[r.patch[2 * q]] = r.patch[2 * q + 1];
-  }
-  d->tape.data()[0] = jt::tape_word(jt::kTagRoot, E);
-  *out = d;
-  if (trace)
-    fprintf(stderr, "parse_pieces: %u pieces, all done %.0f us, document %.0f us (early %d)\n", G, t4 - t0,
-            now_us() - t0, (int)early);
-  return e;
-}
-
-// The calls that read the parser's resident state after a parse_pieces
-// (index positions, jt_stage2, device views, distinct_values) parse the
-// resident input once more here.
-void materialize(const jt_parser *cp) {
-  jt_parser *p = const_cast<jt_parser *>(cp);
-  if (!p->needs_mat) return;
-  p->needs_mat = false;
-  parse_resident(p, p->in_len, nullptr, nullptr);
 }
 
 }  // namespace
@@ -1389,13 +1092,9 @@ jt_parser *jt_parser_new(void) {
 }
 
 void jt_parser_free(jt_parser *p) {
+  DevGuard dg_(p);
   if (!p) return;
   cudaStreamSynchronize(p->stream);
-  for (jt_parser *k : p->kids) {  // children run on this parser's stream
-    k->stream = k->own_stream;
-    jt_parser_free(k);
-  }
-  p->kids.clear();
   for (auto &g : p->graph)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto &g : p->graph_s1)
@@ -1424,8 +1123,6 @@ void jt_parser_free(jt_parser *p) {
   if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->ev_s1) cudaEventDestroy(p->ev_s1);
   if (p->h_ctrl_s1) cudaFreeHost(p->h_ctrl_s1);
-  for (cudaEvent_t e : p->done_ev) cudaEventDestroy(e);
-  if (p->ev_fin) cudaEventDestroy(p->ev_fin);
   if (p->s2_stream) {
     cudaStreamSynchronize(p->s2_stream);
     cudaStreamDestroy(p->s2_stream);
@@ -1438,12 +1135,11 @@ void jt_parser_free(jt_parser *p) {
     cudaStreamSynchronize(p->ta_stream);
     cudaStreamDestroy(p->ta_stream);
   }
-  if (p->h_sum1_init) cudaFreeHost(p->h_sum1_init);
-  if (p->h_sum3) cudaFreeHost(p->h_sum3);
   delete p;
 }
 
 void jt_parser_set_flags(jt_parser *p, int use_clmul, int fast_extract, int vector_classify) {
+  DevGuard dg_(p);
   (void)p;
   (void)use_clmul;
   (void)fast_extract;
@@ -1452,17 +1148,14 @@ void jt_parser_set_flags(jt_parser *p, int use_clmul, int fast_extract, int vect
 
 jt_error jt_parse(jt_parser *p, const char *data, size_t len, jt_document **out,
                   long long *error_offset) {
+  DevGuard dg_(p);
   if (out) *out = nullptr;
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
   if ((uint64_t)len >= kStreamMin) {
-    // stream mode 1: stage 2 per piece as well (parse_pieces).  Measured
-    // slower on C1 (25.4 vs 27.7 GB/s e2e): the shard phases of a piece take
-    // longer on the GPU than the piece's upload (~250 vs ~170 us per 8 MiB)
-    return p->stream_mode == 1 ? parse_pieces(p, data, len, out, error_offset)
-                               : parse_stream(p, data, len, out, error_offset);
+    return parse_stream(p, data, len, out, error_offset);
   }
   if (!upload(p, data, len)) {
     set_off(error_offset, -1);
@@ -1472,6 +1165,7 @@ jt_error jt_parse(jt_parser *p, const char *data, size_t len, jt_document **out,
 }
 
 jt_error jt_stage1(jt_parser *p, const char *data, size_t len, long long *error_offset) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -1486,7 +1180,7 @@ jt_error jt_stage1(jt_parser *p, const char *data, size_t len, long long *error_
 size_t jt_index_count(const jt_parser *p) { return p->have_index ? (size_t)p->index_count : 0; }
 
 const uint32_t *jt_index_positions(const jt_parser *p) {
-  materialize(p);
+  DevGuard dg_(p);
   if (!p->h_index_valid) {
     p->h_index.assign(p->index_count + 8, 0u);
     if (p->index_count)
@@ -1497,8 +1191,8 @@ const uint32_t *jt_index_positions(const jt_parser *p) {
 }
 
 jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
+  DevGuard dg_(p);
   if (out) *out = nullptr;
-  materialize(p);
   uint64_t len = p->in_len;
   if (!ensure_stage2(p, len)) {
     set_off(error_offset, -1);
@@ -1788,7 +1482,7 @@ char *jt_document_distinct(const jt_document *doc, const char *path) {
 // jt_document_distinct on the downloaded document.  NULL without such a
 // parse or on a device error.
 char *jt_b200_distinct(jt_parser *p, const char *path) {
-  materialize(p);
+  DevGuard dg_(p);
   if (!p || !p->last_ok || !path) return nullptr;
   std::set<DVal> vals;
   if (!*path) return malloc_string(std::string());
@@ -1806,13 +1500,11 @@ char *jt_b200_distinct(jt_parser *p, const char *path) {
     kb += keys[k];
   }
   q.key_off[keys.size()] = (uint32_t)kb.size();
-  // qbuf: count | keys | match[S] | vals[S] | len[S] | off[S] | scan temp
+  // qbuf: count | keys | match[S] | vals[S] | len[S] | off[S]
   const size_t a_keys = 256, a_match = round_up(a_keys + kb.size() + 1, 256);
   const size_t a_vals = round_up(a_match + 4 * S + 4, 256), a_len = round_up(a_vals + 16 * S, 256);
   const size_t a_off = round_up(a_len + 4 * S + 4, 256), a_tmp = round_up(a_off + 4 * S + 4, 256);
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(S + 1));
-  if (!p->qbuf.ensure(a_tmp + tmp_bytes + 256)) {
+  if (!p->qbuf.ensure(a_tmp + 256)) {
     p->err = "distinct: out of memory";
     return nullptr;
   }
@@ -1834,11 +1526,9 @@ char *jt_b200_distinct(jt_parser *p, const char *path) {
   std::vector<uint32_t> last(2, 0);
   std::vector<uint8_t> hs;
   if (count) {
-    size_t tb = tmp_bytes;
     if (!cuda_ok(p, jt::distinct_values_launch(a, d_match, count, d_vals, d_len, p->stream), "distinct values") ||
         !cuda_ok(p, cudaMemsetAsync(d_len + count, 0, 4, p->stream), "memset") ||
-        !cuda_ok(p, cub::DeviceScan::ExclusiveSum(qb + a_tmp, tb, d_len, d_off, (int)count + 1, p->stream),
-                 "scan") ||
+        !cuda_ok(p, jt::scan_u32_launch(d_len, d_off, count + 1, p->stream), "scan") ||
         !cuda_ok(p, cudaMemcpyAsync(hv.data(), d_vals, 16 * (size_t)count, cudaMemcpyDeviceToHost, p->stream),
                  "values D2H") ||
         !cuda_ok(p, cudaMemcpyAsync(last.data(), d_off + count, 4, cudaMemcpyDeviceToHost, p->stream), "D2H") ||
@@ -1881,6 +1571,7 @@ void jt_string_free(char *s) { free(s); }
 // GPU (k_minify) over the same resident input and its K0 carry-ins
 jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t *dst_len,
                    long long *error_offset) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -1923,6 +1614,7 @@ jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t
 // reductions over the token records, tape tags and input (k_stats)
 jt_error jt_compute_stats(jt_parser *p, const char *data, size_t len, jt_stats *out,
                           long long *error_offset) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -1995,14 +1687,15 @@ const char *jt_error_name(jt_error code) {
 // ---- B200 extensions -------------------------------------------------------
 
 void *jt_b200_input_buffer(jt_parser *p, size_t len) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) return nullptr;
-  materialize(p);  // the resident state of a streamed parse still needs its input
   if (!ensure_input(p, len) || !zero_tail(p, len)) return nullptr;
   if (!cuda_ok(p, cudaStreamSynchronize(p->stream), "sync")) return nullptr;
   return p->in.p;
 }
 
 int jt_b200_copy_in(jt_parser *p, const void *src, size_t len) {
+  DevGuard dg_(p);
   if (!jt_b200_input_buffer(p, len)) return -1;
   if (len && !cuda_ok(p, cudaMemcpyAsync(p->in.p, src, len, cudaMemcpyDefault, p->stream), "copy_in"))
     return -1;
@@ -2013,7 +1706,7 @@ int jt_b200_copy_in(jt_parser *p, const void *src, size_t len) {
 // Enqueue (no wait) a copy of bytes [offset, offset + n) of a host or device
 // document `src` into the same positions of the input buffer.
 int jt_b200_copy_in_range(jt_parser *p, const void *src, size_t offset, size_t n) {
-  materialize(p);
+  DevGuard dg_(p);
   if (offset + n > p->in.cap) return -1;
   if (n && !cuda_ok(p, cudaMemcpyAsync(p->in.as<uint8_t>() + offset, (const uint8_t *)src + offset, n,
                                        cudaMemcpyDefault, p->stream),
@@ -2023,6 +1716,7 @@ int jt_b200_copy_in_range(jt_parser *p, const void *src, size_t offset, size_t n
 }
 
 jt_error jt_b200_stage1_resident(jt_parser *p, size_t len, long long *error_offset) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -2037,11 +1731,13 @@ jt_error jt_b200_stage1_resident(jt_parser *p, size_t len, long long *error_offs
 }
 
 jt_error jt_b200_parse_resident(jt_parser *p, size_t len, long long *error_offset) {
+  DevGuard dg_(p);
   p->in_len = len;
   return parse_resident(p, len, nullptr, error_offset);
 }
 
 jt_error jt_b200_parse_async(jt_parser *p, size_t len) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) return JT_CAPACITY;
   p->in_len = len;
   int which = p->cur ^ 1;
@@ -2054,6 +1750,7 @@ jt_error jt_b200_parse_async(jt_parser *p, size_t len) {
 }
 
 jt_error jt_b200_stage1_async(jt_parser *p, size_t len) {
+  DevGuard dg_(p);
   if ((uint64_t)len >= (1ULL << 32)) return JT_CAPACITY;
   p->in_len = len;
   int which = p->cur ^ 1;
@@ -2065,6 +1762,7 @@ jt_error jt_b200_stage1_async(jt_parser *p, size_t len) {
 }
 
 jt_error jt_b200_finish(jt_parser *p, long long *error_offset) {
+  DevGuard dg_(p);
   if (p->pending_idx < 0) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -2075,34 +1773,56 @@ jt_error jt_b200_finish(jt_parser *p, long long *error_offset) {
 }
 
 const uint32_t *jt_b200_device_index(const jt_parser *p, size_t *count) {
-  materialize(p);
+  DevGuard dg_(p);
   if (count) *count = jt_index_count(p);
   return p->idx[p->cur].as<uint32_t>();
 }
 
 const uint64_t *jt_b200_device_tape(const jt_parser *p, size_t *words) {
-  materialize(p);
+  DevGuard dg_(p);
   if (words) *words = p->last_ok ? p->last_tape_len : 0;
   return p->tape.as<uint64_t>();
 }
 
 const uint8_t *jt_b200_device_strings(const jt_parser *p, size_t *bytes) {
-  materialize(p);
+  DevGuard dg_(p);
   if (bytes) *bytes = p->last_ok ? p->last_string_bytes : 0;
   return p->strings.as<uint8_t>();
 }
 
+const uint64_t *jt_b200_document_tape(const jt_document *doc, size_t *words) {
+  if (words) *words = doc ? doc->tape.size() : 0;
+  return doc ? doc->tape.data() : nullptr;
+}
+
+const uint8_t *jt_b200_document_strings(const jt_document *doc, size_t *bytes) {
+  if (bytes) *bytes = doc ? doc->strings.size() : 0;
+  return doc ? doc->strings.data() : nullptr;
+}
+
+jt_document *jt_b200_document_from(const uint64_t *tape, size_t words, const uint8_t *strings, size_t bytes) {
+  jt_document *d = new (std::nothrow) jt_document;
+  if (!d) return nullptr;
+  if (!d->alloc(words, bytes)) {
+    delete d;
+    return nullptr;
+  }
+  if (words) memcpy(d->tape.p, tape, words * 8);
+  if (bytes) memcpy(d->strings.p, strings, bytes);
+  return d;
+}
+
 jt_error jt_b200_download(jt_parser *p, jt_document **out) {
+  DevGuard dg_(p);
   *out = nullptr;
-  materialize(p);
   if (!p->last_ok) return JT_CAPACITY;
   *out = download(p);
   return *out ? JT_OK : JT_CAPACITY;
 }
 
-void jt_b200_set_stream_mode(jt_parser *p, int mode) { p->stream_mode = mode == 1 ? 1 : 0; }
 
 void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
+  DevGuard dg_(p);
   p->stream = cuda_stream ? (cudaStream_t)cuda_stream : p->own_stream;
 }
 
@@ -2111,8 +1831,8 @@ void jt_b200_set_stream(jt_parser *p, void *cuda_stream) {
 // Parse the len resident bytes as '\n'-separated records, each as jt_parse of
 // the record alone would.  Waits; one host sync after the newline count.
 int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
+  DevGuard dg_(p);
   if (n_records) *n_records = 0;
-  p->needs_mat = false;  // the resident state becomes this parse's
   if ((uint64_t)len >= (1ULL << 32) || !ensure_input(p, len) || !ensure_stage1(p, len, 0) ||
       !ensure_stage2(p, len) ||
       !p->nlbuf.ensure(jt::stage1_records(len) * 2 * sizeof(uint32_t) + 64)) {
@@ -2196,6 +1916,10 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
       !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
     return -1;
   p->launches = 1 + 2 + 2 + 1 + n2;
+  if (p->h_ctrl->string_bytes >= (1ULL << 32) || p->h_ctrl->tape_words >= (1ULL << 32)) {
+    p->err = "parse_records: string buffer or tape reaches 2^32 (u32 offsets)";
+    return -1;
+  }
   // the input's last byte decides whether a record follows the last '\n'
   // (read from the pinned control copy: no extra sync)
   const uint64_t n = nl + ((len > 0 && p->rec_last_byte != '\n') ? 1 : 0);
@@ -2211,6 +1935,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
 
 // host copy of the last jt_b200_parse_records results (made on first use)
 const void *jt_b200_records(jt_parser *p) {
+  DevGuard dg_(p);
   if (!p->h_records_valid) {
     try {
       p->h_records.resize(p->rec_n);
@@ -2232,6 +1957,7 @@ const void *jt_b200_device_records(const jt_parser *p) { return p->rec_results; 
 
 // Copy all records' tape words and string bytes (jt_b200_record ranges) to host.
 int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {
+  DevGuard dg_(p);
   if (p->last_tape_len &&
       !cuda_ok(p, cudaMemcpy(tape, p->tape.p, p->last_tape_len * 8, cudaMemcpyDeviceToHost), "tape D2H"))
     return -1;
@@ -2244,6 +1970,7 @@ int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {
 
 // Sizes of the last jt_b200_parse_records output: out[0] tape words, out[1] string bytes.
 void jt_b200_records_size(const jt_parser *p, unsigned long long *out) {
+  DevGuard dg_(p);
   out[0] = p->last_tape_len;
   out[1] = p->last_string_bytes;
 }
@@ -2261,6 +1988,7 @@ size_t jt_b200_shard_summary_bytes(int phase) {
 }
 
 int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {
+  DevGuard dg_(p);
   return shard_setup(p, len, g, G, begin, end);
 }
 
@@ -2268,6 +1996,7 @@ int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t
 // to the G summaries of the previous phase (ignored for phase 0); this
 // phase's summary goes to the device pointer `summary`.
 int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *summary) {
+  DevGuard dg_(p);
   if (!p->shard_on || !summary || (phase > 0 && !gathered)) {
     p->err = "shard_phase: no shard or missing buffers";
     return -1;
@@ -2322,6 +2051,7 @@ int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *sum
 // stream.  On JT_OK this shard's tape words and string bytes stay on the
 // device (jt_b200_device_tape / _strings, placed by jt_b200_shard_extent).
 jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *error_offset) {
+  DevGuard dg_(p);
   if (!p->shard_on || !gathered) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
@@ -2358,6 +2088,7 @@ jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *err
 // document string offset of local string byte 0, out[4] = string bytes,
 // out[5] = document index of the shard's first token, out[6] = its tokens.
 int jt_b200_shard_extent(const jt_parser *p, unsigned long long *out) {
+  DevGuard dg_(p);
   if (!p->shard_on || !p->h_shard) return -1;
   const jt::Shard &h = *p->h_shard;
   const jt::Ctrl &c = *p->h_ctrl;
@@ -2376,6 +2107,7 @@ int jt_b200_shard_extent(const jt_parser *p, unsigned long long *out) {
 // Copy this shard's tape words (extent out[2] words) and string bytes
 // (out[4]) into host buffers.
 int jt_b200_shard_download(jt_parser *p, uint64_t *tape, uint8_t *strings) {
+  DevGuard dg_(p);
   unsigned long long e[7];
   if (jt_b200_shard_extent(p, e) != 0) return -1;
   if (e[2] && !cuda_ok(p, cudaMemcpyAsync(tape, p->tape.as<uint64_t>() + e[1], e[2] * 8,
@@ -2399,12 +2131,14 @@ int jt_b200_timeline(unsigned long long *host, size_t n) {
 #endif
 
 void jt_b200_profile(jt_parser *p, int enable) {
+  DevGuard dg_(p);
   if (enable && !p->ev[0])
     for (auto &e : p->ev) cudaEventCreate(&e);
   p->prof = enable != 0;
 }
 
 int jt_b200_kernel_times(jt_parser *p, float *ms, int max) {
+  DevGuard dg_(p);
   if (!p->prof || p->prof_n == 0) return 0;
   cudaStreamSynchronize(p->stream);
   int n = 0;

@@ -15,6 +15,8 @@
 // in shared memory and written out coalesced.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "lookback.cuh"
 #include "shard.h"
 #include "stage1.h"
@@ -1441,10 +1443,25 @@ __global__ void __launch_bounds__(kThreads) k_minify(MinifyArgs a) {
 
 }  // namespace
 
+// Kernel attributes (dynamic shared memory limits) and occupancy-derived grid
+// sizes are per device: cached per device ordinal, set on first use there.
+constexpr int kMaxDevices = 64;
+template <class T, class F>
+T per_device(std::once_flag (&once)[kMaxDevices], T (&val)[kMaxDevices], F f) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = dev < 0 ? 0 : dev % kMaxDevices;
+  std::call_once(once[dev], [&] { val[dev] = f(); });
+  return val[dev];
+}
+
 cudaError_t minify_launch(const MinifyArgs &args, cudaStream_t stream) {
   constexpr int kSmemMin = 2 * kStage1Tile + 16;
-  static const cudaError_t configured =
-      cudaFuncSetAttribute(k_minify, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMin);
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t val[kMaxDevices];
+  const cudaError_t configured = per_device(once, val, [] {
+    return cudaFuncSetAttribute(k_minify, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMin);
+  });
   if (configured != cudaSuccess) return configured;
   k_minify<<<(unsigned)args.ntiles, kThreads, kSmemMin, stream>>>(args);
   return cudaGetLastError();
@@ -1470,14 +1487,15 @@ size_t stage1_records(uint64_t len) {
 }
 
 cudaError_t stage1_configure() {
-  static const cudaError_t configured = [] {
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t val[kMaxDevices];
+  return per_device(once, val, [] {
     cudaError_t e = cudaFuncSetAttribute(k_stage1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemBytes);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_stage1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemBytesRec);
-  }();
-  return configured;
+  });
 }
 
 static Stage1Args with_tiles(const Stage1Args &args_in) {
@@ -1565,14 +1583,16 @@ cudaError_t stage1_chunk_main(const Stage1Args &args_in, cudaStream_t stream) {
 
 cudaError_t index_launch(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  static const unsigned grid_max = [] {
+  static std::once_flag once[kMaxDevices];
+  static unsigned val[kMaxDevices];
+  const unsigned grid_max = per_device(once, val, [] {
     int dev = 0, sms = 148, occ = kIdxMinBlocks;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_index, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(IdxSmem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_index, kIdxThreads, sizeof(IdxSmem));
     return (unsigned)(sms * (occ > 0 ? occ : 1));
-  }();
+  });
   const unsigned grid = a.ntiles < grid_max ? (unsigned)a.ntiles : grid_max;
   k_index<<<grid, kIdxThreads, sizeof(IdxSmem), stream>>>(a);
   return cudaGetLastError();

@@ -1906,6 +1906,39 @@ __global__ void k_distinct_strings(Stage2Args a, const DistinctVal *vals, const 
   for (uint32_t j = lane; j < r.len; j += 32) out[off[k] + j] = s[j];
 }
 
+// Exclusive prefix sum of n u32 values (n <= 2^32 - 1; sums wrap mod 2^32,
+// the caller bounds them): one CTA, each thread a contiguous chunk summed in
+// registers, a CTA scan of the chunk sums, then each chunk rewritten.  The
+// distinct_values string offsets (count = selected values) are its only user.
+__global__ void __launch_bounds__(1024) k_scan_u32(const uint32_t *in, uint32_t *out, uint32_t n) {
+  __shared__ uint32_t s_warp[32];
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t k = lo; k < hi; k++) sum += in[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+  for (int k = 0; k < warp; k++) run += s_warp[k];
+  for (uint32_t k = lo; k < hi; k++) {
+    const uint32_t v = in[k];
+    out[k] = run;
+    run += v;
+  }
+}
+
+cudaError_t scan_u32_launch(const uint32_t *in, uint32_t *out, uint32_t n, cudaStream_t stream) {
+  if (n) k_scan_u32<<<1, 1024, 0, stream>>>(in, out, n);
+  return cudaGetLastError();
+}
+
 cudaError_t distinct_match_launch(const Stage2Args &a, const DistinctQuery &q, uint32_t *match,
                                   uint32_t *count, cudaStream_t stream) {
   const int sms = a.num_sms > 0 ? a.num_sms : 148;

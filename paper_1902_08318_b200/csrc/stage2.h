@@ -124,6 +124,8 @@ cudaError_t distinct_match_launch(const Stage2Args &a, const DistinctQuery &q, u
 // values of count matches; string lengths into len[] (for the caller's scan)
 cudaError_t distinct_values_launch(const Stage2Args &a, const uint32_t *match, uint32_t count,
                                    DistinctVal *vals, uint32_t *len, cudaStream_t stream);
+// exclusive prefix sum of n u32 values (one CTA; the distinct string offsets)
+cudaError_t scan_u32_launch(const uint32_t *in, uint32_t *out, uint32_t n, cudaStream_t stream);
 // string bytes of the matches to out at the scanned offsets off[]
 cudaError_t distinct_strings_launch(const Stage2Args &a, const DistinctVal *vals, const uint32_t *off,
                                     uint32_t count, uint8_t *out, cudaStream_t stream);

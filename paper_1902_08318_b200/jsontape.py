@@ -33,7 +33,7 @@ EXPORTS = [
     "jt_minify", "jt_compute_stats", "jt_oracle_validate", "jt_generate", "jt_error_name",
     "jt_b200_input_buffer", "jt_b200_stage1_resident", "jt_b200_parse_resident",
     "jt_b200_parse_async", "jt_b200_stage1_async", "jt_b200_finish", "jt_b200_device_index", "jt_b200_device_tape",
-    "jt_b200_device_strings", "jt_b200_download", "jt_b200_set_stream", "jt_b200_set_stream_mode",
+    "jt_b200_device_strings", "jt_b200_download", "jt_b200_document_tape", "jt_b200_document_strings", "jt_b200_document_from", "jt_b200_set_stream",
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_distinct", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
@@ -86,8 +86,6 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_device_strings.restype = vp
     L.jt_b200_download.argtypes = [vp, C.POINTER(vp)]
     L.jt_b200_set_stream.argtypes = [vp, vp]
-    L.jt_b200_set_stream_mode.argtypes = [vp, C.c_int]
-    L.jt_b200_set_stream_mode.restype = None
     L.jt_b200_last_launches.argtypes = [vp]
     L.jt_b200_device.argtypes = [vp]
     L.jt_b200_last_error.argtypes = [vp]
@@ -353,10 +351,6 @@ class Parser:
         out = C.string_at(sp)
         self._lib.jt_string_free(sp)
         return out
-
-    def set_stream_mode(self, mode: int):
-        """0: stage 1 streamed per piece (default); 1: whole pieces as shards."""
-        self._lib.jt_b200_set_stream_mode(self._h, mode)
 
     def set_stream(self, stream_handle: int | None):
         self._lib.jt_b200_set_stream(self._h, stream_handle)

@@ -58,8 +58,6 @@ def main():
     args = ap.parse_args()
     rng = random.Random(args.seed)
     o, p = Oracle(), Parser()
-    pp = Parser()  # stream mode 1: pieces parsed as byte-range shards
-    pp.set_stream_mode(1)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     t0 = time.time()
     n = fails = 0
@@ -105,9 +103,7 @@ def main():
             if r.code == 0 and reps * len(d) < (40 << 20):
                 big = b"[" + b",".join([d] * reps) + b"]"
                 rb = o.parse(big)
-                for mode, q in (("streamed", p), ("streamed pieces", pp)):
-                    if mode == "streamed pieces" and rng.random() < 0.5:
-                        continue
+                for mode, q in (("streamed", p),):
                     gb = q.parse(big)
                     counts["streamed"] += 1
                     if (gb.name, gb.offset) != (rb.name, rb.offset) or (

@@ -203,22 +203,19 @@ def test_streamed_stage2_ranges(parser, oracle):
 
 
 def _piece_cut(length: int) -> int:
-    """First cut of parse_pieces (engine.cu piece_count, 8 MiB pieces, >= 2)."""
-    piece = 8 << 20
-    tiles = (length + 16383) // 16384
-    G = max(2, min(64, (length + piece // 2) // piece))
-    return (tiles // G) * 16384
+    """A piece boundary of the streamed jt_parse (engine.cu parse_stream:
+    4 MiB pieces, K1 one 16 KiB tile behind each boundary)."""
+    return 2 * (4 << 20)
 
 
 def test_streamed_pieces(parser, oracle):
-    """Streamed jt_parse with stage 2 per piece (engine.cu parse_pieces):
-    escapes, numbers, atoms and brackets across the piece cut, a piece
-    without a token start (resident re-parse), deep nesting across pieces,
-    and the resident state (index, jt_stage2) read after the streamed parse."""
+    """Streamed jt_parse (engine.cu parse_stream): escapes, numbers, atoms
+    and brackets across a piece boundary, a piece without a token start, deep
+    nesting across pieces, and the resident state (index, jt_stage2) read
+    after the streamed parse."""
     from paper_1902_08318_b200 import Parser
     from tools.gen import generate
     parser = Parser()
-    parser.set_stream_mode(1)
     n = 12 << 20
     cut = _piece_cut(n)
     filler = generate(0, cut - 4096, seed=11)[1:-1]  # object members of a top-level array
@@ -237,7 +234,7 @@ def test_streamed_pieces(parser, oracle):
         for tok in (b"-12345678901234567.5e-7", b"true", b"null", b"[[]]", b'{"a":{}}'):
             doc = head + b" " * pad + tok + b"," + generate(0, n - cut, seed=13)[1:]
             check_same(parser, oracle, doc, f"token {tok!r} at cut-{shift}")
-    # a middle piece without any token start: resident re-parse
+    # middle pieces without any token start
     s = b'[1,"' + b"z" * (20 << 20) + b'",2]'
     check_same(parser, oracle, s, "token-free piece")
     # nesting deeper than 64 opened in one piece and closed in a later one
