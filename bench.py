@@ -1,7 +1,8 @@
 """bench.py — JSON parse throughput on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[1] = C1, a 64 MiB pretty-printed
-document (random tree, 30% non-ASCII string chars, escapes), seeded synthetic
+Headline workload (N=1): BASELINE.json configs[4] = C4, the 1 GiB
+adversarial single document (strings dense in backslash runs, depth up to
+1024, mixed UTF-8) — the largest single-GPU config; seeded synthetic
 (tools/jtgen.c) standing in for the paper's public datasets.  One step = one
 full parse (stage 1 + stage 2, the jt_parse path) of that document.
 
@@ -9,24 +10,34 @@ full parse (stage 1 + stage 2, the jt_parse path) of that document.
            (CUDA events on the parser's stream; L2 flushed before every step by
            a 256 MiB memset outside the events)
   e2e    = same metric through the public C ABI jt_parse with a pinned host
-           input and the host document (tape + strings) read back every step
+           input and the host document (tape + strings) read back every step;
+           e2e_pageable = the same from an ordinary (pageable) host buffer
+  parity = the timed document's structural index, tape and string buffer
+           (sha256) equal what the UNMODIFIED reference produced for it
+           (tests/golden/large_outputs.json); also the e2e document
   roofline = dominant kernel: algorithmic bytes / its event-timed duration
-  cpu_baseline = the unmodified reference (oracle/_ref) on 1 core
+  cpu_baseline = the unmodified reference (oracle/_ref, jt_parse) on all host
+           cores (oracle/ref_driver.c: one pthread + parser per core, each
+           parsing the document) and on one core
+  configs = the other BASELINE configs, one short measurement each (C0 1 MiB,
+           C1 64 MiB, C2 256 MiB, C3 1 GiB NDJSON records), same keys.
 
-N > 1 (torchrun, one process per GPU): ONE document of N x 64 MiB, split
-into N tile-aligned byte ranges; rank g parses shard g (paper_1902_08318_b200
-.shard: four phases with an NCCL all_gather of a small summary after each:
-carry functions, counts, open-container stacks, first error + bracket
-patches).  Per-GPU work is fixed as N grows (weak scaling); value = document
-bytes / max-over-ranks device time.  --shard runs this path at N = 1 too.
+N > 1 (torchrun, one process per GPU), strong scaling on the 1 GiB inputs:
+  * --config 4 (default): ONE 1 GiB document split into N tile-aligned byte
+    ranges; rank g uploads only [begin - 64, end + 64 KiB) of it and parses
+    shard g (paper_1902_08318_b200.shard: four phases, an NCCL all_gather of a
+    small summary after each).  value = document bytes / max-over-ranks time.
+  * --config 3: the 1 GiB NDJSON buffer cut on record boundaries; rank g
+    parses its records (no data exchange; an all_gather of record counts).
 
 --impl reference: the reference's own CPU parser (oracle/_ref, jt_parse) on
-the same document, rank 0 only.
+the same workload on all host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
 import statistics
@@ -39,11 +50,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "JSON parsed GB/s (stage1 & full tape) at 1/2/4/8 B200; % of HBM roofline"
-WORKLOAD = ("C1: 64 MiB single document, pretty-printed (2-space, LF), random tree "
-            "branching 1-10 depth<=8, 30% non-ASCII string chars, 10% strings with escapes")
-CONFIG = 1
-PROFILE = "r01d_ncu_full_c1.json"  # ncu --set full capture of the current kernels (traffic)
-SIZE = 64 << 20
+WORKLOADS = {
+    0: "C0: 1 MiB minified document, ~5,000 flat 6-key objects",
+    1: ("C1: 64 MiB single document, pretty-printed (2-space, LF), random tree branching 1-10 "
+        "depth<=8, 30% non-ASCII string chars, 10% strings with escapes"),
+    2: "C2: 256 MiB number-heavy document, 1M rows x 16 numbers (90% %.17g floats, 10% int64)",
+    3: "C3: 1 GiB NDJSON, ~3.9M lognormal records (mean 256 B), each parsed as jt_parse(record)",
+    4: ("C4: 1 GiB adversarial single document: strings up to 64 KiB dense in backslash runs 1-9 "
+        "and embedded quotes, nesting up to 1024, mixed UTF-8"),
+}
+CONFIG = 4           # headline: the largest single-GPU config
+TABLE = (0, 1, 2, 3)  # the other configs, one short line each inside the headline's JSON
+# ncu --set full captures of the current kernels (DRAM traffic per launch)
+PROFILES = {4: "r02_ncu_full_c4.json"}
+FIXTURE = os.path.join(ROOT, "tests", "golden", "large_outputs.json")
+L2_NOTE = "flushed before every step (256 MiB memset, outside the events)"
 
 
 def peaks():
@@ -127,94 +148,489 @@ def max_over_ranks(value: float, dist=None, device="cpu") -> float:
 
 
 def job_throughput(bytes_per_rank: int, steps: int, world: int, max_total_ms: float) -> float:
-    """Whole-job GB/s: every rank parses its own copy (replicas, weak
-    scaling), so all ranks' bytes divided by the slowest rank's time."""
+    """Whole-job GB/s when every rank parses its own copy (replicas)."""
     return world * bytes_per_rank * steps / (max_total_ms / 1e3) / 1e9
 
 
-def reference_all_threads(data: bytes, steps: int, warmup: int = 1):
-    """The reference's parse on all host cores: one jt_parser per thread
-    (thread-compatible, jsontape.h:1-4; the reference cannot split one
-    document), every thread parsing `data` once per step.  Returns
-    (aggregate GB/s, threads, one-thread GB/s, kind, step times)."""
-    import threading
-    from oracle.pyoracle import REF_SO, Oracle, Reference
+def sha(b) -> str:
+    return hashlib.sha256(b).hexdigest()
+
+
+def fixture(config: int, n: int):
+    """The reference's results for the seeded config document of n bytes
+    (tests/golden/large_outputs.json, made from oracle/_ref), or None."""
+    try:
+        with open(FIXTURE) as f:
+            fx = json.load(f)
+    except OSError:
+        return None
+    rows = [fx["records"]] if config == 3 else fx["clean"]
+    return next((r for r in rows if r["config"] == config and r["bytes"] == n), None)
+
+
+def generate(config: int, size=None) -> bytes:
+    from tools.gen import generate as gen
+    return gen(config, size)
+
+
+# ---- CPU baseline: the unmodified reference on the host cores ---------------
+
+def host_threads(n: int, bytes_per_input_byte: float) -> int:
+    """All host cores, bounded so the reference's per-thread buffers (padded
+    copy, index, tape, strings: ~7 bytes per input byte) fit in 60% of the
+    available host memory."""
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    return max(1, min(cores, 128, int(0.6 * avail // max(1, bytes_per_input_byte * n))))
+
+
+def reference_document(data: bytes, reps: int = 2):
+    """The reference's jt_parse of the whole document on all host cores (each
+    thread its own parser, oracle/ref_driver.c) and on one core."""
+    from oracle.pyoracle import REF_SO, RefDriver
     n = len(data)
-    kind = "reference" if os.path.exists(REF_SO) else "port"
+    if not os.path.exists(REF_SO):
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built on this box"}
+    d = RefDriver()
+    t1, code = d.parse_many(data, 1, 1)
+    threads = host_threads(n, 7.0)
+    tn, code_n = d.parse_many(data, threads, reps)
+    assert code == code_n == 0, (code, code_n)
+    return {"value": threads * n * reps / tn / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "sample": (f"the full document: {reps} passes of {threads} pthreads, each jt_parse()ing it with "
+                       f"its own parser (the reference cannot split one document; oracle/ref_driver.c); "
+                       f"1 thread alone: {n / t1 / 1e9:.3f} GB/s"),
+            "one_thread_gbs": n / t1 / 1e9}
 
-    def make():
-        return Reference() if kind == "reference" else Oracle()
 
-    def parse_once(obj):
-        if kind == "reference":
-            obj.parse_code(data)
-        else:
-            obj.parse(data)
-    # bounded so the per-thread buffers (~7 x the document) stay within 24 GB
-    threads = max(1, min(os.cpu_count() or 1, 64, (24 << 30) // max(1, 7 * n)))
-    objs = [make() for _ in range(threads)]
-    t0 = time.perf_counter()
-    parse_once(objs[0])
-    one = time.perf_counter() - t0
-
-    def step():
-        ths = [threading.Thread(target=parse_once, args=(o,)) for o in objs]
-        t = time.perf_counter()
-        for th in ths:
-            th.start()
-        for th in ths:
-            th.join()
-        return time.perf_counter() - t
-    times = []
-    for i in range(warmup + steps):
-        dt = step()
-        if i >= warmup:
-            times.append(dt)
-    return threads * n * len(times) / sum(times) / 1e9, threads, n / one / 1e9, kind, times
+def reference_records(data: bytes, reps: int = 2):
+    """The reference's jt_parse of every NDJSON record on all host cores
+    (records dealt to the threads in contiguous slices) and on one core (a
+    64 MiB prefix)."""
+    from oracle.pyoracle import REF_SO, RefDriver
+    n = len(data)
+    if not os.path.exists(REF_SO):
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built on this box"}
+    d = RefDriver()
+    cut = data.find(b"\n", min(n, 64 << 20))
+    head = data if cut < 0 else data[:cut + 1]
+    t1, _, _ = d.parse_records(head, 1, 1)
+    threads = host_threads(n, 0.2)
+    tn, nr, ok = d.parse_records(data, threads, reps)
+    return {"value": n * reps / tn / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "sample": (f"all {nr} records, {reps} passes, dealt to {threads} pthreads in contiguous slices, "
+                       f"each record jt_parse()d alone (oracle/ref_driver.c); {ok} OK; 1 thread on the "
+                       f"first {len(head) >> 20} MiB: {len(head) / t1 / 1e9:.3f} GB/s"),
+            "one_thread_gbs": len(head) / t1 / 1e9, "records": nr}
 
 
 def run_reference(args, rank: int, world: int):
-    """The reference's own CPU parse (oracle/_ref: the unmodified sources) on
-    this box's host cores, all threads (reference_all_threads); the
-    one-thread rate is reported beside it."""
+    """--impl reference: the reference's own CPU parse (oracle/_ref: the
+    unmodified sources) of the same workload on this box's host cores."""
     if rank != 0:
         return
-    from tools.gen import generate
-    size = args.size or (SIZE if args.config == CONFIG else None)
-    data = generate(args.config, size)
+    data = generate(args.config, args.size)
     n = len(data)
-    v, threads, one, kind, times = reference_all_threads(data, args.steps, args.warmup)
-    sample = (f"per step {threads} threads, each jt_parse of the full document (incl. its padded copy) "
-              f"with its own parser; 1 thread alone: {one:.3f} GB/s")
+    from oracle.pyoracle import REF_SO, RefDriver
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return
+    d = RefDriver()
+    if args.config == 3:
+        d.parse_records(data[:1 << 20], 1, 1)
+        threads = host_threads(n, 0.2)
+        times = []
+        for i in range(args.warmup + args.steps):
+            dt, nr, ok = d.parse_records(data, threads, 1)
+            if i >= args.warmup:
+                times.append(dt)
+        v = n * len(times) / sum(times) / 1e9
+        sample = f"all {nr} records per step dealt to {threads} pthreads, each record jt_parse()d alone"
+    else:
+        threads = host_threads(n, 7.0)
+        # a 1 GiB document takes seconds per thread: one untimed pass inside
+        # the driver per call, then args.steps timed passes (bounded)
+        reps = max(1, min(args.steps, 3 if n >= (256 << 20) else args.steps))
+        dt, code = d.parse_many(data, threads, reps)
+        assert code == 0, code
+        times = [dt / reps] * reps
+        v = threads * n * reps / dt / 1e9
+        sample = (f"{reps} passes of {threads} pthreads, each jt_parse()ing the whole document with its "
+                  f"own parser (the reference cannot split one document)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.config == CONFIG else f"config {args.config}", "bytes": n,
-                   "parallelism": f"{threads} host threads (one document each)"},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample,
-                         "one_thread_gbs": one},
+        "config": {"workload": WORKLOADS[args.config], "bytes": n,
+                   "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_sharded(args, rank: int, world: int, local: int, torch, dist):
-    """One document, world byte-range shards, NCCL exchanges (see header)."""
+# ---- one GPU: single documents -------------------------------------------------
+
+def kernel_profile(p, n, flush, reps):
+    """per-kernel event times (ms) of the full parse, median of `reps`"""
+    p.profile(True)
+    runs = []
+    for _ in range(reps):
+        flush.zero_()
+        p.parse_async(n)
+        p.finish()
+        runs.append(p.kernel_times())
+    p.profile(False)
+    return {k: statistics.median(r[k] for r in runs) for k in runs[0]}
+
+
+def e2e_loop(torch, p, stream, ptr, n, steps, warmup):
+    """jt_parse through the C ABI from host memory at `ptr`, host document
+    back; returns (ms per call list, the last document handle)."""
+    ms, last = [], None
+    for k in range(warmup + steps):
+        doc = C.c_void_p()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rr = p._lib.jt_parse(p._h, C.c_char_p(ptr), n, C.byref(doc), None)
+        e1.record(stream)
+        e1.synchronize()
+        assert rr == 0, rr
+        if k >= warmup:
+            ms.append(e0.elapsed_time(e1))
+        if last is not None:
+            p._lib.jt_document_free(last)
+        last = doc
+    return ms, last
+
+
+def measure_document(torch, config, steps, warmup, flush, full, clk_index=None, size=None):
+    """Device-resident full parse, jt_stage1, e2e (pinned; + pageable when
+    `full`) and parity against the reference's fixture for one config."""
     from paper_1902_08318_b200 import Parser
-    from paper_1902_08318_b200 import shard as SH
-    from tools.gen import generate
-    size = args.size or SIZE
-    data = generate(args.config, size * world)
+    from paper_1902_08318_b200.jsontape import Document
+    data = generate(config, size)
     n = len(data)
-    begin, end = SH.layout(n, world)[rank]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    # a real (non-NULL) stream: torch's default stream is the legacy NULL
+    # stream, which the C ABI treats as "use the parser's own stream"
+    p = Parser()
+    p.set_stream(stream.cuda_stream)
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    p.copy_in(host.data_ptr(), n)
+    torch.cuda.synchronize()
+    r = p.parse_resident(n)
+    assert r.name == "OK", (r.name, r.offset)
+    S = p.device_index()[1]
+    T = p.device_tape()[1]
+    SB = p.device_strings()[1]
+    launches = p.last_launches()
+    for _ in range(warmup):
+        flush.zero_()
+        p.parse_async(n)
+        assert p.finish().code == 0
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    clk = ClockSampler(clk_index) if clk_index is not None else None
+    if clk:
+        clk.__enter__()
+        clk.wait_first()
+    for k in range(steps):
+        flush.zero_()
+        starts[k].record(stream)
+        p.parse_async(n)
+        ends[k].record(stream)
+        assert p.finish().code == 0
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    out = {"bytes": n, "S": S, "T": T, "SB": SB, "launches": launches, "steps": steps,
+           "tot_ms": sum(step_ms), "ms_per_step": sum(step_ms) / steps,
+           "value": n * steps / (sum(step_ms) / 1e3) / 1e9,
+           "clocks": clk.summary() if clk else None}
+
+    # parity of the timed document: the last timed parse is what is on the device
+    fx = fixture(config, n)
+    par = {"checked": False}
+    if fx is not None:
+        assert sha(data) == fx["input_sha"], "generator drifted"
+        idx = p.index()
+        doc = p.download()
+        got = {"index_sha": sha(idx.tobytes()), "tape_sha": sha(doc.tape.tobytes()),
+               "strings_sha": sha(doc.strings), "S": len(idx), "T": len(doc.tape),
+               "string_bytes": len(doc.strings)}
+        bad = [k for k, v in got.items() if v != fx[k]]
+        assert not bad, f"parity: config {config} timed document differs from the reference in {bad}"
+        par = {"checked": True, "against": "tests/golden/large_outputs.json (oracle/_ref)",
+               "index": True, "tape": True, "strings": True}
+        del idx, doc
+
+    # per-kernel event times (separate profiled passes) for the roofline
+    out["kernel_ms"] = kernel_profile(p, n, flush, max(3, min(steps, 10)))
+
+    # jt_stage1 alone (k_index), device-resident input
+    s1 = []
+    for k in range(warmup + steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        p.stage1_async(n)
+        e1.record(stream)
+        r1 = p.finish()
+        assert r1.name == "OK" and p.device_index()[1] == S
+        if k >= warmup:
+            s1.append(e0.elapsed_time(e1))
+    out["stage1_ms"] = statistics.median(s1)
+
+    # e2e through the public C ABI: host input -> jt_parse -> host document
+    ms, last = e2e_loop(torch, p, stream, host.data_ptr(), n, steps, warmup)
+    out["e2e_ms"] = ms
+    if fx is not None:
+        d = Document(last.value)
+        assert sha(d.tape.tobytes()) == fx["tape_sha"] and sha(d.strings) == fx["strings_sha"], \
+            "parity: e2e document differs from the reference"
+        par["e2e_document"] = True
+        del d
+    else:
+        p._lib.jt_document_free(last)
+    if full:
+        buf = C.create_string_buffer(data, n)  # ordinary malloc'd (pageable) host memory
+        msp, lastp = e2e_loop(torch, p, stream, C.addressof(buf), n, steps, warmup)
+        p._lib.jt_document_free(lastp)
+        out["e2e_pageable_ms"] = msp
+        del buf
+    out["parity"] = par
+    out["data"] = data if full else None
+    p.close()
+    del host
+    return out
+
+
+def measure_records(torch, steps, warmup, flush, size=None, with_cpu=True):
+    """C3 on one GPU: device-resident record-mode parse, e2e (pinned input up,
+    per-record results + tape + strings down) and parity of every record."""
+    import numpy as np
+    from paper_1902_08318_b200 import Parser
+    data = generate(3, size)
+    n = len(data)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     p = Parser()
     p.set_stream(stream.cuda_stream)
     host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
-    p.copy_in(host.data_ptr(), n)  # whole document resident: the halo is everything
+    p.copy_in(host.data_ptr(), n)
+    torch.cuda.synchronize()
+    cnt = C.c_size_t()
+    for _ in range(warmup):
+        flush.zero_()
+        assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
+    launches = p.last_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.zero_()
+        starts[k].record(stream)
+        assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0  # one host sync inside
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    tot = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    sz = (C.c_ulonglong * 2)()
+    p._lib.jt_b200_records_size(p._h, sz)
+    nrec = cnt.value
+    # e2e: pinned host buffer -> device, record parse, per-record results
+    # (jt_b200_records) + all records' tape words and strings -> host
+    tape_h = torch.empty(max(1, int(sz[0])) * 8, dtype=torch.uint8).pin_memory()
+    str_h = torch.empty(max(1, int(sz[1])), dtype=torch.uint8).pin_memory()
+    e2e = []
+    for k in range(warmup + steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        p.copy_in(host.data_ptr(), n)
+        assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
+        assert p._lib.jt_b200_records(p._h)
+        assert p._lib.jt_b200_records_download(p._h, tape_h.data_ptr(), str_h.data_ptr()) == 0
+        e1.record(stream)
+        e1.synchronize()
+        if k >= warmup:
+            e2e.append(e0.elapsed_time(e1))
+    # parity: every record's code / offset, and the OK records' tape words and strings
+    arr, tape, strings = p.parse_records_arrays(n)
+    fx = fixture(3, n)
+    par = {"checked": False}
+    if fx is not None:
+        assert sha(data) == fx["input_sha"], "generator drifted"
+        ok = arr["code"] == 0
+        got = {"records": int(len(arr)), "ok": int(ok.sum()),
+               "codes_sha": sha(np.ascontiguousarray(arr["code"], dtype=np.int32).tobytes()),
+               "offsets_sha": sha(np.ascontiguousarray(arr["offset"], dtype=np.int64).tobytes()),
+               "tape_sha": sha(gather(tape, arr["tape_begin"][ok], arr["tape_words"][ok]).tobytes()),
+               "strings_sha": sha(gather(strings, arr["string_begin"][ok], arr["string_bytes"][ok]).tobytes())}
+        bad = [k for k, v in got.items() if v != fx[k]]
+        assert not bad, f"parity: C3 records differ from the reference in {bad}"
+        par = {"checked": True, "against": "tests/golden/large_outputs.json (oracle/_ref, per record)",
+               "records": got["records"]}
+    out = {"bytes": n, "records": nrec, "tape_words": int(sz[0]), "string_bytes": int(sz[1]),
+           "steps": steps, "ms_per_step": tot / steps, "value": n * steps / (tot / 1e3) / 1e9,
+           "launches": launches, "parity": par,
+           "e2e": {"value": n * steps / (sum(e2e) / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": n,
+                   "d2h_bytes_per_step": 8 * int(sz[0]) + int(sz[1]) + 48 * nrec}}
+    if with_cpu:
+        out["cpu_baseline"] = reference_records(data)
+    p.close()
+    return out
+
+
+def gather(buf, begin, count):
+    """Concatenate buf[begin[k]:begin[k]+count[k]] (vectorised)."""
+    import numpy as np
+    count = count.astype(np.int64)
+    total = int(count.sum())
+    if total == 0:
+        return buf[:0]
+    starts = np.repeat(begin.astype(np.int64) - np.concatenate(([0], np.cumsum(count)[:-1])), count)
+    return buf[starts + np.arange(total, dtype=np.int64)]
+
+
+def roofline_of(out, config, n):
+    """Dominant kernel of the full parse: algorithmic bytes
+    over its event-timed duration; DRAM traffic from the committed ncu
+    capture of this workload when there is one."""
+    peak, peak_src = peaks()
+    kt = out["kernel_ms"]
+    S, T, SB = out["S"], out["T"], out["SB"]
+    B1 = n + 4 * S               # stage 1: input read, index written
+    B2 = n + 8 * T + SB          # full parse: input read, tape + string buffer written
+    # token pass: reads the index (4S) and the input (N), writes token
+    # records (4S), scalar tape words (8T) and the string buffer
+    kern_bytes = {"stage1": B1, "tokens": n + 8 * S + 8 * T + SB, "struct": 4 * S + 8 * T}
+    dom = max(kern_bytes, key=lambda k: kt.get(k, 0.0))
+    ach = kern_bytes[dom] / (kt[dom] / 1e3) / 1e9
+    traffic, traffic_src, alu = None, None, None
+    prof = PROFILES.get(config)
+    if prof:
+        try:
+            with open(os.path.join(ROOT, "profiles", prof)) as f:
+                pr = json.load(f)
+            kname = {"stage1": ("k_carry_fn<0>", "k_carry_scan", "k_stage1<0>"), "tokens": ("k_scalars",),
+                     "struct": ("k_struct<0, 0>",)}[dom]
+            es = [v for k, v in pr.items() if k != "units" and k.endswith(kname)]
+            if "units" in pr and pr.get("input_bytes", n) == n and len(es) == len(kname):
+                traffic = sum(float(e["dram__bytes_read.sum"]) + float(e["dram__bytes_write.sum"]) for e in es)
+                traffic_src = f"profiles/{prof}: {'+'.join(kname)} DRAM read+write per launch (ncu --set full)"
+            alu = float(es[-1]["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"])
+        except Exception:
+            pass
+    per_step_s = out["ms_per_step"] / 1e3
+    return {
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": kern_bytes[dom], "peak_source": peak_src,
+                     # the integer ALU pipe is what binds these kernels (DESIGN.md §5)
+                     "alu_pipe_pct_of_peak": alu},
+        "roofline_stage1": {"achieved": B1 / (out["stage1_ms"] / 1e3) / 1e9,
+                            "frac": B1 / (out["stage1_ms"] / 1e3) / 1e9 / peak, "bytes": B1,
+                            "path": "jt_stage1 (k_index)"},
+        "roofline_full": {"achieved": B2 / per_step_s / 1e9, "frac": B2 / per_step_s / 1e9 / peak,
+                          "bytes": B2, "path": "full parse (all kernels)"},
+    }
+
+
+def doc_line(out, config, steps):
+    n = out["bytes"]
+    e2e_v = n * steps / (sum(out["e2e_ms"]) / 1e3) / 1e9
+    line = {"value": out["value"], "unit": "GB/s", "ms_per_step": out["ms_per_step"],
+            "config": {"workload": WORKLOADS[config], "bytes": n, "structurals": out["S"],
+                       "tape_words": out["T"], "string_bytes": out["SB"], "l2": L2_NOTE},
+            "stage1_gbs": n / (out["stage1_ms"] / 1e3) / 1e9, "stage1_ms": out["stage1_ms"],
+            "kernel_ms": out["kernel_ms"],
+            "e2e": {"value": e2e_v, "unit": "GB/s", "h2d_bytes_per_step": n,
+                    "d2h_bytes_per_step": 8 * out["T"] + out["SB"]},
+            "parity": out["parity"]}
+    if "e2e_pageable_ms" in out:
+        line["e2e_pageable"] = {"value": n * steps / (sum(out["e2e_pageable_ms"]) / 1e3) / 1e9, "unit": "GB/s",
+                                "h2d_bytes_per_step": n, "d2h_bytes_per_step": 8 * out["T"] + out["SB"],
+                                "input": "ordinary malloc'd host buffer"}
+    line.update(roofline_of(out, config, n))
+    return line
+
+
+def run_single(args, torch, local):
+    """N = 1: the headline config, then one short line per other config."""
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    head = measure_document(torch, args.config, args.steps, args.warmup, flush, True, clk_index=local,
+                            size=args.size)
+    data = head.pop("data")
+    line = {"metric": METRIC, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (tools/jtgen.c, seeded; BASELINE.json config shapes)"}
+    line.update(doc_line(head, args.config, args.steps))
+    line["config"]["parallelism"] = "1 GPU"
+    line["gpu_launches"] = head["launches"] * args.steps
+    line["clocks"] = head["clocks"]
+    line["cpu_baseline"] = None if args.no_cpu else reference_document(data)
+    del data
+    if not args.no_table:
+        table = {}
+        ksteps = max(3, min(args.steps, 10))
+        for c in TABLE:
+            if c == args.config:
+                continue
+            if c == 3:
+                r = measure_records(torch, ksteps, args.warmup, flush, with_cpu=not args.no_cpu)
+                table["C3"] = {"value": r["value"], "unit": "GB/s", "ms_per_step": r["ms_per_step"],
+                               "config": {"workload": WORKLOADS[3], "bytes": r["bytes"], "records": r["records"],
+                                          "tape_words": r["tape_words"], "string_bytes": r["string_bytes"],
+                                          "l2": L2_NOTE},
+                               "e2e": r["e2e"], "parity": r["parity"], "cpu_baseline": r.get("cpu_baseline"),
+                               "gpu_launches": r["launches"] * ksteps}
+                continue
+            o = measure_document(torch, c, ksteps, args.warmup, flush, False)
+            t = doc_line(o, c, ksteps)
+            t["gpu_launches"] = o["launches"] * ksteps
+            if not args.no_cpu:
+                t["cpu_baseline"] = reference_document(generate(c), reps=1)
+            table[f"C{c}"] = t
+        line["configs"] = table
+    print(json.dumps(line), flush=True)
+
+
+# ---- N > 1: byte-range shards of one document (strong scaling) -----------------
+
+HALO = 64 << 10  # bytes after a shard's end resident on its GPU (tokens crossing the cut)
+
+
+def run_sharded(args, rank: int, world: int, local: int, torch, dist):
+    """ONE document, world byte-range shards, NCCL exchanges; each rank holds
+    only its halo range [begin - 64, end + HALO) (see header)."""
+    from paper_1902_08318_b200 import Parser
+    from paper_1902_08318_b200 import shard as SH
+    data = generate(args.config, args.size)
+    n = len(data)
+    begin, end = SH.layout(n, world)[rank]
+    lo, hi = max(0, begin - 64), min(n, end + HALO)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    p = Parser()
+    p.set_stream(stream.cuda_stream)
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    p.input_buffer(n)  # document-sized address space, zero tail; only [lo, hi) is uploaded
+    assert p._lib.jt_b200_copy_in_range(p._h, host.data_ptr(), lo, hi - lo) == 0
+    SH.set_resident(p, lo, hi)
     torch.cuda.synchronize()
     if dist is None:  # --shard at N = 1: a one-rank NCCL group for the same exchanges
         import torch.distributed as D
@@ -253,9 +669,18 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
     tot_ms = max_over_ranks(sum(step_ms), dist, "cuda")
     value = n * args.steps / (tot_ms / 1e3) / 1e9
 
-    # e2e: pinned host bytes of this shard (+64 B before, 64 KiB after) -> device,
-    # sharded parse, this shard's tape words and string bytes -> pinned host
-    lo, hi = max(0, begin - 64), min(n, end + (64 << 10))
+    # parity: the shards' totals equal the reference's document
+    tot = torch.tensor([ext[2], ext[4], ext[6]], dtype=torch.int64, device="cuda")
+    dist.all_reduce(tot)
+    fx = fixture(args.config, n)
+    par = {"checked": False}
+    if fx is not None:
+        got = [int(v) for v in tot.tolist()]
+        want = [fx["T"] - 2, fx["string_bytes"], fx["S"]]  # shard tapes exclude the two root words
+        par = {"checked": "counts", "tape_words_strings_tokens": got == want}
+
+    # e2e: pinned host bytes of this shard's halo range -> device, sharded
+    # parse, this shard's tape words and string bytes -> pinned host
     tape_h = torch.empty(max(1, ext[2]) * 8, dtype=torch.uint8).pin_memory()
     str_h = torch.empty(max(1, ext[4]), dtype=torch.uint8).pin_memory()
     e2e_ms = []
@@ -282,12 +707,10 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": (WORKLOAD if args.config == CONFIG else f"config {args.config}")
-                       + f"; one document of {world} x {size} bytes, {world} byte-range shards",
-                       "bytes": n, "shard_bytes": rn,
-                       "l2": "flushed before every step (256 MiB memset, outside the events)",
-                       "parallelism": f"{world} shards (NCCL all_gather x4 per parse)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config] + f"; {world} byte-range shards of the one document",
+                       "bytes": n, "shard_bytes_rank0": rn, "resident_bytes_rank0": hi - lo,
+                       "l2": L2_NOTE, "parallelism": f"{world} shards (NCCL all_gather x4 per parse)"},
             "stage1_gbs": n / (s1_ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "full parse of rank 0's shard",
                          "achieved": B2 / (per_step / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
@@ -295,6 +718,7 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
                          "peak_source": peak_src},
             "roofline_stage1": {"achieved": B1 / (s1_ms / 1e3) / 1e9,
                                 "frac": B1 / (s1_ms / 1e3) / 1e9 / peak, "bytes": B1},
+            "parity": par,
             "cpu_baseline": None,
             "e2e": {"value": e2e_v, "unit": "GB/s", "h2d_bytes_per_step": hi - lo,
                     "d2h_bytes_per_step": 8 * ext[2] + ext[4]},
@@ -308,7 +732,7 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
 
 def record_ranges(data: bytes, world: int) -> list[tuple[int, int]]:
     """Split an NDJSON buffer on record boundaries: rank g starts after the
-    first '\n' at or after g/world of the bytes."""
+    first '\\n' at or after g/world of the bytes."""
     n = len(data)
     cuts = [0]
     for g in range(1, world):
@@ -318,15 +742,27 @@ def record_ranges(data: bytes, world: int) -> list[tuple[int, int]]:
     return [(cuts[g], cuts[g + 1]) for g in range(world)]
 
 
+def record_numbering(dist, world: int, rank: int, count: int, device="cpu") -> tuple[int, int]:
+    """Global numbering of the ranks' records: (first record of this rank,
+    total records) from an all_gather of the per-rank counts."""
+    import torch
+    counts = torch.tensor([count], dtype=torch.int64, device=device)
+    allc = torch.empty(world, dtype=torch.int64, device=device)
+    try:
+        dist.all_gather_into_tensor(allc, counts)
+    except (RuntimeError, NotImplementedError, AttributeError):  # backends without it (gloo)
+        parts = [torch.empty_like(counts) for _ in range(world)]
+        dist.all_gather(parts, counts)
+        allc = torch.cat(parts)
+    return int(allc[:rank].sum().item()), int(allc.sum().item())
+
+
 def run_records(args, rank: int, world: int, local: int, torch, dist):
-    """C3: NDJSON records, each parsed as jt_parse(record) would, in one pass
-    per GPU (jt_b200_parse_records).  N > 1: one buffer of N x size bytes cut
-    on record boundaries; ranks need no exchange but an all_gather of their
-    record counts (global record numbering)."""
+    """C3 at N > 1: the 1 GiB NDJSON buffer cut on record boundaries, each
+    rank parses its records (jt_b200_parse_records); the only exchange is an
+    all_gather of record counts (global record numbering)."""
     from paper_1902_08318_b200 import Parser
-    from tools.gen import generate
-    size = args.size or (64 << 20)
-    data = generate(3, size * world)
+    data = generate(3, args.size)
     b, e = record_ranges(data, world)[rank]
     mine = data[b:e]
     n = len(mine)
@@ -338,25 +774,16 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
     p.copy_in(host.data_ptr(), n)
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    res = p.parse_records(n, download=False)
-    nrec = len(res)
-    bad = sum(1 for r in res if r[0] != "OK")
-    counts = torch.tensor([nrec], dtype=torch.int64, device="cuda")
-    if dist:
-        allc = torch.empty(world, dtype=torch.int64, device="cuda")
-        dist.all_gather_into_tensor(allc, counts)
-        first_record = int(allc[:rank].sum().item())
-    else:
-        first_record = 0
     cnt = C.c_size_t()
+    assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
+    first_record, total_records = record_numbering(dist, world, rank, cnt.value, "cuda")
     for _ in range(args.warmup):
         flush.zero_()
         assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
     launches = p.last_launches()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         clk.wait_first()
@@ -366,70 +793,64 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
             assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0  # one host sync inside
             ends[k].record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    dist.barrier()
     tot_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dist, "cuda")
-    total_bytes = len(data)
-    value = total_bytes * args.steps / (tot_ms / 1e3) / 1e9
-    peak, peak_src = peaks()
+    value = len(data) * args.steps / (tot_ms / 1e3) / 1e9
+    # e2e: this rank's records up, results + tape + strings down
     sz = (C.c_ulonglong * 2)()
     p._lib.jt_b200_records_size(p._h, sz)
+    tape_h = torch.empty(max(1, int(sz[0])) * 8, dtype=torch.uint8).pin_memory()
+    str_h = torch.empty(max(1, int(sz[1])), dtype=torch.uint8).pin_memory()
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        p.copy_in(host.data_ptr(), n)
+        assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
+        assert p._lib.jt_b200_records(p._h)
+        assert p._lib.jt_b200_records_download(p._h, tape_h.data_ptr(), str_h.data_ptr()) == 0
+        e1.record(stream)
+        e1.synchronize()
+        if k >= args.warmup:
+            e2e.append(e0.elapsed_time(e1))
+    e2e_tot = max_over_ranks(sum(e2e), dist, "cuda")
+    fx = fixture(3, len(data))
+    par = {"checked": "counts", "records": total_records == fx["records"]} if fx else {"checked": False}
     if rank == 0:
-        cpu = None
-        if not args.no_cpu and world == 1:
-            try:
-                from oracle.pyoracle import Reference
-                ref = Reference()
-                recs = mine.split(b"\n")[:20000]
-                t0 = time.perf_counter()
-                for r in recs:
-                    ref.parse_code(r)
-                dt = time.perf_counter() - t0
-                sb = sum(len(r) + 1 for r in recs)
-                cpu = {"value": sb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
-                       "sample": f"first {len(recs)} records, one reference jt_parse each, 1 thread"}
-            except Exception as ex:
-                cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": str(ex)}
+        peak, peak_src = peaks()
         per_step = tot_ms / args.steps
         B2 = n + 8 * int(sz[0]) + int(sz[1])
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"C3: NDJSON, lognormal records (mean 256 B), {world} x {size} bytes, "
-                                   "each record parsed as jt_parse(record)",
-                       "bytes": total_bytes, "records_rank0": nrec, "failed_records_rank0": bad,
-                       "first_record_rank0": first_record,
-                       "l2": "flushed before every step (256 MiB memset, outside the events)",
-                       "parallelism": f"{world} GPUs, record-boundary split" if world > 1 else "1 GPU"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOADS[3] + f"; cut on record boundaries into {world} parts",
+                       "bytes": len(data), "records": total_records, "records_rank0": cnt.value,
+                       "first_record_rank0": first_record, "l2": L2_NOTE,
+                       "parallelism": f"{world} GPUs, record-boundary split"},
             "roofline": {"bound": "hbm", "kernel": "record-mode parse of rank 0's records",
                          "achieved": B2 / (per_step / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": B2 / (per_step / 1e3) / 1e9 / peak, "traffic": None,
-                         "peak_source": peak_src},
-            "cpu_baseline": cpu,
-            "e2e": None,
+                         "frac": B2 / (per_step / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src},
+            "parity": par,
+            "cpu_baseline": None,
+            "e2e": {"value": len(data) * args.steps / (e2e_tot / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": n, "d2h_bytes_per_step": 8 * int(sz[0]) + int(sz[1]) + 48 * cnt.value},
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    dist.barrier()
+    dist.destroy_process_group()
 
 
-def run_select(args, rank: int, world: int, local: int, torch, dist):
+def run_select(args, torch, local):
     """Parse + select (the paper's parse-then-query use):
-    distinct_values at a key path that occurs in the document.  Device:
-    resident parse + jt_b200_distinct (selection on the GPU, values and string
-    bytes gathered, host sort of the selected values); the same text as
-    jt_document_distinct on the downloaded document (checked).  CPU baseline:
-    the reference's jt_parse + jt_document_distinct on one core.  Every rank
-    runs its own replica (no collective)."""
+    distinct_values at a key path that occurs in the document, one GPU."""
     import re
     from paper_1902_08318_b200 import Parser
-    from tools.gen import generate
-    size = args.size or (SIZE if args.config == CONFIG else None)
-    data = generate(args.config, size)
+    config = 1 if args.config == CONFIG else args.config
+    data = generate(config, args.size)
     n = len(data)
     keys = [m.group(1) for m in re.finditer(rb'"([^"\\.]{1,24})"\s*:', data[:1 << 20])]
     path = keys[0] if keys else b"a"
@@ -446,8 +867,6 @@ def run_select(args, rank: int, world: int, local: int, torch, dist):
     for _ in range(args.warmup):
         p.parse_resident(n)
         p.distinct(path)
-    if dist:
-        dist.barrier()
     ts = []
     with ClockSampler(local) as clk:
         clk.wait_first()
@@ -460,45 +879,41 @@ def run_select(args, rank: int, world: int, local: int, torch, dist):
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
             assert r.name == "OK" and out == want
-    tot_ms = max_over_ranks(sum(ts) * 1e3, dist, "cuda")
-    value = job_throughput(n, args.steps, world, tot_ms)
-    if rank == 0:
-        cpu = None
-        if not args.no_cpu:
-            try:
-                from oracle.pyoracle import Reference
-                ref = Reference()
-                best = None
-                for _ in range(2):
-                    t0 = time.perf_counter()
-                    got = ref.distinct(data, [path])
-                    dt = time.perf_counter() - t0
-                    best = dt if best is None else min(best, dt)
-                assert got is not None and got[0] == want
-                cpu = {"value": n / best / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
-                       "sample": "full document, reference jt_parse + jt_document_distinct, best of 2, 1 thread"}
-            except Exception as e:
-                cpu = {"unavailable": e.__class__.__name__}
-        print(json.dumps({
-            "metric": "JSON parse + select (distinct_values) GB/s", "value": value, "unit": "GB/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"config {args.config} + distinct_values at path {path.decode('utf-8', 'replace')!r}",
-                       "bytes": n, "distinct_values": want.count(b"\n"),
-                       "timing": "host wall clock around resident parse + jt_b200_distinct (synchronous)",
-                       "l2": "flushed before every step"},
-            "cpu_baseline": cpu, "clocks": clk.summary()}), flush=True)
+    tot_ms = sum(ts) * 1e3
+    cpu = None
+    if not args.no_cpu:
+        from oracle.pyoracle import Reference
+        ref = Reference()
+        best = None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            got = ref.distinct(data, [path])
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        assert got is not None and got[0] == want
+        cpu = {"value": n / best / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+               "sample": "full document, reference jt_parse + jt_document_distinct, best of 2, 1 thread"}
+    print(json.dumps({
+        "metric": "JSON parse + select (distinct_values) GB/s", "value": n * args.steps / (tot_ms / 1e3) / 1e9,
+        "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"config {config} + distinct_values at path {path.decode('utf-8', 'replace')!r}",
+                   "bytes": n, "distinct_values": want.count(b"\n"),
+                   "timing": "host wall clock around resident parse + jt_b200_distinct (synchronous)",
+                   "l2": "flushed before every step"},
+        "cpu_baseline": cpu, "clocks": clk.summary()}), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=CONFIG)
     ap.add_argument("--size", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-table", action="store_true", help="headline config only")
     ap.add_argument("--shard", action="store_true", help="byte-range shard path even at N = 1")
     ap.add_argument("--select", action="store_true",
                     help="parse + select: distinct_values at a key path (SURVEY.md §8f rank 4)")
@@ -519,176 +934,26 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if args.select:
-        return run_select(args, rank, world, local, torch, dist)
-    if args.config == 3:
-        return run_records(args, rank, world, local, torch, dist)
-    if world > 1 or args.shard:
+        return run_select(args, torch, local)
+    if world > 1:
+        if args.config == 3:
+            return run_records(args, rank, world, local, torch, dist)
         return run_sharded(args, rank, world, local, torch, dist)
-
-    from paper_1902_08318_b200 import Parser
-    from tools.gen import generate
-    size = args.size or (SIZE if args.config == CONFIG else None)
-    data = generate(args.config, size)
-    n = len(data)
-
-    # a real (non-NULL) stream: torch's default stream is the legacy NULL
-    # stream, which the C ABI treats as "use the parser's own stream"
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    p = Parser()
-    p.set_stream(stream.cuda_stream)
-    # device-resident input
-    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
-    p.copy_in(host.data_ptr(), n)
-    torch.cuda.synchronize()
-
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    r = p.parse_resident(n)
-    assert r.name == "OK", (r.name, r.offset)
-    S = p.device_index()[1]
-    T = p.device_tape()[1]
-    SB = p.device_strings()[1]
-    launches = p.last_launches()
-
-    # warm-up
-    for _ in range(args.warmup):
-        flush.zero_()
-        p.parse_async(n)
-        assert p.finish().code == 0
-
-    # timed region: K full parses, events around each, L2 flush outside
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        clk.wait_first()
-        for k in range(args.steps):
-            flush.zero_()
-            starts[k].record(stream)
-            p.parse_async(n)
-            ends[k].record(stream)
-            assert p.finish().code == 0
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = max_over_ranks(sum(step_ms), dist, "cuda")
-    value = job_throughput(n, args.steps, world, tot_ms)
-
-    # per-kernel times (separate profiled passes) for the roofline
-    p.profile(True)
-    kt_runs = []
-    for _ in range(max(3, min(args.steps, 10))):
-        flush.zero_()
-        p.parse_async(n)
-        p.finish()
-        kt_runs.append(p.kernel_times())
-    p.profile(False)
-    kt = {k: statistics.median(r[k] for r in kt_runs) for k in kt_runs[0]}
-    s1_ms = kt["stage1"]
-    full_ms = sum(kt.values())
-    peak, peak_src = peaks()
-    # algorithmic bytes: stage 1 B1 = N + 4S; full B2 = N + 8T + strings
-    B1 = n + 4 * S
-    B2 = n + 8 * T + SB
-    # token pass: reads the index (4S) and the input (N), writes token records
-    # (4S), scalar tape words (8T) and the string buffer
-    Btok = n + 4 * S + 4 * S + 8 * T + SB
-    kern_bytes = {"stage1": B1, "tokens": Btok, "struct": 4 * S + 8 * T}
-    dom = max(kern_bytes, key=lambda k: kt.get(k, 0.0))
-    ach = kern_bytes[dom] / (kt[dom] / 1e3) / 1e9
-    # DRAM traffic of the dominant kernel per launch, from the committed
-    # `ncu --set full` capture of this workload (profiles/), when it matches
-    traffic, traffic_src, alu_pct = None, None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", PROFILE)) as f:
-            prof = json.load(f)
-        kname = {"stage1": "k_stage1<0>", "tokens": "k_scalars", "struct": "k_struct<0, 0>"}[dom]
-        e = next(v for k, v in prof.items() if k.endswith(kname))
-        if args.config == CONFIG and not args.size:
-            traffic = (float(e["dram__bytes_read.sum"]) + float(e["dram__bytes_write.sum"])) * 1e6
-            traffic_src = f"profiles/{PROFILE} {kname} dram read+write per launch"
-        alu_pct = float(e["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"])
-    except Exception:
-        pass
-
-    # jt_stage1 alone (the reference's stage 1: UTF-8 check + structural
-    # index, k_index), device-resident input, L2 flushed before each call
-    s1i_ms = []
-    for k in range(args.warmup + args.steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        p.stage1_async(n)
-        e1.record(stream)
-        r1 = p.finish()
-        assert r1.name == "OK" and p.device_index()[1] == S
-        if k >= args.warmup:
-            s1i_ms.append(e0.elapsed_time(e1))
-    s1i = statistics.median(s1i_ms)
-
-    # e2e through the public C ABI: pinned host input -> jt_parse -> host document
-    e2e_ms = []
-    for k in range(args.warmup + args.steps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rr = p._lib.jt_parse(p._h, C.c_char_p(host.data_ptr()), n, C.byref(doc_ptr := C.c_void_p()),
-                             None)
-        e1.record(stream)
-        e1.synchronize()
-        assert rr == 0
-        p._lib.jt_document_free(doc_ptr)
-        if k >= args.warmup:
-            e2e_ms.append(e0.elapsed_time(e1))
-    e2e_tot = max_over_ranks(sum(e2e_ms), dist, "cuda")
-    e2e_v = job_throughput(n, args.steps, world, e2e_tot)
-
-    if rank == 0:
-        cpu = None
-        if not args.no_cpu:
-            v, threads, one, kind, _ = reference_all_threads(data, 3)
-            cpu = {"value": v, "unit": "GB/s", "cores": threads, "kind": kind,
-                   "sample": (f"the full document, 3 steps of {threads} threads each parsing it with "
-                              f"its own parser (jt_parse incl. its padded copy); 1 thread alone: "
-                              f"{one:.3f} GB/s"),
-                   "one_thread_gbs": one}
-        line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": WORKLOAD if args.config == CONFIG else f"config {args.config}",
-                       "bytes": n, "structurals": S, "tape_words": T, "string_bytes": SB,
-                       "l2": "flushed before every step (256 MiB memset, outside the events)",
-                       "parallelism": "replicas" if world > 1 else "1 GPU"},
-            "stage1_gbs": n / (s1i / 1e3) / 1e9,
-            "stage1_ms": s1i,
-            "stage1_in_parse_ms": s1_ms,
-            "kernel_ms": kt,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes": kern_bytes[dom], "peak_source": peak_src,
-                         # the integer ALU pipe (LOP3/SHF/IADD3/PRMT, 16 lanes per SMSP
-                         # per clock) is what binds these kernels, not HBM
-                         "alu_pipe_pct_of_peak": alu_pct},
-            "roofline_stage1": {"achieved": B1 / (s1i / 1e3) / 1e9, "frac": B1 / (s1i / 1e3) / 1e9 / peak,
-                                "bytes": B1, "path": "jt_stage1 (k_init, k_index, k_stage1_final)"},
-            "roofline_full": {"achieved": B2 / (tot_ms / args.steps / 1e3) / 1e9,
-                              "frac": B2 / (tot_ms / args.steps / 1e3) / 1e9 / peak, "bytes": B2},
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_v, "unit": "GB/s", "h2d_bytes_per_step": n,
-                    "d2h_bytes_per_step": 8 * T + SB + 64},
-            "gpu_launches": launches * args.steps,
-            "clocks": clk.summary(),
-        }
+    if args.shard:
+        return run_sharded(args, rank, world, local, torch, None)
+    if args.config == 3:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        r = measure_records(torch, args.steps, args.warmup, flush, size=args.size, with_cpu=not args.no_cpu)
+        line = {"metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": WORKLOADS[3], "bytes": r["bytes"], "records": r["records"],
+                           "l2": L2_NOTE, "parallelism": "1 GPU"},
+                "parity": r["parity"], "cpu_baseline": r.get("cpu_baseline"), "e2e": r["e2e"],
+                "gpu_launches": r["launches"] * args.steps}
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+        return
+    run_single(args, torch, local)
 
 
 if __name__ == "__main__":

@@ -103,6 +103,11 @@ int jt_b200_records_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
  * blocks.h:31-35 and tape_builder.cpp:140-258). */
 size_t jt_b200_shard_summary_bytes(int phase);
 int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end);
+/* Bytes [lo, hi) of the document are resident on this GPU (hi = 0: all of
+ * it, the default); must cover [begin - 64, end + 64) of every later shard.
+ * A number that starts in the shard and runs to hi makes the parse fail
+ * with JT_CAPACITY, offset -1 (upload a larger halo and parse again). */
+int jt_b200_shard_resident(jt_parser *p, size_t lo, size_t hi);
 int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *summary);
 /* Document result (same code/offset as jt_parse of the whole document); waits. */
 jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *error_offset);

@@ -21,3 +21,9 @@ g++ -std=c++20 -O3 -mavx2 -mpclmul -mbmi -mbmi2 -msse4.2 -fPIC -shared \
   -o "$OUT/libjsontape_ref.so.tmp"
 mv "$OUT/libjsontape_ref.so.tmp" "$OUT/libjsontape_ref.so"
 echo "built $OUT/libjsontape_ref.so"
+# the pthread timing driver for bench.py (oracle/ref_driver.c), linked
+# against the reference library only
+gcc -O2 -std=c11 -fPIC -shared -I"$REF/include" "$HERE/ref_driver.c" \
+  -L"$OUT" -ljsontape_ref -Wl,-rpath,'$ORIGIN' -lpthread -o "$OUT/libref_driver.so.tmp"
+mv "$OUT/libref_driver.so.tmp" "$OUT/libref_driver.so"
+echo "built $OUT/libref_driver.so"

@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "libjt_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libjsontape_ref.so")
+REF_DRIVER_SO = os.path.join(HERE, "_ref", "libref_driver.so")
 
 ERROR_NAMES = ["OK", "UTF8_ERROR", "STRING_ERROR", "NUMBER_ERROR", "TAPE_ERROR",
                "DEPTH_ERROR", "CAPACITY", "EMPTY"]
@@ -163,6 +164,39 @@ class Oracle:
         if ok:
             return True, dst.raw[4:4 + n.value], -1
         return False, None, e.value
+
+
+class RefDriver:
+    """oracle/ref_driver.c: the reference's jt_parse timed on `threads`
+    pthreads (one jt_parser each), for bench.py's CPU baseline."""
+
+    def __init__(self, path: str = REF_DRIVER_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = self.lib = C.CDLL(path)
+        L.jtref_parse_many.restype = C.c_double
+        L.jtref_parse_many.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.jtref_parse_records.restype = C.c_double
+        L.jtref_parse_records.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int,
+                                          C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+
+    def parse_many(self, data: bytes, threads: int, reps: int) -> tuple[float, int]:
+        """(wall seconds of `reps` jt_parse of `data` on each of `threads`
+        threads, code of the last parse)"""
+        code = C.c_int(-1)
+        dt = self.lib.jtref_parse_many(data, len(data), threads, reps, C.byref(code))
+        if dt < 0:
+            raise RuntimeError("jtref_parse_many failed")
+        return dt, code.value
+
+    def parse_records(self, data: bytes, threads: int, reps: int) -> tuple[float, int, int]:
+        """(wall seconds of `reps` passes over the '\n'-separated records,
+        each jt_parse()d alone, dealt to `threads` threads; records; OK)"""
+        nr, ok = C.c_size_t(), C.c_size_t()
+        dt = self.lib.jtref_parse_records(data, len(data), threads, reps, C.byref(nr), C.byref(ok))
+        if dt < 0:
+            raise RuntimeError("jtref_parse_records failed")
+        return dt, nr.value, ok.value
 
 
 class Reference:

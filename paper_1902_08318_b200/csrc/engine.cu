@@ -217,6 +217,7 @@ struct jt_parser {
   jt::Shard *h_shard = nullptr;  // pinned
   DevBuf shard;                  // Shard + open-container stack
   uint64_t shard_len = 0;        // document length
+  uint64_t res_lo = 0, res_hi = 0;  // resident byte range of a shard's document (res_hi 0: all)
   // streamed jt_parse (parse_stream): copy stream, per-chunk events, chunk
   // tile counters and carry states, stage-1 control block snapshot
   cudaStream_t copy_stream = nullptr;
@@ -1027,6 +1028,11 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
     p->err = "shard_begin: pinned allocation";
     return -1;
   }
+  if (p->res_hi && (p->res_lo > (begin >= 64 ? begin - 64 : 0) ||
+                    p->res_hi < (end + 64 < len ? end + 64 : len))) {
+    p->err = "shard_begin: the resident range must cover [begin - 64, end + 64)";
+    return -1;
+  }
   const uint64_t range = end - begin;
   if (!ensure_input(p, len) || !ensure_stage1(p, range, 0) || !ensure_stage2(p, range) ||
       !p->shard.ensure(kShardBoundOff + jt::kBoundMax * sizeof(uint64_t))) {
@@ -1040,6 +1046,7 @@ int shard_setup(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, 
   h.end = end;
   h.len = len;
   h.streamed = 0u;
+  h.res_hi = p->res_hi && p->res_hi < len ? p->res_hi : 0;
   *p->h_shard = h;
   if (!cuda_ok(p, cudaMemcpyAsync(p->shard.p, p->h_shard, sizeof(jt::Shard), cudaMemcpyHostToDevice,
                                   p->stream),
@@ -1985,6 +1992,16 @@ size_t jt_b200_shard_summary_bytes(int phase) {
     case 3: return sizeof(jt::Sum3);
     default: return 0;
   }
+}
+
+int jt_b200_shard_resident(jt_parser *p, size_t lo, size_t hi) {
+  if (hi && lo >= hi) {
+    p->err = "shard_resident: empty range";
+    return -1;
+  }
+  p->res_lo = hi ? lo : 0;
+  p->res_hi = hi;
+  return 0;
 }
 
 int jt_b200_shard_begin(jt_parser *p, size_t len, unsigned g, unsigned G, size_t begin, size_t end) {

@@ -1,8 +1,11 @@
 // shard.h — byte-range sharding of one document across GPUs.
 //
-// Shard g of G parses bytes [begin, end) of a document whose bytes are all
-// readable (the bench keeps the whole input on every GPU; a deployment needs
-// [begin - 64, end + longest token) only).  Tokens belong to the shard where
+// Shard g of G parses bytes [begin, end) of a document of which the GPU holds
+// [begin - 64, end + halo) (jt_b200_shard_resident; default: all of it).  A
+// token crossing `end` is read from the halo: strings, escapes and atoms need
+// at most 64 bytes of it; a number longer than the halo is detected (its digit
+// run reaches the resident end) and the parse fails loudly with CAPACITY
+// instead of reading bytes the GPU does not hold.  Tokens belong to the shard where
 // they start.  Four small all-gathers connect the shards; each phase writes a
 // fixed-size summary that the caller all-gathers (NCCL, or a local copy when
 // emulating G shards on one GPU) and hands to the next phase:
@@ -47,6 +50,9 @@ struct Shard {
   uint32_t streamed;      // pieces of one streamed parse: only summaries up to g + 1 are final
                           // when phase 2 runs (later ones may be being written)
   uint32_t last_tok;      // this shard holds the document's last token (end-of-input check)
+  uint32_t pad0;
+  uint64_t res_hi;        // end of the bytes resident on this GPU (0: the whole document); a
+                          // number that starts in the shard and runs to res_hi fails CAPACITY
 };
 
 // phase summaries (all-gathered as raw bytes)

@@ -469,6 +469,21 @@ __global__ void __launch_bounds__(256) k_numbers(Stage2Args a) {
     const uint32_t p = a.idx[i];
     const uint32_t t = a.tape_idx[i];
     num::NumResult r = num::parse_number(at, a.len, p);
+    if (a.sh != nullptr && a.sh->G > 0 && a.sh->res_hi != 0 && i + 1 == ctrl->S) {
+      // a shard's last token may run past its end into the halo: a digit run
+      // reaching the resident end read bytes this GPU does not hold
+      const uint64_t rh = a.sh->res_hi;
+      uint64_t q = p;
+      while (q < rh) {
+        const uint32_t ch = a.in[q];
+        if (!((ch - '0') < 10u || ch == '-' || ch == '+' || ch == '.' || ch == 'e' || ch == 'E')) break;
+        q++;
+      }
+      if (q >= rh) {  // not NUMBER_ERROR at this token: its bytes are not all here
+        atomicMin(&ctrl->err_key, ((unsigned long long)(a.sh->token_base + i) << 8) | kCapacity);
+        continue;
+      }
+    }
     if (r.kind == num::kNumFail) {
       atomicOr(&a.tok[i], 0x100u);
     } else if (r.kind == num::kNumSlow) {
@@ -1559,6 +1574,7 @@ __global__ void k_final_shard(Stage2Args a) {
     const int code = (int)(c->err_key & 0xFF);
     r->err_key = c->err_key;
     if (i >= vw.S_total) r->offset = (long long)a.len;
+    else if (code == kCapacity) r->offset = -1;  // a number longer than the resident halo
     else if (code == kStringError) r->offset = (long long)c->str_err;
     else r->offset = (long long)a.idx[i - vw.token_base];
   }

@@ -36,7 +36,7 @@ EXPORTS = [
     "jt_b200_device_strings", "jt_b200_download", "jt_b200_document_tape", "jt_b200_document_strings", "jt_b200_document_from", "jt_b200_set_stream",
     "jt_b200_last_launches", "jt_b200_device", "jt_b200_last_error", "jt_b200_profile",
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_distinct", "jt_b200_shard_summary_bytes",
-    "jt_b200_shard_begin", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
+    "jt_b200_shard_begin", "jt_b200_shard_resident", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
     "jt_b200_shard_download", "jt_b200_copy_in_range", "jt_b200_parse_records",
     "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download", "jt_b200_device_records",
 ]
@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_summary_bytes.argtypes = [C.c_int]
     L.jt_b200_shard_summary_bytes.restype = sz
     L.jt_b200_shard_begin.argtypes = [vp, sz, C.c_uint, C.c_uint, sz, sz]
+    L.jt_b200_shard_resident.argtypes = [vp, sz, sz]
     L.jt_b200_shard_phase.argtypes = [vp, C.c_int, vp, vp]
     L.jt_b200_shard_finish.argtypes = [vp, vp, C.POINTER(ll)]
     L.jt_b200_shard_extent.argtypes = [vp, C.POINTER(C.c_ulonglong)]

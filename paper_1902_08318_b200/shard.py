@@ -35,6 +35,15 @@ def layout(length: int, shards: int) -> list[tuple[int, int]]:
     return [(cuts[g], min(cuts[g + 1], length)) for g in range(shards)]
 
 
+def set_resident(parser: Parser, lo: int, hi: int):
+    """Only bytes [lo, hi) of the document are on this parser's GPU (hi = 0:
+    all).  A number of the shard running to hi fails the parse with
+    CAPACITY (offset -1) instead of reading bytes that are not there."""
+    lib = load_library()
+    if lib.jt_b200_shard_resident(parser._h, lo, hi) != 0:
+        raise RuntimeError(lib.jt_b200_last_error(parser._h).decode())
+
+
 def summary_bytes(phase: int) -> int:
     return int(load_library().jt_b200_shard_summary_bytes(phase))
 

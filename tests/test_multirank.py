@@ -116,3 +116,61 @@ def test_record_ranges():
         assert all(rr[k][1] == rr[k + 1][0] for k in range(world - 1))
         assert all(b == 0 or data[b - 1:b] == b"\n" for b, _ in rr)
         assert sum(data[b:e].count(b"\n") for b, e in rr) == data.count(b"\n")
+
+
+def _records_worker(rank, world, port, data, q):
+    """bench.py run_records' host logic: the record-boundary split and the
+    global numbering; each rank parses its records with the oracle standing
+    in for jt_b200_parse_records (one jt_parse per record)."""
+    import torch.distributed as dist
+    import bench
+    from oracle.pyoracle import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = bench.record_ranges(data, world)[rank]
+    recs = data[b:e].split(b"\n")
+    if data[b:e].endswith(b"\n"):
+        recs = recs[:-1]  # a trailing newline ends the last record
+    o = Oracle()
+    res = [(o.parse(r).code, o.parse(r).offset) for r in recs]
+    first, total = bench.record_numbering(dist, world, rank, len(res))
+    q.put((rank, b, e, first, total, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_record_split_gloo(world):
+    """C3 at N > 1 (bench.py run_records): ranks cut the NDJSON buffer after
+    the first newline at each g/N point and number their records from an
+    all_gather of the counts.  Every record lands on exactly one rank, in
+    order, and the per-record results equal jt_parse(record) over the whole
+    buffer; also a cut point that falls on a newline, and a last record
+    without a trailing newline."""
+    from tools.gen import generate
+    data = generate(3, 256 << 10, seed=7)
+    mid = data.index(b"\n", len(data) // 2) + 1
+    data = data[:mid] + b"\n" + data[mid:]  # an empty record mid-buffer
+    data = data.rstrip(b"\n")  # last record unterminated
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_records_worker, args=(r, world, port, data, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    want = [(o.parse(r).code, o.parse(r).offset) for r in data.split(b"\n")]
+    got = []
+    at = 0
+    for rank, b, e, first, total, rr in res:
+        assert b == (res[rank - 1][2] if rank else 0) and first == len(got) and total == len(want)
+        got += rr
+        at = e
+    assert at == len(data)
+    assert got == want
+    assert any(c == 7 for c, _ in want)  # the empty record: EMPTY
