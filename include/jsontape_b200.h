@@ -122,6 +122,8 @@ int jt_b200_shard_download(jt_parser *p, uint64_t *tape, uint8_t *strings);
 
 /* CUDA device ordinal the parser was created on. */
 int jt_b200_device(const jt_parser *p);
+/* Bytes of device memory the parser holds (its grow-only arena). */
+size_t jt_b200_device_bytes(const jt_parser *p);
 
 /* Last CUDA error string seen by the parser ("" if none). */
 const char *jt_b200_last_error(const jt_parser *p);

@@ -263,7 +263,7 @@ class Reference:
         out = ParseResult(code, off.value)
         if code == 0:
             n = self.lib.jt_index_count(self.p)
-            out.index = C.string_at(self.lib.jt_index_positions(self.p), 4 * n) if n else b""
+            out.index = _bytes_at(C.cast(self.lib.jt_index_positions(self.p), C.c_void_p).value, 4 * n) if n else b""
         return out
 
     def distinct(self, data: bytes, paths):
@@ -293,11 +293,16 @@ class Reference:
         out = ParseResult(code, off.value)
         n = self.lib.jt_index_count(self.p)
         if code != 1:  # index is refreshed unless stage 1 failed on UTF-8
-            out.index = C.string_at(self.lib.jt_index_positions(self.p), 4 * n) if n else b""
+            out.index = _bytes_at(C.cast(self.lib.jt_index_positions(self.p), C.c_void_p).value, 4 * n) if n else b""
         if code == 0:
             out.tape, out.strings = _doc_words(doc.value)
             self.lib.jt_document_free(doc)
         return out
+
+
+def _bytes_at(ptr: int, n: int) -> bytes:
+    """ctypes.string_at for any size (its size argument is a C int)"""
+    return bytes((C.c_char * n).from_address(ptr)) if n else b""
 
 
 def _doc_words(doc_ptr: int):
@@ -306,6 +311,6 @@ def _doc_words(doc_ptr: int):
     two libstdc++ std::vector triples (begin, end, cap)."""
     words = (C.c_uint64 * 6).from_address(doc_ptr)
     tb, te, _, sb, se, _ = list(words)
-    tape = C.string_at(tb, te - tb) if te > tb else b""
-    strings = C.string_at(sb, se - sb) if se > sb else b""
+    tape = _bytes_at(tb, te - tb) if te > tb else b""
+    strings = _bytes_at(sb, se - sb) if se > sb else b""
     return tape, strings

@@ -20,8 +20,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <charconv>
+#include <condition_variable>
 #include <functional>
+#include <thread>
 #include <map>
 #include <mutex>
 #include <set>
@@ -125,6 +128,84 @@ struct Span {
   bool operator==(const Span &o) const { return n == o.n && (n == 0 || memcmp(p, o.p, n * sizeof(T)) == 0); }
 };
 
+// Parallel host memcpy for pageable jt_parse input: a copy engine can only
+// read page-locked memory, so a pageable document goes up through a small
+// pinned staging ring, and one core's memcpy (~10 GB/s) cannot keep a
+// ~55 GB/s PCIe link busy.  `copy` splits the bytes over the helper threads
+// and the caller; persistent threads, one pool per parser.
+class CopyPool {
+ public:
+  explicit CopyPool(int helpers) {
+    for (int w = 0; w < helpers; w++) th_.emplace_back([this, w] { run(w + 1); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+  void copy(void *dst, const void *src, size_t n) {
+    const int parts = (int)th_.size() + 1;
+    if (n < ((size_t)1 << 20) || parts == 1) {
+      memcpy(dst, src, n);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = (uint8_t *)dst;
+      src_ = (const uint8_t *)src;
+      n_ = n;
+      left_.store(parts - 1);
+      gen_++;
+    }
+    cv_.notify_all();
+    part(0, parts);
+    while (left_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+  }
+
+ private:
+  void part(int w, int parts) {
+    const size_t step = (n_ / parts + 4095) & ~(size_t)4095;
+    const size_t b = std::min(n_, step * (size_t)w), e = std::min(n_, b + step);
+    const size_t end = w + 1 == parts ? n_ : e;
+    if (end > b) memcpy(dst_ + b, src_ + b, end - b);
+  }
+  void run(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> g(m_);
+      cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      g.unlock();
+      part(w, (int)th_.size() + 1);
+      left_.fetch_sub(1, std::memory_order_release);
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::atomic<int> left_{0};
+  uint8_t *dst_ = nullptr;
+  const uint8_t *src_ = nullptr;
+  size_t n_ = 0;
+};
+
+// host memory the copy engines cannot read directly (not page-locked or
+// registered): jt_parse stages it
+bool is_pageable(const void *ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
 }  // namespace
 
 // Layout read by paper_1902_08318_b200/jsontape.py (Document): tape pointer,
@@ -181,7 +262,7 @@ struct jt_parser {
   cudaStream_t stream = nullptr;
   DevBuf in;               // padded input
   DevBuf idx[2];           // structural index, double-buffered
-  DevBuf aux[2];           // per index entry: string-buffer prefix
+  DevBuf aux;              // per index entry: string-buffer prefix (with the last K1 run)
   int cur = 0;             // idx[cur] = index of the last successful stage 1
   DevBuf s1rec, s2rec;     // look-back records
   DevBuf tok, tape_idx, m1, m2, mhi, slow, numlist, scopebits, tile_flags;  // m3 lives in s2rec (zeroed by init)
@@ -249,6 +330,12 @@ struct jt_parser {
   const jt::RecordResult *rec_results = nullptr;
   uint64_t rec_n = 0;
   uint8_t rec_last_byte = 0;
+  // pageable jt_parse input: pinned staging slots (one upload group each),
+  // the event after each slot's H2D copy, and the memcpy pool that fills them
+  std::vector<void *> stage_slot;
+  std::vector<cudaEvent_t> stage_ev;
+  size_t stage_bytes = 0;
+  CopyPool *copy_pool = nullptr;
   // optional per-kernel timing: ev[0] before init, then one per launch
   bool prof = false;
   cudaEvent_t ev[8] = {};
@@ -303,13 +390,16 @@ bool zero_tail(jt_parser *p, uint64_t len) {
                  "memset input tail");
 }
 
-// Device buffers sized from len (S <= len); the tape/strings worst cases
-// follow the reference's reservations (tape_builder.cpp:148, 152).
+// Device buffers sized from len before the parse knows S (S <= len: every
+// byte can be structural).  The string buffer is at most 2 len + 2 bytes:
+// each byte weighs at most 1 except an opening quote (4), and every opening
+// quote is followed by content or a closing quote (0).  (The reference
+// reserves len + 4 S + 64, tape_builder.cpp:152.)
 bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
   size_t cap_tok = (size_t)len + 16;
   if (!p->idx[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
-  if (!p->aux[which].ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
-  if (!p->strings.ensure((size_t)len + 4 * cap_tok + 128)) return false;
+  if (!p->aux.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
+  if (!p->strings.ensure(2 * (size_t)len + 256)) return false;
   if (!p->tok.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
   if (!p->tape_idx.ensure((cap_tok + 16) * sizeof(uint32_t))) return false;
   if (!p->tile_flags.ensure(jt::stage1_records(len) * sizeof(uint32_t) + 64)) return false;
@@ -318,16 +408,26 @@ bool ensure_stage1(jt_parser *p, uint64_t len, int which) {
   return true;
 }
 
-bool ensure_stage2(jt_parser *p, uint64_t len) {
+// Number tokens start at least two bytes apart (a number token's first byte
+// follows whitespace or a structural character), so the number and slow-float
+// lists hold at most len / 2 + 1 entries.  The tape of a document that parses
+// has at most len + 3 words (a bracket, string or atom costs at least as many
+// bytes as words; a number's second word is paid by the separator or closer
+// after it); longer tapes only come from documents that fail, whose tape
+// writes past the capacity are dropped (Stage2Args::tape_cap).  The reference
+// reserves 2 S + 3 words (tape_builder.cpp:148).  NDJSON records add two root
+// words per record (a record can be 2 bytes: "1\n"), so they keep 2 len.
+bool ensure_stage2(jt_parser *p, uint64_t len, bool records = false) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
+  const uint64_t nums = len / 2 + 32;
   bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 128 + (cap / 256 + 2) * 32) &&
             p->m1.ensure(z.n1 * sizeof(int16_t)) && p->m2.ensure(z.n2 * sizeof(int16_t)) &&
             p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
-            p->slow.ensure((cap + 16) * 2 * sizeof(uint32_t)) &&
-            p->numlist.ensure((cap + 16) * sizeof(uint32_t)) &&
+            p->slow.ensure(nums * sizeof(uint32_t)) &&
+            p->numlist.ensure(nums * sizeof(uint32_t)) &&
             p->scopebits.ensure((cap / 32 + 16) * sizeof(uint32_t)) &&
-            p->tape.ensure((2 * cap + 8) * sizeof(uint64_t));
+            p->tape.ensure(((records ? 2 * cap : cap) + 16) * sizeof(uint64_t));
   return ok;
 }
 
@@ -343,7 +443,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0
   a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
-  a.aux = p->aux[which].as<uint32_t>();
+  a.aux = p->aux.as<uint32_t>();
   a.strings = p->strings.as<uint8_t>();
   a.tokrec = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
@@ -370,7 +470,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
   a.in = p->in.as<uint8_t>();
   a.len = len;
   a.idx = p->idx[which].as<uint32_t>();
-  a.aux = p->aux[which].as<uint32_t>();
+  a.aux = p->aux.as<uint32_t>();
   a.ctrl = p->ctrl.as<jt::Ctrl>();
   a.tok = p->tok.as<uint32_t>();
   a.tape_idx = p->tape_idx.as<uint32_t>();
@@ -386,6 +486,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
   a.scopebits = p->scopebits.as<uint32_t>();
   a.stk_rec = (uint64_t *)((uint8_t *)p->s2rec.p + ((z.n3 * sizeof(int32_t) + 64 + 63) & ~(size_t)63));
   a.tape = p->tape.as<uint64_t>();
+  a.tape_cap = p->tape.cap / sizeof(uint64_t);
   a.strings = p->strings.as<uint8_t>();
   a.cap_tokens = cap_len + 16;
   a.num_sms = p->num_sms;
@@ -398,7 +499,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
 
 // signature of every device pointer baked into a captured graph
 uint64_t buffers_sig(jt_parser *p, int which) {
-  const void *ptrs[] = {p->in.p, p->idx[which].p, p->aux[which].p, p->s1rec.p, p->s2rec.p,
+  const void *ptrs[] = {p->in.p, p->idx[which].p, p->aux.p, p->s1rec.p, p->s2rec.p,
                         p->tok.p, p->tape_idx.p, p->m1.p, p->m2.p, p->mhi.p, p->slow.p,
                         p->tape.p, p->strings.p, p->ctrl.p, p->numlist.p, p->scopebits.p,
                         p->tile_flags.p,
@@ -657,6 +758,42 @@ bool ensure_ranges(jt_parser *p) {
          p->patchbuf.ensure(kPatchWords * 8);
 }
 
+// pinned staging ring for pageable input: kStageSlots slots of `bytes`
+constexpr int kStageSlots = 4;
+bool ensure_stager(jt_parser *p, size_t bytes) {
+  if (p->stage_bytes < bytes) {
+    for (void *s : p->stage_slot) cudaFreeHost(s);
+    p->stage_slot.clear();
+    p->stage_bytes = 0;
+    for (int k = 0; k < kStageSlots; k++) {
+      void *s = nullptr;
+      if (cudaMallocHost(&s, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      p->stage_slot.push_back(s);
+    }
+    p->stage_bytes = bytes;
+  }
+  while (p->stage_ev.size() < (size_t)kStageSlots) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    p->stage_ev.push_back(e);
+  }
+  if (!p->copy_pool) {
+    // JT_COPY_THREADS: threads filling the slots (default: up to 8 of the cores)
+    const char *e = getenv("JT_COPY_THREADS");
+    long t = e ? atol(e) : 0;
+    if (t <= 0) t = std::min<long>(8, std::max<unsigned>(1u, std::thread::hardware_concurrency()));
+    p->copy_pool = new (std::nothrow) CopyPool((int)t - 1);
+    if (!p->copy_pool) return false;
+  }
+  return true;
+}
+
 jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document **out, long long *off) {
   static const bool trace = getenv("JT_TRACE") != nullptr;
   auto now_us = []() {
@@ -738,57 +875,29 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     const long v = e ? atol(e) : -1;
     return v >= 0 ? (uint64_t)v << 10 : (uint64_t)4 << 20;
   }();
-  for (uint64_t c0 = 0; ok && c0 < nch; c0 += up_pieces) {
+  // A pageable document goes up through the pinned staging ring: each
+  // upload group is memcpy'd into a free slot by the copy pool, then copied
+  // from there; its pieces' stage 1 is enqueued right after it, and the
+  // string pieces of finished pieces start back in between.
+  const bool staged = is_pageable(data) && ensure_stager(p, up_pieces * kStreamChunk);
+  auto upload_group = [&](uint64_t c0) {
     const uint64_t c1 = std::min(nch, c0 + up_pieces);
     const uint64_t b = c0 * kStreamChunk, e = std::min(len, c1 * kStreamChunk);
-    ok = cuda_ok(p, cudaMemcpyAsync(in + b, data + b, e - b, cudaMemcpyHostToDevice, cs), "H2D");
-    for (uint64_t c = c0; ok && c < c1; c++) ok = cuda_ok(p, cudaEventRecord(p->chunk_ev[c], cs), "event");
-  }
-  // stage 1 piece by piece, each after its upload
-  for (uint64_t c = 0; ok && c < nch; c++) {
-    const uint64_t b = c * kStreamChunk, e = std::min(len, b + kStreamChunk);
-    jt::Stage1Args a = s1_args(p, len, which, b, e, ntiles);
-    a.rec_tile0 = b / jt::kStage1Tile;
-    a.last_tile = ntiles - 1;
-    a.fn += a.rec_tile0;
-    a.carry += a.rec_tile0;
-    a.tile_counter = counters + c;
-    a.init_state = c ? states + c - 1 : nullptr;
-    a.out_state = states + c;
-    a.sb_out = p->h_piece_sb + c;
-    // K1 runs one tile behind the piece boundaries: a tile's last block may
-    // read a few bytes past the tile (an escape straddling it), which for a
-    // piece's last tile are the next piece's, still uploading
-    jt::Stage1Args k1 = a;
-    k1.begin = c == 0 ? 0 : b - jt::kStage1Tile;
-    k1.end = c + 1 == nch ? len : e - jt::kStage1Tile;
-    k1.rec_tile0 = k1.begin / jt::kStage1Tile;
-    k1.carry = a.carry - a.rec_tile0 + k1.rec_tile0;
-    k1.fn = a.fn - a.rec_tile0 + k1.rec_tile0;
-    int rk = -1;  // early range starting after this piece
-    for (int q = 0; q < nR; q++)
-      if (rcut[q] == (int64_t)c) rk = q;
-    if (rk >= 0) k1.tok_out = tokA + rk;
-    ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
-         cuda_ok(p, jt::stage1_chunk_carry(a, p->stream), "stage1 carry") &&
-         cuda_ok(p, jt::stage1_chunk_main(k1, p->stream), "stage1 chunk") &&
-         cuda_ok(p, cudaEventRecord(p->piece_ev[c], p->stream), "event");
-    p->launches += jt::kStage1Launches;
-    if (ok && rk >= 0) {  // early range rk next to the later pieces' stage 1
-      jt::Stage2Args s2a = s2_args(p, len, which);
-      s2a.patch = p->patchbuf.as<unsigned long long>();
-      int nA = 0;
-      ok = cuda_ok(p, cudaStreamWaitEvent(p->s2_stream, p->piece_ev[c], 0), "wait") &&
-           (!trace || cudaEventRecord(tr_ev[2 * rk], p->s2_stream) == cudaSuccess) &&
-           cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->h_range + rk,
-                                         p->s2_stream, &nA, stage2_fork(p)),
-                   "range") &&
-           cuda_ok(p, cudaEventRecord(p->ev_rng[rk], p->s2_stream), "event");
-      if (trace) cudaEventRecord(tr_ev[2 * rk + 1], p->s2_stream);
-      p->launches += nA;
+    if (staged) {
+      const uint64_t grp = c0 / up_pieces;
+      const int s = (int)(grp % kStageSlots);
+      void *slot = p->stage_slot[s];
+      ok = ok && (grp < (uint64_t)kStageSlots || cuda_ok(p, cudaEventSynchronize(p->stage_ev[s]), "slot"));
+      if (ok) p->copy_pool->copy(slot, data + b, e - b);
+      ok = ok && cuda_ok(p, cudaMemcpyAsync(in + b, slot, e - b, cudaMemcpyHostToDevice, cs), "H2D") &&
+           cuda_ok(p, cudaEventRecord(p->stage_ev[s], cs), "event");
+    } else {
+      ok = ok && cuda_ok(p, cudaMemcpyAsync(in + b, data + b, e - b, cudaMemcpyHostToDevice, cs), "H2D");
     }
-  }
-  if (trace) fprintf(stderr, " enqueued %.0f us\n", now_us() - t0);
+    for (uint64_t c = c0; ok && c < c1; c++) ok = cuda_ok(p, cudaEventRecord(p->chunk_ev[c], cs), "event");
+  };
+  if (!staged)
+    for (uint64_t c0 = 0; ok && c0 < nch; c0 += up_pieces) upload_group(c0);
   // the string bytes of each piece go back as soon as its stage 1 is done,
   // while later pieces are still uploading (the copy engines run both
   // directions at once); the string-buffer size is not known yet, so the
@@ -837,17 +946,27 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
     // plain copies after stage 1 instead)
     early = d && d->alloc_strings(len + len / 4 + 64) && d->spinned;
     if (early && cA >= 0 && d->alloc_tape(len / 8 + 1024)) tape_cap = d->tape.n;
-    for (uint64_t c = 0; early && c < nch; c++) {
+  }
+  // string pieces of the pieces whose stage 1 is enqueued (c < enq) and done
+  uint64_t c_next = 0, enq = 0;
+  auto drain = [&](bool block) {
+    while (early && c_next < enq) {
+      const uint64_t c = c_next;
+      if (!block && cudaEventQuery(p->piece_ev[c]) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
       if (!cuda_ok(p, cudaEventSynchronize(p->piece_ev[c]), "sync")) {
         early = false;
-        break;
+        return;
       }
       if (trace && (c < 2 || c + 2 >= nch || c % 4 == 0)) fprintf(stderr, " piece %d done %.0f us\n", (int)c, now_us() - t0);
       const uint64_t e = p->h_piece_sb[c];
       if (e > d->sblock_cap - 64 || e < sb_done) {  // too large: fetched whole below
         early = false;
-        break;
+        return;
       }
+      c_next++;
       if ((int64_t)c > cA) tape_a(false);
       if (e < sb_done + d2h_min && c + 1 < nch) continue;  // batch small string pieces
       if (e > sb_done &&
@@ -855,10 +974,64 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
                                       cudaMemcpyDeviceToHost, p->d2h_stream),
                    "strings piece D2H")) {
         early = false;
-        break;
+        return;
       }
       sb_done = e;
     }
+  };
+  // stage 1 piece by piece, each after its upload
+  for (uint64_t c = 0; ok && c < nch; c++) {
+    if (staged && c % up_pieces == 0) {
+      drain(false);
+      upload_group(c);
+      if (!ok) break;
+    }
+    const uint64_t b = c * kStreamChunk, e = std::min(len, b + kStreamChunk);
+    jt::Stage1Args a = s1_args(p, len, which, b, e, ntiles);
+    a.rec_tile0 = b / jt::kStage1Tile;
+    a.last_tile = ntiles - 1;
+    a.fn += a.rec_tile0;
+    a.carry += a.rec_tile0;
+    a.tile_counter = counters + c;
+    a.init_state = c ? states + c - 1 : nullptr;
+    a.out_state = states + c;
+    a.sb_out = p->h_piece_sb + c;
+    // K1 runs one tile behind the piece boundaries: a tile's last block may
+    // read a few bytes past the tile (an escape straddling it), which for a
+    // piece's last tile are the next piece's, still uploading
+    jt::Stage1Args k1 = a;
+    k1.begin = c == 0 ? 0 : b - jt::kStage1Tile;
+    k1.end = c + 1 == nch ? len : e - jt::kStage1Tile;
+    k1.rec_tile0 = k1.begin / jt::kStage1Tile;
+    k1.carry = a.carry - a.rec_tile0 + k1.rec_tile0;
+    k1.fn = a.fn - a.rec_tile0 + k1.rec_tile0;
+    int rk = -1;  // early range starting after this piece
+    for (int q = 0; q < nR; q++)
+      if (rcut[q] == (int64_t)c) rk = q;
+    if (rk >= 0) k1.tok_out = tokA + rk;
+    ok = cuda_ok(p, cudaStreamWaitEvent(p->stream, p->chunk_ev[c], 0), "wait") &&
+         cuda_ok(p, jt::stage1_chunk_carry(a, p->stream), "stage1 carry") &&
+         cuda_ok(p, jt::stage1_chunk_main(k1, p->stream), "stage1 chunk") &&
+         cuda_ok(p, cudaEventRecord(p->piece_ev[c], p->stream), "event");
+    p->launches += jt::kStage1Launches;
+    if (ok && rk >= 0) {  // early range rk next to the later pieces' stage 1
+      jt::Stage2Args s2a = s2_args(p, len, which);
+      s2a.patch = p->patchbuf.as<unsigned long long>();
+      int nA = 0;
+      ok = cuda_ok(p, cudaStreamWaitEvent(p->s2_stream, p->piece_ev[c], 0), "wait") &&
+           (!trace || cudaEventRecord(tr_ev[2 * rk], p->s2_stream) == cudaSuccess) &&
+           cuda_ok(p, jt::range_a_launch(s2a, tokA + rk, rk ? dr + rk - 1 : nullptr, dr + rk, p->h_range + rk,
+                                         p->s2_stream, &nA, stage2_fork(p)),
+                   "range") &&
+           cuda_ok(p, cudaEventRecord(p->ev_rng[rk], p->s2_stream), "event");
+      if (trace) cudaEventRecord(tr_ev[2 * rk + 1], p->s2_stream);
+      p->launches += nA;
+    }
+    enq = c + 1;
+  }
+  if (trace) fprintf(stderr, " enqueued %.0f us\n", now_us() - t0);
+  if (ok && d) {
+    drain(true);
     // length fields left to k_tile_lengths are patched into the host copy
     // too, after the last piece is down
     ok = cuda_ok(p, cudaEventRecord(p->ev_d2h, p->d2h_stream), "event") &&
@@ -1136,6 +1309,9 @@ void jt_parser_free(jt_parser *p) {
   }
   if (p->h_range) cudaFreeHost(p->h_range);
   if (p->h_patch) cudaFreeHost(p->h_patch);
+  for (void *s : p->stage_slot) cudaFreeHost(s);
+  for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
+  delete p->copy_pool;
   for (cudaEvent_t e : p->ev_rng)
     if (e) cudaEventDestroy(e);
   if (p->ta_stream) {
@@ -1841,7 +2017,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   DevGuard dg_(p);
   if (n_records) *n_records = 0;
   if ((uint64_t)len >= (1ULL << 32) || !ensure_input(p, len) || !ensure_stage1(p, len, 0) ||
-      !ensure_stage2(p, len) ||
+      !ensure_stage2(p, len, true) ||
       !p->nlbuf.ensure(jt::stage1_records(len) * 2 * sizeof(uint32_t) + 64)) {
     p->err = "parse_records: allocation";
     return -1;
@@ -2165,6 +2341,16 @@ int jt_b200_kernel_times(jt_parser *p, float *ms, int max) {
 }
 
 int jt_b200_device(const jt_parser *p) { return p->device; }
+
+size_t jt_b200_device_bytes(const jt_parser *p) {
+  const DevBuf *bufs[] = {&p->in, &p->idx[0], &p->idx[1], &p->aux, &p->s1rec, &p->s2rec, &p->tok,
+                          &p->tape_idx, &p->m1, &p->m2, &p->mhi, &p->slow, &p->numlist, &p->scopebits,
+                          &p->tile_flags, &p->tape, &p->strings, &p->ctrl, &p->shard, &p->stream_words,
+                          &p->qbuf, &p->qstr, &p->rngbuf, &p->patchbuf, &p->recs, &p->nlbuf, &p->minbuf};
+  size_t t = 0;
+  for (const DevBuf *b : bufs) t += b->cap;
+  return t;
+}
 
 const char *jt_b200_last_error(const jt_parser *p) { return p->err.c_str(); }
 

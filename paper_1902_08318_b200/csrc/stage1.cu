@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   sb::EscClass ec{0, 0, 0, 0};
   if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? tbyte(64) : 0u);
   // escapes reaching into the next block: ov | spill << 8 (strblock.cuh)
-  int ov_out = E ? sb::escape_overhang(gat, blk, ec) : 0;
+  int ov_out = E ? sb::escape_overhang(tbyte, ec) : 0;  // reads the tile copy (nothing rewritten yet)
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
   // unterminated string: the reference reads the NUL padding at len (in
@@ -524,6 +524,10 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   }
   const int vin = ov_in >> 8;
   ov_in &= 0xFF;
+  // the tile's first block: the decoded bytes an escape of the previous tile
+  // spills into it go to their weight positions of the tile copy (the copy
+  // below takes every weighted byte in order)
+  for (int k = 0; k < vin && threadIdx.x == 0; k++) s_in[k] = (uint8_t)(spill_bytes >> (8 * k));
   // string weight mask: the plain string bytes, or for blocks with escapes
   // the weight positions of each escape (strblock.cuh)
   if (ov_in) ec = sb::restrict_from(ec, ov_in);
@@ -532,7 +536,14 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   {
     uint64_t serr = ctl ? blk + (uint64_t)ctz64(ctl) : ~0ULL;
     uint64_t em = ctl;  // record mode: every error candidate of the block
-    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr, kRec ? &em : nullptr);
+    // decoded escape bytes in place over their weight positions of the tile
+    // copy (strblock.cuh); an escape straddling the tile end leaves its
+    // spilled bytes to the next tile's first block
+    auto rewrite = [&](int k, uint8_t b) {
+      const uint32_t r = local + (uint32_t)k;
+      if (r < (uint32_t)kStage1Tile) s_in[r] = b;
+    };
+    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr, kRec ? &em : nullptr, rewrite);
     if constexpr (kRec) {
       while (em) {  // the first error of each record in the block
         const int q = ctz64(em);
@@ -679,9 +690,9 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     a.tape_idx[gbase + slot] = (uint32_t)(1 + gtbase + t + 2 * rid);
   };
   {
-    // plain runs (escape positions get placeholder bytes, rewritten below;
-    // the first vin bits belong to the previous block's escape)
-    uint64_t cm = W & ~sb::low_bits(vin);
+    // the weighted bytes in order (escapes already decoded in place; the
+    // first vin bits are the spill of the previous block's escape)
+    uint64_t cm = W;
     if (!pay_direct) {
       // each lane copies its own block into the staging buffer, bytes in
       // order with a running destination (+1 per weight bit, +4 per opening
@@ -692,23 +703,21 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
         uint32_t d = soff;
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-          const uint32_t cmw = (uint32_t)(cm >> (16 * c)) & 0xFFFFu;
           const uint32_t ww = (uint32_t)(W >> (16 * c)) & 0xFFFFu;
           const uint32_t ow = (uint32_t)(openq >> (16 * c)) & 0xFFFFu;
-          if (cmw == 0) {
-            d += (uint32_t)__popc(ww) + 4u * (uint32_t)__popc(ow);
+          if (ww == 0) {
+            d += 4u * (uint32_t)__popc(ow);
             continue;
           }
           const uint4 v = src[c];
           const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int b = 0; b < 16; b++) {
-            if ((cmw >> b) & 1) s_pay[d] = (uint8_t)(wd[b >> 2] >> (8 * (b & 3)));
+            if ((ww >> b) & 1) s_pay[d] = (uint8_t)(wd[b >> 2] >> (8 * (b & 3)));
             d += ((ww >> b) & 1) + 4u * ((ow >> b) & 1);
           }
         }
       }
-      __syncwarp();  // before the escape fix-ups overwrite placeholder bytes
       cm = 0;
     }
     // direct (spilled) tiles: warp-uniform choice by the slowest lane's estimated cost (a warp runs
@@ -725,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
       // fragmented (escape-dense) block: byte by byte, destinations counted
       // as the bits go by (an opening quote adds its 4-byte length field)
       uint64_t bits = cm | openq;
-      uint32_t wdst = 4u * popc64(openq & sb::low_bits(vin)) + popc64(W & sb::low_bits(vin));
+      uint32_t wdst = 0;
       while (bits) {
         const int k = ctz64(bits);
         bits &= bits - 1;
@@ -752,14 +761,6 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
         smem_copy(smem, kOffPay + soff + wdst, local + a0, n);
       }
       cm &= ~(sb::low_bits(n) << a0);
-    }
-    if (esc_work) {
-      auto put = [&](uint32_t pos, uint8_t b) {
-        if (pay_direct) a.strings[gsbase + soff + pos] = b;
-        else s_pay[soff + pos] = b;
-      };
-      for (int k = 0; k < vin && threadIdx.x == 0; k++) put((uint32_t)k, (uint8_t)(spill_bytes >> (8 * k)));
-      sb::escape_fixups(tbyte, ec, openq, W, sw, put);
     }
     uint64_t fm = fin;
     uint32_t slot = off;

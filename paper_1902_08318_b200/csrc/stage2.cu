@@ -125,6 +125,7 @@ __device__ __forceinline__ Rng rng_of(const Stage2Args &a, const Ctrl *c) {
 // an opener's tape word; below a partial range's patch_lim it is on the host
 // already and goes to the patch list too
 __device__ __forceinline__ void put_opener(const Stage2Args &a, uint64_t at, uint64_t w) {
+  if (at >= a.tape_cap) return;  // a failing document's tape (ensure_stage2)
   a.tape[at] = w;
   if (a.range && at < a.range->patch_lim) {
     const unsigned long long k = atomicAdd(a.patch, 1ULL);
@@ -419,11 +420,11 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
             f[2] = (uint8_t)(len >> 16);
             f[3] = (uint8_t)(len >> 24);
           }
-          a.tape[ti[k]] = tape_word('"', vw.string_base + so[k] - sbase);
+          if (ti[k] < a.tape_cap) a.tape[ti[k]] = tape_word('"', vw.string_base + so[k] - sbase);
         }
       } else if (c == 't' || c == 'f' || c == 'n') {
         fail = !str::atom_ok8(aw[k], a.len, pos[k], c);
-        if (!fail) a.tape[ti[k]] = (uint64_t)c << 56;
+        if (!fail && ti[k] < a.tape_cap) a.tape[ti[k]] = (uint64_t)c << 56;
       }
       if (fail) a.tok[i] = rec[k] | 0x100u;
     }
@@ -486,11 +487,11 @@ __global__ void __launch_bounds__(256) k_numbers(Stage2Args a) {
     }
     if (r.kind == num::kNumFail) {
       atomicOr(&a.tok[i], 0x100u);
+    } else if (t + 1 >= a.tape_cap) {
+      // a failing document's tape (ensure_stage2): nothing to write
     } else if (r.kind == num::kNumSlow) {
       a.tape[t] = (uint64_t)'d' << 56;
-      uint32_t slot = atomicAdd(&ctrl->slow_count, 1u);
-      a.slow[2 * slot] = i;
-      a.slow[2 * slot + 1] = t;
+      a.slow[atomicAdd(&ctrl->slow_count, 1u)] = i;  // its tape slot is tape_idx[i]
     } else {
       a.tape[t] = (uint64_t)(r.kind == num::kNumInt ? 'l' : 'd') << 56;
       a.tape[t + 1] = r.bits;
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(128) k_slow(Stage2Args a) {
   const uint32_t n = ctrl->slow_count, k0 = a.range ? a.range->slow_lo : 0u;
   const InAt at{a.in};
   for (uint32_t k = k0 + blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    uint32_t tokn = a.slow[2 * k], slot = a.slow[2 * k + 1];
+    const uint32_t tokn = a.slow[k], slot = a.tape_idx[tokn];
     num::Decimal dec;
     uint64_t bits;
     if (num::slow_decimal(at, a.len, a.idx[tokn], dec, &bits)) a.tape[slot + 1] = bits;
@@ -893,12 +894,12 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
       if (j >= 0 && (j < (int64_t)cb)) tj = a.tape_idx[j];
       const uint64_t ow = tape_word(cl == C_OCL ? '{' : '[', (kShard ? sp.tb : 0u) + ti + 1);
       if (j >= 0) {
-        a.tape[ti] = tape_word((uint8_t)c, (kShard ? sp.tb : 0u) + tj);
+        if (ti < a.tape_cap) a.tape[ti] = tape_word((uint8_t)c, (kShard ? sp.tb : 0u) + tj);
         put_opener(a, tj, ow);
       } else if (kShard && Dd - 1 >= 0 && Dd - 1 < sp.open_n) {
         // the opener lives in an earlier shard: patched after the last exchange
         const uint64_t at = a.bound[Dd - 1] & ((1ULL << 56) - 1);
-        a.tape[ti] = tape_word((uint8_t)c, at);
+        if (ti < a.tape_cap) a.tape[ti] = tape_word((uint8_t)c, at);
         const uint32_t k = atomicAdd(&a.sum3->patch_n, 1u);
         if (k < (uint32_t)kBoundMax) {
           a.sum3->patch[2 * k] = at;
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
         if (close && have_top) {
           if (top_local) sp--;
           else far_level = -100;
-          a.tape[t] = tape_word((uint8_t)c, top_tape - rtb);
+          if (t < a.tape_cap) a.tape[t] = tape_word((uint8_t)c, top_tape - rtb);
           const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1 - rtb);
           if (!kShard || top_tape > tb) {
             put_opener(a, top_tape - tb, ow);
@@ -1619,7 +1620,7 @@ __global__ void __launch_bounds__(256) k_shard_finish(Stage2Args a, const Sum3 *
     const uint32_t n = gs[k].patch_n < (uint32_t)kBoundMax ? gs[k].patch_n : (uint32_t)kBoundMax;
     for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
       const uint64_t at = gs[k].patch[2 * e];
-      if (at > lo && at < hi) a.tape[at - lo] = gs[k].patch[2 * e + 1];
+      if (at > lo && at < hi && at - lo < a.tape_cap) a.tape[at - lo] = gs[k].patch[2 * e + 1];
     }
   }
 }

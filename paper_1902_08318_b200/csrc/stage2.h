@@ -82,11 +82,12 @@ struct Stage2Args {
   int32_t *m3;          // tree level 3 (per 4096 tokens), encoded, zeroed by init
   int16_t *mhi;         // tree levels 4..7, at offsets hi_off[0..3]
   uint64_t hi_off[4];
-  uint32_t *slow;       // slow-number token list (token, tape slot pairs)
+  uint32_t *slow;       // slow-number token list
   uint32_t *numlist;    // number tokens (compacted by k_scalars)
   uint32_t *scopebits;  // bit i: innermost container of token i is an object
   uint64_t *stk_rec;    // k_scalars look-back records (4 words per 256 tokens), zeroed
-  uint64_t *tape;       // >= 2 * cap + 3 words
+  uint64_t *tape;       // tape_cap words: writes at or past it are dropped (only a failing
+  uint64_t tape_cap;    // document's tape can be longer, engine.cu ensure_stage2)
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
   uint64_t cap_tokens;  // capacity bound on S (for grid sizing)
   int num_sms;

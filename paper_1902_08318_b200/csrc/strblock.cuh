@@ -15,8 +15,10 @@
 // failing string is the one holding the minimum position.
 //
 // Blocks with escapes decode them (escape_weights) into a weight mask W so
-// that every block uses the same popcount formulas; the decoded bytes are
-// written after the plain runs (escape_emit).
+// that every block uses the same popcount formulas, and write each escape's
+// decoded bytes IN PLACE over its own weight positions of the tile's shared
+// copy (n <= L decoded bytes over the L-byte sequence): the string payload of
+// a block is then just its weighted bytes in order, one copy, no fix-ups.
 #pragma once
 
 #include "jt_common.cuh"
@@ -58,6 +60,45 @@ JT_HD int encode(uint32_t cp, uint8_t out[4]) {
   return 4;
 }
 
+JT_HD uint64_t low_bits(int n) { return n >= 64 ? ~0ULL : ((1ULL << n) - 1); }
+
+JT_HD int hexv(uint32_t c) {
+  uint32_t d = c - '0';
+  if (d < 10u) return (int)d;
+  uint32_t l = (c | 0x20) - 'a';
+  return l < 6u ? (int)(l + 10) : -1;
+}
+
+JT_HD int hex4w(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  int a = hexv(b0), b = hexv(b1), c = hexv(b2), d = hexv(b3);
+  if ((a | b | c | d) < 0) return -1;
+  return (a << 12) | (b << 8) | (c << 4) | d;
+}
+
+// handle_escape (stringparse.cpp:73-102) on a 12-byte register window
+// starting at the backslash: w[k] holds bytes 4k..4k+3 (little endian).
+// Returns the consumed length (2, 6 or 12) and the code point, 0 if invalid.
+JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
+  const uint32_t e = (w[0] >> 8) & 0xFF;
+  if (e != 'u') {
+    uint32_t d = str::escape_char(e);
+    *cp = d;
+    return d ? 2 : 0;
+  }
+  int v = hex4w((w[0] >> 16) & 0xFF, w[0] >> 24, w[1] & 0xFF, (w[1] >> 8) & 0xFF);
+  if (v < 0) return 0;
+  if (v >= 0xD800 && v <= 0xDBFF) {
+    if (((w[1] >> 16) & 0xFF) != '\\' || (w[1] >> 24) != 'u') return 0;
+    int lo = hex4w(w[2] & 0xFF, (w[2] >> 8) & 0xFF, (w[2] >> 16) & 0xFF, w[2] >> 24);
+    if (lo < 0xDC00 || lo > 0xDFFF) return 0;
+    *cp = 0x10000u + ((((uint32_t)v - 0xD800u) << 10) | ((uint32_t)lo - 0xDC00u));
+    return 12;
+  }
+  if (v >= 0xDC00 && v <= 0xDFFF) return 0;
+  *cp = (uint32_t)v;
+  return 6;
+}
+
 // Bytes of the NEXT block covered by the last escape sequence of this block
 // (escape starts E are known for the whole block).  Only a start at bit >= 52
 // can overhang, and whether it is consumed as the low half of a surrogate
@@ -79,8 +120,8 @@ JT_HD int spill_of(int p, int L, int n, int end) {
 
 // Returns ov | spill << 8: ov = input bytes, spill = weight bytes (see
 // escape_weights) of the last escape that fall into the next block.
-template <class At>
-JT_HD int overhang_out(At at, uint64_t blk, uint64_t E) {
+template <class Byte>
+JT_HD int overhang_out(Byte byte, uint64_t E) {
   uint64_t cand = E & (~0ULL << 40);
   if (!(E >> 52)) return 0;
   // walk starts from bit 40 upward, skipping consumed lows
@@ -90,8 +131,9 @@ JT_HD int overhang_out(At at, uint64_t blk, uint64_t E) {
     uint64_t rest = cand >> p;
     if (!rest) break;
     p += ctz64(rest);
-    uint32_t cp;
-    int L = str::escape_at(at, blk + (uint64_t)p, &cp);
+    uint32_t cp, win[3];
+    byte.window12((uint64_t)p, win);
+    int L = escape_window(win, &cp);
     int n = L ? out_len(L, cp) : 0;
     if (L == 0) L = 2;  // invalid: the document fails anyway; stay bounded
     if (p + L > 64) {
@@ -166,45 +208,6 @@ JT_HD int overhang_in_scan(At at, uint64_t blk, bool in_str, uint32_t *spill_byt
   return ov | (spill << 8);
 }
 
-JT_HD uint64_t low_bits(int n) { return n >= 64 ? ~0ULL : ((1ULL << n) - 1); }
-
-JT_HD int hexv(uint32_t c) {
-  uint32_t d = c - '0';
-  if (d < 10u) return (int)d;
-  uint32_t l = (c | 0x20) - 'a';
-  return l < 6u ? (int)(l + 10) : -1;
-}
-
-JT_HD int hex4w(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
-  int a = hexv(b0), b = hexv(b1), c = hexv(b2), d = hexv(b3);
-  if ((a | b | c | d) < 0) return -1;
-  return (a << 12) | (b << 8) | (c << 4) | d;
-}
-
-// handle_escape (stringparse.cpp:73-102) on a 12-byte register window
-// starting at the backslash: w[k] holds bytes 4k..4k+3 (little endian).
-// Returns the consumed length (2, 6 or 12) and the code point, 0 if invalid.
-JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
-  const uint32_t e = (w[0] >> 8) & 0xFF;
-  if (e != 'u') {
-    uint32_t d = str::escape_char(e);
-    *cp = d;
-    return d ? 2 : 0;
-  }
-  int v = hex4w((w[0] >> 16) & 0xFF, w[0] >> 24, w[1] & 0xFF, (w[1] >> 8) & 0xFF);
-  if (v < 0) return 0;
-  if (v >= 0xD800 && v <= 0xDBFF) {
-    if (((w[1] >> 16) & 0xFF) != '\\' || (w[1] >> 24) != 'u') return 0;
-    int lo = hex4w(w[2] & 0xFF, (w[2] >> 8) & 0xFF, (w[2] >> 16) & 0xFF, w[2] >> 24);
-    if (lo < 0xDC00 || lo > 0xDFFF) return 0;
-    *cp = 0x10000u + ((((uint32_t)v - 0xD800u) << 10) | ((uint32_t)lo - 0xDC00u));
-    return 12;
-  }
-  if (v >= 0xDC00 && v <= 0xDFFF) return 0;
-  *cp = (uint32_t)v;
-  return 6;
-}
-
 // Escape starts of a block by the class of the following byte: two-byte
 // escapes whose output is that byte (\" \\ \/), two-byte escapes that are
 // translated (\b \f \n \r \t), \u escapes, and invalid ones (handle_escape,
@@ -258,11 +261,11 @@ JT_HD EscClass restrict_from(const EscClass &c, int ov_in) {
 
 // ov | spill << 8 of a block's escapes (see overhang_out).  A two-byte escape
 // at bit 63 covers the next block's byte 0, which also carries its weight.
-template <class At>
-JT_HD int escape_overhang(At at, uint64_t blk, const EscClass &c) {
+template <class Byte>
+JT_HD int escape_overhang(Byte byte, const EscClass &c) {
   if ((c.sim | c.tr) >> 63) return 1 | (1 << 8);
   if (c.bad >> 63) return 1;
-  return c.u ? overhang_out(at, blk, c.u) : 0;
+  return c.u ? overhang_out(byte, c.u) : 0;
 }
 
 // Weight mask of a block with escapes.  Every valid escape sequence [p, p+L)
@@ -276,14 +279,22 @@ JT_HD int escape_overhang(At at, uint64_t blk, const EscClass &c) {
 // minimum invalid-escape position.
 // errmask (optional) collects every invalid-escape position of the block
 // (record mode: each record needs its own first error).
-template <class Byte>
+// rewrite(k, b): the decoded byte b of an escape goes to block-relative
+// position k (its weight position; k can be >= 64 for an escape that
+// straddles into the next block — the caller drops positions past its tile).
+// \" \\ \/ decode to their own second byte and need no rewrite.
+template <class Byte, class Rewrite>
 JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const EscClass &c, int ov_in,
-                              int vin, uint64_t *err, uint64_t *errmask = nullptr) {
+                              int vin, uint64_t *err, uint64_t *errmask, Rewrite rewrite) {
   uint64_t cov = low_bits(ov_in) | c.sim | c.tr, virt = low_bits(vin);
   if (c.bad) {
     const uint64_t x = blk + (uint64_t)ctz64(c.bad);
     if (x < *err) *err = x;
     if (errmask) *errmask |= c.bad;
+  }
+  for (uint64_t t = c.tr; t; t &= t - 1) {
+    const int q = ctz64(t) + 1;
+    rewrite(q, (uint8_t)simple_decode(byte((uint64_t)q)));
   }
   uint64_t rest = c.u;
   while (rest) {
@@ -297,45 +308,15 @@ JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const E
       if (errmask) *errmask |= 1ULL << p;
     } else {
       end = p + L;
+      uint8_t b[4];
+      const int n = encode(cp, b);
+      for (int k = 0; k < n; k++) rewrite(p + k, b[k]);
       cov |= low_bits(end) & ~low_bits(p);
-      virt |= low_bits(p + out_len(L, cp)) & ~low_bits(p);
+      virt |= low_bits(p + n) & ~low_bits(p);
     }
     rest = c.u & ~low_bits(end);
   }
   return (content & ~cov) | virt;
-}
-
-// Decoded bytes that the plain-run copy did not produce: translated two-byte
-// escapes, a two-byte escape at bit 63 (its byte belongs to the next block's
-// weight, which that block does not copy), and \u escapes.  `put(w, b)`, w
-// block-relative; sw = the block's total weight.
-template <class Byte, class Put>
-JT_HD void escape_fixups(Byte byte, const EscClass &c, uint64_t openq, uint64_t W, uint32_t sw,
-                         Put put) {
-  uint64_t t = c.tr | (c.sim & (1ULL << 63));
-  while (t) {
-    const int q = ctz64(t) + 1;
-    t &= t - 1;
-    const uint32_t w = q < 64 ? 4u * popc64(openq & low_bits(q)) + popc64(W & low_bits(q)) : sw;
-    put(w, (uint8_t)simple_decode(byte((uint64_t)q)));
-  }
-  uint64_t rest = c.u;
-  while (rest) {
-    const int p = ctz64(rest);
-    uint32_t cp = 0, win[3];
-    byte.window12((uint64_t)p, win);
-    const int L = escape_window(win, &cp);
-    int end = p + 1;
-    if (L != 0) {
-      uint8_t b[4];
-      const int n = encode(cp, b);
-      const uint64_t below = low_bits(p);
-      const uint32_t w = 4u * popc64(openq & below) + popc64(W & below);
-      for (int k = 0; k < n; k++) put(w + (uint32_t)k, b[k]);
-      end = p + L;
-    }
-    rest = c.u & ~low_bits(end);
-  }
 }
 
 }  // namespace sb

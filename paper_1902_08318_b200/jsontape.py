@@ -38,7 +38,7 @@ EXPORTS = [
     "jt_b200_kernel_times", "jt_b200_copy_in", "jt_b200_distinct", "jt_b200_shard_summary_bytes",
     "jt_b200_shard_begin", "jt_b200_shard_resident", "jt_b200_shard_phase", "jt_b200_shard_finish", "jt_b200_shard_extent",
     "jt_b200_shard_download", "jt_b200_copy_in_range", "jt_b200_parse_records",
-    "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download", "jt_b200_device_records",
+    "jt_b200_records", "jt_b200_records_size", "jt_b200_records_download", "jt_b200_device_records", "jt_b200_device_bytes",
 ]
 KERNELS = ["init", "stage1", "tokens", "slow", "tree", "struct", "final"]
 
@@ -99,6 +99,8 @@ def load_library(path: str = LIB_PATH):
     L.jt_b200_shard_summary_bytes.restype = sz
     L.jt_b200_shard_begin.argtypes = [vp, sz, C.c_uint, C.c_uint, sz, sz]
     L.jt_b200_shard_resident.argtypes = [vp, sz, sz]
+    L.jt_b200_device_bytes.argtypes = [vp]
+    L.jt_b200_device_bytes.restype = sz
     L.jt_b200_shard_phase.argtypes = [vp, C.c_int, vp, vp]
     L.jt_b200_shard_finish.argtypes = [vp, vp, C.POINTER(ll)]
     L.jt_b200_shard_extent.argtypes = [vp, C.POINTER(C.c_ulonglong)]
@@ -125,6 +127,11 @@ class JtStats(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+def _bytes_at(ptr: int, n: int) -> bytes:
+    """ctypes.string_at for any size (its size argument is a C int)"""
+    return bytes((C.c_char * n).from_address(ptr)) if n else b""
+
+
 def error_name(code: int) -> str:
     return load_library().jt_error_name(code).decode()
 
@@ -148,12 +155,12 @@ class Document:
     @property
     def tape(self) -> np.ndarray:
         tp, tn = self._raw()[0:2]
-        return np.frombuffer(C.string_at(tp, tn * 8), dtype=np.uint64) if tn else np.zeros(0, np.uint64)
+        return np.frombuffer(_bytes_at(tp, tn * 8), dtype=np.uint64) if tn else np.zeros(0, np.uint64)
 
     @property
     def strings(self) -> bytes:
         sp, sn = self._raw()[2:4]
-        return C.string_at(sp, sn) if sn else b""
+        return _bytes_at(sp, sn)
 
     def distinct(self, path: bytes) -> bytes:
         """jt_document_distinct: sorted distinct scalars at a dotted key path"""
@@ -226,7 +233,7 @@ class Parser:
         if n == 0:
             return np.zeros(0, np.uint32)
         p = self._lib.jt_index_positions(self._h)
-        return np.frombuffer(C.string_at(p, 4 * n), dtype=np.uint32)
+        return np.frombuffer(_bytes_at(C.cast(p, C.c_void_p).value, 4 * n), dtype=np.uint32)
 
     def stage2(self, want_document: bool = True) -> Result:
         doc = C.c_void_p()
@@ -313,7 +320,7 @@ class Parser:
             raise RuntimeError(self.last_error())
         k = cnt.value
         rec = self.RECORD
-        arr = np.frombuffer(C.string_at(self._lib.jt_b200_records(self._h), k * rec.itemsize),
+        arr = np.frombuffer(_bytes_at(self._lib.jt_b200_records(self._h), k * rec.itemsize),
                             dtype=rec) if k else np.zeros(0, rec)
         tape = strings = None
         if download:
@@ -367,6 +374,10 @@ class Parser:
         buf = (C.c_float * 8)()
         n = self._lib.jt_b200_kernel_times(self._h, buf, 8)
         return {KERNELS[k]: buf[k] for k in range(n)}
+
+    def device_bytes(self) -> int:
+        """device memory held by this parser's arena"""
+        return int(self._lib.jt_b200_device_bytes(self._h))
 
     def last_error(self) -> str:
         return self._lib.jt_b200_last_error(self._h).decode()

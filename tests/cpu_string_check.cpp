@@ -24,7 +24,12 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
   uint64_t serr = ~0ULL;
   int ov_prev = 0;
   *ov_mismatch = 0;
+  // K1's shared copy of the current 16 KiB tile: escapes are decoded in
+  // place there (the global input is never written)
+  std::vector<uint8_t> tile(16384);
   for (uint64_t b = 0; b < nblocks; b++) {
+    if ((b * 64) % 16384 == 0)
+      for (uint64_t k = 0; k < 16384; k++) tile[k] = at(b * 64 + k);
     uint32_t w[16];
     memcpy(w, buf.data() + b * 64, 64);
     s1::Masks m;
@@ -41,7 +46,6 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content, ctl = sb::control_mask(m.P) & content;
     sb::EscClass ec{0, 0, 0, 0};
     if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? at(blk + 64) : 0u);
-    const sb::EscClass ec_full = ec;
     int ov_in = ov_prev;
     uint32_t spill_bytes = 0;
     int ov_scan = (state & 2) ? sb::overhang_in_scan(at, blk, true, &spill_bytes) : 0;
@@ -49,17 +53,25 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     int rem = (int)(len - blk);
     if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) serr = serr < len ? serr : len;
     uint64_t base = sw_total;
-    struct Byte {
+    struct Byte {  // the tile copy inside the tile, the global input past it
       const std::vector<uint8_t> *b;
+      const std::vector<uint8_t> *t;
       uint64_t blk;
-      uint32_t operator()(uint64_t k) const { return blk + k < b->size() ? (*b)[blk + k] : 0; }
+      uint32_t operator()(uint64_t k) const {
+        const uint64_t rel = blk % 16384 + k;
+        if (rel < 16384) return (*t)[rel];
+        return blk + k < b->size() ? (*b)[blk + k] : 0;
+      }
       void window12(uint64_t k, uint32_t w[3]) const {
         for (int q = 0; q < 3; q++) {
           w[q] = 0;
           for (int j = 0; j < 4; j++) w[q] |= (*this)(k + 4 * q + j) << (8 * j);
         }
       }
-    } byte{&buf, blk};
+    } byte{&buf, &tile, blk};
+    // the overhang into the next block is computed before any rewrite (K1:
+    // before the barrier that precedes escape_weights)
+    const int ov_next = E ? sb::escape_overhang(byte, ec) : 0;
     // K1's order: weight mask, block weight, runs, escape bytes, entries
     const int vin = ov_in >> 8, ov = ov_in & 0xFF;
     if (ctl) {
@@ -67,28 +79,29 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
       if (x < serr) serr = x;
     }
     if (ov) ec = sb::restrict_from(ec, ov);
+    // the first block of a tile: the bytes an escape of the previous tile
+    // spills into it (that tile drops its rewrites past its end)
+    const uint64_t local = blk % 16384;
+    if (local == 0)
+      for (int k = 0; k < vin; k++) tile[k] = (uint8_t)(spill_bytes >> (8 * k));
     uint64_t W = content;
-    if (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov) W = sb::escape_weights(byte, blk, content, ec, ov, vin, &serr);
+    auto rewrite = [&](int k, uint8_t v) {
+      if (local + (uint64_t)k < 16384) tile[local + k] = v;
+    };
+    if (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov)
+      W = sb::escape_weights(byte, blk, content, ec, ov, vin, &serr, nullptr, rewrite);
     const uint32_t we = 4u * popc64(openq) + popc64(W);
-    uint64_t cm = W & ~sb::low_bits(vin);
-    while (cm) {
-      const int a0 = ctz64(cm);
-      const uint64_t sh = cm >> a0;
-      const int nb = ~sh == 0 ? 64 - a0 : ctz64(~sh);
-      const uint64_t below = sb::low_bits(a0);
-      memcpy(out + base + 4u * popc64(openq & below) + popc64(W & below), buf.data() + blk + a0, nb);
-      cm &= ~(sb::low_bits(nb) << a0);
+    // the payload: every weighted byte of the tile copy in order, a 4-byte
+    // gap for each opening quote
+    uint32_t wdst = 0;
+    for (uint64_t bits = W | openq; bits; bits &= bits - 1) {
+      const int k = ctz64(bits);
+      if ((openq >> k) & 1) {
+        wdst += 4;
+      } else {
+        out[base + wdst++] = tile[local + k];
+      }
     }
-    // K1 tiles (16 KiB): the first block of a tile writes the bytes an
-    // escape of the previous tile spills into it; that tile's own writes
-    // past its end are dropped (staging)
-    const bool tile_first = (blk % 16384) == 0;
-    const uint64_t tile_end = (blk / 16384) * 16384 + 16384;
-    if (tile_first)
-      for (int k = 0; k < vin; k++) out[base + k] = (uint8_t)(spill_bytes >> (8 * k));
-    sb::escape_fixups(byte, ec, openq, W, we, [&](uint32_t pos, uint8_t v) {
-      if (blk + 64 < tile_end || pos < we) out[base + pos] = v;
-    });
     for (uint64_t fm = fin; fm; fm &= fm - 1) {
       const int p = ctz64(fm);
       const uint64_t below = sb::low_bits(p);
@@ -96,7 +109,7 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
       aux[n++] = (uint32_t)(base + 4u * popc64(openq & below) + popc64(W & below));
     }
     sw_total += we;
-    ov_prev = E ? sb::escape_overhang(at, blk, ec_full) : 0;
+    ov_prev = ov_next;
     state = s1::apply(f, state);
   }
   // stage 2's share: length fields from aux differences

@@ -39,7 +39,8 @@ def generate(config: int, size: int | None = None, seed: int | None = None, err:
     p = L.jtg_generate(config, SIZES[config] if size is None else size,
                        SEEDS[config] if seed is None else seed, err, C.byref(n))
     try:
-        return C.string_at(p, n.value)
+        # ctypes.string_at takes an int size (< 2 GiB)
+        return bytes((C.c_char * n.value).from_address(p)) if n.value else b""
     finally:
         L.jtg_free(p)
 
