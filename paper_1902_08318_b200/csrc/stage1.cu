@@ -65,32 +65,34 @@ __device__ __forceinline__ void smem_copy(uint8_t *base, uint32_t dst, uint32_t 
   }
 }
 
-// Block-relative bytes of the tile: shared memory inside the tile, global
-// memory past its end; window12 loads 12 bytes at once (aligned 32-bit loads
-// + funnel shifts) for the escape decoder.
+// Block-relative bytes: the tile's shared copy for the block's own 64 bytes,
+// the (never written) global input past them.  Escapes are decoded in place
+// in the shared copy, so a window reaching into the NEXT block must not read
+// it there: that block may already have rewritten an escape of its own (a
+// decoded byte can turn an invalid escape of this block into a valid one).
+// window12 loads 12 bytes at once (aligned 32-bit loads + funnel shifts).
 struct TileBytes {
   const uint8_t *s;    // shared tile copy
-  const uint8_t *g;    // global tile base
+  const uint8_t *g;    // global tile base (4-byte aligned)
   uint32_t local;      // block offset in the tile
   __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
-    uint64_t rel = local + k;
-    return rel < (uint64_t)kStage1Tile ? (uint32_t)s[rel] : (uint32_t)g[rel];
+    const uint64_t rel = local + k;
+    return k < 64 ? (uint32_t)s[rel] : (uint32_t)g[rel];
   }
   __device__ __forceinline__ void window12(uint64_t k, uint32_t w[3]) const {
     const uint32_t rel = (uint32_t)(local + k);
-    if (rel + 16 <= (uint32_t)kStage1Tile) {
+    const uint32_t sh = (rel & 3) * 8;
+    uint32_t a0, a1, a2, a3;
+    if ((k & ~3ULL) + 16 <= 64) {
       const uint32_t *s4 = (const uint32_t *)s + (rel >> 2);
-      const uint32_t sh = (rel & 3) * 8;
-      uint32_t a0 = s4[0], a1 = s4[1], a2 = s4[2], a3 = s4[3];
-      w[0] = __funnelshift_r(a0, a1, sh);
-      w[1] = __funnelshift_r(a1, a2, sh);
-      w[2] = __funnelshift_r(a2, a3, sh);
+      a0 = s4[0], a1 = s4[1], a2 = s4[2], a3 = s4[3];
     } else {
-#pragma unroll
-      for (int q = 0; q < 3; q++)
-        w[q] = (uint32_t)g[rel + 4 * q] | ((uint32_t)g[rel + 4 * q + 1] << 8) |
-               ((uint32_t)g[rel + 4 * q + 2] << 16) | ((uint32_t)g[rel + 4 * q + 3] << 24);
+      const uint32_t *g4 = (const uint32_t *)g + (rel >> 2);
+      a0 = g4[0], a1 = g4[1], a2 = g4[2], a3 = g4[3];
     }
+    w[0] = __funnelshift_r(a0, a1, sh);
+    w[1] = __funnelshift_r(a1, a2, sh);
+    w[2] = __funnelshift_r(a2, a3, sh);
   }
 };
 
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   sb::EscClass ec{0, 0, 0, 0};
   if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? tbyte(64) : 0u);
   // escapes reaching into the next block: ov | spill << 8 (strblock.cuh)
-  int ov_out = E ? sb::escape_overhang(tbyte, ec) : 0;  // reads the tile copy (nothing rewritten yet)
+  int ov_out = E ? sb::escape_overhang(tbyte, ec) : 0;
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
   // unterminated string: the reference reads the NUL padding at len (in

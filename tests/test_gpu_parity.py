@@ -149,6 +149,25 @@ def test_escape_block_and_tile_boundaries(parser, oracle):
                 check_same(parser, oracle, doc2, f"esc run {esc!r} at {boundary}-{shift}")
 
 
+def test_escape_decode_in_place_neighbours(parser, oracle):
+    """K1 decodes escapes in place in its shared copy of the tile; a block's
+    escape window reaching into the next block must see the original bytes.
+    An invalid half pair '\\uD83D\\uDC0' ending a block, followed by
+    '\\u0030' at the next block's start: decoded in place, the '0' would
+    complete the low surrogate (DC00) and hide the STRING_ERROR.  An earlier
+    escape in the same block makes the reader's decode come after the
+    neighbour's rewrite (a later loop iteration)."""
+    for blk in (64, 128, 16384 - 64, 32768 - 64):
+        for lead in (b"", b"\\u0041", b"\\u0041\\n\\u00e9"):
+            for tail in (b"\\u0030", b"\\u0063", b"\\u0046\\u0030"):
+                b = blk + 53  # the half pair occupies the block's last 11 bytes
+                mid = b"\\uD83D\\uDC0"
+                head = b'["' + b"a" * (b - 2 - len(lead) - 3) + lead + b"bbb"
+                doc = head + mid + tail + b'c", 1]'
+                assert doc.index(mid) == b and doc.index(tail, b) == blk + 64
+                check_same(parser, oracle, doc, f"half pair at {b}, lead {lead!r}, tail {tail!r}")
+
+
 def test_error_sweep(parser, oracle):
     from tools.gen import generate
     for seed in range(1, 200):

@@ -115,6 +115,12 @@ def test_string_emission(string_lib, oracle):
             for shift in range(0, 14):
                 head = b'["' + b"b" * (boundary - shift - 2)
                 docs += [head + esc + b'xyz", 1]', head + esc * 8 + b'"]']
+    # an invalid half pair ending a block before a valid escape (GPU: the
+    # neighbour's in-place decode must not be seen, test_gpu_parity)
+    for blk in (64, 16384 - 64):
+        for tail in (b"\\u0030", b"\\u0046\\u0030"):
+            b = blk + 53
+            docs.append(b'["' + b"a" * (b - 2 - 9) + b"\\u0041bbb" + b"\\uD83D\\uDC0" + tail + b'c", 1]')
     for d in docs:
         r = oracle.parse(d)
         if r.code == 1:
