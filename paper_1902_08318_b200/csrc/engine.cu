@@ -43,18 +43,38 @@ namespace {
 constexpr size_t kPad = 64;  // proj/src/indexer.h:17
 constexpr size_t kShardBoundOff = (sizeof(jt::Shard) + 255) & ~(size_t)255;
 
+// JT_CANARY=1 (the test environment's overrun check; compute-sanitizer is
+// not available on the GPU pool): every device buffer keeps >= 64 KiB past
+// what the current call asked for, filled with 0xA5 when it is sized, and
+// canary_check verifies them after the call, aborting with the buffer and
+// offset of the first byte a kernel wrote past its capacity.
+bool canary_on() {
+  static const bool v = [] {
+    const char *e = getenv("JT_CANARY");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+constexpr uint8_t kCanary = 0xA5;
+constexpr size_t kCanaryBytes = 64 << 10;
+
 struct DevBuf {
   void *p = nullptr;
   size_t cap = 0;
+  size_t req = 0;  // bytes the last ensure asked for (canary mode: [req, cap) is the canary)
   ~DevBuf() {
     if (p) cudaFree(p);
   }
   bool ensure(size_t bytes) {
-    if (bytes <= cap) return true;
+    const bool canary = canary_on();
+    if (bytes + (canary ? kCanaryBytes : 0) <= cap) {
+      if (canary) arm(bytes);
+      return true;
+    }
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
-    size_t want = std::max(bytes, (size_t)1 << 20);
+    size_t want = std::max(bytes + (canary ? kCanaryBytes : 0), (size_t)1 << 20);
     want = (want + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
     if (cudaMalloc(&p, want) != cudaSuccess) {
       cudaGetLastError();
@@ -62,7 +82,14 @@ struct DevBuf {
       return false;
     }
     cap = want;
+    if (canary) arm(bytes);
     return true;
+  }
+  void arm(size_t bytes) {
+    req = bytes;
+    cudaDeviceSynchronize();  // nothing in flight may still write the buffer
+    cudaMemset((uint8_t *)p + bytes, kCanary, cap - bytes);
+    cudaDeviceSynchronize();
   }
   template <class T>
   T *as() const {
@@ -358,6 +385,44 @@ struct DevGuard {
   }
 };
 
+__global__ void k_canary(const uint8_t *b, size_t n, unsigned long long *first) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    if (b[i] != kCanary) atomicMin(first, (unsigned long long)i);
+}
+
+// canary mode: abort if any kernel of the call `what` wrote past a buffer's
+// requested bytes
+void canary_check(jt_parser *p, const char *what) {
+  if (!canary_on()) return;
+  struct Named {
+    const char *name;
+    const DevBuf *b;
+  } bufs[] = {{"in", &p->in}, {"idx0", &p->idx[0]}, {"idx1", &p->idx[1]}, {"aux", &p->aux},
+              {"s1rec", &p->s1rec}, {"s2rec", &p->s2rec}, {"tok", &p->tok}, {"tape_idx", &p->tape_idx},
+              {"m1", &p->m1}, {"m2", &p->m2}, {"mhi", &p->mhi}, {"slow", &p->slow},
+              {"numlist", &p->numlist}, {"scopebits", &p->scopebits}, {"tile_flags", &p->tile_flags},
+              {"tape", &p->tape}, {"strings", &p->strings}, {"ctrl", &p->ctrl}, {"shard", &p->shard},
+              {"stream_words", &p->stream_words}, {"qbuf", &p->qbuf}, {"qstr", &p->qstr},
+              {"rngbuf", &p->rngbuf}, {"patchbuf", &p->patchbuf}, {"recs", &p->recs}, {"nlbuf", &p->nlbuf},
+              {"minbuf", &p->minbuf}};
+  unsigned long long *d = nullptr, h = ~0ULL;
+  cudaDeviceSynchronize();
+  if (cudaMalloc(&d, 8) != cudaSuccess) return;
+  for (const Named &x : bufs) {
+    if (!x.b->p || x.b->cap <= x.b->req) continue;
+    cudaMemcpy(d, &h, 8, cudaMemcpyHostToDevice);
+    k_canary<<<256, 256>>>((const uint8_t *)x.b->p + x.b->req, x.b->cap - x.b->req, d);
+    unsigned long long f = ~0ULL;
+    cudaMemcpy(&f, d, 8, cudaMemcpyDeviceToHost);
+    if (f != ~0ULL) {
+      fprintf(stderr, "JT_CANARY: after %s: buffer %s (%zu bytes requested) written at +%llu past its end\n",
+              what, x.name, x.b->req, f);
+      abort();
+    }
+  }
+  cudaFree(d);
+}
+
 bool cuda_ok(jt_parser *p, cudaError_t e, const char *what) {
   if (e == cudaSuccess) return true;
   p->err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -599,6 +664,7 @@ jt_error finish(jt_parser *p, int which, bool full, long long *off) {
     set_off(off, -1);
     return JT_CAPACITY;
   }
+  canary_check(p, full ? "parse" : "stage 1");
   const jt::Ctrl &c = *p->h_ctrl;
   p->last_ok = false;
   if (c.code != jt::kUtf8Error) {  // the reference refreshes the index only then
@@ -1436,6 +1502,7 @@ jt_error jt_stage2(jt_parser *p, jt_document **out, long long *error_offset) {
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
+  canary_check(p, "stage 2");
   const jt::Ctrl &c = *p->h_ctrl;
   set_off(error_offset, c.offset);
   p->last_ok = c.code == jt::kOk;
@@ -1734,6 +1801,7 @@ char *jt_b200_distinct(jt_parser *p, const char *path) {
         if (hv[k].tag == '"') hv[k].bits = ho[k];
     }
   }
+  canary_check(p, "distinct");
   for (const jt::DistinctVal &r : hv) {
     switch (r.tag) {
       case 'n': vals.insert({0, 0, {}}); break;
@@ -1789,6 +1857,7 @@ jt_error jt_minify(jt_parser *p, const char *data, size_t len, char *dst, size_t
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
+  canary_check(p, "minify");
   if (dst_len) *dst_len = total;
   return JT_OK;
 }
@@ -1821,6 +1890,7 @@ jt_error jt_compute_stats(jt_parser *p, const char *data, size_t len, jt_stats *
     set_off(error_offset, -1);
     return JT_CAPACITY;
   }
+  canary_check(p, "stats");
   jt_stats s{};
   s.integers = h[0];
   s.floats = h[1];
@@ -2099,6 +2169,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
       !cuda_ok(p, cudaStreamSynchronize(p->stream), "sync"))
     return -1;
   p->launches = 1 + 2 + 2 + 1 + n2;
+  canary_check(p, "parse_records");
   if (p->h_ctrl->string_bytes >= (1ULL << 32) || p->h_ctrl->tape_words >= (1ULL << 32)) {
     p->err = "parse_records: string buffer or tape reaches 2^32 (u32 offsets)";
     return -1;
@@ -2265,6 +2336,7 @@ jt_error jt_b200_shard_finish(jt_parser *p, const void *gathered, long long *err
     return JT_CAPACITY;
   }
   p->launches += 1;
+  canary_check(p, "shard_finish");
   const jt::Ctrl &c = *p->h_ctrl;
   set_off(error_offset, c.offset);
   if (c.code != jt::kUtf8Error) {

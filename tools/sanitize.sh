@@ -9,7 +9,7 @@ for tool in memcheck racecheck synccheck; do
   extra=""
   [ "$tool" = memcheck ] && extra="--leak-check full"
   [ "$tool" = racecheck ] && extra="--racecheck-report analysis"
-  JT_SAN_SMALL=1 timeout 1500 $CS --tool $tool $extra --print-limit 50 \
+  JT_SAN_SMALL=1 timeout 900 $CS --tool $tool $extra --print-limit 50 \
     python tools/sanitize_driver.py > "$OUT/sanitize_$tool.log" 2>&1
   echo "$tool rc=$?" >> "$OUT/sanitize_$tool.log"
   tail -4 "$OUT/sanitize_$tool.log"
