@@ -85,10 +85,13 @@ struct DevBuf {
     if (canary) arm(bytes);
     return true;
   }
+  // the canary: [req, req + kCanaryBytes) (a grow-only buffer reused for a
+  // smaller call has far more slack than that; overruns land right past req)
+  size_t canary_end() const { return std::min(cap, req + kCanaryBytes); }
   void arm(size_t bytes) {
     req = bytes;
     cudaDeviceSynchronize();  // nothing in flight may still write the buffer
-    cudaMemset((uint8_t *)p + bytes, kCanary, cap - bytes);
+    cudaMemset((uint8_t *)p + bytes, kCanary, canary_end() - bytes);
     cudaDeviceSynchronize();
   }
   template <class T>
@@ -409,9 +412,9 @@ void canary_check(jt_parser *p, const char *what) {
   cudaDeviceSynchronize();
   if (cudaMalloc(&d, 8) != cudaSuccess) return;
   for (const Named &x : bufs) {
-    if (!x.b->p || x.b->cap <= x.b->req) continue;
+    if (!x.b->p || x.b->canary_end() <= x.b->req) continue;
     cudaMemcpy(d, &h, 8, cudaMemcpyHostToDevice);
-    k_canary<<<256, 256>>>((const uint8_t *)x.b->p + x.b->req, x.b->cap - x.b->req, d);
+    k_canary<<<64, 256>>>((const uint8_t *)x.b->p + x.b->req, x.b->canary_end() - x.b->req, d);
     unsigned long long f = ~0ULL;
     cudaMemcpy(&f, d, 8, cudaMemcpyDeviceToHost);
     if (f != ~0ULL) {
@@ -491,7 +494,7 @@ bool ensure_stage2(jt_parser *p, uint64_t len, bool records = false) {
             p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
             p->slow.ensure(nums * sizeof(uint32_t)) &&
             p->numlist.ensure(nums * sizeof(uint32_t)) &&
-            p->scopebits.ensure((cap / 32 + 16) * sizeof(uint32_t)) &&
+            p->scopebits.ensure(2 * (cap / 32 + 16) * sizeof(uint32_t)) &&  // + scopeunk
             p->tape.ensure(((records ? 2 * cap : cap) + 16) * sizeof(uint64_t));
   return ok;
 }
@@ -549,6 +552,7 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
   a.slow = p->slow.as<uint32_t>();
   a.numlist = p->numlist.as<uint32_t>();
   a.scopebits = p->scopebits.as<uint32_t>();
+  a.scopeunk = a.scopebits + (cap_len + 16) / 32 + 16;
   a.stk_rec = (uint64_t *)((uint8_t *)p->s2rec.p + ((z.n3 * sizeof(int32_t) + 64 + 63) & ~(size_t)63));
   a.tape = p->tape.as<uint64_t>();
   a.tape_cap = p->tape.cap / sizeof(uint64_t);

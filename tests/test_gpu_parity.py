@@ -168,6 +168,81 @@ def test_escape_decode_in_place_neighbours(parser, oracle):
                 check_same(parser, oracle, doc, f"half pair at {b}, lead {lead!r}, tail {tail!r}")
 
 
+def _deep_doc(rng, n_items, max_excursion):
+    """Containers of both kinds nested past k_stack's 64-kind register, then
+    commas, keys and closers back at the outer levels (their container kinds
+    were evicted: k_struct looks them up)."""
+    out = []
+
+    def value(depth):
+        r = rng.random()
+        if depth < max_excursion and r < 0.08:  # a deep chain of mixed kinds
+            kinds = [rng.choice("{[") for _ in range(rng.randrange(60, max_excursion - depth + 1))]
+            for k in kinds:
+                out.append('{"k":' if k == "{" else "[")
+            out.append(str(rng.randrange(100)))
+            for k in reversed(kinds):
+                out.append("}" if k == "{" else "]")
+        elif r < (0.5 if depth < 3 else 0.25):  # subcritical branching below depth 3
+            if rng.random() < 0.5:
+                out.append("[")
+                for q in range(rng.randrange(1, 5)):
+                    if q:
+                        out.append(",")
+                    value(depth + 1)
+                out.append("]")
+            else:
+                out.append("{")
+                for q in range(rng.randrange(1, 5)):
+                    if q:
+                        out.append(",")
+                    out.append('"k%d":' % q)
+                    value(depth + 1)
+                out.append("}")
+        else:
+            out.append(rng.choice(['1', '"s"', 'true', 'null', '-2.5e3']))
+
+    out.append("{")
+    for q in range(n_items):
+        if q:
+            out.append(",")
+        out.append('"i%d":' % q)
+        value(1)
+    out.append("}")
+    return "".join(out).encode()
+
+
+def test_deep_nesting_scope(parser, oracle):
+    """Token-parallel k_struct at any depth: kinds evicted from k_stack's
+    64-kind register (scopeunk) come from the depth tree; closers check their
+    kind against the opener found.  Valid documents, kind swaps and stray
+    commas / keys after deep excursions, across 4096-token tiles."""
+    rng = random.Random(1024)
+    for trial in range(40):
+        d = _deep_doc(rng, rng.randrange(20, 400), rng.choice([70, 130, 300, 1000]))
+        check_same(parser, oracle, d, f"deep {trial}")
+        b = bytearray(d)
+        for _ in range(3):  # swap a closer's kind / turn a comma into a colon
+            k = rng.randrange(len(b))
+            while b[k] not in b"}],":
+                k = (k + 1) % len(b)
+            b[k] = {ord("}"): ord("]"), ord("]"): ord("}"), ord(","): ord(":")}[b[k]]
+            check_same(parser, oracle, bytes(b), f"deep {trial} mutated")
+    # the same through 2 and 3 emulated shards
+    from paper_1902_08318_b200.shard import LocalShards
+    for trial in range(6):
+        d = _deep_doc(rng, 300, 1000)
+        d = d + b" " * ((3 << 14) - len(d)) if len(d) < (3 << 14) else d
+        r = oracle.parse(d)
+        for G in (2, 3):
+            sh = LocalShards(d, G)
+            assert sh.run() == (r.name, r.offset), (trial, G)
+            if r.code == 0:
+                tape, strings = sh.assemble()
+                assert np.array_equal(tape, r.tape_array()) and strings == r.strings
+            sh.close()
+
+
 def test_error_sweep(parser, oracle):
     from tools.gen import generate
     for seed in range(1, 200):
