@@ -355,7 +355,11 @@ struct jt_parser {
   // NDJSON record mode (jt_b200_parse_records)
   DevBuf recs, nlbuf;
   DevBuf minbuf;  // jt_minify: look-back records, counter, total, output
-  std::vector<jt::RecordResult> h_records;
+  // host copy of the per-record results: a page-locked block from the pool
+  // (4M records = 188 MB come back at link speed, no zero fill)
+  jt::RecordResult *h_records = nullptr;
+  size_t h_records_cap = 0;  // block bytes
+  bool h_records_pinned = false;
   bool h_records_valid = false;
   const jt::RecordResult *rec_results = nullptr;
   uint64_t rec_n = 0;
@@ -494,7 +498,7 @@ bool ensure_stage2(jt_parser *p, uint64_t len, bool records = false) {
             p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
             p->slow.ensure(nums * sizeof(uint32_t)) &&
             p->numlist.ensure(nums * sizeof(uint32_t)) &&
-            p->scopebits.ensure(2 * (cap / 32 + 16) * sizeof(uint32_t)) &&  // + scopeunk
+            p->scopebits.ensure((cap / 32 + 16) * sizeof(uint32_t)) &&
             p->tape.ensure(((records ? 2 * cap : cap) + 16) * sizeof(uint64_t));
   return ok;
 }
@@ -552,7 +556,6 @@ jt::Stage2Args s2_args(jt_parser *p, uint64_t len, int which, uint64_t cap_len =
   a.slow = p->slow.as<uint32_t>();
   a.numlist = p->numlist.as<uint32_t>();
   a.scopebits = p->scopebits.as<uint32_t>();
-  a.scopeunk = a.scopebits + (cap_len + 16) / 32 + 16;
   a.stk_rec = (uint64_t *)((uint8_t *)p->s2rec.p + ((z.n3 * sizeof(int32_t) + 64 + 63) & ~(size_t)63));
   a.tape = p->tape.as<uint64_t>();
   a.tape_cap = p->tape.cap / sizeof(uint64_t);
@@ -832,7 +835,8 @@ bool ensure_ranges(jt_parser *p) {
 constexpr int kStageSlots = 4;
 bool ensure_stager(jt_parser *p, size_t bytes) {
   if (p->stage_bytes < bytes) {
-    for (void *s : p->stage_slot) cudaFreeHost(s);
+    jt_document::release(p->h_records, p->h_records_cap, p->h_records_pinned);
+  for (void *s : p->stage_slot) cudaFreeHost(s);
     p->stage_slot.clear();
     p->stage_bytes = 0;
     for (int k = 0; k < kStageSlots; k++) {
@@ -2195,19 +2199,24 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
 const void *jt_b200_records(jt_parser *p) {
   DevGuard dg_(p);
   if (!p->h_records_valid) {
-    try {
-      p->h_records.resize(p->rec_n);
-    } catch (...) {
-      return nullptr;
+    const size_t bytes = p->rec_n * sizeof(jt::RecordResult);
+    if (bytes > p->h_records_cap) {
+      jt_document::release(p->h_records, p->h_records_cap, p->h_records_pinned);
+      p->h_records = (jt::RecordResult *)PinnedPool::get().take(bytes, &p->h_records_cap, &p->h_records_pinned);
+      if (!p->h_records) {
+        p->h_records_cap = 0;
+        return nullptr;
+      }
     }
-    if (p->rec_n && cudaMemcpy(p->h_records.data(), p->rec_results, p->rec_n * sizeof(jt::RecordResult),
-                               cudaMemcpyDeviceToHost) != cudaSuccess) {
+    if (bytes && (cudaMemcpyAsync(p->h_records, p->rec_results, bytes, cudaMemcpyDeviceToHost, p->stream) !=
+                      cudaSuccess ||
+                  cudaStreamSynchronize(p->stream) != cudaSuccess)) {
       cudaGetLastError();
       return nullptr;
     }
     p->h_records_valid = true;
   }
-  return p->h_records.data();
+  return p->h_records;
 }
 
 // device pointer to the last jt_b200_parse_records results (jt_b200_record[n])

@@ -172,49 +172,19 @@ __device__ __forceinline__ uint64_t stack_apply(const StackT &t, uint64_t S) {
 
 constexpr uint64_t kV = 1ULL << 63;
 
-// How many of the register's low bits are known kinds.  Pushes beyond 64
-// evict the outermost kind, so a document more than 64 levels deep below a
-// container loses that container's kind until the container is revisited:
-// those tokens get an "unknown" bit and k_struct looks the kind up in the
-// depth tree instead.  Per token the count moves as V -> clamp(V + d, lo,
-// hi) (opener d = +1, closer d = -1, clamped to [0, 64]); clamps compose.
-struct ValidT {
-  int d, lo, hi;
-};
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : v > hi ? hi : v; }
-// t2 after t1
-__device__ __forceinline__ ValidT valid_compose(const ValidT &t2, const ValidT &t1) {
-  return ValidT{t1.d + t2.d, clampi(t1.lo + t2.d, t2.lo, t2.hi), clampi(t1.hi + t2.d, t2.lo, t2.hi)};
-}
-__device__ __forceinline__ int valid_apply(const ValidT &t, int v) { return clampi(v + t.d, t.lo, t.hi); }
-__device__ __forceinline__ uint64_t valid_pack(const ValidT &t, int vin) {
-  return (uint64_t)(uint32_t)t.d | ((uint64_t)t.lo << 32) | ((uint64_t)t.hi << 40) | ((uint64_t)vin << 48);
-}
-__device__ __forceinline__ ValidT valid_unpack(uint64_t w) {
-  return ValidT{(int)(uint32_t)w, (int)((w >> 32) & 0xFF), (int)((w >> 40) & 0xFF)};
-}
-__device__ __forceinline__ ValidT valid_shfl_up(const ValidT &t, int d) {
-  return ValidT{__shfl_up_sync(0xffffffffu, t.d, d), __shfl_up_sync(0xffffffffu, t.lo, d),
-                __shfl_up_sync(0xffffffffu, t.hi, d)};
-}
-
 // ---- K2K: container-kind stack scan -----------------------------------------
 // 4096 tokens per CTA (16 per thread); per token the kind of its innermost
-// open container (scopebits, 16 bits per thread), whether that kind is known
-// (scopeunk: 1 = evicted, see ValidT) and the max depth.
+// open container (scopebits, 16 bits per thread) and the max depth.
 constexpr int kStkTok = 16;
 
 // kPass 0: each tile's stack transfer (reduce); kPass 1: scope bits from the
 // tile's carry-in (scan).  k_stack_scan runs between them: no chained
 // look-back, so no CTA waits on another.  Records: stk_rec[4t] = P,
-// [4t+1] = k | m << 32, [4t+2] = carry-in register, [4t+3] = the tile's
-// ValidT | carry-in valid count << 48.
+// [4t+1] = k | m << 32, [4t+2] = carry-in register.
 template <int kPass>
 __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   __shared__ StackT s_wt[8];
-  __shared__ ValidT s_wv[8];
   __shared__ uint64_t s_wS[8];
-  __shared__ int s_wV[8];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const Rng R = rng_of(a, ctrl);
@@ -238,38 +208,27 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
     }
     // thread transfer over its 16 tokens (scope bits need the incoming stack)
     StackT tt{0, 0, 0};
-    ValidT tv{0, 0, 64};
     int dmax = 0;
 #pragma unroll
     for (int k = 0; k < kStkTok; k++) {
       const uint32_t c = recs[k] & 0xFF;
       if (c == '{' || c == '[') {
         tt = stack_compose(StackT{c == '{' ? 1ULL : 0ULL, 0, 1}, tt);
-        tv = valid_compose(ValidT{1, 0, 64}, tv);
         dmax = max(dmax, (int)(int16_t)(recs[k] >> 16) + 1);
       } else if (c == '}' || c == ']') {
         tt = stack_compose(StackT{0, 1, 0}, tt);
-        tv = valid_compose(ValidT{-1, 0, 64}, tv);
       }
     }
     StackT inc = tt;
-    ValidT incv = tv;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       StackT o;
       o.P = __shfl_up_sync(0xffffffffu, inc.P, d);
       o.k = __shfl_up_sync(0xffffffffu, inc.k, d);
       o.m = __shfl_up_sync(0xffffffffu, inc.m, d);
-      const ValidT ov = valid_shfl_up(incv, d);
-      if (lane >= d) {
-        inc = stack_compose(inc, o);
-        incv = valid_compose(incv, ov);
-      }
+      if (lane >= d) inc = stack_compose(inc, o);
     }
-    if (lane == 31) {
-      s_wt[warp] = inc;
-      s_wv[warp] = incv;
-    }
+    if (lane == 31) s_wt[warp] = inc;
     if (kPass == 0) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -282,14 +241,9 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
       __syncthreads();
       if (threadIdx.x == 0) {
         StackT agg = s_wt[0];
-        ValidT aggv = s_wv[0];
-        for (int k = 1; k < 8; k++) {
-          agg = stack_compose(s_wt[k], agg);
-          aggv = valid_compose(s_wv[k], aggv);
-        }
+        for (int k = 1; k < 8; k++) agg = stack_compose(s_wt[k], agg);
         a.stk_rec[4 * tile] = agg.P;
         a.stk_rec[4 * tile + 1] = (uint64_t)agg.k | ((uint64_t)agg.m << 32);
-        a.stk_rec[4 * tile + 3] = valid_pack(aggv, 0);
       }
       __syncthreads();
       continue;
@@ -298,44 +252,26 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
     ex.P = __shfl_up_sync(0xffffffffu, inc.P, 1);
     ex.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
     ex.m = __shfl_up_sync(0xffffffffu, inc.m, 1);
-    ValidT exv = valid_shfl_up(incv, 1);
-    if (lane == 0) {
-      ex = StackT{0, 0, 0};
-      exv = ValidT{0, 0, 64};
-    }
+    if (lane == 0) ex = StackT{0, 0, 0};
     __syncthreads();
     if (threadIdx.x == 0) {
       uint64_t sw = a.stk_rec[4 * tile + 2];  // carry-in (k_stack_scan)
-      int sv = (int)((a.stk_rec[4 * tile + 3] >> 48) & 0xFF);
       for (int k = 0; k < 8; k++) {
         s_wS[k] = sw;
-        s_wV[k] = sv;
         sw = stack_apply(s_wt[k], sw);
-        sv = valid_apply(s_wv[k], sv);
       }
     }
     __syncthreads();
     uint64_t St = stack_apply(ex, s_wS[warp]);
-    int V = valid_apply(exv, s_wV[warp]);
-    uint32_t bits = 0, unk = 0;
+    uint32_t bits = 0;
 #pragma unroll
     for (int k = 0; k < kStkTok; k++) {
       const uint32_t c = recs[k] & 0xFF;
       bits |= (uint32_t)(St & 1) << k;
-      // kind unknown: evicted (V == 0) while a container is open
-      unk |= (uint32_t)(V == 0 && (int)(int16_t)(recs[k] >> 16) + (int)vw.depth_base > 0) << k;
-      if (c == '{' || c == '[') {
-        St = (St << 1) | (c == '{' ? 1ULL : 0ULL);
-        V = min(V + 1, 64);
-      } else if (c == '}' || c == ']') {
-        St >>= 1;
-        V = max(V - 1, 0);
-      }
+      if (c == '{' || c == '[') St = (St << 1) | (c == '{' ? 1ULL : 0ULL);
+      else if (c == '}' || c == ']') St >>= 1;
     }
-    if (i0 < S) {
-      ((uint16_t *)a.scopebits)[i0 / kStkTok] = (uint16_t)bits;
-      ((uint16_t *)a.scopeunk)[i0 / kStkTok] = (uint16_t)unk;
-    }
+    if (i0 < S) ((uint16_t *)a.scopebits)[i0 / kStkTok] = (uint16_t)bits;
     __syncthreads();
   }
 }
@@ -345,7 +281,6 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
 constexpr int kStkScan = 1024;
 __global__ void __launch_bounds__(kStkScan) k_stack_scan(Stage2Args a) {
   __shared__ StackT s_w[kStkScan / 32];
-  __shared__ ValidT s_v[kStkScan / 32];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   const uint64_t S = rng_of(a, ctrl).hi;  // a partial range rescans all tiles below its end
@@ -358,52 +293,28 @@ __global__ void __launch_bounds__(kStkScan) k_stack_scan(Stage2Args a) {
     return StackT{a.stk_rec[4 * t], (uint32_t)km, (uint32_t)(km >> 32)};
   };
   StackT acc{0, 0, 0};
-  ValidT accv{0, 0, 64};
-  for (uint64_t t = lo; t < hi; t++) {
-    acc = stack_compose(tile_t(t), acc);
-    accv = valid_compose(valid_unpack(a.stk_rec[4 * t + 3]), accv);
-  }
+  for (uint64_t t = lo; t < hi; t++) acc = stack_compose(tile_t(t), acc);
   StackT inc = acc;
-  ValidT incv = accv;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     StackT o;
     o.P = __shfl_up_sync(0xffffffffu, inc.P, d);
     o.k = __shfl_up_sync(0xffffffffu, inc.k, d);
     o.m = __shfl_up_sync(0xffffffffu, inc.m, d);
-    const ValidT ov = valid_shfl_up(incv, d);
-    if (lane >= d) {
-      inc = stack_compose(inc, o);
-      incv = valid_compose(incv, ov);
-    }
+    if (lane >= d) inc = stack_compose(inc, o);
   }
-  if (lane == 31) {
-    s_w[warp] = inc;
-    s_v[warp] = incv;
-  }
+  if (lane == 31) s_w[warp] = inc;
   __syncthreads();
-  const View vw = view_of(a);
-  uint64_t St = vw.S0;
-  int V = vw.open_n < 64 ? vw.open_n : 64;  // kinds carried into a shard (0 unsharded)
-  for (int k = 0; k < warp; k++) {
-    St = stack_apply(s_w[k], St);
-    V = valid_apply(s_v[k], V);
-  }
+  uint64_t St = view_of(a).S0;
+  for (int k = 0; k < warp; k++) St = stack_apply(s_w[k], St);
   StackT ex;
   ex.P = __shfl_up_sync(0xffffffffu, inc.P, 1);
   ex.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
   ex.m = __shfl_up_sync(0xffffffffu, inc.m, 1);
-  const ValidT exv = valid_shfl_up(incv, 1);
-  if (lane > 0) {
-    St = stack_apply(ex, St);
-    V = valid_apply(exv, V);
-  }
+  if (lane > 0) St = stack_apply(ex, St);
   for (uint64_t t = lo; t < hi; t++) {
-    const uint64_t w3 = a.stk_rec[4 * t + 3];
     a.stk_rec[4 * t + 2] = St;
-    a.stk_rec[4 * t + 3] = (w3 & ((1ULL << 48) - 1)) | ((uint64_t)V << 48);
     St = stack_apply(tile_t(t), St);
-    V = valid_apply(valid_unpack(w3), V);
   }
 }
 
@@ -770,14 +681,7 @@ __device__ __forceinline__ int last_bit(uint32_t m) { return 31 - __clz(m); }
 
 // Deep documents (containers span many groups): one masked step per tree
 // level instead of scanning entries one at a time.
-__device__ int64_t psv_in_tile(const TileTree &T, int64_t i, int L);
 __device__ int64_t psv_tile_masked(const Stage2Args &a, const TileTree &T, int64_t i, int L) {
-  const int64_t j = psv_in_tile(T, i, L);
-  return j != -2 ? j : psv(a, T.base, L);
-}
-
-// the in-tile part of psv_tile_masked; -2: no such token in the tile
-__device__ int64_t psv_in_tile(const TileTree &T, int64_t i, int L) {
   const int64_t x = i - 1 - T.base;
   if (x >= 0) {
     const int g = (int)(x >> 4), G = g >> 4;
@@ -796,7 +700,7 @@ __device__ int64_t psv_in_tile(const TileTree &T, int64_t i, int L) {
     }
     if (h >= 0) return T.base + h * 16 + last_bit(tok_mask_le(T.tok + h * 16, L));
   }
-  return -2;
+  return psv(a, T.base, L);
 }
 
 // nearest j < i (j >= tile base) with depth_before <= L inside the tile, or
@@ -906,34 +810,9 @@ template <bool kShard, class Tree>
 __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, uint64_t S, const Tree &T,
                                               uint64_t tbase, uint64_t tend, const uint16_t *s_tr,
                                               const uint8_t *s_cls, const uint8_t *s_arr, const ShardPos &sp,
-                                              uint64_t cstart, uint8_t *s_kind) {
+                                              uint64_t cstart) {
   const int lane = threadIdx.x & 31;
   const bool bound_obj = kShard && sp.open_n > 0 && (a.bound[sp.open_n - 1] >> 56) == '{';
-  // kind (1 = object) of the container open at shard-relative level L
-  // before the shard (bound stack), 0 if none
-  auto bound_kind = [&](int L) -> uint32_t {
-    const int Ld = L + (kShard ? sp.db : 0);
-    return (kShard && Ld >= 0 && Ld < sp.open_n && (a.bound[Ld] >> 56) == '{') ? 1u : 0u;
-  };
-  // kind of token j's innermost container (j at shard-relative depth D) when
-  // k_stack's register had evicted it: the tile tree, else one depth-tree
-  // search per level and tile (s_kind caches the containers open at the
-  // tile start), else the shard's bound stack
-  auto scope_lookup = [&](int64_t j, int D) -> uint32_t {
-    const int L = D - 1;
-    if (j < (int64_t)tbase) {  // a token of the previous tile (lanes 0 / 1): no cache
-      const int64_t q = psv(a, j, L);
-      return q >= 0 ? ((a.tok[q] & 0xFF) == '{' ? 1u : 0u) : bound_kind(L);
-    }
-    int64_t o = psv_in_tile(T, j, L);
-    if (o >= 0) return (T.tok[o - tbase] & 0xFF) == '{' ? 1u : 0u;
-    const bool cache = L >= 0 && L <= kMaxDepth;
-    if (cache && s_kind[L] != 0xFF) return s_kind[L];
-    o = psv(a, (int64_t)tbase, L);
-    const uint32_t k = o >= 0 ? ((a.tok[o] & 0xFF) == '{' ? 1u : 0u) : bound_kind(L);
-    if (cache) s_kind[L] = (uint8_t)k;
-    return k;
-  };
   // tokens before the shard: their bytes, and the innermost container open
   // at the boundary for their scope bit (only read for , and key strings)
   auto rec = [&](int64_t j) -> uint32_t {
@@ -951,26 +830,16 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
     const uint32_t cl = s_cls[c];
     const bool fail = (v >> 8) & 1;
     const int D = tok_depth(v);
-    // a comma's scope (kind of the container it is in) decides its
-    // successors' arrival states: k_stack's bit, or the lookup when evicted
-    const uint32_t sw = a.scopebits[cb >> 5], uw = a.scopeunk[cb >> 5];  // bit l: token cb + l
-    uint32_t sc0 = (sw >> lane) & 1;
-    if (live && cl == C_COM && ((uw >> lane) & 1)) sc0 = scope_lookup((int64_t)i, D);
-    uint32_t sc1 = __shfl_up_sync(0xffffffffu, sc0, 1), sc2 = __shfl_up_sync(0xffffffffu, sc0, 2);
+    const uint32_t sw = a.scopebits[cb >> 5];             // bit l: token cb + l in an object
+    const uint32_t swp = cb ? a.scopebits[(cb >> 5) - 1] : (bound_obj ? ~0u : 0u);
+    const uint64_t sw2 = ((uint64_t)sw << 32) | swp;     // bit 32 + l - k: token i - k
+    const uint32_t sc0 = (sw >> lane) & 1, sc1 = (uint32_t)(sw2 >> (31 + lane)) & 1,
+                   sc2 = (uint32_t)(sw2 >> (30 + lane)) & 1;
     uint32_t cl1 = __shfl_up_sync(0xffffffffu, cl, 1), cl2 = __shfl_up_sync(0xffffffffu, cl, 2);
     if (lane < 2) {
       const int64_t gi = (int64_t)i + (kShard ? sp.before : 0);  // tokens before i in the document
       if (lane == 0) cl1 = gi >= 1 ? s_cls[rec((int64_t)i - 1) & 0xFF] : C_BAD;
       cl2 = gi >= 2 ? s_cls[rec((int64_t)i - 2) & 0xFF] : C_BAD;
-      // tokens before this warp's chunk (before the shard: the innermost
-      // container at its start)
-      auto sc_before = [&](int64_t j) -> uint32_t {
-        if (j < 0) return bound_obj ? 1u : 0u;
-        if ((a.scopeunk[j >> 5] >> (j & 31)) & 1) return scope_lookup(j, tok_depth(rec(j)));
-        return (a.scopebits[j >> 5] >> (j & 31)) & 1;
-      };
-      if (lane == 0 && cl1 == C_COM) sc1 = sc_before((int64_t)i - 1);
-      if (cl2 == C_COM && cl1 == C_STR) sc2 = sc_before((int64_t)i - 2);
     }
     const uint32_t ti = live ? a.tape_idx[i] : 0u;
     // arrival state from the two previous tokens (App. A.5)
@@ -982,8 +851,7 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
     const int Dd = D + (kShard ? sp.db : 0);  // document depth
     if ((e & kTrOpen) && Dd >= kMaxDepth && !err) err = kDepthError;
     if (mode == M_A && Dd <= 0) err = kTapeError;
-    // a closer after a value must match its container's kind: checked below
-    // against the opener the bracket search finds (kTrKind)
+    if ((e & kTrKind) && sc0 != (cl == C_OCL ? 1u : 0u)) err = kTapeError;
     const int after = (e & kTrComma) ? (sc0 ? M_K : M_V) : (int)((e >> 6) & 7);
     // bracket partners: the opener is the previous token with depth <= D - 1;
     // inside the warp by ballots (one per distinct depth), else the tile tree
@@ -1025,17 +893,7 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
       if (j == -2) j = psv_tile_masked(a, T, (int64_t)pb, D - 1);
       if (j >= 0 && (j < (int64_t)cb)) tj = a.tape_idx[j];
       const uint64_t ow = tape_word(cl == C_OCL ? '{' : '[', (kShard ? sp.tb : 0u) + ti + 1);
-      if (e & kTrKind) {  // the container's kind: its opener's byte, or the bound stack
-        const uint32_t want = cl == C_OCL ? 1u : 0u;
-        const uint32_t kind = j >= 0 ? (((j >= (int64_t)tbase ? T.tok[j - tbase] : a.tok[j]) & 0xFF) == '{' ? 1u : 0u)
-                                     : bound_kind(D - 1);
-        if (kind != want && (j >= 0 || (kShard && Dd - 1 >= 0 && Dd - 1 < sp.open_n))) {
-          err = kTapeError;
-          j = -3;  // no bracket words
-        }
-      }
-      if (j == -3) {
-      } else if (j >= 0) {
+      if (j >= 0) {
         if (ti < a.tape_cap) a.tape[ti] = tape_word((uint8_t)c, (kShard ? sp.tb : 0u) + tj);
         put_opener(a, tj, ow);
       } else if (kShard && Dd - 1 >= 0 && Dd - 1 < sp.open_n) {
@@ -1078,7 +936,6 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   __shared__ uint16_t s_tr[6 * kNCls];
   __shared__ uint8_t s_cls[256];
   __shared__ uint8_t s_arr[2 * kNCls];
-  __shared__ uint8_t s_kind[kMaxDepth + 4];  // token-parallel path: kinds of containers open at the tile start
   if (kMode <= 1) {
     s_cls[threadIdx.x] = (uint8_t)token_class(threadIdx.x);
     if (threadIdx.x < 2 * kNCls) s_arr[threadIdx.x] = (uint8_t)arrival_state(threadIdx.x >> 1, threadIdx.x & 1);
@@ -1147,7 +1004,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   // token-parallel path on few tiles (a streamed piece, a small document):
   // kSplit CTAs share a tile (each loads it for the tree, checks a quarter),
   // so the per-tile latency of 16 chunk rounds per warp is spread out
-  const uint32_t split = (kMode <= 1 && 2 * (ntiles - tile0) <= (uint64_t)gridDim.x) ? 4u : 1u;
+  const uint32_t split = (kMode <= 1 && shallow && 2 * (ntiles - tile0) <= (uint64_t)gridDim.x) ? 4u : 1u;
   for (uint64_t work = blockIdx.x; work < (ntiles - tile0) * split; work += gridDim.x) {
     const uint64_t tile = tile0 + work / split;
     const uint64_t tbase = tile * kK3Tile;
@@ -1171,8 +1028,6 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
         }
       }
       s_l1[threadIdx.x] = (int16_t)m;
-      if (kMode <= 1)
-        for (int k = threadIdx.x; k < kMaxDepth + 4; k += blockDim.x) s_kind[k] = 0xFF;
     }
     __syncthreads();
     if (threadIdx.x < 16) {
@@ -1182,10 +1037,10 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
     }
     __syncthreads();
     const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase};
-    if (kMode <= 1) {  // token-parallel grammar check (any depth: evicted kinds are looked up)
+    if (kMode <= 1 && shallow) {  // token-parallel grammar check
       const ShardPos sp{db, tb, token_base, prev0, prev1, before, open_n, is_last};
       const uint64_t part = kK3Tile / split, c0 = tbase + (work % split) * part;
-      struct_tokens<kShard>(a, ctrl, S, T, tbase, min(c0 + part, S), s_tr, s_cls, s_arr, sp, c0, s_kind);
+      struct_tokens<kShard>(a, ctrl, S, T, tbase, min(c0 + part, S), s_tr, s_cls, s_arr, sp, c0);
       __syncthreads();
       continue;
     }

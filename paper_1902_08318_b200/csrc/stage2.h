@@ -85,8 +85,7 @@ struct Stage2Args {
   uint32_t *slow;       // slow-number token list
   uint32_t *numlist;    // number tokens (compacted by k_scalars)
   uint32_t *scopebits;  // bit i: innermost container of token i is an object
-  uint32_t *scopeunk;   // bit i: that kind is not known (evicted from k_stack's 64-kind register)
-  uint64_t *stk_rec;    // k_stack per-tile records (4 words per 4096 tokens)
+  uint64_t *stk_rec;    // k_scalars look-back records (4 words per 256 tokens), zeroed
   uint64_t *tape;       // tape_cap words: writes at or past it are dropped (only a failing
   uint64_t tape_cap;    // document's tape can be longer, engine.cu ensure_stage2)
   uint8_t *strings;     // >= len + 4 * cap + 64 bytes
