@@ -12,7 +12,10 @@ constexpr int kStage1Tile = kStage1Threads * 64;  // bytes per CTA tile
 // shared-memory staging capacities per tile (larger tiles spill to direct
 // global stores)
 constexpr int kStageIdx = 4096;     // index entries
-constexpr int kStagePay = 20480;    // string-buffer bytes
+#ifndef JT_STAGE_PAY
+#define JT_STAGE_PAY 20480
+#endif
+constexpr int kStagePay = JT_STAGE_PAY;  // string-buffer bytes
 
 struct Stage1Args {
   const uint8_t *in;   // padded: readable and zero from len up to the tile end + 64
