@@ -1102,6 +1102,11 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
     int far_level = -100;  // cache of the last far container lookup
     uint32_t far_tape = 0;  // document tape index
     bool far_obj = false;
+    // The opener of the last far container this chunk closed: every later
+    // far lookup of the chunk is for a container enclosing it, so the search
+    // starts there instead of at the token (a run of closers ]]]] of a deep
+    // chain finds each opener next to the previous one's).
+    int64_t far_j = -1, hint = -1;
     int err = 0;
     bool dead = false;  // record mode: the current record already failed
     uint64_t i = i0;
@@ -1117,6 +1122,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
           mode = M_V;
           sp = 0;
           far_level = -100;
+          hint = -1;
           dead = false;
         }
         if (dead) {
@@ -1193,8 +1199,11 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
               top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
             } else {
               if (far_level != D - 1) {
-                int64_t j = deep ? psv_tile_masked(a, T, (int64_t)i, D - 1 - db)
-                                 : psv_tile(a, T, (int64_t)i, D - 1 - db);
+                const int64_t from = hint >= 0 ? hint : (int64_t)i;
+                int64_t j = from < (int64_t)tbase ? psv(a, from, D - 1 - db)
+                            : deep                ? psv_tile_masked(a, T, from, D - 1 - db)
+                                                  : psv_tile(a, T, from, D - 1 - db);
+                far_j = j;
                 if (j >= 0) {
                   far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
                   far_tape = tb + tape_of(a, j);
@@ -1215,8 +1224,12 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
           }
         }
         if (close && have_top) {
-          if (top_local) sp--;
-          else far_level = -100;
+          if (top_local) {
+            sp--;
+          } else {
+            far_level = -100;
+            hint = far_j;
+          }
           if (t < a.tape_cap) a.tape[t] = tape_word((uint8_t)c, top_tape - rtb);
           const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1 - rtb);
           if (!kShard || top_tape > tb) {
