@@ -643,6 +643,11 @@ struct TileTree {
   const int16_t *l1;    // shared: 256 group minima
   const int16_t *l2;    // shared: 16 group minima
   int64_t base;
+  // shared, per level: the opener of the container open at the tile start
+  // (psv from the tile base; kOpenUnknown = not looked up yet, kOpenNone = -1).
+  // Every chunk of a tile inside a container opened before it needs the
+  // same few of these, and each is a global depth-tree walk.
+  uint32_t *open;
 };
 
 // 16-bit masks "depth <= L" of one group from vector loads (the records
@@ -681,6 +686,18 @@ __device__ __forceinline__ int last_bit(uint32_t m) { return 31 - __clz(m); }
 
 // Deep documents (containers span many groups): one masked step per tree
 // level instead of scanning entries one at a time.
+constexpr uint32_t kOpenUnknown = 0xFFFFFFFFu, kOpenNone = 0xFFFFFFFEu;
+constexpr int kOpenLevels = kMaxDepth + 4;
+
+__device__ __forceinline__ int64_t psv_below(const Stage2Args &a, const TileTree &T, int L) {
+  if (L < 0 || L >= kOpenLevels) return psv(a, T.base, L);
+  const uint32_t c = T.open[L];
+  if (c != kOpenUnknown) return c == kOpenNone ? -1 : (int64_t)c;
+  const int64_t j = psv(a, T.base, L);
+  T.open[L] = j < 0 ? kOpenNone : (uint32_t)j;  // racing writers store the same value
+  return j;
+}
+
 __device__ int64_t psv_tile_masked(const Stage2Args &a, const TileTree &T, int64_t i, int L) {
   const int64_t x = i - 1 - T.base;
   if (x >= 0) {
@@ -700,7 +717,7 @@ __device__ int64_t psv_tile_masked(const Stage2Args &a, const TileTree &T, int64
     }
     if (h >= 0) return T.base + h * 16 + last_bit(tok_mask_le(T.tok + h * 16, L));
   }
-  return psv(a, T.base, L);
+  return psv_below(a, T, L);
 }
 
 // nearest j < i (j >= tile base) with depth_before <= L inside the tile, or
@@ -731,7 +748,7 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
       for (int k = 15; k >= 0; --k)
         if (tok_depth(T.tok[hit * 16 + k]) <= L) return T.base + hit * 16 + k;
   }
-  return psv(a, T.base, L);
+  return psv_below(a, T, L);
 }
 
 // Token-parallel grammar check for one document no deeper than 64 (the
@@ -936,6 +953,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
   __shared__ uint16_t s_tr[6 * kNCls];
   __shared__ uint8_t s_cls[256];
   __shared__ uint8_t s_arr[2 * kNCls];
+  __shared__ uint32_t s_open[kOpenLevels];
   if (kMode <= 1) {
     s_cls[threadIdx.x] = (uint8_t)token_class(threadIdx.x);
     if (threadIdx.x < 2 * kNCls) s_arr[threadIdx.x] = (uint8_t)arrival_state(threadIdx.x >> 1, threadIdx.x & 1);
@@ -1028,6 +1046,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
         }
       }
       s_l1[threadIdx.x] = (int16_t)m;
+      for (int k = threadIdx.x; k < kOpenLevels; k += blockDim.x) s_open[k] = kOpenUnknown;
     }
     __syncthreads();
     if (threadIdx.x < 16) {
@@ -1036,7 +1055,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
       s_l2[threadIdx.x] = (int16_t)m;
     }
     __syncthreads();
-    const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase};
+    const TileTree T{s_tok, s_l1, s_l2, (int64_t)tbase, s_open};
     if (kMode <= 1 && shallow) {  // token-parallel grammar check
       const ShardPos sp{db, tb, token_base, prev0, prev1, before, open_n, is_last};
       const uint64_t part = kK3Tile / split, c0 = tbase + (work % split) * part;
