@@ -75,6 +75,23 @@ JT_HD int hex4w(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return (a << 12) | (b << 8) | (c << 4) | d;
 }
 
+// The four hex digits of a \uXXXX escape held in one word (first digit in
+// byte 0) as their value, or -1 if any is not a hex digit: every byte at once
+// (bytes < 0x80, so the byte-wise range tests carry into no neighbour).
+// Same result as hex4w on every word (tests/cpu_string_check.cpp
+// jt_cpu_hex4_check, all 2^32).
+JT_HD int hex4_swar(uint32_t x) {
+  if (x & 0x80808080u) return -1;
+  const uint32_t l = x | 0x20202020u;                                           // letters lowered
+  const uint32_t dig = (x + 0x50505050u) & ~(x + 0x46464646u);                  // 0x30..0x39
+  const uint32_t let = (l + 0x1F1F1F1Fu) & ~(l + 0x19191919u);                  // 0x61..0x66
+  if (((dig | let) & 0x80808080u) != 0x80808080u) return -1;
+  const uint32_t n = (x & 0x0F0F0F0Fu) + ((let >> 7) & 0x01010101u) * 9u;       // nibble values
+  const uint32_t q = byte_perm(n, 0, 0x0123);                                   // n3 n2 n1 n0
+  const uint32_t r = q | (q >> 4);
+  return (int)((r & 0xFFu) | ((r >> 8) & 0xFF00u));
+}
+
 // handle_escape (stringparse.cpp:73-102) on a 12-byte register window
 // starting at the backslash: w[k] holds bytes 4k..4k+3 (little endian).
 // Returns the consumed length (2, 6 or 12) and the code point, 0 if invalid.
@@ -85,11 +102,11 @@ JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
     *cp = d;
     return d ? 2 : 0;
   }
-  int v = hex4w((w[0] >> 16) & 0xFF, w[0] >> 24, w[1] & 0xFF, (w[1] >> 8) & 0xFF);
+  int v = hex4_swar((w[0] >> 16) | (w[1] << 16));
   if (v < 0) return 0;
   if (v >= 0xD800 && v <= 0xDBFF) {
     if (((w[1] >> 16) & 0xFF) != '\\' || (w[1] >> 24) != 'u') return 0;
-    int lo = hex4w(w[2] & 0xFF, (w[2] >> 8) & 0xFF, (w[2] >> 16) & 0xFF, w[2] >> 24);
+    int lo = hex4_swar(w[2]);
     if (lo < 0xDC00 || lo > 0xDFFF) return 0;
     *cp = 0x10000u + ((((uint32_t)v - 0xD800u) << 10) | ((uint32_t)lo - 0xDC00u));
     return 12;

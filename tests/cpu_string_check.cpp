@@ -142,3 +142,14 @@ extern "C" int jt_cpu_atoms(const uint8_t *data, uint64_t len) {
   }
   return bad;
 }
+
+// hex4_swar (the four hex digits of a \\u escape in one word) = hex4w, the
+// byte-at-a-time decode, on words [lo, hi); returns the number of mismatches
+extern "C" uint64_t jt_cpu_hex4_check(uint64_t lo, uint64_t hi) {
+  uint64_t bad = 0;
+  for (uint64_t x = lo; x < hi; x++) {
+    const uint32_t w = (uint32_t)x;
+    if (sb::hex4_swar(w) != sb::hex4w(w & 0xFF, (w >> 8) & 0xFF, (w >> 16) & 0xFF, w >> 24)) bad++;
+  }
+  return bad;
+}

@@ -235,3 +235,14 @@ def test_atom_register_check(string_lib):
         d = b"".join(rng.choice(lits) + rng.choice(ends) for _ in range(rng.randrange(1, 8)))
         assert L.jt_cpu_atoms(d, len(d)) == 0, d
         assert L.jt_cpu_atoms(d, max(0, len(d) - rng.randrange(0, 3))) == 0, d
+
+
+def test_hex4_swar_exhaustive(string_lib):
+    """K1's word-at-a-time \\uXXXX digit decode equals the byte-at-a-time one
+    on all 2^32 four-byte words (split in chunks)"""
+    L = string_lib
+    L.jt_cpu_hex4_check.restype = C.c_uint64
+    L.jt_cpu_hex4_check.argtypes = [C.c_uint64, C.c_uint64]
+    step = 1 << 30
+    for lo in range(0, 1 << 32, step):
+        assert L.jt_cpu_hex4_check(lo, lo + step) == 0, hex(lo)
