@@ -345,11 +345,6 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   const int64_t tile = s_tile;  // tile of the range; byte offset below is global
   if (threadIdx.x == 0) {
     JT_TL(tile, 0);
-#ifdef JT_TIMELINE
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    JT_TLV(tile, 8, smid);
-#endif
   }
   const uint64_t tile_base = a.begin + (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
@@ -517,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   }
   if (lane == 31) s_warp_cnt[warp] = ci;
   __syncthreads();
+  if (threadIdx.x == 0) JT_TL(tile, 1);
   // the tile's first block also gets the decoded bytes an escape of the
   // previous tile spills into it (that tile's staging drops them)
   uint32_t spill_bytes = 0;
@@ -588,7 +584,9 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     s_warp_td[warp] = di;
     s_warp_tdf[warp] = df;
   }
+  if (lane == 0 && warp < 6) JT_TL(tile, 10 + warp);  // arrival at the barrier
   __syncthreads();
+  if (threadIdx.x == 0) JT_TL(tile, 2);
   uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
   int wdoff = 0, dtotal = 0;
 #pragma unroll
@@ -778,8 +776,10 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
       slot++;
     }
   }
+  if (threadIdx.x == 0) JT_TL(tile, 8);  // warp 0's own staging done
   if (!direct && warp == 0) resolve_counts();
   __syncthreads();
+  if (threadIdx.x == 0) JT_TL(tile, 3);
 
   const uint32_t tb = (uint32_t)tile_base;
   const uint64_t gb2 = s_base, gsb2 = s_sbase;  // published before the last barrier
@@ -846,6 +846,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     }
   }
   __syncthreads();  // length fields staged before the payload copy-out
+  if (threadIdx.x == 0) JT_TL(tile, 9);
   if (!pay_direct && stotal) {
     uint8_t *dst = a.strings + gsb2;
     const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3) < stotal
