@@ -1050,8 +1050,14 @@ __device__ __forceinline__ uint64_t idx_fin(const s1::Masks &m, uint64_t uq0, ui
 // entry state + base written).
 constexpr int kIdxCompute = kThreads;       // 256 compute threads
 constexpr int kIdxThreads = kThreads + 32;  // + look-back warp
-constexpr int kIdxMinBlocks = 3;
-constexpr int kIdxRing = 4;
+#ifndef JT_IDX_MINB
+#define JT_IDX_MINB 3
+#endif
+#ifndef JT_IDX_RING
+#define JT_IDX_RING 4
+#endif
+constexpr int kIdxMinBlocks = JT_IDX_MINB;
+constexpr int kIdxRing = JT_IDX_RING;
 
 template <int kId, int kN>
 __device__ __forceinline__ void bar_sync() {

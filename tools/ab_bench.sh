@@ -14,7 +14,8 @@ for f in gpurun_out/ab_*.json; do
 import json, sys
 try:
     d = json.load(open(sys.argv[1]))
-    print(sys.argv[1], round(d["value"], 1), "GB/s;", {k: round(v, 4) for k, v in d["kernel_ms"].items()})
+    print(sys.argv[1], round(d["value"], 1), "GB/s; jt_stage1", round(d["stage1_ms"], 4), "ms;",
+          {k: round(v, 4) for k, v in d["kernel_ms"].items()})
 except Exception as e:
     print(sys.argv[1], "failed", e)
 PY
