@@ -65,6 +65,11 @@ TABLE = (0, 1, 2, 3)  # the other configs, one short line each inside the headli
 PROFILES = {4: "r02_ncu_full_c4.json"}
 FIXTURE = os.path.join(ROOT, "tests", "golden", "large_outputs.json")
 L2_NOTE = "flushed before every step (256 MiB memset, outside the events)"
+# JT_BENCH_GLOO=1 runs the N > 1 paths with every rank on cuda:0 and gloo
+# collectives over host tensors: a functional check of the multi-GPU code on a
+# one-GPU box (ranks share the GPU; its times are not a scaling measurement)
+GLOO_TEST = os.environ.get("JT_BENCH_GLOO") == "1"
+COLL = "cpu" if GLOO_TEST else "cuda"  # device of the collectives' tensors
 
 
 def peaks():
@@ -638,7 +643,7 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
         os.environ.setdefault("MASTER_PORT", "29533")
         D.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         dist = D
-    ex = SH.nccl_exchange(dist, world)
+    ex = SH.host_exchange(dist, world) if GLOO_TEST else SH.nccl_exchange(dist, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     name, off = SH.run_shard(p, n, rank, world, ex)
@@ -666,18 +671,32 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
     dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     s1_ms = statistics.median(s.elapsed_time(m) for s, m in zip(starts, mids))
-    tot_ms = max_over_ranks(sum(step_ms), dist, "cuda")
+    tot_ms = max_over_ranks(sum(step_ms), dist, COLL)
     value = n * args.steps / (tot_ms / 1e3) / 1e9
 
-    # parity: the shards' totals equal the reference's document
-    tot = torch.tensor([ext[2], ext[4], ext[6]], dtype=torch.int64, device="cuda")
-    dist.all_reduce(tot)
+    # parity: the shards' tape and string parts, concatenated in rank order on
+    # rank 0, are the reference's document (sha256 against the fixture)
     fx = fixture(args.config, n)
     par = {"checked": False}
     if fx is not None:
-        got = [int(v) for v in tot.tolist()]
-        want = [fx["T"] - 2, fx["string_bytes"], fx["S"]]  # shard tapes exclude the two root words
-        par = {"checked": "counts", "tape_words_strings_tokens": got == want}
+        _, tape_part, _, str_part = SH.download(p)
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object((tape_part.tobytes(), str_part), parts, dst=0)
+        del tape_part, str_part
+        if rank == 0:
+            h_t, h_s = hashlib.sha256(), hashlib.sha256()
+            nt = ns = 0
+            for t, st in parts:
+                h_t.update(t)
+                h_s.update(st)
+                nt += len(t) // 8
+                ns += len(st)
+            ok = (name == fx["code"] and h_t.hexdigest() == fx["tape_sha"] and h_s.hexdigest() == fx["strings_sha"]
+                  and nt == fx["T"] and ns == fx["string_bytes"])
+            assert ok, "parity: the sharded document differs from the reference's"
+            par = {"checked": True, "against": "tests/golden/large_outputs.json (oracle/_ref)",
+                   "tape": True, "strings": True, "shards": world}
+        del parts
 
     # e2e: pinned host bytes of this shard's halo range -> device, sharded
     # parse, this shard's tape words and string bytes -> pinned host
@@ -695,7 +714,7 @@ def run_sharded(args, rank: int, world: int, local: int, torch, dist):
         e1.synchronize()
         if k >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
-    e2e_tot = max_over_ranks(sum(e2e_ms), dist, "cuda")
+    e2e_tot = max_over_ranks(sum(e2e_ms), dist, COLL)
     e2e_v = n * args.steps / (e2e_tot / 1e3) / 1e9
 
     peak, peak_src = peaks()
@@ -776,7 +795,7 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     cnt = C.c_size_t()
     assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
-    first_record, total_records = record_numbering(dist, world, rank, cnt.value, "cuda")
+    first_record, total_records = record_numbering(dist, world, rank, cnt.value, COLL)
     for _ in range(args.warmup):
         flush.zero_()
         assert p._lib.jt_b200_parse_records(p._h, n, C.byref(cnt)) == 0
@@ -794,7 +813,7 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
             ends[k].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
-    tot_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dist, "cuda")
+    tot_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(starts, ends)), dist, COLL)
     value = len(data) * args.steps / (tot_ms / 1e3) / 1e9
     # e2e: this rank's records up, results + tape + strings down
     sz = (C.c_ulonglong * 2)()
@@ -814,9 +833,34 @@ def run_records(args, rank: int, world: int, local: int, torch, dist):
         e1.synchronize()
         if k >= args.warmup:
             e2e.append(e0.elapsed_time(e1))
-    e2e_tot = max_over_ranks(sum(e2e), dist, "cuda")
+    e2e_tot = max_over_ranks(sum(e2e), dist, COLL)
+    # parity: every rank's per-record results and OK records' tape words and
+    # strings, concatenated in rank order on rank 0, digest to the reference's
     fx = fixture(3, len(data))
-    par = {"checked": "counts", "records": total_records == fx["records"]} if fx else {"checked": False}
+    par = {"checked": False}
+    if fx is not None:
+        import numpy as np
+        arr, tape, strings = p.parse_records_arrays(n)
+        ok = arr["code"] == 0
+        mine_part = (np.ascontiguousarray(arr["code"], dtype=np.int32).tobytes(),
+                     np.ascontiguousarray(arr["offset"], dtype=np.int64).tobytes(),
+                     gather(tape, arr["tape_begin"][ok], arr["tape_words"][ok]).tobytes(),
+                     gather(strings, arr["string_begin"][ok], arr["string_bytes"][ok]).tobytes())
+        del arr, tape, strings
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object(mine_part, parts, dst=0)
+        del mine_part
+        if rank == 0:
+            hs = [hashlib.sha256() for _ in range(4)]
+            for part in parts:
+                for h, b in zip(hs, part):
+                    h.update(b)
+            got = [h.hexdigest() for h in hs]
+            want = [fx["codes_sha"], fx["offsets_sha"], fx["tape_sha"], fx["strings_sha"]]
+            assert got == want and total_records == fx["records"], "parity: records differ from the reference's"
+            par = {"checked": True, "against": "tests/golden/large_outputs.json (oracle/_ref, per record)",
+                   "records": total_records, "ranks": world}
+        del parts
     if rank == 0:
         peak, peak_src = peaks()
         per_step = tot_ms / args.steps
@@ -927,11 +971,14 @@ def main():
         return run_reference(args, rank, world)
 
     import torch
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(0 if GLOO_TEST else local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if GLOO_TEST:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if args.select:
         return run_select(args, torch, local)

@@ -107,6 +107,19 @@ def nccl_exchange(dist, world: int):
     return ex
 
 
+def host_exchange(dist, world: int):
+    """The same all_gather staged through host memory (gloo: ranks that share
+    one GPU, as the multi-process tests and bench.py's JT_BENCH_GLOO mode)."""
+    import torch
+
+    def ex(phase, local):
+        h = local.cpu()
+        parts = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(parts, h)
+        return torch.cat(parts).to(local.device)
+    return ex
+
+
 class LocalShards:
     """G shards of one document on the current GPU (one parser each), phases
     in lock step on torch's current stream; the exchange is in-place: every
