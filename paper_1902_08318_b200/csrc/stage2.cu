@@ -1130,6 +1130,103 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
     bool dead = false;  // record mode: the current record already failed
     uint64_t i = i0;
     int depth_after = 0;
+    if (!kRecs) {
+      // one document / shard: every token is one lookup in the (state,
+      // class) table of the token-parallel path; only a comma or closer after
+      // a value needs its enclosing container (this chunk's stack, the scope
+      // bits, or the far search)
+      for (int k = 0; k < kK3Tok; k++) {
+        if (i >= i1) break;
+        const uint32_t v = recs[k];
+        const uint32_t c = v & 0xFF;
+        const int D = tok_depth(v) + db;  // document depth
+        const uint32_t e = s_tr[mode * kNCls + s_cls[c]];
+        err = (int)((((v >> 8) & 1) ? e >> 3 : e) & 7);
+        if ((e & kTrOpen) && D >= kMaxDepth && !err) err = kDepthError;
+        if (mode == M_A && D <= 0) err = kTapeError;
+        if (err) break;
+        depth_after = D + tok_delta(c);
+        int next = (int)((e >> 6) & 7);
+        bool close = false, top_obj = false, top_local = false;
+        uint32_t top_tape = 0;  // document tape index of the enclosing opener
+        if (e & kTrOpen) {
+          stk[sp++] = t | (c == '{' ? 0x80000000u : 0u);
+        } else if (e & (kTrComma | kTrKind)) {  // a comma or closer after a value
+          if (sp > 0) {
+            top_local = true;
+            top_tape = tb + (stk[sp - 1] & 0x7FFFFFFFu);
+            top_obj = stk[sp - 1] >> 31;
+          } else if (shallow && c == ',') {
+            top_obj = (a.scopebits[i >> 5] >> (i & 31)) & 1;  // no opener needed
+          } else {
+            if (far_level != D - 1) {
+              const int64_t from = hint >= 0 ? hint : (int64_t)i;
+              int64_t j = from < (int64_t)tbase ? psv(a, from, D - 1 - db)
+                          : deep                ? psv_tile_masked(a, T, from, D - 1 - db)
+                                                : psv_tile(a, T, from, D - 1 - db);
+              far_j = j;
+              if (j >= 0) {
+                far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';
+                far_tape = tb + tape_of(a, j);
+              } else if (!bound_at(D - 1, &far_tape, &far_obj)) {
+                err = kTapeError;
+                break;
+              }
+              far_level = D - 1;
+            }
+            top_tape = far_tape;
+            top_obj = far_obj;
+          }
+          if (e & kTrComma) {
+            next = top_obj ? M_K : M_V;
+          } else if ((c == '}') != top_obj) {
+            err = kTapeError;
+            break;
+          } else {
+            close = true;
+          }
+        } else if (e & kTrClose) {  // an empty container: the opener is the previous token
+          close = true;
+          top_obj = mode == M_OF;
+          if (sp > 0) {
+            top_local = true;
+            top_tape = tb + (stk[sp - 1] & 0x7FFFFFFFu);
+          } else {
+            top_tape = tb + t - 1;
+          }
+        }
+        if (close) {
+          if (top_local) {
+            sp--;
+          } else if (e & kTrKind) {  // the far container: later searches start at its opener
+            far_level = -100;
+            hint = far_j;
+          }
+          if (t < a.tape_cap) a.tape[t] = tape_word((uint8_t)c, top_tape);
+          const uint64_t ow = tape_word(top_obj ? '{' : '[', tb + t + 1);
+          if (!kShard || top_tape > tb) {
+            put_opener(a, top_tape - tb, ow);
+          } else {  // the opener lives in an earlier shard: patched after the last exchange
+            const uint32_t q = atomicAdd(&a.sum3->patch_n, 1u);
+            if (q < (uint32_t)kBoundMax) {
+              a.sum3->patch[2 * q] = top_tape;
+              a.sum3->patch[2 * q + 1] = ow;
+            }
+          }
+          next = M_A;
+        }
+        mode = next;
+        t += tok_width(c);
+        i++;
+      }
+      if (err) {
+        report(ctrl, token_base + i, err);
+        break;
+      }
+      if (i1 == S && is_last && !(mode == M_A && depth_after == 0))
+        report(ctrl, token_base + S, kTapeError);
+      break;
+    }
     for (int k = 0; k < kK3Tok; k++) {
       if (i >= i1) break;
       if (kRecs) {
