@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   __shared__ int s_warp_td[kWarps];
   __shared__ int s_warp_ov[kWarps];
   __shared__ unsigned long long s_base, s_sbase, s_tbase;
+  __shared__ uint32_t s_lb_claim;  // the first warp done staging resolves the tile's counts
   __shared__ long long s_dbase;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *s_in = smem;
@@ -340,7 +341,10 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   RecBlk *s_rec = (RecBlk *)(smem + kOffRec);  // record mode only
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(a.tile_counter, 1u);
+    s_lb_claim = 0;
+  }
   __syncthreads();
   const int64_t tile = s_tile;  // tile of the range; byte offset below is global
   if (threadIdx.x == 0) {
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   const Quad tot{{total, stotal, ttotal, tdepth}};
   const int64_t gt = (int64_t)a.rec_tile0 + tile;  // tile in the document's records
   const int64_t last_tile = a.last_tile == ~0ULL ? (int64_t)a.ntiles - 1 : (int64_t)a.last_tile;
-  auto resolve_counts = [&]() {  // warp 0
+  auto resolve_counts = [&]() {  // one full warp
     Quad base{{0, 0, 0, 0}};
     if (gt > 0) base = quad_lookback<kRec>(a.rec_count, gt);
     if (lane == 0) {
@@ -777,7 +781,13 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     }
   }
   if (threadIdx.x == 0) JT_TL(tile, 8);  // warp 0's own staging done
-  if (!direct && warp == 0) resolve_counts();
+  if (!direct) {
+    // the look-back waits on predecessors: the first warp done with its own
+    // staging runs it, not always warp 0
+    uint32_t won = 0;
+    if (lane == 0) won = atomicCAS(&s_lb_claim, 0u, 1u) == 0u;
+    if (__shfl_sync(0xffffffffu, won, 0)) resolve_counts();
+  }
   __syncthreads();
   if (threadIdx.x == 0) JT_TL(tile, 3);
 
