@@ -95,4 +95,17 @@ JT_HD uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t sel) {
 #endif
 }
 
+// bit select: mask bits from a, the others from b (one LOP3, LUT 0xE4; spelled
+// in PTX because the compiler otherwise re-associates the shifted operand's
+// masks into extra instructions)
+JT_HD uint32_t bit_select(uint32_t a, uint32_t b, uint32_t mask) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(mask));
+  return r;
+#else
+  return (a & mask) | (b & ~mask);
+#endif
+}
+
 }  // namespace jt

@@ -7,13 +7,16 @@
 
 namespace jt {
 
-constexpr int kStage1Threads = 256;
+#ifndef JT_K1_THREADS
+#define JT_K1_THREADS 256
+#endif
+constexpr int kStage1Threads = JT_K1_THREADS;
 constexpr int kStage1Tile = kStage1Threads * 64;  // bytes per CTA tile
 // shared-memory staging capacities per tile (larger tiles spill to direct
 // global stores)
-constexpr int kStageIdx = 4096;     // index entries
+constexpr int kStageIdx = 16 * kStage1Threads;     // index entries
 #ifndef JT_STAGE_PAY
-#define JT_STAGE_PAY 20480
+#define JT_STAGE_PAY (80 * JT_K1_THREADS)
 #endif
 constexpr int kStagePay = JT_STAGE_PAY;  // string-buffer bytes
 

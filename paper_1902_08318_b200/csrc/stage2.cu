@@ -26,6 +26,7 @@
 
 #include "lookback.cuh"
 #include "numparse.cuh"
+#include "stage1.h"
 #include "stage2.h"
 #include "strparse.cuh"
 
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
     for (int k = 0; k < 4; k++) {
       const uint32_t c = rec[k] & 0xFF;
       const bool live = i0 + k < S;
-      const uint64_t lt = ((uint64_t)pos[k] - vw.begin) >> 14;
+      const uint64_t lt = ((uint64_t)pos[k] - vw.begin) / (uint64_t)jt::kStage1Tile;
       tflag[k] = live && c == '"' && !a.records ? __ldg(a.tile_flags + lt) : 0u;
       aw[k] = live && (c == 't' || c == 'f' || c == 'n') ? at.load8(pos[k]) : 0ULL;
     }
@@ -410,8 +411,8 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
         if (!fail) {
           // stage 1 wrote the length unless the next token is in another
           // stage-1 tile or that tile spilled (kStage1Tile = 16 KiB)
-          const uint64_t lt = (p - vw.begin) >> 14;
-          if (end > a.len || lt != ((end - vw.begin) >> 14) || (a.records ? a.tile_flags[lt] : tflag[k])) {
+          const uint64_t lt = (p - vw.begin) / (uint64_t)jt::kStage1Tile;
+          if (end > a.len || lt != ((end - vw.begin) / (uint64_t)jt::kStage1Tile) || (a.records ? a.tile_flags[lt] : tflag[k])) {
             const uint32_t nx = i + 1 < Sa ? so_next : (uint32_t)vw.next_aux;
             const uint32_t len = nx - so[k] - 4;
             uint8_t *f = a.strings + so[k];
