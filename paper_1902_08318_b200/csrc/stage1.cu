@@ -79,6 +79,17 @@ struct TileBytes {
     const uint64_t rel = local + k;
     return k < 64 ? (uint32_t)s[rel] : (uint32_t)g[rel];
   }
+  // 12 bytes from block-relative k out of the shared copy only (for escapes
+  // that lie inside the block: bytes past it are loaded but not used)
+  __device__ __forceinline__ void window_own(uint64_t k, uint32_t w[3]) const {
+    const uint32_t rel = (uint32_t)(local + k);
+    const uint32_t sh = (rel & 3) * 8;
+    const uint32_t *s4 = (const uint32_t *)s + (rel >> 2);
+    const uint32_t a0 = s4[0], a1 = s4[1], a2 = s4[2], a3 = s4[3];
+    w[0] = __funnelshift_r(a0, a1, sh);
+    w[1] = __funnelshift_r(a1, a2, sh);
+    w[2] = __funnelshift_r(a2, a3, sh);
+  }
   __device__ __forceinline__ void window12(uint64_t k, uint32_t w[3]) const {
     const uint32_t rel = (uint32_t)(local + k);
     const uint32_t sh = (rel & 3) * 8;
@@ -486,10 +497,21 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   const uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content;
   const uint64_t ctl = sb::control_mask(m.P) & content;
   const TileBytes tbyte{s_in, a.in + tile_base, local};
-  sb::EscClass ec{0, 0, 0, 0};
-  if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? tbyte(64) : 0u);
-  // escapes reaching into the next block: ov | spill << 8 (strblock.cuh)
-  int ov_out = E ? sb::escape_overhang(tbyte, ec) : 0;
+  // decoded escape bytes go in place over their weight positions of the tile
+  // copy (strblock.cuh); an escape straddling the tile end leaves its spilled
+  // bytes to the next tile's first block
+  auto rewrite = [&](int k, uint8_t b) {
+    const uint32_t r = local + (uint32_t)k;
+    if (r < (uint32_t)kStage1Tile) s_in[r] = b;
+  };
+  // step 1 (strblock.cuh): classes, \u masks, failing starts; an escape
+  // reaching into the next block is decoded and written now: ov | spill << 8
+  sb::BlockEsc be;
+  be.ec = sb::EscClass{0, 0, 0, 0};
+  be.bmp = be.pair = be.ucov = be.uvirt = be.bad = 0;
+  be.ov_out = 0;
+  if (E) be = sb::block_escapes(m.P, m.qt, m.bs, E, tbyte, rewrite);
+  const int ov_out = be.ov_out;
   int ov_in = __shfl_up_sync(0xffffffffu, ov_out, 1);
   if (lane == 31) s_warp_ov[warp] = ov_out;
   // unterminated string: the reference reads the NUL padding at len (in
@@ -530,22 +552,16 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   // spills into it go to their weight positions of the tile copy (the copy
   // below takes every weighted byte in order)
   for (int k = 0; k < vin && threadIdx.x == 0; k++) s_in[k] = (uint8_t)(spill_bytes >> (8 * k));
-  // string weight mask: the plain string bytes, or for blocks with escapes
-  // the weight positions of each escape (strblock.cuh)
-  if (ov_in) ec = sb::restrict_from(ec, ov_in);
-  const bool esc_work = (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov_in) != 0;
+  // step 2: the string weight mask -- the plain string bytes, or for blocks
+  // with escapes the weight positions of each escape (strblock.cuh)
+  const bool esc_work = (E | (uint64_t)ov_in) != 0;
   uint64_t W = content;
   {
-    uint64_t serr = ctl ? blk + (uint64_t)ctz64(ctl) : ~0ULL;
-    uint64_t em = ctl;  // record mode: every error candidate of the block
-    // decoded escape bytes in place over their weight positions of the tile
-    // copy (strblock.cuh); an escape straddling the tile end leaves its
-    // spilled bytes to the next tile's first block
-    auto rewrite = [&](int k, uint8_t b) {
-      const uint32_t r = local + (uint32_t)k;
-      if (r < (uint32_t)kStage1Tile) s_in[r] = b;
-    };
-    if (esc_work) W = sb::escape_weights(tbyte, blk, content, ec, ov_in, vin, &serr, kRec ? &em : nullptr, rewrite);
+    uint64_t em = ctl;  // every error candidate of the block
+    if (esc_work) {
+      W = sb::block_weights(content, be, ov_in, vin);
+      em |= be.bad;
+    }
     if constexpr (kRec) {
       while (em) {  // the first error of each record in the block
         const int q = ctz64(em);
@@ -553,10 +569,13 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
         const uint64_t nxt = nl & ~sb::low_bits(q + 1);
         em = nxt ? em & ~sb::low_bits(ctz64(nxt) + 1) : 0;
       }
-    } else if (serr != ~0ULL) {
-      atomicMin(a.str_err, (unsigned long long)serr);
+    } else if (em) {
+      atomicMin(a.str_err, (unsigned long long)(blk + (uint64_t)ctz64(em)));
     }
   }
+  // step 3 (the escapes inside the block, decoded in place) waits until the
+  // tile's counts are published: only this block's payload copy needs it
+  const uint64_t dec_tr = be.ec.tr, dec_bmp = be.bmp, dec_pair = be.pair;
   const uint32_t sw = 4u * popc64(openq) + popc64(W);
   uint32_t si = sw;
 #pragma unroll
@@ -697,6 +716,9 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     // the weighted bytes in order (escapes already decoded in place; the
     // first vin bits are the spill of the previous block's escape)
     uint64_t cm = W;
+    if (dec_tr | dec_bmp | dec_pair)
+      sb::decode_in_place(dec_tr, dec_bmp, dec_pair,
+                          [&](uint64_t k, uint32_t w3[3]) { tbyte.window_own(k, w3); }, tbyte, rewrite);
     if (!pay_direct) {
       // each lane copies its own block into the staging buffer, bytes in
       // order with a running destination (+1 per weight bit, +4 per opening

@@ -1162,9 +1162,21 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
           } else {
             if (far_level != D - 1) {
               const int64_t from = hint >= 0 ? hint : (int64_t)i;
-              int64_t j = from < (int64_t)tbase ? psv(a, from, D - 1 - db)
-                          : deep                ? psv_tile_masked(a, T, from, D - 1 - db)
-                                                : psv_tile(a, T, from, D - 1 - db);
+              const int L = D - 1 - db;
+              // after a far close the next enclosing opener usually sits right
+              // before the last one ("[[[" or "{ key : {" of a deep chain):
+              // probe the three tokens before it, then search
+              int64_t j = -2;
+              if (hint >= 0 && from - 3 >= (int64_t)tbase) {
+                const uint32_t *q = s_tok + (from - (int64_t)tbase);
+                if (tok_depth(q[-1]) <= L) j = from - 1;
+                else if (tok_depth(q[-2]) <= L) j = from - 2;
+                else if (tok_depth(q[-3]) <= L) j = from - 3;
+              }
+              if (j == -2)
+                j = from < (int64_t)tbase ? psv(a, from, L)
+                    : deep                ? psv_tile_masked(a, T, from, L)
+                                          : psv_tile(a, T, from, L);
               far_j = j;
               if (j >= 0) {
                 far_obj = ((j >= (int64_t)tbase ? s_tok[j - tbase] : a.tok[j]) & 0xFF) == '{';

@@ -14,8 +14,8 @@
 // escape, unterminated string) are reported as byte positions; the first
 // failing string is the one holding the minimum position.
 //
-// Blocks with escapes decode them (escape_weights) into a weight mask W so
-// that every block uses the same popcount formulas, and write each escape's
+// Blocks with escapes turn them into a weight mask W (block_escapes /
+// block_weights) so that every block uses the same popcount formulas, and write each escape's
 // decoded bytes IN PLACE over its own weight positions of the tile's shared
 // copy (n <= L decoded bytes over the L-byte sequence): the string payload of
 // a block is then just its weighted bytes in order, one copy, no fix-ups.
@@ -116,17 +116,12 @@ JT_HD int escape_window(const uint32_t w[3], uint32_t *cp) {
   return 6;
 }
 
-// Bytes of the NEXT block covered by the last escape sequence of this block
-// (escape starts E are known for the whole block).  Only a start at bit >= 52
-// can overhang, and whether it is consumed as the low half of a surrogate
-// pair depends on starts >= 40, so the answer does not depend on the
-// block's own incoming overhang (<= 11 bytes).
 // Decoded length of a valid escape (L = 2, 6 or 12 input bytes).
 JT_HD int out_len(int L, uint32_t cp) {
   return L == 2 ? 1 : cp < 0x80 ? 1 : cp < 0x800 ? 2 : cp < 0x10000 ? 3 : 4;
 }
 
-// Weight positions of a valid escape at p (see escape_weights): a two-byte
+// Weight positions of a valid escape at p (see block_escapes): a two-byte
 // escape weighs on its second byte [p+1, p+2), so that \\ \" \/ need no
 // rewrite; a \u escape on [p, p+n).  Returns how many of them are >= end.
 JT_HD int spill_of(int p, int L, int n, int end) {
@@ -135,35 +130,8 @@ JT_HD int spill_of(int p, int L, int n, int end) {
   return b > end ? b - (a > end ? a : end) : 0;
 }
 
-// Returns ov | spill << 8: ov = input bytes, spill = weight bytes (see
-// escape_weights) of the last escape that fall into the next block.
-template <class Byte>
-JT_HD int overhang_out(Byte byte, uint64_t E) {
-  uint64_t cand = E & (~0ULL << 40);
-  if (!(E >> 52)) return 0;
-  // walk starts from bit 40 upward, skipping consumed lows
-  int p = 40;
-  int ov = 0, spill = 0;
-  while (p < 64) {
-    uint64_t rest = cand >> p;
-    if (!rest) break;
-    p += ctz64(rest);
-    uint32_t cp, win[3];
-    byte.window12((uint64_t)p, win);
-    int L = escape_window(win, &cp);
-    int n = L ? out_len(L, cp) : 0;
-    if (L == 0) L = 2;  // invalid: the document fails anyway; stay bounded
-    if (p + L > 64) {
-      ov = p + L - 64;
-      spill = spill_of(p, L, n, 64);
-    }
-    p += L;
-  }
-  return ov | (spill << 8);
-}
-
 // Overhang into block `blk` from the bytes before it (ov | spill << 8 as
-// overhang_out; *spill_bytes = the spilled decoded bytes, little endian),
+// block_escapes' ov_out; *spill_bytes = the spilled decoded bytes, little endian),
 // computed without the previous block's masks: odd_in = parity of the backslash run ending at
 // blk-1, in_str = blk-1 is inside a string.  Used for a tile's first block.
 template <class At>
@@ -271,49 +239,85 @@ JT_HD EscClass classify_escapes(const uint64_t P[8], uint64_t qt, uint64_t bs, u
   return EscClass{E & nS, E & nT, E & nU, E & ~(nS | nT | nU)};
 }
 
-JT_HD EscClass restrict_from(const EscClass &c, int ov_in) {
-  const uint64_t k = ~low_bits(ov_in);
-  return EscClass{c.sim & k, c.tr & k, c.u & k, c.bad & k};
+// ---- \u escapes decided from the bit planes ---------------------------------
+// handle_escape's \uXXXX checks (stringparse.cpp:86-101) for every escape
+// start of a block at once: hex-digit, 'D', "8..B" and "C..F" byte classes
+// from the planes, shifted onto the start's bit.  A start p is decided here
+// when every byte it depends on lies in the block (p + 5 <= 63, for the high
+// half of a pair p + 11 <= 63); the rest (`und`) are decoded one at a time
+// from the bytes (decode_und).  In a prefix without errors the set of valid
+// escapes equals the sequential walk's: a start is skipped by the walk iff it
+// is the low half of a valid pair (the only backslash a valid escape covers),
+// which is `pair << 6` here; after the first error only the minimum matters.
+struct UClass {
+  uint64_t bmp, pair;  // valid \uXXXX (no surrogate) / \uD8..\uDC.. pairs inside the block
+  uint64_t n1, n3;     // bmp escapes that decode to 1 byte / to 3 bytes (else 2)
+  uint64_t bad;        // failing starts: a non-hex digit, a lone surrogate half
+  uint64_t und;        // starts that need bytes of the next block
+};
+
+JT_HD UClass classify_u(const uint64_t P[8], uint64_t U) {
+  const uint64_t n7 = ~P[7], n6 = ~P[6], n4 = ~P[4], n3 = ~P[3], n2 = ~P[2], n1 = ~P[1], n0 = ~P[0];
+  const uint64_t dig = n7 & n6 & P[5] & P[4] & (n3 | (n2 & n1));               // 0..9
+  const uint64_t let = n7 & P[6] & n4 & n3 & (P[2] | P[1] | P[0]) & ~(P[2] & P[1] & P[0]);  // A..F a..f
+  const uint64_t hexd = dig | let;
+  const uint64_t zero = dig & n3 & n2 & n1 & n0;                                // 0
+  const uint64_t lt8 = dig & n3;                                                // 0..7
+  const uint64_t isD = let & P[2] & n1 & n0;                                    // D d
+  const uint64_t c8B = (dig & P[3]) | (let & n2 & (P[1] ^ P[0]));               // 8 9 A B a b
+  const uint64_t cCF = let & (P[2] | (P[1] & P[0]));                            // C..F c..f
+  const uint64_t h4 = (hexd >> 2) & (hexd >> 3) & (hexd >> 4) & (hexd >> 5);
+  const uint64_t kDec6 = (1ULL << 59) - 1, kDec12 = (1ULL << 53) - 1;
+  const uint64_t Ud = U & kDec6;
+  const uint64_t ok = Ud & h4;
+  const uint64_t d0D = isD >> 2;
+  const uint64_t hiS = ok & d0D & (c8B >> 3), loS = ok & d0D & (cCF >> 3);
+  UClass r;
+  r.bmp = ok & ~(hiS | loS);
+  r.pair = hiS & (loS >> 6) & kDec12;
+  r.bad = (Ud & ~h4) | (hiS & kDec12 & ~(loS >> 6)) | (loS & ~(r.pair << 6));
+  r.und = (U & ~kDec6) | (hiS & ~kDec12);
+  const uint64_t t = (zero >> 2) & (lt8 >> 3);  // code point < 0x800
+  r.n3 = r.bmp & ~t;
+  r.n1 = r.bmp & t & (zero >> 3) & (lt8 >> 4);  // < 0x80
+  return r;
 }
 
-// ov | spill << 8 of a block's escapes (see overhang_out).  A two-byte escape
-// at bit 63 covers the next block's byte 0, which also carries its weight.
+// bytes the decided escapes cover / the weight positions of their decoded
+// bytes (the first n bytes of each sequence, see escape_weights)
+JT_HD void u_masks(const UClass &u, uint64_t *cov, uint64_t *virt) {
+  const uint64_t a = u.bmp | u.pair;
+  const uint64_t h = a | (u.pair << 6);  // six-byte halves
+  const uint64_t s2 = h | (h << 1);
+  const uint64_t s4 = s2 | (s2 << 2);
+  *cov = s4 | (s2 << 4);
+  *virt = a | ((a & ~u.n1) << 1) | ((u.n3 | u.pair) << 2) | (u.pair << 3);
+}
+
+// four hex digits known to be valid (first digit in byte 0) -> value
+JT_HD uint32_t hex4_value(uint32_t x) {
+  const uint32_t n = (x & 0x0F0F0F0Fu) + ((x >> 6) & 0x01010101u) * 9u;
+  const uint32_t q = byte_perm(n, 0, 0x0123);
+  const uint32_t r = q | (q >> 4);
+  return (r & 0xFFu) | ((r >> 8) & 0xFF00u);
+}
+
+// code point of a decided escape from its 12-byte window (w[k] = bytes
+// 4k..4k+3 from the backslash); is_pair: the low half follows at byte 6
+JT_HD uint32_t decided_cp(const uint32_t w[3], bool is_pair) {
+  const uint32_t v = hex4_value((w[0] >> 16) | (w[1] << 16));
+  if (!is_pair) return v;
+  const uint32_t lo = hex4_value(w[2]);
+  return 0x10000u + (((v - 0xD800u) << 10) | (lo - 0xDC00u));
+}
+
+// The undecided starts in order (each reads bytes of the next block through
+// `byte`): failing ones go to *bad; returns p | L << 6 | cp << 10 of the last
+// valid one (it reaches past the block: at most one in a block), 0 if none.
 template <class Byte>
-JT_HD int escape_overhang(Byte byte, const EscClass &c) {
-  if ((c.sim | c.tr) >> 63) return 1 | (1 << 8);
-  if (c.bad >> 63) return 1;
-  return c.u ? overhang_out(byte, c.u) : 0;
-}
-
-// Weight mask of a block with escapes.  Every valid escape sequence [p, p+L)
-// carries the weight of its decoded bytes on n of its own positions: the
-// second byte of a two-byte escape (so that \\ \" \/ are already right when
-// the plain runs are copied), the first n bytes of a \u escape; its other
-// bytes weigh 0.  Then every block's string-buffer prefix at bit x is
-// 4*popc(openq below x) + popc(W below x), the same formula as for blocks
-// without escapes.  ov_in / vin = input / weight bytes of an escape begun in
-// the previous block; c must be restrict_from(ov_in).  *err gets the
-// minimum invalid-escape position.
-// errmask (optional) collects every invalid-escape position of the block
-// (record mode: each record needs its own first error).
-// rewrite(k, b): the decoded byte b of an escape goes to block-relative
-// position k (its weight position; k can be >= 64 for an escape that
-// straddles into the next block — the caller drops positions past its tile).
-// \" \\ \/ decode to their own second byte and need no rewrite.
-template <class Byte, class Rewrite>
-JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const EscClass &c, int ov_in,
-                              int vin, uint64_t *err, uint64_t *errmask, Rewrite rewrite) {
-  uint64_t cov = low_bits(ov_in) | c.sim | c.tr, virt = low_bits(vin);
-  if (c.bad) {
-    const uint64_t x = blk + (uint64_t)ctz64(c.bad);
-    if (x < *err) *err = x;
-    if (errmask) *errmask |= c.bad;
-  }
-  for (uint64_t t = c.tr; t; t &= t - 1) {
-    const int q = ctz64(t) + 1;
-    rewrite(q, (uint8_t)simple_decode(byte((uint64_t)q)));
-  }
-  uint64_t rest = c.u;
+JT_HD uint32_t decode_und(Byte byte, uint64_t und, uint64_t *bad) {
+  uint32_t res = 0;
+  uint64_t rest = und;
   while (rest) {
     const int p = ctz64(rest);
     uint32_t cp = 0, win[3];
@@ -321,19 +325,123 @@ JT_HD uint64_t escape_weights(Byte byte, uint64_t blk, uint64_t content, const E
     const int L = escape_window(win, &cp);
     int end = p + 1;
     if (L == 0) {
-      if (blk + (uint64_t)p < *err) *err = blk + (uint64_t)p;
-      if (errmask) *errmask |= 1ULL << p;
+      *bad |= 1ULL << p;
     } else {
       end = p + L;
-      uint8_t b[4];
-      const int n = encode(cp, b);
-      for (int k = 0; k < n; k++) rewrite(p + k, b[k]);
-      cov |= low_bits(end) & ~low_bits(p);
-      virt |= low_bits(p + n) & ~low_bits(p);
+      res = (uint32_t)p | ((uint32_t)L << 6) | (cp << 10);
     }
-    rest = c.u & ~low_bits(end);
+    rest = und & ~low_bits(end);
   }
-  return (content & ~cov) | virt;
+  return res;
+}
+
+// \b \f \n \r \t -> the control byte (a 16 x 4-bit table indexed by bits 1..4
+// of the letter: b 1, f 3, n 7, r 9, t 10)
+JT_HD uint32_t translate_letter(uint32_t c) {
+  const uint32_t k = (c >> 1) & 15;
+  const uint32_t lo = 0xA000C080u;  // nibble 1 = 8 (\b), 3 = C (\f), 7 = A (\n)
+  const uint32_t hi = 0x000009D0u;  // nibble 9 = D (\r), 10 = 9 (\t)
+  return (((k & 8) ? hi : lo) >> (4 * (k & 7))) & 15;
+}
+
+JT_HD EscClass restrict_from(const EscClass &c, int ov_in) {
+  const uint64_t k = ~low_bits(ov_in);
+  return EscClass{c.sim & k, c.tr & k, c.u & k, c.bad & k};
+}
+
+// ---- a block's escapes in three steps ---------------------------------------
+// Every valid escape sequence [p, p+L) carries the weight of its decoded bytes
+// on n of its own positions: the second byte of a two-byte escape (so that
+// \\ \" \/ are already right when the weighted bytes are copied), the first n
+// bytes of a \u escape; its other bytes weigh 0.  Then every block's
+// string-buffer prefix at bit x is 4*popc(openq below x) + popc(W below x),
+// the same formula as for blocks without escapes.
+//
+// 1. block_escapes (needs nothing from other blocks): the escape classes,
+//    the coverage / weight masks of the \u escapes, the failing starts, and
+//    ov | spill << 8 = input bytes / weight bytes of the last escape that fall
+//    into the NEXT block.  An escape that reaches past the block is decoded
+//    here and its bytes go to their weight positions right away (rewrite(k, b)
+//    with k possibly >= 64: the next block copies them as its first `spill`
+//    weighted bytes; the caller drops positions past its tile).
+// 2. block_weights, once ov_in / vin (the previous block's ov / spill) are
+//    known: the weight mask W and the failing starts outside the overhang.
+// 3. decode_in_place, any time before the block's weighted bytes are copied:
+//    the decoded bytes of the escapes inside the block over their weight
+//    positions (\" \\ \/ decode to their own second byte: nothing to do).
+struct BlockEsc {
+  EscClass ec;
+  uint64_t bmp, pair;    // decided \u escapes (see UClass)
+  uint64_t ucov, uvirt;  // bytes covered by / weight positions of the block's \u escapes
+  uint64_t bad;          // failing escape starts
+  int ov_out;
+};
+
+template <class Byte, class Rewrite>
+JT_HD BlockEsc block_escapes(const uint64_t P[8], uint64_t qt, uint64_t bs, uint64_t E, Byte byte,
+                             Rewrite rewrite) {
+  BlockEsc r;
+  r.ec = classify_escapes(P, qt, bs, E, (E >> 63) ? byte(64) : 0u);
+  r.bmp = r.pair = r.ucov = r.uvirt = 0;
+  r.bad = r.ec.bad;
+  r.ov_out = 0;
+  if (r.ec.u) {
+    const UClass uc = classify_u(P, r.ec.u);
+    u_masks(uc, &r.ucov, &r.uvirt);
+    r.bmp = uc.bmp;
+    r.pair = uc.pair;
+    r.bad |= uc.bad;
+    if (uc.und) {
+      const uint32_t res = decode_und(byte, uc.und, &r.bad);
+      if (res) {
+        const int p = (int)(res & 63), L = (int)((res >> 6) & 15);
+        uint8_t b[4];
+        const int n = encode(res >> 10, b);
+        for (int k = 0; k < n; k++) rewrite(p + k, b[k]);
+        if (p + L > 64) r.ov_out = (p + L - 64) | (spill_of(p, L, n, 64) << 8);
+        r.ucov |= low_bits(p + L) & ~low_bits(p);
+        r.uvirt |= low_bits(p + n) & ~low_bits(p);
+      }
+    }
+  }
+  // a two-byte escape at bit 63 covers the next block's byte 0, which also
+  // carries its weight
+  if ((r.ec.sim | r.ec.tr) >> 63) {
+    r.ov_out = 1 | (1 << 8);
+    if (r.ec.tr >> 63) rewrite(64, (uint8_t)translate_letter(byte(64)));
+  } else if (r.ec.bad >> 63) {
+    r.ov_out = 1;
+  }
+  return r;
+}
+
+// ov_in / vin = input / weight bytes of an escape begun in the previous block
+JT_HD uint64_t block_weights(uint64_t content, BlockEsc &e, int ov_in, int vin) {
+  const uint64_t over = low_bits(ov_in);
+  e.bad &= ~over;
+  e.bmp &= ~over;
+  e.pair &= ~over;
+  e.ec.tr &= ~over;
+  return (content & ~(over | e.ec.sim | e.ec.tr | e.ucov)) | low_bits(vin) | e.uvirt;
+}
+
+// window(p, w): 12 bytes from block-relative p (only bytes inside the block
+// are used); byte(q): block-relative byte q < 64
+template <class Window, class Byte, class Rewrite>
+JT_HD void decode_in_place(uint64_t tr, uint64_t bmp, uint64_t pair, Window window, Byte byte,
+                           Rewrite rewrite) {
+  for (uint64_t t = tr & ~(1ULL << 63); t; t &= t - 1) {
+    const int q = ctz64(t) + 1;
+    rewrite(q, (uint8_t)translate_letter(byte((uint64_t)q)));
+  }
+  for (uint64_t r = bmp | pair; r; r &= r - 1) {
+    const int p = ctz64(r);
+    uint32_t win[3];
+    window((uint64_t)p, win);
+    uint8_t b[4];
+    const int n = encode(decided_cp(win, (pair >> p) & 1), b);
+    for (int k = 0; k < n; k++) rewrite(p + k, b[k]);
+  }
 }
 
 }  // namespace sb

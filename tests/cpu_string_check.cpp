@@ -44,8 +44,6 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     uint64_t fin = s1::final_mask(m, esc0, tog, state, valid);
     uint64_t openq = uq & instr & valid, content = instr & ~openq & valid;
     uint64_t E = s1::unescaped_backslash(m.bs, state & 1) & content, ctl = sb::control_mask(m.P) & content;
-    sb::EscClass ec{0, 0, 0, 0};
-    if (E) ec = sb::classify_escapes(m.P, m.qt, m.bs, E, (E >> 63) ? at(blk + 64) : 0u);
     int ov_in = ov_prev;
     uint32_t spill_bytes = 0;
     int ov_scan = (state & 2) ? sb::overhang_in_scan(at, blk, true, &spill_bytes) : 0;
@@ -53,13 +51,13 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
     int rem = (int)(len - blk);
     if (rem > 0 && rem <= 64 && ((instr >> (rem - 1)) & 1)) serr = serr < len ? serr : len;
     uint64_t base = sw_total;
-    struct Byte {  // the tile copy inside the tile, the global input past it
+    struct Byte {  // the tile copy for the block's own bytes, the global input past them
       const std::vector<uint8_t> *b;
       const std::vector<uint8_t> *t;
       uint64_t blk;
       uint32_t operator()(uint64_t k) const {
         const uint64_t rel = blk % 16384 + k;
-        if (rel < 16384) return (*t)[rel];
+        if (k < 64 && rel < 16384) return (*t)[rel];
         return blk + k < b->size() ? (*b)[blk + k] : 0;
       }
       void window12(uint64_t k, uint32_t w[3]) const {
@@ -69,27 +67,36 @@ extern "C" int jt_cpu_strings(const uint8_t *data, uint64_t len, uint8_t *out, u
         }
       }
     } byte{&buf, &tile, blk};
-    // the overhang into the next block is computed before any rewrite (K1:
-    // before the barrier that precedes escape_weights)
-    const int ov_next = E ? sb::escape_overhang(byte, ec) : 0;
-    // K1's order: weight mask, block weight, runs, escape bytes, entries
+    const uint64_t local = blk % 16384;
+    auto rewrite = [&](int k, uint8_t v) {
+      if (local + (uint64_t)k < 16384) tile[local + k] = v;
+    };
+    // K1's order: step 1 before the previous block's overhang is known
+    // (an escape reaching past the block is decoded and written here), ...
+    sb::BlockEsc be{};
+    if (E) be = sb::block_escapes(m.P, m.qt, m.bs, E, byte, rewrite);
+    const int ov_next = E ? be.ov_out : 0;
     const int vin = ov_in >> 8, ov = ov_in & 0xFF;
     if (ctl) {
       uint64_t x = blk + (uint64_t)ctz64(ctl);
       if (x < serr) serr = x;
     }
-    if (ov) ec = sb::restrict_from(ec, ov);
     // the first block of a tile: the bytes an escape of the previous tile
     // spills into it (that tile drops its rewrites past its end)
-    const uint64_t local = blk % 16384;
     if (local == 0)
       for (int k = 0; k < vin; k++) tile[k] = (uint8_t)(spill_bytes >> (8 * k));
+    // ... step 2 with it: weights and errors ...
     uint64_t W = content;
-    auto rewrite = [&](int k, uint8_t v) {
-      if (local + (uint64_t)k < 16384) tile[local + k] = v;
-    };
-    if (ec.sim | ec.tr | ec.u | ec.bad | (uint64_t)ov)
-      W = sb::escape_weights(byte, blk, content, ec, ov, vin, &serr, nullptr, rewrite);
+    if (E || ov) {
+      W = sb::block_weights(content, be, ov, vin);
+      if (be.bad) {
+        const uint64_t x = blk + (uint64_t)ctz64(be.bad);
+        if (x < serr) serr = x;
+      }
+      // ... step 3 before the payload copy: the escapes inside the block
+      sb::decode_in_place(be.ec.tr, be.bmp, be.pair,
+                          [&](uint64_t k, uint32_t w[3]) { byte.window12(k, w); }, byte, rewrite);
+    }
     const uint32_t we = 4u * popc64(openq) + popc64(W);
     // the payload: every weighted byte of the tile copy in order, a 4-byte
     // gap for each opening quote

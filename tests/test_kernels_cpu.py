@@ -138,6 +138,58 @@ def test_string_emission(string_lib, oracle):
             assert se.value == r.offset, d[:80]
 
 
+def _u(v):
+    return b"\\u%04x" % v if v & 1 else b"\\u%04X" % v
+
+
+def _escape_soup(rng, faulty):
+    """A string of escape sequences at a random alignment: valid \\u escapes of every decoded length,
+    surrogate pairs, two-byte escapes, plain and UTF-8 bytes; `faulty` adds lone / mismatched
+    surrogate halves, bad hex digits, truncated and unknown escapes."""
+    good = [lambda: _u(rng.randrange(0, 0x80)), lambda: _u(rng.randrange(0x80, 0x800)),
+            lambda: _u(rng.choice([rng.randrange(0x800, 0xD800), rng.randrange(0xE000, 0x10000)])),
+            lambda: _u(rng.randrange(0xD800, 0xDC00)) + _u(rng.randrange(0xDC00, 0xE000)),
+            lambda: rng.choice([b'\\"', b"\\\\", b"\\/", b"\\b", b"\\f", b"\\n", b"\\r", b"\\t"]),
+            lambda: bytes([rng.randrange(0x20, 0x7F)]).replace(b'"', b"d").replace(b"\\", b"D"),
+            lambda: rng.choice(["é", "€", "𝄞"]).encode(), lambda: b"\\\\" * rng.randrange(1, 5)]
+    bad = [lambda: _u(rng.randrange(0xD800, 0xDC00)), lambda: _u(rng.randrange(0xDC00, 0xE000)),
+           lambda: _u(rng.randrange(0xD800, 0xDC00)) + _u(rng.randrange(0, 0xD800)),
+           lambda: _u(rng.randrange(0xD800, 0xDC00)) + b"\\n",
+           lambda: _u(rng.randrange(0xD800, 0xDC00)) + b"\\uDC0",
+           lambda: b"\\u" + bytes(rng.choice(b"0123456789abcdefABCDEFgG:@`/ ") for _ in range(4)),
+           lambda: b"\\u" + b"12"[:rng.randrange(0, 3)], lambda: b"\\" + bytes([rng.choice(b"xqU0a ")]),
+           lambda: bytes([rng.randrange(0, 0x20)])]
+    body = b""
+    for _ in range(rng.randrange(1, 40)):
+        body += rng.choice(bad)() if faulty and rng.random() < 0.08 else rng.choice(good)()
+    pad = b"p" * rng.randrange(0, 140)
+    return b'["' + pad + body + b'", "k"]'
+
+
+def test_escape_soup(string_lib, oracle):
+    # the \\u escapes decided from the bit planes (strblock.cuh classify_u) against the oracle's
+    # sequential handle_escape: every alignment to the 64-byte blocks, errors at the first failing escape
+    rng = random.Random(11)
+    n_err = 0
+    for it in range(12000):
+        d = _escape_soup(rng, it % 2 == 1)
+        r = oracle.parse(d)
+        out = C.create_string_buffer(5 * len(d) + 128)
+        ol, n, se, ov = C.c_uint64(), C.c_uint64(), C.c_longlong(), C.c_int()
+        idx = (C.c_uint32 * (len(d) + 8))()
+        aux = (C.c_uint32 * (len(d) + 8))()
+        string_lib.jt_cpu_strings(d, len(d), out, C.byref(ol), idx, aux, C.byref(n), C.byref(se), C.byref(ov))
+        if r.code == 0:
+            assert ov.value == 0, d  # (after an error the two overhang computations may differ)
+            assert se.value == -1, d
+            assert out.raw[:ol.value] == r.strings, d
+        else:
+            assert r.name == "STRING_ERROR", (r.name, d)
+            assert se.value == r.offset, d
+            n_err += 1
+    assert n_err > 1000
+
+
 def _rand_number(rng):
     k = rng.randrange(8)
     if k < 3:
