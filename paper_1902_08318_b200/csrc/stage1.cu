@@ -107,11 +107,6 @@ struct TileBytes {
   }
 };
 
-struct GlobalAt {
-  const uint8_t *in;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
-};
-
 // shared memory layout (dynamic)
 constexpr int kSmemIn = kStage1Tile;            // tile input bytes
 constexpr int kSmemIdx = kStageIdx * 2;         // u16 positions
@@ -163,19 +158,47 @@ __device__ __forceinline__ int clamp16(long long d) { return d < -8192 ? -8192 :
 // K0a: transfer function of each tile.  128 threads x 2 blocks per tile, all
 // four 32-byte loads of a thread issued together.
 constexpr int kFnThreads = kStage1Tile / 128;
+// It also leaves, per tile, the escape overhang INTO the tile (strblock.cuh
+// overhang_in_scan: input / weight bytes of an escape begun before the tile
+// that reach into it, and the decoded bytes that spill) for the case that the
+// tile starts inside a string -- K1's first block needs it, and there the
+// scan would be a chain of dependent byte reads by one thread with its CTA
+// waiting at a barrier.  tile_ov[t] = ov | spill << 4 | spill bytes << 8.
+struct AbsAt {
+  const uint8_t *in;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return in[i]; }
+};
+
 template <bool kRec>
-__global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in, uint32_t *fn,
-                                                          uint32_t *nl_count) {
+__global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in0, uint64_t begin, uint32_t *fn,
+                                                          uint32_t *nl_count, uint32_t *tile_ov) {
   __shared__ uint32_t s_f[kFnThreads / 32];
   __shared__ uint32_t s_nl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (kRec && threadIdx.x == 0) s_nl = 0;
+  const uint8_t *in = in0 + begin;
   const uint64_t blk = (uint64_t)blockIdx.x * kStage1Tile + (uint64_t)threadIdx.x * 128;
   uint32_t w[32];
   ld256(in + blk, w);
   ld256(in + blk + 32, w + 8);
   ld256(in + blk + 64, w + 16);
   ld256(in + blk + 96, w + 24);
+  if (threadIdx.x == kFnThreads - 1) {  // while the loads are in flight
+    const uint64_t tb = begin + (uint64_t)blockIdx.x * kStage1Tile;  // document offset of the tile
+    uint32_t packed = 0;
+    if (tb >= 16) {
+      // no backslash among the 12 bytes before the tile: no escape reaches in
+      const uint4 q = *(const uint4 *)(in0 + tb - 16);
+      const uint32_t x1 = q.y ^ 0x5C5C5C5Cu, x2 = q.z ^ 0x5C5C5C5Cu, x3 = q.w ^ 0x5C5C5C5Cu;
+      const uint32_t z = ((x1 - 0x01010101u) & ~x1) | ((x2 - 0x01010101u) & ~x2) | ((x3 - 0x01010101u) & ~x3);
+      if (z & 0x80808080u) {
+        uint32_t spill_bytes = 0;
+        const int r = sb::overhang_in_scan(AbsAt{in0}, tb, true, &spill_bytes);
+        packed = (uint32_t)(r & 15) | ((uint32_t)(r >> 8) << 4) | (spill_bytes << 8);
+      }
+    }
+    tile_ov[blockIdx.x] = packed;
+  }
   uint32_t f2[2];
   uint32_t nlc = 0;
 #pragma unroll
@@ -364,9 +387,11 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   const uint64_t tile_base = a.begin + (uint64_t)tile * kStage1Tile;
   const uint64_t blk = tile_base + (uint64_t)threadIdx.x * 64;
   const uint32_t local = threadIdx.x * 64;
-  const GlobalAt gat{a.in};
 
   const uint32_t carry_in = a.carry[tile];  // K0b output, read early
+  // K0a: the escape overhang into the tile if it starts inside a string
+  // (the slot becomes the tile's flag when the tile is done)
+  const uint32_t tile_ov = threadIdx.x == 0 ? a.tile_flags[a.rec_tile0 + tile] : 0u;
   uint32_t w[16];
   ld256(a.in + blk, w);
   ld256(a.in + blk + 32, w + 8);
@@ -544,7 +569,12 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   uint32_t spill_bytes = 0;
   if (lane == 0) {
     if (warp > 0) ov_in = s_warp_ov[warp - 1];
-    else ov_in = (state & 2) ? sb::overhang_in_scan(gat, blk, true, &spill_bytes) : 0;
+    else if (state & 2) {
+      ov_in = (int)((tile_ov & 15) | (((tile_ov >> 4) & 15) << 8));
+      spill_bytes = tile_ov >> 8;
+    } else {
+      ov_in = 0;
+    }
   }
   const int vin = ov_in >> 8;
   ov_in &= 0xFF;
@@ -1553,13 +1583,13 @@ cudaError_t stage1_launch(const Stage1Args &args_in, cudaStream_t stream) {
   const cudaError_t configured = stage1_configure();
   if (configured != cudaSuccess) return configured;
   if (a.records) {
-    k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, a.nl_count);
+    k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in, a.begin, a.fn, a.nl_count, a.tile_flags + a.rec_tile0);
     k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
                                                  a.nl_count, a.nl_base, a.nl_total);
     k_rec_init<<<1184, 256, 0, stream>>>(a);
     k_stage1<true><<<(unsigned)a.ntiles, kThreads, kSmemBytesRec, stream>>>(a);
   } else {
-    k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+    k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in, a.begin, a.fn, nullptr, a.tile_flags + a.rec_tile0);
     k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
                                                  nullptr, nullptr, nullptr);
     k_stage1<false><<<(unsigned)a.ntiles, kThreads, kSmemBytes, stream>>>(a);
@@ -1609,7 +1639,7 @@ cudaError_t stage1_lengths_launch(const Stage1Args &a, uint64_t ntiles, cudaStre
 
 cudaError_t stage1_chunk_carry(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in, a.begin, a.fn, nullptr, a.tile_flags + a.rec_tile0);
   k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr, nullptr, nullptr,
                                                nullptr, a.init_state, a.out_state);
   return cudaGetLastError();
@@ -1642,7 +1672,7 @@ cudaError_t index_launch(const Stage1Args &args_in, cudaStream_t stream) {
 
 cudaError_t stage1_records_count(const Stage1Args &args_in, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, a.nl_count);
+  k_carry_fn<true><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in, a.begin, a.fn, a.nl_count, a.tile_flags + a.rec_tile0);
   k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, a.carry, a.ntiles, nullptr, 0, nullptr,
                                                a.nl_count, a.nl_base, a.nl_total);
   return cudaGetLastError();
@@ -1659,7 +1689,7 @@ cudaError_t stage1_records_main(const Stage1Args &args_in, cudaStream_t stream) 
 
 cudaError_t stage1_shard_phase0(const Stage1Args &args_in, Sum0 *out, cudaStream_t stream) {
   const Stage1Args a = with_tiles(args_in);
-  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in + a.begin, a.fn, nullptr);
+  k_carry_fn<false><<<(unsigned)a.ntiles, kFnThreads, 0, stream>>>(a.in, a.begin, a.fn, nullptr, a.tile_flags + a.rec_tile0);
   k_carry_scan<<<1, kScanThreads, 0, stream>>>(a.fn, nullptr, a.ntiles, nullptr, 0, out, nullptr,
                                                nullptr, nullptr);
   return cudaGetLastError();
