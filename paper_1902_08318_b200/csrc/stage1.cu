@@ -183,22 +183,10 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in0, uin
   ld256(in + blk + 32, w + 8);
   ld256(in + blk + 64, w + 16);
   ld256(in + blk + 96, w + 24);
-  if (threadIdx.x == kFnThreads - 1) {  // while the loads are in flight
-    const uint64_t tb = begin + (uint64_t)blockIdx.x * kStage1Tile;  // document offset of the tile
-    uint32_t packed = 0;
-    if (tb >= 16) {
-      // no backslash among the 12 bytes before the tile: no escape reaches in
-      const uint4 q = *(const uint4 *)(in0 + tb - 16);
-      const uint32_t x1 = q.y ^ 0x5C5C5C5Cu, x2 = q.z ^ 0x5C5C5C5Cu, x3 = q.w ^ 0x5C5C5C5Cu;
-      const uint32_t z = ((x1 - 0x01010101u) & ~x1) | ((x2 - 0x01010101u) & ~x2) | ((x3 - 0x01010101u) & ~x3);
-      if (z & 0x80808080u) {
-        uint32_t spill_bytes = 0;
-        const int r = sb::overhang_in_scan(AbsAt{in0}, tb, true, &spill_bytes);
-        packed = (uint32_t)(r & 15) | ((uint32_t)(r >> 8) << 4) | (spill_bytes << 8);
-      }
-    }
-    tile_ov[blockIdx.x] = packed;
-  }
+  // the 16 bytes before the tile, for the overhang scan at the end
+  const uint64_t tb = begin + (uint64_t)blockIdx.x * kStage1Tile;  // document offset of the tile
+  uint4 before = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == kFnThreads - 1 && tb >= 16) before = *(const uint4 *)(in0 + tb - 16);
   uint32_t f2[2];
   uint32_t nlc = 0;
 #pragma unroll
@@ -233,6 +221,22 @@ __global__ void __launch_bounds__(kFnThreads) k_carry_fn(const uint8_t *in0, uin
     for (int k = 1; k < kFnThreads / 32; k++) agg = s1::compose(s_f[k], agg);
     fn[blockIdx.x] = agg;
     if (kRec) nl_count[blockIdx.x] = s_nl;
+  }
+  // after the CTA's barrier: nobody waits for this chain of byte reads
+  if (threadIdx.x == kFnThreads - 1) {
+    uint32_t packed = 0;
+    if (tb >= 16) {
+      // no backslash among the 12 bytes before the tile: no escape reaches in
+      const uint4 q = before;
+      const uint32_t x1 = q.y ^ 0x5C5C5C5Cu, x2 = q.z ^ 0x5C5C5C5Cu, x3 = q.w ^ 0x5C5C5C5Cu;
+      const uint32_t z = ((x1 - 0x01010101u) & ~x1) | ((x2 - 0x01010101u) & ~x2) | ((x3 - 0x01010101u) & ~x3);
+      if (z & 0x80808080u) {
+        uint32_t spill_bytes = 0;
+        const int r = sb::overhang_in_scan(AbsAt{in0}, tb, true, &spill_bytes);
+        packed = (uint32_t)(r & 15) | ((uint32_t)(r >> 8) << 4) | (spill_bytes << 8);
+      }
+    }
+    tile_ov[blockIdx.x] = packed;
   }
 }
 
