@@ -1321,6 +1321,11 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
     const uint64_t uq1 = uq0 ^ tq;
     const uint64_t px0 = s1::prefix_xor(uq0), px1 = px0 ^ (0ULL - tq);
     bar_sync<1, kIdxCompute>();
+    // the next tile is claimed here, after the classification (claim order ~
+    // aggregate order), but its round trip runs under the counting below
+    // instead of in front of the next barrier
+    uint32_t claimed = 0;
+    if (threadIdx.x == 0) claimed = atomicAdd(a.tile_counter, 1u);
     const bool four = S.two != 0;  // CTA-uniform
     // G: tile entry -> this block's entry
     uint32_t wf = lane < kWarps ? S.wf[lane] : 0u;
@@ -1351,12 +1356,18 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
       c1 = popc64(fin1);
       c3 = popc64(fin3);
     }
+    // a separator before the tile only adds the pseudo-structural start at
+    // the tile's byte 0: bit x = byte 0 is no structural, quote or whitespace
+    // byte and lies outside a string for entry x (idx_fin's terms at bit 0;
+    // thread 0's own masks -- the other threads' value is not used)
     uint32_t dsep = 0;
-    if (threadIdx.x == 0) {
-      dsep = (uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 4u, valid) ^ fin0) & 1) |
-             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 5u, valid) ^ fin1) & 1) << 1) |
-             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 6u, valid) ^ fin2) & 1) << 2) |
-             ((uint32_t)((idx_fin(m, uq0, uq1, px0, px1, 7u, valid) ^ fin3) & 1) << 3);
+    {
+      const uint32_t plain0 = (uint32_t)(~m.st & ~m.ws & valid) & 1u;
+      const uint32_t o0 = (uint32_t)(~uq0 & ~px0) & 1u;  // entry odd = 0: no quote, outside
+      const uint32_t o1 = (uint32_t)(~uq1 & ~px1) & 1u;
+      const uint32_t i0 = (uint32_t)(~uq0 & px0) & 1u;   // in_string entry flips instr
+      const uint32_t i1 = (uint32_t)(~uq1 & px1) & 1u;
+      dsep = plain0 ? (o0 | (o1 << 1) | (i0 << 2) | (i1 << 3)) : 0u;
     }
     const uint64_t cnt = (uint64_t)c0 | ((uint64_t)c1 << 16) | ((uint64_t)c2 << 32) | ((uint64_t)c3 << 48);
     uint64_t ci = cnt;
@@ -1366,9 +1377,9 @@ __global__ void __launch_bounds__(kIdxThreads, kIdxMinBlocks) k_index(Stage1Args
       if (lane >= d) ci += o;
     }
     if (lane == 31) S.wc[warp] = ci;
-    if (threadIdx.x == 0) {  // claimed late: claim order ~ aggregate order
-      S.claim = atomicAdd(a.tile_counter, 1u);
-      JT_TL(S.claim, 7);
+    if (threadIdx.x == 0) {
+      S.claim = claimed;
+      JT_TL(claimed, 7);
       S.snap = S.done;       // look-backs finished so far (extracted below)
     }
     bar_sync<1, kIdxCompute>();
