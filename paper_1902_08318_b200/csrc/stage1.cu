@@ -752,7 +752,8 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     uint64_t cm = W;
     if (dec_tr | dec_bmp | dec_pair)
       sb::decode_in_place(dec_tr, dec_bmp, dec_pair,
-                          [&](uint64_t k, uint32_t w3[3]) { tbyte.window_own(k, w3); }, tbyte, rewrite);
+                          [&](uint64_t k, uint32_t w3[3]) { tbyte.window_own(k, w3); }, tbyte,
+                          [&](int k, uint8_t b) { s_in[local + (uint32_t)k] = b; });
     if (!pay_direct) {
       // each lane copies its own block into the staging buffer, bytes in
       // order with a running destination (+1 per weight bit, +4 per opening

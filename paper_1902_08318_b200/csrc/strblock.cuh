@@ -302,15 +302,6 @@ JT_HD uint32_t hex4_value(uint32_t x) {
   return (r & 0xFFu) | ((r >> 8) & 0xFF00u);
 }
 
-// code point of a decided escape from its 12-byte window (w[k] = bytes
-// 4k..4k+3 from the backslash); is_pair: the low half follows at byte 6
-JT_HD uint32_t decided_cp(const uint32_t w[3], bool is_pair) {
-  const uint32_t v = hex4_value((w[0] >> 16) | (w[1] << 16));
-  if (!is_pair) return v;
-  const uint32_t lo = hex4_value(w[2]);
-  return 0x10000u + (((v - 0xD800u) << 10) | (lo - 0xDC00u));
-}
-
 // The undecided starts in order (each reads bytes of the next block through
 // `byte`): failing ones go to *bad; returns p | L << 6 | cp << 10 of the last
 // valid one (it reaches past the block: at most one in a block), 0 if none.
@@ -425,22 +416,52 @@ JT_HD uint64_t block_weights(uint64_t content, BlockEsc &e, int ov_in, int vin) 
   return (content & ~(over | e.ec.sim | e.ec.tr | e.ucov)) | low_bits(vin) | e.uvirt;
 }
 
+// UTF-8 bytes of a code point as a little-endian word (first byte lowest)
+JT_HD uint32_t encode4_word(uint32_t cp) {  // cp >= 0x10000
+  return 0x808080F0u | (cp >> 18) | (((cp >> 12) & 0x3Fu) << 8) | (((cp >> 6) & 0x3Fu) << 16) |
+         ((cp & 0x3Fu) << 24);
+}
+JT_HD uint32_t encode123_word(uint32_t cp, int *n) {  // cp < 0x10000
+  if (cp < 0x80u) {
+    *n = 1;
+    return cp;
+  }
+  if (cp < 0x800u) {
+    *n = 2;
+    return 0x80C0u | (cp >> 6) | ((cp & 0x3Fu) << 8);
+  }
+  *n = 3;
+  return 0x8080E0u | (cp >> 12) | (((cp >> 6) & 0x3Fu) << 8) | ((cp & 0x3Fu) << 16);
+}
+
 // window(p, w): 12 bytes from block-relative p (only bytes inside the block
-// are used); byte(q): block-relative byte q < 64
-template <class Window, class Byte, class Rewrite>
-JT_HD void decode_in_place(uint64_t tr, uint64_t bmp, uint64_t pair, Window window, Byte byte,
-                           Rewrite rewrite) {
+// are used); byte(q): block-relative byte q < 64; put(k, b): decoded byte b to
+// block-relative k < 64
+template <class Window, class Byte, class Put>
+JT_HD void decode_in_place(uint64_t tr, uint64_t bmp, uint64_t pair, Window window, Byte byte, Put put) {
   for (uint64_t t = tr & ~(1ULL << 63); t; t &= t - 1) {
     const int q = ctz64(t) + 1;
-    rewrite(q, (uint8_t)translate_letter(byte((uint64_t)q)));
+    put(q, (uint8_t)translate_letter(byte((uint64_t)q)));
   }
   for (uint64_t r = bmp | pair; r; r &= r - 1) {
     const int p = ctz64(r);
     uint32_t win[3];
     window((uint64_t)p, win);
-    uint8_t b[4];
-    const int n = encode(decided_cp(win, (pair >> p) & 1), b);
-    for (int k = 0; k < n; k++) rewrite(p + k, b[k]);
+    const uint32_t v = hex4_value((win[0] >> 16) | (win[1] << 16));
+    if ((pair >> p) & 1) {
+      const uint32_t lo = hex4_value(win[2]);
+      const uint32_t w = encode4_word(0x10000u + (((v - 0xD800u) << 10) | (lo - 0xDC00u)));
+      put(p, (uint8_t)w);
+      put(p + 1, (uint8_t)(w >> 8));
+      put(p + 2, (uint8_t)(w >> 16));
+      put(p + 3, (uint8_t)(w >> 24));
+    } else {
+      int n;
+      const uint32_t w = encode123_word(v, &n);
+      put(p, (uint8_t)w);
+      if (n > 1) put(p + 1, (uint8_t)(w >> 8));
+      if (n > 2) put(p + 2, (uint8_t)(w >> 16));
+    }
   }
 }
 

@@ -32,7 +32,11 @@ from tools.gen import generate  # noqa: E402
 
 
 def draw(rng: random.Random) -> bytes:
-    k = rng.randrange(10)
+    k = rng.randrange(12)
+    if k >= 10:  # strings of escape sequences at every block alignment (some with failing escapes)
+        from tests.test_kernels_cpu import _escape_soup
+        parts = [_escape_soup(rng, rng.random() < 0.15) for _ in range(rng.randrange(1, 60))]
+        return b"[" + b",".join(parts) + b"]"
     if k < 4:
         cfg = rng.choice([0, 1, 2, 4])
         size = rng.choice([1 << 12, 1 << 14, 100000, 1 << 18, 1 << 20, 3 << 20])
