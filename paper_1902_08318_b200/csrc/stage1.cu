@@ -134,16 +134,6 @@ struct RecBlk {
 constexpr int kOffRec = (kSmemBytes + 15) & ~15;
 constexpr int kSmemBytesRec = kOffRec + kThreads * (int)sizeof(RecBlk);
 
-__device__ __forceinline__ int tok_width(uint32_t c) {  // tape words per token
-  if (c == ',' || c == ':') return 0;
-  if (c == '-' || (c - '0') < 10u) return 2;
-  return 1;
-}
-
-__device__ __forceinline__ int tok_delta(uint32_t c) {
-  return (c == '{' || c == '[') ? 1 : (c == '}' || c == ']') ? -1 : 0;
-}
-
 // depth_before, relative to the range start (a shard adds its base in stage
 // 2); clamped where the document has already failed (|d| > kMaxDepth + base)
 __device__ __forceinline__ int clamp16(long long d) { return d < -8192 ? -8192 : d > 8192 ? 8192 : (int)d; }
@@ -646,8 +636,8 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   if (threadIdx.x == 0) JT_TL(tile, 2);
   uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
   int wdoff = 0, dtotal = 0;
-#pragma unroll
   uint32_t wdf = 0, dtf = 0;  // record mode: resets before this warp / in the tile
+#pragma unroll
   for (int k = 0; k < kWarps; k++) {
     uint32_t c = s_warp_cnt[k], s = s_warp_sw[k], t = s_warp_tw[k];
     int dd = s_warp_td[k];
