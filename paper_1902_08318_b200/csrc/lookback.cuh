@@ -187,12 +187,17 @@ __device__ __forceinline__ int quad_read(const uint64_t *rec, int64_t tile, Quad
   return 0;
 }
 
-// Window of the look-back: each lane reads kLbPer predecessor records per
-// round, so one round covers 32 * kLbPer tiles.  All loads of a round are
+// Window of the look-back: each lane reads kQuadPer predecessor records per
+// round, so one round covers 32 * kQuadPer tiles.  All loads of a round are
 // issued before any is waited on (a round costs one L2 round trip, ~1 us
 // under load); only records still empty are re-polled.
 constexpr int kLbPer = 4;
-constexpr int kQuadPer = 2;
+// A/B on C4 (stage 1): 1 record per lane 2.65 ms, 2 -> 2.98, 3 -> 3.15, 4 -> 3.40: the
+// round's cost is its L2 requests (8 per record and lane), not the number of rounds
+#ifndef JT_QUAD_PER
+#define JT_QUAD_PER 1
+#endif
+constexpr int kQuadPer = JT_QUAD_PER;
 __device__ __forceinline__ void quad_issue(const uint64_t *rec, int64_t tile, uint64_t x[8]) {
   const uint64_t *r = rec + 8 * tile;
 #pragma unroll

@@ -631,7 +631,6 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     s_warp_td[warp] = di;
     s_warp_tdf[warp] = df;
   }
-  if (lane == 0 && warp < 6) JT_TL(tile, 10 + warp);  // arrival at the barrier
   __syncthreads();
   if (threadIdx.x == 0) JT_TL(tile, 2);
   uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
@@ -828,6 +827,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     }
   }
   if (threadIdx.x == 0) JT_TL(tile, 8);  // warp 0's own staging done
+  if (lane == 0 && warp < 6) JT_TL(tile, 10 + warp);  // each warp's staging done
   if (!direct) {
     // the look-back waits on predecessors: the first warp done with its own
     // staging runs it, not always warp 0
