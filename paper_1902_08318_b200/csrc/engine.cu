@@ -523,7 +523,7 @@ jt::Stage1Args s1_args(jt_parser *p, uint64_t len, int which, uint64_t begin = 0
   uint64_t nt = layout_tiles ? layout_tiles : jt::stage1_records(a.end - a.begin);
   a.fn = (uint32_t *)p->s1rec.as<uint64_t>();  // 2 x ntiles u32 in the ntiles-word channel-1 area
   a.carry = a.fn + nt;
-  a.rec_count = p->s1rec.as<uint64_t>() + nt;
+  a.rec_count = p->s1rec.as<uint64_t>() + ((nt + 1) & ~1ULL);  // 16-byte aligned: the look-back's vector loads
   a.tile_counter = &c->s1_tile_counter;
   a.utf8_pos = &c->utf8_pos;
   a.str_err = &c->str_err;
@@ -630,7 +630,7 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
   p->prof_n = 0;
   if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
-  uint64_t s1w = jt::stage1_records(len) * 9;
+  uint64_t s1w = jt::stage1_records(len) * 9 + 1;  // + the alignment word before the count records (s1_args)
   // m3 (int32) + k_scalars look-back records, zeroed together
   uint64_t s2w = full ? ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4 : 0;
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
@@ -921,7 +921,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   uint32_t *counters = p->stream_words.as<uint32_t>(), *states = counters + nch;
   p->launches = 0;
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
-  const uint64_t s1w = ntiles * 9;
+  const uint64_t s1w = ntiles * 9 + 1;
   const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
   bool ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                        p->s2rec.as<uint64_t>(), s2w, p->stream),
@@ -2112,7 +2112,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   p->h_index_valid = false;
   p->last_ok = false;
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
-  const uint64_t s1w = jt::stage1_records(len) * 9;
+  const uint64_t s1w = jt::stage1_records(len) * 9 + 1;
   const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
   jt::Ctrl *ctrl = p->ctrl.as<jt::Ctrl>();
   jt::Stage1Args a1 = s1_args(p, len, 0);
@@ -2291,7 +2291,7 @@ int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *sum
   switch (phase) {
     case 0: {
       jt::Stage2Sizes z = jt::stage2_sizes(range + 16);
-      uint64_t s1w = jt::stage1_records(range) * 9;
+      uint64_t s1w = jt::stage1_records(range) * 9 + 1;
       uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((range + 16) / 256 + 2) * 4;
       ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                       p->s2rec.as<uint64_t>(), s2w, p->stream),

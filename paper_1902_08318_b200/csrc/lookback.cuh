@@ -153,8 +153,8 @@ __device__ __forceinline__ Pair pair_lookback(const uint64_t *rec, int64_t tile)
 
 namespace jt {
 
-// Four-counter channel (8 words per tile: [0..3] aggregate, [4..7]
-// inclusive; bit 63 = valid).  Signed counters travel as 63-bit two's
+// Four-counter channel (8 words per tile: [0] the packed aggregate, [4..7]
+// the inclusive prefix; bit 63 = valid).  Signed counters travel as 63-bit two's
 // complement and are sign-extended by the reader (sext63).
 struct Quad {
   unsigned long long v[4];
@@ -170,50 +170,43 @@ __device__ __forceinline__ void quad_publish(uint64_t *rec, int64_t tile, int sl
   for (int k = 0; k < 4; k++) lb_store(r + k, kPairValid | (q.v[k] & kQuadMask));
 }
 
-__device__ __forceinline__ int quad_read(const uint64_t *rec, int64_t tile, Quad &q) {
-  const uint64_t *r = rec + 8 * tile;
-#pragma unroll
-  for (int slot = 1; slot >= 0; --slot) {
-    uint64_t x0 = lb_load(r + 4 * slot), x1 = lb_load(r + 4 * slot + 1);
-    uint64_t x2 = lb_load(r + 4 * slot + 2), x3 = lb_load(r + 4 * slot + 3);
-    if ((x0 & x1 & x2 & x3) >> 63) {
-      q.v[0] = x0 & kQuadMask;
-      q.v[1] = x1 & kQuadMask;
-      q.v[2] = x2 & kQuadMask;
-      q.v[3] = x3 & kQuadMask;
-      return slot + 1;
-    }
-  }
-  return 0;
+// A tile's AGGREGATE travels as one word (slot 0, word 0): bit 63 valid, bit 62
+// the segment flag of the depth counter (record mode), then the tile's depth
+// change (16 bits, signed), string-buffer bytes (16), tape words (15) and index
+// entries (15) -- a 16 KiB tile has at most 16384 entries, 24576 tape words
+// ("[1" is 3 words in 2 bytes), 32768 + 3 string bytes ('""' is 4 in 2 bytes)
+// and a depth change within +-16384.  The INCLUSIVE prefix keeps four words
+// (slot 1, words 4..7).  A look-back round costs its L2 requests: one 8-byte
+// and two 16-byte loads per predecessor (eight 8-byte loads before).
+__device__ __forceinline__ uint64_t quad_pack_agg(uint32_t total, uint32_t stotal, uint32_t ttotal,
+                                                  int depth, bool seg) {
+  return (1ULL << 63) | (seg ? (1ULL << 62) : 0ULL) | ((uint64_t)(uint16_t)depth << 46) |
+         ((uint64_t)(stotal & 0xFFFFu) << 30) | ((uint64_t)(ttotal & 0x7FFFu) << 15) | (uint64_t)(total & 0x7FFFu);
+}
+__device__ __forceinline__ void quad_publish_agg(uint64_t *rec, int64_t tile, uint64_t packed) {
+  lb_store(rec + 8 * tile, packed);
+}
+
+__device__ __forceinline__ void lb_load2(const uint64_t *p, uint64_t &x, uint64_t &y) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
 }
 
 // Window of the look-back: each lane reads kQuadPer predecessor records per
 // round, so one round covers 32 * kQuadPer tiles.  All loads of a round are
-// issued before any is waited on (a round costs one L2 round trip, ~1 us
-// under load); only records still empty are re-polled.
-constexpr int kLbPer = 4;
+// issued before any is waited on; only records still empty are re-polled.
 // A/B on C4 (stage 1): 1 record per lane 2.65 ms, 2 -> 2.98, 3 -> 3.15, 4 -> 3.40: the
-// round's cost is its L2 requests (8 per record and lane), not the number of rounds
+// round's cost is its L2 requests, not the number of rounds
 #ifndef JT_QUAD_PER
 #define JT_QUAD_PER 1
 #endif
 constexpr int kQuadPer = JT_QUAD_PER;
-__device__ __forceinline__ void quad_issue(const uint64_t *rec, int64_t tile, uint64_t x[8]) {
+constexpr int kLbPer = 4;
+// x[0] = the aggregate word, x[1..4] = the inclusive words
+__device__ __forceinline__ void quad_issue(const uint64_t *rec, int64_t tile, uint64_t x[5]) {
   const uint64_t *r = rec + 8 * tile;
-#pragma unroll
-  for (int k = 0; k < 8; k++) x[k] = lb_load(r + k);
-}
-__device__ __forceinline__ int quad_decode(const uint64_t x[8], Quad &q) {
-#pragma unroll
-  for (int slot = 1; slot >= 0; --slot) {
-    const uint64_t *y = x + 4 * slot;
-    if ((y[0] & y[1] & y[2] & y[3]) >> 63) {
-#pragma unroll
-      for (int k = 0; k < 4; k++) q.v[k] = y[k] & kQuadMask;
-      return slot + 1;
-    }
-  }
-  return 0;
+  x[0] = lb_load(r);
+  lb_load2(r + 4, x[1], x[2]);
+  lb_load2(r + 6, x[3], x[4]);
 }
 // Segmented counter (record mode depth): bit 62 = the span contains a
 // reset, bits 61:0 = the change since its last reset (62-bit two's
@@ -224,6 +217,27 @@ __device__ __forceinline__ uint64_t seg_combine(uint64_t e, uint64_t l) {
   return (l & kSegFlag) ? l : ((e & kSegFlag) | ((e + l) & kSegMask));
 }
 __device__ __forceinline__ long long seg_value(uint64_t v) { return (long long)(v << 2) >> 2; }
+
+// 2 = the inclusive prefix, 1 = the aggregate (unpacked into the counters'
+// sum form), 0 = nothing published yet
+template <bool kSeg3>
+__device__ __forceinline__ int quad_decode(const uint64_t x[5], Quad &q) {
+  if ((x[1] & x[2] & x[3] & x[4]) >> 63) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) q.v[k] = x[1 + k] & kQuadMask;
+    return 2;
+  }
+  const uint64_t a = x[0];
+  if (a >> 63) {
+    q.v[0] = a & 0x7FFFu;
+    q.v[2] = (a >> 15) & 0x7FFFu;
+    q.v[1] = (a >> 30) & 0xFFFFu;
+    const long long d = (long long)(int16_t)(uint16_t)(a >> 46);
+    q.v[3] = kSeg3 ? ((a & kSegFlag) | ((uint64_t)d & kSegMask)) : ((uint64_t)d & kQuadMask);
+    return 1;
+  }
+  return 0;
+}
 
 // exclusive prefix (mod 2^63 per counter) of tile `tile` > 0, one full warp;
 // kSeg3: counter 3 is a segmented counter (seg_combine) instead of a sum
@@ -236,7 +250,7 @@ __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile)
     // lane l owns predecessors base - kQuadPer*l - j, j = 0 (nearest) .. kQuadPer-1
     Quad q[kQuadPer];
     int st[kQuadPer];
-    uint64_t x[kQuadPer][8];
+    uint64_t x[kQuadPer][5];
 #pragma unroll
     for (int j = 0; j < kQuadPer; j++) {
       int64_t pred = base - (int64_t)kQuadPer * lane - j;
@@ -248,7 +262,7 @@ __device__ __forceinline__ Quad quad_lookback(const uint64_t *rec, int64_t tile)
       q[j] = Quad{{0, 0, 0, 0}};
       st[j] = 2;
       if (pred >= 0) {
-        while ((st[j] = quad_decode(x[j], q[j])) == 0) {
+        while ((st[j] = quad_decode<kSeg3>(x[j], q[j])) == 0) {
           __nanosleep(32);
           quad_issue(rec, pred, x[j]);
           JT_TLADD(tile, 12, 1);

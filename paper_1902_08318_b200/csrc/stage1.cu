@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   };
   if (threadIdx.x == 0 && gt > 0) {
     JT_TL(tile, 4);
-    quad_publish(a.rec_count, gt, 0, tot);
+    quad_publish_agg(a.rec_count, gt, quad_pack_agg(total, stotal, ttotal, dtotal, kRec && dtf));
   }
   if (direct && warp == 0) resolve_counts();
   if (threadIdx.x == 0) JT_TL(tile, 6);
