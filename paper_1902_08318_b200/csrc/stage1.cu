@@ -981,11 +981,15 @@ __device__ __forceinline__ IdxAgg idx_shfl_down(const IdxAgg &v, int d) {
 constexpr uint64_t kIdxValid = 1ULL << 63;
 
 // Look-back of tile `tile` (> 0) by one full warp: entry state and base.
-// Each round covers 128 predecessors (4 per lane, nearest first), all 12
+// Each round covers 64 predecessors (2 per lane, nearest first), all 6
 // record words of a lane loaded together: one L2 round trip per round.  A
 // persistent k_index resolves tiles in waves of ~G = #CTAs, so a tile may
-// sit up to G tiles past the last inclusive record.
-constexpr int kLbPer = 4;
+// sit up to G tiles past the last inclusive record.  A/B (jt_stage1, C4 / C2):
+// 4 per lane 0.894 / 0.229 ms, 2 -> 0.858 / 0.216, 1 -> 0.880 / 0.220.
+#ifndef JT_IDX_LB_PER
+#define JT_IDX_LB_PER 2
+#endif
+constexpr int kLbPer = JT_IDX_LB_PER;
 __device__ __forceinline__ void idx_lookback(const uint64_t *agg, const uint64_t *incl, int64_t tile,
                                              uint32_t &state, uint64_t &base) {
   const int lane = threadIdx.x & 31;
