@@ -1066,6 +1066,20 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
     }
     const uint64_t i0 = tbase + threadIdx.x * kK3Tok;
     const uint64_t i1 = min(i0 + kK3Tok, S);
+    // innermost container of token j is an object -- for a token of this tile
+    // in a deep document through the tile's shared tree (scope_obj walks the
+    // global one: a chain of dependent loads at every chunk entry)
+    auto scope_obj_tile = [&](int64_t j) -> bool {
+      if (shallow || j < (int64_t)tbase) return scope_obj(j);
+      const int D = tok_depth(s_tok[j - (int64_t)tbase]);
+      const int64_t o = psv_tile_masked(a, T, j, D - 1);
+      if (o < 0) {
+        uint32_t tp;
+        bool ob = false;
+        return bound_at(D + db - 1, &tp, &ob) && ob;
+      }
+      return ((o >= (int64_t)tbase ? s_tok[o - (int64_t)tbase] : a.tok[o]) & 0xFF) == '{';
+    };
     if (i0 < S) do {
     const uint32_t *recs = s_tok + threadIdx.x * kK3Tok;
     uint32_t t = a.tape_idx[i0];  // local tape index (document index = tb + t)
@@ -1101,7 +1115,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
       else if (c1 == '[') mode = M_AF;
       else if (c1 == ':') mode = M_V;
       else if (c1 == ',') {
-        mode = scope_obj((int64_t)i0 - 1) ? M_K : M_V;
+        mode = scope_obj_tile((int64_t)i0 - 1) ? M_K : M_V;
       } else if (c1 == '"') {
         mode = M_A;
         if (rbefore >= 2) {
@@ -1109,7 +1123,7 @@ __global__ void __launch_bounds__(256, JT_STRUCT_MINB) k_struct(Stage2Args a) {
           uint32_t c2 = v2 & 0xFF;
           if (c2 == '{') mode = M_C;
           else if (c2 == ',') {
-            if (scope_obj((int64_t)i0 - 2)) mode = M_C;
+            if (scope_obj_tile((int64_t)i0 - 2)) mode = M_C;
           }
         }
       } else {
