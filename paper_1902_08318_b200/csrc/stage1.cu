@@ -38,6 +38,30 @@ __device__ __forceinline__ void ld256(const uint8_t *p, uint32_t *w) {
 }
 
 
+// A 16-byte chunk of a block's payload copy: every byte is stored at the
+// running shared-memory address d if its weight bit (ww) is set; d += 1 for a
+// weight bit, += 4 for an opening quote (ow: the length field).  Written as
+// predicated instructions on one address register: the arithmetic form
+// (d += bit + 4 * quote bit, address = base + d) was 8 instructions per byte.
+#define JT_PB(BIT, WORD, SH)                                                                        \
+  "and.b32 t, %5, " #BIT ";\n\tsetp.ne.u32 p, t, 0;\n\tand.b32 t, %6, " #BIT ";\n\tsetp.ne.u32 q, t, 0;\n\t" \
+  "shr.u32 v, " WORD ", " #SH ";\n\t@p st.shared.u8 [%0], v;\n\t@p add.u32 %0, %0, 1;\n\t@q add.u32 %0, %0, 4;\n\t"
+#define JT_PW(B0, B1, B2, B3, WORD) JT_PB(B0, WORD, 0) JT_PB(B1, WORD, 8) JT_PB(B2, WORD, 16) JT_PB(B3, WORD, 24)
+__device__ __forceinline__ void pay_chunk(uint32_t &d, const uint4 v, uint32_t ww, uint32_t ow) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .b32 t, v;\n\t"
+      JT_PW(1, 2, 4, 8, "%1") JT_PW(16, 32, 64, 128, "%2") JT_PW(256, 512, 1024, 2048, "%3")
+      JT_PW(4096, 8192, 16384, 32768, "%4")
+      "}"
+      : "+r"(d)
+      : "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(ww), "r"(ow)
+      : "memory");
+}
+#undef JT_PW
+#undef JT_PB
+
 // byte run copy inside shared memory (offsets from the dynamic smem base):
 // head bytes to align the destination, then funnel-shifted words
 __device__ __forceinline__ void smem_copy(uint8_t *base, uint32_t dst, uint32_t src, int n) {
@@ -389,11 +413,12 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_nl[kWarps];
   __shared__ uint32_t s_warp_tdf[kWarps];
-  __shared__ uint32_t s_warp_f[kWarps];
-  __shared__ uint32_t s_warp_cnt[kWarps];
-  __shared__ uint32_t s_warp_sw[kWarps];
-  __shared__ uint32_t s_warp_tw[kWarps];
-  __shared__ int s_warp_td[kWarps];
+  __shared__ __align__(16) uint32_t s_warp_f[kWarps];
+  static_assert(kWarps == 8, "the per-warp totals are read as two 16-byte words");
+  __shared__ __align__(16) uint32_t s_warp_cnt[kWarps];
+  __shared__ __align__(16) uint32_t s_warp_sw[kWarps];
+  __shared__ __align__(16) uint32_t s_warp_tw[kWarps];
+  __shared__ __align__(16) int s_warp_td[kWarps];
   __shared__ int s_warp_ov[kWarps];
   __shared__ unsigned long long s_base, s_sbase, s_tbase;
   __shared__ uint32_t s_lb_claim;  // the first warp done staging resolves the tile's counts
@@ -513,7 +538,14 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   // through the earlier warps' functions, folded by every warp itself (no
   // second barrier)
   uint32_t state = carry_in;
-  for (int k = 0; k < warp; k++) state = s1::apply(s_warp_f[k], state);
+  {
+    // all eight functions loaded at once: the chain below is register-only
+    const uint4 f03 = *(const uint4 *)&s_warp_f[0], f47 = *(const uint4 *)&s_warp_f[4];
+    const uint32_t wf[kWarps] = {f03.x, f03.y, f03.z, f03.w, f47.x, f47.y, f47.z, f47.w};
+#pragma unroll
+    for (int k = 0; k < kWarps - 1; k++)
+      if (k < warp) state = s1::apply(wf[k], state);
+  }
   if (lane > 0) state = s1::apply(excl, state);
   int64_t rem = (int64_t)a.len - (int64_t)blk;
   const uint64_t valid = rem >= 64 ? ~0ULL : rem <= 0 ? 0ULL : ((1ULL << rem) - 1);
@@ -673,10 +705,21 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   uint32_t woff = 0, total = 0, wsoff = 0, stotal = 0, wtoff = 0, ttotal = 0;
   int wdoff = 0, dtotal = 0;
   uint32_t wdf = 0, dtf = 0;  // record mode: resets before this warp / in the tile
+  uint32_t wc8[kWarps], ws8[kWarps], wt8[kWarps], wd8[kWarps];
+  {
+    auto ld8 = [](const void *p, uint32_t v[kWarps]) {
+      const uint4 lo = ((const uint4 *)p)[0], hi = ((const uint4 *)p)[1];
+      v[0] = lo.x, v[1] = lo.y, v[2] = lo.z, v[3] = lo.w, v[4] = hi.x, v[5] = hi.y, v[6] = hi.z, v[7] = hi.w;
+    };
+    ld8(s_warp_cnt, wc8);
+    ld8(s_warp_sw, ws8);
+    ld8(s_warp_tw, wt8);
+    ld8(s_warp_td, wd8);
+  }
 #pragma unroll
   for (int k = 0; k < kWarps; k++) {
-    uint32_t c = s_warp_cnt[k], s = s_warp_sw[k], t = s_warp_tw[k];
-    int dd = s_warp_td[k];
+    uint32_t c = wc8[k], s = ws8[k], t = wt8[k];
+    int dd = (int)wd8[k];
     const uint32_t fk = kRec ? s_warp_tdf[k] : 0u;
     woff += k < warp ? c : 0;
     wsoff += k < warp ? s : 0;
@@ -787,7 +830,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
       // predicated, 16-byte chunks without string bytes skipped
       if (cm) {
         const uint4 *src = reinterpret_cast<const uint4 *>(s_in + local);
-        uint32_t d = soff;
+        uint32_t d = (uint32_t)__cvta_generic_to_shared(s_pay) + soff;  // shared-window address
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           const uint32_t ww = (uint32_t)(W >> (16 * c)) & 0xFFFFu;
@@ -797,12 +840,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
             continue;
           }
           const uint4 v = src[c];
-          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int b = 0; b < 16; b++) {
-            if ((ww >> b) & 1) s_pay[d] = (uint8_t)(wd[b >> 2] >> (8 * (b & 3)));
-            d += ((ww >> b) & 1) + 4u * ((ow >> b) & 1);
-          }
+          pay_chunk(d, v, ww, ow);
         }
       }
       cm = 0;
@@ -951,10 +989,22 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     uint32_t *dw = (uint32_t *)(dst + head);
     const uint32_t *sp = (const uint32_t *)s_pay;
     const uint32_t sh = head * 8;
-    for (uint32_t k = threadIdx.x; k < nw; k += kThreads) {
-      uint32_t o = (head >> 2) + k;  // head < 4, so o = k
-      dw[k] = __funnelshift_r(sp[o], sp[o + 1], sh);
+    // words up to the destination's 16-byte alignment, then 16 bytes per
+    // thread and round (five staged words funnel-shifted into one store)
+    const uint32_t pre = nw < (uint32_t)((4 - (((uintptr_t)dw >> 2) & 3)) & 3)
+                             ? nw
+                             : (uint32_t)((4 - (((uintptr_t)dw >> 2) & 3)) & 3);
+    if (threadIdx.x < pre) dw[threadIdx.x] = __funnelshift_r(sp[threadIdx.x], sp[threadIdx.x + 1], sh);
+    const uint32_t nq = (nw - pre) / 4;
+    uint4 *dq = (uint4 *)(dw + pre);
+    for (uint32_t k = threadIdx.x; k < nq; k += kThreads) {
+      const uint32_t o = pre + 4 * k;
+      const uint32_t x0 = sp[o], x1 = sp[o + 1], x2 = sp[o + 2], x3 = sp[o + 3], x4 = sp[o + 4];
+      dq[k] = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
+                         __funnelshift_r(x3, x4, sh));
     }
+    for (uint32_t k = pre + 4 * nq + threadIdx.x; k < nw; k += kThreads)
+      dw[k] = __funnelshift_r(sp[k], sp[k + 1], sh);
     for (uint32_t k = head + 4 * nw + threadIdx.x; k < stotal; k += kThreads) dst[k] = s_pay[k];
   }
   if (threadIdx.x == 0) JT_TL(tile, 7);

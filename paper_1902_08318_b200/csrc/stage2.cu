@@ -188,6 +188,9 @@ __global__ void __launch_bounds__(256) k_stack(Stage2Args a) {
   __shared__ uint64_t s_wS[8];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
+  // deeper than the 64-kind register (pass 0 left the maximum): nobody reads
+  // the scope bits (k_struct's `shallow`; max_depth only grows)
+  if (kPass == 1 && ctrl->max_depth > 64) return;
   const Rng R = rng_of(a, ctrl);
   const uint64_t S = R.hi;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(kStkScan) k_stack_scan(Stage2Args a) {
   __shared__ StackT s_w[kStkScan / 32];
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
+  if (ctrl->max_depth > 64) return;  // the scope bits are not used (k_stack pass 1)
   const uint64_t S = rng_of(a, ctrl).hi;  // a partial range rescans all tiles below its end
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (S + 256 * kStkTok - 1) / (256 * kStkTok);
