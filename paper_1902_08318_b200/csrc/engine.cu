@@ -493,7 +493,7 @@ bool ensure_stage2(jt_parser *p, uint64_t len, bool records = false) {
   uint64_t cap = len + 16;
   jt::Stage2Sizes z = jt::stage2_sizes(cap);
   const uint64_t nums = len / 2 + 32;
-  bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 128 + (cap / 256 + 2) * 32) &&
+  bool ok = p->s2rec.ensure(z.n3 * sizeof(int32_t) + 128 + (cap / 4096 + 2) * 32)  /* m3 + 4 words per k_stack tile */ &&
             p->m1.ensure(z.n1 * sizeof(int16_t)) && p->m2.ensure(z.n2 * sizeof(int16_t)) &&
             p->mhi.ensure(z.nhi * sizeof(int16_t) + 64) &&
             p->slow.ensure(nums * sizeof(uint32_t)) &&
@@ -631,8 +631,8 @@ bool enqueue_direct(jt_parser *p, uint64_t len, int which, bool full) {
   if (p->prof) cudaEventRecord(p->ev[0], p->stream);
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   uint64_t s1w = jt::stage1_records(len) * 9 + 1;  // + the alignment word before the count records (s1_args)
-  // m3 (int32) + k_scalars look-back records, zeroed together
-  uint64_t s2w = full ? ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4 : 0;
+  // m3 (int32, built by atomicMax); the k_stack records behind it are written before they are read
+  uint64_t s2w = full ? ((z.n3 * 4 + 64 + 63) / 64) * 8 : 0;
   if (!cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                   p->s2rec.as<uint64_t>(), s2w, p->stream),
                "init"))
@@ -922,7 +922,7 @@ jt_error parse_stream(jt_parser *p, const char *data, uint64_t len, jt_document 
   p->launches = 0;
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   const uint64_t s1w = ntiles * 9 + 1;
-  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
+  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8;  // m3 only (enqueue_direct)
   bool ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                        p->s2rec.as<uint64_t>(), s2w, p->stream),
                     "init") &&
@@ -2113,7 +2113,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   p->last_ok = false;
   jt::Stage2Sizes z = jt::stage2_sizes(len + 16);
   const uint64_t s1w = jt::stage1_records(len) * 9 + 1;
-  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((len + 16) / 256 + 2) * 4;
+  const uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8;  // m3 only (enqueue_direct)
   jt::Ctrl *ctrl = p->ctrl.as<jt::Ctrl>();
   jt::Stage1Args a1 = s1_args(p, len, 0);
   a1.records = true;
@@ -2176,7 +2176,7 @@ int jt_b200_parse_records(jt_parser *p, size_t len, size_t *n_records) {
   int n2 = 0;
   if (!cuda_ok(p, jt::records_init_launch(a2, p->stream), "records init") ||
       !cuda_ok(p, jt::stage1_records_main(a1, p->stream), "records stage 1") ||
-      !cuda_ok(p, jt::records_stage2_launch(a2, p->stream, &n2), "records stage 2") ||
+      !cuda_ok(p, jt::records_stage2_launch(a2, p->stream, &n2, stage2_fork(p)), "records stage 2") ||
       !cuda_ok(p, cudaMemcpyAsync(p->h_ctrl, p->ctrl.p, sizeof(jt::Ctrl), cudaMemcpyDeviceToHost,
                                   p->stream),
                "ctrl D2H") ||
@@ -2292,7 +2292,7 @@ int jt_b200_shard_phase(jt_parser *p, int phase, const void *gathered, void *sum
     case 0: {
       jt::Stage2Sizes z = jt::stage2_sizes(range + 16);
       uint64_t s1w = jt::stage1_records(range) * 9 + 1;
-      uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8 + ((range + 16) / 256 + 2) * 4;
+      uint64_t s2w = ((z.n3 * 4 + 64 + 63) / 64) * 8;  // m3 only (enqueue_direct)
       ok = cuda_ok(p, jt::init_launch(p->ctrl.as<jt::Ctrl>(), p->s1rec.as<uint64_t>(), s1w,
                                       p->s2rec.as<uint64_t>(), s2w, p->stream),
                    "init") &&

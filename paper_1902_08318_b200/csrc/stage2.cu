@@ -340,7 +340,11 @@ __device__ __forceinline__ void ld4(const uint32_t *p, uint64_t i, uint64_t S, u
 }
 
 __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
-  __shared__ int s_wmin[8];
+  // warp minima of the current pass, double-buffered by pass parity: a pair of
+  // warps (256 tokens) meets at its own 64-thread barrier once per pass
+  // instead of the CTA at two
+  __shared__ int s_wmin[2][8];
+  int par = 0;
   Ctrl *ctrl = a.ctrl;
   if (ctrl->utf8_pos != ~0ULL) return;
   // tokens [R.lo, S); the next token is readable below R.avail
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
     if ((lane & 3) == 0 && i0 < S) a.m1[i0 >> 4] = (int16_t)m;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_wmin[warp] = m;  // 128 tokens
+    if (lane == 0) s_wmin[par][warp] = m;  // 128 tokens
     // every load that depends on the four positions goes out before any of
     // them is used: the string's stage-1 tile flag, and the 8 bytes of an
     // atom (atom_ok8), instead of a chain of dependent byte loads
@@ -450,16 +454,21 @@ __global__ void __launch_bounds__(256) k_scalars(Stage2Args a) {
         for (uint32_t q = nummask; q; q &= q - 1) a.numlist[basep++] = (uint32_t)(i0 + __ffs(q) - 1);
       }
     }
-    __syncthreads();
-    if (threadIdx.x < 4) {  // m2 = 256 tokens = 2 warps
-      const int mm = min(s_wmin[2 * threadIdx.x], s_wmin[2 * threadIdx.x + 1]);
-      const uint64_t g2 = (base >> 8) + threadIdx.x;
+    switch (warp >> 1) {  // constant barrier ids: the kernel reserves 5, not all 16
+      case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+      case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+      case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+      default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+    }
+    if (lane == 0 && !(warp & 1)) {  // m2 = 256 tokens = 2 warps
+      const int mm = min(s_wmin[par][warp], s_wmin[par][warp + 1]);
+      const uint64_t g2 = (base >> 8) + (warp >> 1);
       if ((g2 << 8) < S) {
         a.m2[g2] = (int16_t)mm;
         atomicMax(&a.m3[g2 >> 4], 0x7FFF - mm);
       }
     }
-    __syncthreads();
+    par ^= 1;
   }
 }
 
@@ -1866,13 +1875,24 @@ cudaError_t records_init_launch(const Stage2Args &a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches) {
+cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
+                                  const Stage2Fork *fork) {
   const unsigned g2 = grid_tokens(a);
+  if (fork) {
+    // side stream: the container kinds next to the scalars / numbers (k_stack
+    // reads only stage 1's token records; k_struct needs the fail flags
+    // k_scalars and k_numbers leave in them, so it stays behind both)
+    cudaEventRecord(fork->fork, stream);
+    cudaStreamWaitEvent(fork->side, fork->fork, 0);
+    launch_stack(a, fork->side);
+    cudaEventRecord(fork->join, fork->side);
+  }
   k_scalars<<<g2, 256, 0, stream>>>(a);
   k_numbers<<<g2, 256, 0, stream>>>(a);
   k_slow<<<8, 64, 0, stream>>>(a);
   k_tree<<<1, 1024, 0, stream>>>(a);
-  launch_stack(a, stream);
+  if (fork) cudaStreamWaitEvent(stream, fork->join, 0);
+  else launch_stack(a, stream);
   launch_struct(a, stream);
   k_final_records<<<1184, 256, 0, stream>>>(a);
   *launches = 9;
@@ -2164,6 +2184,8 @@ cudaError_t stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launche
   if (ev) cudaEventRecord(ev[2], stream);
   if (forked) cudaStreamWaitEvent(stream, fork->join, 0);
   else launch_stack(a, stream);  // container kinds (scope bits) for k_struct
+  // k_struct reads the fail flags k_scalars / k_numbers leave in the token
+  // records (errors are reported in token order): it cannot run next to them
   launch_struct(a, stream);
   if (ev) cudaEventRecord(ev[3], stream);
   k_final<<<1, 1, 0, stream>>>(a);

@@ -169,7 +169,8 @@ cudaError_t range_b_launch(const Stage2Args &a, const TokRange *ra, TokRange *rb
 // Record mode: per-record error slots, then the whole stage 2 with
 // per-record grammar, and one result per record.
 cudaError_t records_init_launch(const Stage2Args &a, cudaStream_t stream);
-cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches);
+cudaError_t records_stage2_launch(const Stage2Args &a, cudaStream_t stream, int *launches,
+                                  const Stage2Fork *fork = nullptr);
 
 // Sharded stage 2 (shard.h).  phase 2: bases from the gathered Sum1s, then
 // scalars / numbers / depth tree and this shard's open containers (Sum2);
