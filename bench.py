@@ -62,7 +62,7 @@ WORKLOADS = {
 CONFIG = 4           # headline: the largest single-GPU config
 TABLE = (0, 1, 2, 3)  # the other configs, one short line each inside the headline's JSON
 # ncu --set full captures of the current kernels (DRAM traffic per launch)
-PROFILES = {4: "r02c_ncu_full_c4.json"}
+PROFILES = {4: "r02d_ncu_full_c4.json"}
 FIXTURE = os.path.join(ROOT, "tests", "golden", "large_outputs.json")
 L2_NOTE = "flushed before every step (256 MiB memset, outside the events)"
 # JT_BENCH_GLOO=1 runs the N > 1 paths with every rank on cuda:0 and gloo
