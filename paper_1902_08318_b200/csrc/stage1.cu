@@ -431,9 +431,33 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   RecBlk *s_rec = (RecBlk *)(smem + kOffRec);  // record mode only
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef JT_K1_TMA
+  // A/B build (tools/ab_bench.sh): the tile arrives in shared memory by one
+  // bulk async copy (TMA, cp.async.bulk + mbarrier) issued by thread 0 as soon
+  // as it has claimed the tile; every thread then reads its 64 bytes back
+  // from shared memory instead of loading them and storing the copy.
+  __shared__ __align__(8) unsigned long long s_mbar;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+#endif
   if (threadIdx.x == 0) {
+#ifdef JT_K1_TMA
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#endif
     s_tile = atomicAdd(a.tile_counter, 1u);
     s_lb_claim = 0;
+#ifdef JT_K1_TMA
+    {
+      const uint8_t *src = a.in + a.begin + (uint64_t)s_tile * kStage1Tile;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"((uint32_t)kStage1Tile)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(src), "r"((uint32_t)kStage1Tile), "r"(mbar)
+          : "memory");
+    }
+#endif
   }
   __syncthreads();
   const int64_t tile = s_tile;  // tile of the range; byte offset below is global
@@ -449,6 +473,22 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
   // (the slot becomes the tile's flag when the tile is done)
   const uint32_t tile_ov = threadIdx.x == 0 ? a.tile_flags[a.rec_tile0 + tile] : 0u;
   uint32_t w[16];
+#ifdef JT_K1_TMA
+  {
+    uint32_t ok;
+    do {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(mbar)
+          : "memory");
+    } while (!ok);
+    const uint4 *q = (const uint4 *)(s_in + threadIdx.x * 64);
+    const uint4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    w[0] = q0.x, w[1] = q0.y, w[2] = q0.z, w[3] = q0.w, w[4] = q1.x, w[5] = q1.y, w[6] = q1.z, w[7] = q1.w;
+    w[8] = q2.x, w[9] = q2.y, w[10] = q2.z, w[11] = q2.w, w[12] = q3.x, w[13] = q3.y, w[14] = q3.z, w[15] = q3.w;
+  }
+#else
   ld256(a.in + blk, w);
   ld256(a.in + blk + 32, w + 8);
   {
@@ -458,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, JT_K1_MINB) k_stage1(Stage1Args a) {
     d[2] = make_uint4(w[8], w[9], w[10], w[11]);
     d[3] = make_uint4(w[12], w[13], w[14], w[15]);
   }
+#endif
 
   s1::Masks m;
   s1::classify64(w, m);
