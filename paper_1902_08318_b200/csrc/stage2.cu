@@ -765,6 +765,11 @@ __device__ int64_t psv_tile(const Stage2Args &a, const TileTree &T, int64_t i, i
   return psv_below(a, T, L);
 }
 
+// previous 32-token chunks of the tile a closer's opener is searched in by
+// warp ballots before the tile tree takes over (A/B: tools/ab_bench.sh)
+#ifndef JT_STRUCT_BACK
+#define JT_STRUCT_BACK 8
+#endif
 // Token-parallel grammar check for one document no deeper than 64 (the
 // scope bits are exact): the state in which token i arrives follows from the
 // two tokens before it and their innermost containers' kinds (SURVEY.md
@@ -905,7 +910,7 @@ __device__ __forceinline__ void struct_tokens(const Stage2Args &a, Ctrl *ctrl, u
     // openers before this warp's tokens: the previous chunks of the tile by
     // ballots as well (up to 8), then the tile tree
     uint64_t pb = cb;
-    for (int step = 0; step < 8; step++) {
+    for (int step = 0; step < JT_STRUCT_BACK; step++) {
       uint32_t rem = __ballot_sync(0xffffffffu, need && j == -2);
       if (!rem || pb == tbase) break;
       pb -= 32;
