@@ -419,3 +419,16 @@ def test_device_distinct_large(parser):
         assert cfg == 2 or hits > 0, cfg  # C2 has no keys
     assert parser.parse(b"[1, ]").name != "OK"
     assert parser.distinct(b"a") is None  # no successful parse to query
+
+
+def test_carry_scan_chunk_boundary(parser, oracle):
+    """K0b scans the tile functions in chunks of 8192 tiles (128 MiB) with the
+    state carried from chunk to chunk: the odd-backslash and in-string carries
+    cross that boundary in the middle of a string, both ways (the string ends
+    right after it / goes on), and at the last tile before it."""
+    B = 8192 * 16384
+    for nbs, cut in ((6, B), (7, B), (5, B - 16384), (8, B + 16384)):
+        head = b'["' + b"a" * (cut - 2 - nbs // 2)
+        doc = head + b"\\" * nbs + b'"' + b"b" * 20000 + (b'"]' if nbs % 2 else b',"c"]')
+        assert doc[cut - 1:cut + 1] == b"\\\\"  # the run straddles the boundary
+        check_same(parser, oracle, doc, "carry chunk %d %d" % (nbs, cut))
